@@ -1,0 +1,174 @@
+/* flowmoe.h — C ABI of the B200-native FlowMoE block hot path (libflowmoe.so).
+ *
+ * What it computes: one training iteration of a transformer-MoE block —
+ * MHA + top-k gating (task AT), A2A dispatch (D), expert FFN (E), A2A combine
+ * (C), forward and backward — split into R micro-batch chunks and run as one
+ * pipeline in the orders of Eqs.(3)-(6) (§3.2), with the
+ * all-reduce of the replicated MHA and gating gradients (4M²+M·E parameters
+ * per block) cut into S_p-byte chunks and issued at lower priority than
+ * the A2A tasks (Alg. 2).  Block math: P:75-76 (MHA W^Q,W^K,
+ * W^V,W^O ∈ R^{M×M}; gate = linear M×E + softmax + top-k; capacity
+ * C = f·k·B·N/E; experts M×H then H×M).  Readings of points the paper leaves
+ * open are listed in DESIGN.md ("Readings").
+ *
+ * Conventions
+ *  - Row-vector convention y = x·W; every weight is stored [in][out] row-major.
+ *  - "tokens" B (this ABI) = the paper's B·N on one rank; chunk r of R covers
+ *    whole sequences [r·S/R, (r+1)·S/R) (reading Q1), S = B/seq_len.
+ *  - dtype BF16: activations and weights bf16, fp32 accumulation, grads fp32.
+ *    dtype F32: everything fp32 with true-fp32 (non-TF32) arithmetic.
+ *  - All device pointers are CUDA device memory of the ctx's device; every
+ *    enqueueing call is host-synchronous for validation and stream-ordered
+ *    (asynchronous) for the work.  Nothing is enqueued when a call returns an
+ *    error.  Nothing throws or aborts across the ABI.
+ *  - Ownership: the caller owns x, y, dy, dx, params, grads and `saved`
+ *    (sized by flowmoe_saved_bytes, one per block of a stack); pointers must
+ *    stay valid until the enqueued work completes.  The ctx owns its streams,
+ *    events, NCCL communicators and backward workspaces (reused across blocks).
+ */
+#ifndef FLOWMOE_H
+#define FLOWMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FLOWMOE_OK = 0,
+  FLOWMOE_ERR_INVALID = 1,     /* a config field or argument is invalid; message names it */
+  FLOWMOE_ERR_CUDA = 2,        /* a CUDA runtime call or kernel launch failed */
+  FLOWMOE_ERR_NCCL = 3,        /* an NCCL call failed or the communicator reported an async error */
+  FLOWMOE_ERR_OOM = 4,         /* device allocation of a ctx workspace failed */
+  FLOWMOE_ERR_UNSUPPORTED = 5, /* valid but not implemented shape (e.g. d_h not in {16,32,64,128}) */
+  FLOWMOE_ERR_STATE = 6        /* call out of order (e.g. waiting on an unknown ticket) */
+} flowmoe_status;
+
+typedef enum { FLOWMOE_F32 = 0, FLOWMOE_BF16 = 1 } flowmoe_dtype;
+
+typedef struct {
+  int64_t B;               /* tokens on this rank (paper B·N); B % seq_len == 0; (B/seq_len) % R == 0 */
+  int32_t seq_len;         /* N, tokens per sequence (attention span) */
+  int32_t M;               /* model dim; M % n_heads == 0; d_h = M/n_heads in {16,32,64,128} */
+  int32_t n_heads;         /* h (not in the paper; reading Q13) */
+  int32_t E;               /* experts per block, E in {2,4,8,16,32,64}; E % world_size == 0 */
+  int32_t top_k;           /* k, 1 <= k <= min(E, 8) */
+  int32_t d_ffn;           /* expert hidden size (paper H), multiple of 8 */
+  int32_t R;               /* pipelining degree, >= 1 */
+  float capacity_factor;   /* f >= 0; 0 => dropless (C = B/R); else C = ceil(f·k·(B/R)/E) */
+  int32_t causal;          /* 0/1: causal attention mask */
+  int32_t residual;        /* 0/1: I' = ctx·Wo + x and y = MoE(I') + I' */
+  int32_t dtype;           /* flowmoe_dtype */
+  int32_t world_size;      /* P */
+  int32_t rank;            /* p; experts [p·E/P, (p+1)·E/P) are local (reading Q12) */
+} flowmoe_config;
+
+/* Weights of one block (dtype of the config).  Replicated: wqkv [M][3M] (columns
+ * q|k|v), wo [M][M], wg [M][E].  Local experts only: w1 [E/P][M][F],
+ * b1 [E/P][F], w2 [E/P][F][M], b2 [E/P][M]. */
+typedef struct {
+  const void *wqkv, *wo, *wg, *w1, *b1, *w2, *b2;
+} flowmoe_params;
+
+/* Gradients, fp32, ACCUMULATED (+=).  grad_flat = [dWqkv (M×3M) | dWo (M×M) |
+ * dWg (M×E)], 4M²+M·E floats, all-reduced (sum over ranks) by the AR that
+ * flowmoe_block_bwd submits; zero it before an iteration for a plain sum.
+ * dw1 [E/P][M][F], db1 [E/P][F], dw2 [E/P][F][M], db2 [E/P][M] are the local
+ * experts' grads summed over all source ranks (no AR: experts are sharded). */
+typedef struct {
+  float *grad_flat, *dw1, *db1, *dw2, *db2;
+} flowmoe_grads;
+
+typedef struct flowmoe_ctx flowmoe_ctx;
+typedef uint64_t flowmoe_ticket;
+
+/* NCCL unique id for world_size > 1: call on rank 0, broadcast the 128 bytes to
+ * the other ranks (e.g. over torch.distributed), pass to flowmoe_create. */
+flowmoe_status flowmoe_get_unique_id(uint8_t id[128]);
+
+/* Validate the config and create a ctx on `device` (streams, events, NCCL comms
+ * for world_size > 1, backward workspaces).  `id` may be NULL when world_size == 1.
+ * Collective over the world when world_size > 1. */
+flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], int device,
+                              flowmoe_ctx** out);
+
+/* Bytes of the per-block activation stash written by block_fwd, read by block_bwd. */
+size_t flowmoe_saved_bytes(const flowmoe_ctx* ctx);
+
+/* Number of floats of the flat replicated-grad buffer: 4M² + M·E. */
+size_t flowmoe_grad_flat_count(const flowmoe_ctx* ctx);
+
+/* Forward of one block: x [B][M] -> y [B][M] (dtype), saving activations in
+ * `saved`.  Compute tasks AT_1..AT_R, E_1..E_R run in Eq.(3) order on the
+ * compute stream; D_r, C_r (NCCL all-to-all, world_size > 1) in Eq.(4) order on
+ * the high-priority comm stream.  Work is ordered after prior work on `stream`
+ * and `stream` waits for its completion.  Collective when world_size > 1. */
+flowmoe_status flowmoe_block_fwd(flowmoe_ctx* ctx, const flowmoe_params* params, const void* x,
+                                 void* y, void* saved, cudaStream_t stream);
+
+/* Backward of one block given dy [B][M]: dx [B][M] (nullable: skipped), grads
+ * accumulated (+=).  Compute order Eq.(5) (E_R..E_1, AT_R..AT_1), A2A order
+ * Eq.(6).  The AR of grad_flat is auto-submitted in chunks of `chunk_bytes`
+ * (S_p; positive multiple of 16; >= bytes => one chunk; last chunk is the
+ * remainder) at priority 1 as soon as the grads are final
+ * (P:1173), returned in *ar (nullable).  Call flowmoe_allreduce_wait before
+ * reading grad_flat (Alg. 1 line 22). */
+flowmoe_status flowmoe_block_bwd(flowmoe_ctx* ctx, const flowmoe_params* params, const void* x,
+                                 const void* saved, const void* dy, void* dx,
+                                 const flowmoe_grads* grads, size_t chunk_bytes,
+                                 flowmoe_ticket* ar, cudaStream_t stream);
+
+/* Chunked in-place sum all-reduce of buf[count] fp32 over the world on the
+ * low-priority AR stream (Alg. 2 PARTITION + ARQueue).  Starts after `ready`
+ * (nullable: after work already enqueued on the ctx compute stream).
+ * priority >= 1 (lower = sooner; 0 is reserved for A2A).  world_size == 1: no-op. */
+flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* ctx, float* buf, size_t count,
+                                        size_t chunk_bytes, int priority, cudaEvent_t ready,
+                                        flowmoe_ticket* out);
+
+/* Make `stream` wait for every chunk of the ticket's all-reduce; polls NCCL async errors. */
+flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* ctx, flowmoe_ticket ticket, cudaStream_t stream);
+
+/* Test hook: force the top-k indices ([B][k] int32 device array, distinct
+ * experts per row) instead of selecting them; gate weights are still computed
+ * from the logits at those indices.  NULL restores normal routing. */
+flowmoe_status flowmoe_set_forced_routing(flowmoe_ctx* ctx, const int32_t* idx);
+
+/* Byte offsets inside `saved` of the fp32 gate logits [B][E], indices [B][k]
+ * int32, gate weights [B][k] fp32, positions [B][k] int32 (-1 = dropped) and
+ * per-chunk counts [R][E] int32 (test inspection of routing). */
+flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* logits, size_t* idx,
+                                             size_t* w, size_t* pos, size_t* counts);
+
+/* Test/benchmark knobs: key 1 = force the SIMT GEMM for bf16 (debug), key 2 =
+ * swap MN-major descriptor strides (debug).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
+flowmoe_status flowmoe_debug_set(int key, int value);
+
+/* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,
+ * fp32 SIMT for F32).  C(m,n) = epi(sum_k A(m,k) B(k,n)) per batch b, with
+ * A(m,k) = A[b*sA + m*lda + k] (a_mmajor=0) or A[b*sA + k*lda + m] (a_mmajor=1),
+ * B(k,n) = B[b*sB + k*ldb + n] (b_kmajor=0) or B[b*sB + n*ldb + k] (b_kmajor=1).
+ * epi: 0 store (+bias[n] +resid), 1 bias+GELU (aux = pre-activation),
+ * 2 times GELU'(aux), 3 fp32 accumulate C += acc.  bias/resid/aux nullable;
+ * resid and aux share C's ld/stride, bias has stride N per batch. */
+flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch, const void* A,
+                                 int64_t lda, int64_t sA, int a_mmajor, const void* B, int64_t ldb,
+                                 int64_t sB, int b_kmajor, void* C, int64_t ldc, int64_t sC, int epi,
+                                 const void* bias, const void* resid, void* aux, cudaStream_t stream);
+
+/* Number of kernels this library has launched in the calling process (bench accounting). */
+uint64_t flowmoe_kernel_launches(void);
+
+const char* flowmoe_status_string(flowmoe_status s);
+const char* flowmoe_last_error(void); /* thread-local message of the last failing call */
+
+/* Synchronises the ctx streams, destroys NCCL comms, frees workspaces. */
+void flowmoe_destroy(flowmoe_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWMOE_H */

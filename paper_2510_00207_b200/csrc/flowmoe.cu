@@ -1,0 +1,666 @@
+// libflowmoe.so — C ABI + chunk scheduler of the FlowMoE block hot path.
+//
+// One ctx per rank (one process per GPU).  Three CUDA streams:
+//   s_comp (compute tasks AT_r, E_r and their backward, in Eq.(3)/(5) order),
+//   s_a2a  (highest priority: NCCL all-to-all D_r, C_r in Eq.(4)/(6) order),
+//   s_ar   (lowest priority: chunked NCCL all-reduce of the MHA+gate grads).
+// Dependencies between chunks are cudaEvents (the paper's DataQueue);
+// the A2A and AR op orders are static and identical on every rank, so the two
+// NCCL communicators never see diverging op orders (SURVEY.md §7 hard part 4).
+// The AR chunks are released as soon as the grads they cover are final
+// (reading Q10) and run on the low-priority stream/communicator, in
+// the gaps left by the A2A stream (Alg. 2's "A2A first" rule).
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/flowmoe.h"
+#include "kernels.h"
+
+using namespace fm;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+flowmoe_status fail(flowmoe_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+constexpr int NUM_TICKET_EVENTS = 4096;
+
+struct SavedLayout {
+  size_t qkv, ctx, lse, a, logits, idx, w, pos, counts, src, send, xe, z, h, ye, yc, total;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct flowmoe_ctx {
+  flowmoe_config cfg;
+  int dev = 0;
+  int64_t T = 0, Tr = 0, S = 0, C = 0, El = 0, P = 1, F = 0, M = 0, E = 0, k = 1, H = 1, N = 1;
+  size_t es = 2;
+  int dt = DT_BF16;
+  cudaStream_t s_comp = nullptr, s_a2a = nullptr, s_ar = nullptr;
+  ncclComm_t comm_a2a = nullptr, comm_ar = nullptr;
+  // per-chunk events
+  std::vector<cudaEvent_t> ev_at, ev_d, ev_e, ev_c, ev_cb, ev_cba, ev_eb, ev_dba;
+  cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_grads_a = nullptr, ev_grads_b = nullptr;
+  std::vector<cudaEvent_t> ticket_ev;
+  uint64_t next_ticket = 1;
+  SavedLayout L{};
+  // backward workspaces (ctx-owned, reused by every block)
+  void *dyc = nullptr, *dye = nullptr, *dz = nullptr, *dxe = nullptr, *dxc = nullptr;
+  void *dA = nullptr, *dctx = nullptr, *dqkv = nullptr;
+  float *dl = nullptr, *dw = nullptr, *Dbuf = nullptr, *wg_part = nullptr;
+  std::vector<void*> allocs;
+  const int32_t* forced = nullptr;
+};
+
+namespace {
+
+#define FM_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(FLOWMOE_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define FM_NCCL(call)                                                                      \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(FLOWMOE_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));  \
+  } while (0)
+#define FM_K(nk, call)                                                                     \
+  do {                                                                                     \
+    int e_ = (call);                                                                       \
+    g_launches += (nk);                                                                    \
+    if (e_ != 0)                                                                           \
+      return fail(FLOWMOE_ERR_CUDA, std::string(#call) + ": " +                            \
+                                        cudaGetErrorString((cudaError_t)e_));              \
+  } while (0)
+
+flowmoe_status validate(const flowmoe_config* c) {
+  if (!c) return fail(FLOWMOE_ERR_INVALID, "config is NULL");
+  auto bad = [](const char* f, const std::string& why) {
+    return fail(FLOWMOE_ERR_INVALID, std::string("config.") + f + ": " + why);
+  };
+  if (c->B <= 0) return bad("B", "must be > 0");
+  if (c->seq_len <= 0) return bad("seq_len", "must be > 0");
+  if (c->B % c->seq_len) return bad("B", "must be a multiple of seq_len (whole sequences)");
+  if (c->R <= 0) return bad("R", "must be >= 1");
+  if ((c->B / c->seq_len) % c->R)
+    return bad("R", "must divide the number of sequences B/seq_len (chunks are whole sequences, reading Q1)");
+  if (c->M <= 0 || c->M % 8) return bad("M", "must be a positive multiple of 8");
+  if (c->n_heads <= 0 || c->M % c->n_heads) return bad("n_heads", "must divide M");
+  int dh = c->M / c->n_heads;
+  if (dh != 16 && dh != 32 && dh != 64 && dh != 128) return bad("n_heads", "d_h = M/n_heads must be 16, 32, 64 or 128");
+  if (c->E != 2 && c->E != 4 && c->E != 8 && c->E != 16 && c->E != 32 && c->E != 64)
+    return bad("E", "must be one of 2,4,8,16,32,64");
+  if (c->top_k < 1 || c->top_k > c->E || c->top_k > 8) return bad("top_k", "need 1 <= k <= min(E, 8)");
+  if (c->d_ffn <= 0 || c->d_ffn % 8) return bad("d_ffn", "must be a positive multiple of 8");
+  if (!(c->capacity_factor >= 0.f)) return bad("capacity_factor", "must be >= 0");
+  if (c->causal != 0 && c->causal != 1) return bad("causal", "must be 0 or 1");
+  if (c->residual != 0 && c->residual != 1) return bad("residual", "must be 0 or 1");
+  if (c->dtype != FLOWMOE_F32 && c->dtype != FLOWMOE_BF16) return bad("dtype", "must be FLOWMOE_F32 or FLOWMOE_BF16");
+  if (c->world_size < 1) return bad("world_size", "must be >= 1");
+  if (c->rank < 0 || c->rank >= c->world_size) return bad("rank", "must be in [0, world_size)");
+  if (c->E % c->world_size) return bad("E", "must be a multiple of world_size (experts sharded evenly)");
+  return FLOWMOE_OK;
+}
+
+int64_t capacity_of(const flowmoe_config* c, int64_t Tr) {
+  // C = f·k·B·N/E, ceil; f = 0 => dropless (reading Q3)
+  if (c->capacity_factor == 0.f) return Tr;
+  return (int64_t)ceil((double)c->capacity_factor * (double)c->top_k * (double)Tr / (double)c->E);
+}
+
+SavedLayout layout_of(const flowmoe_ctx* x) {
+  SavedLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t es = x->es;
+  const int64_t T = x->T, M = x->M, E = x->E, k = x->k, R = x->cfg.R, C = x->C, F = x->F;
+  L.qkv = take(T * 3 * M * es);
+  L.ctx = take(T * M * es);
+  L.lse = take(T * x->H * 4);
+  L.a = take(T * M * es);
+  L.logits = take(T * E * 4);
+  L.idx = take(T * k * 4);
+  L.w = take(T * k * 4);
+  L.pos = take(T * k * 4);
+  L.counts = take(R * E * 4);
+  L.src = take(R * E * C * 4);
+  L.send = take(R * E * C * M * es);
+  L.xe = x->P > 1 ? take(R * E * C * M * es) : L.send;
+  L.z = take(R * E * C * F * es);  // [R][El][P*C][F] == R*E*C*F elements
+  L.h = take(R * E * C * F * es);
+  L.ye = take(R * E * C * M * es);
+  L.yc = x->P > 1 ? take(R * E * C * M * es) : L.ye;
+  L.total = off;
+  return L;
+}
+
+ncclDataType_t nccl_dt(const flowmoe_ctx* x) { return x->dt == DT_BF16 ? ncclBfloat16 : ncclFloat; }
+
+// send [E][C][M] (experts grouped by owner) -> recv [El][P][C][M] (rows of one expert contiguous)
+flowmoe_status a2a_to_experts(flowmoe_ctx* x, const void* send, void* recv) {
+  const size_t blk = (size_t)x->C * x->M;
+  FM_NCCL(ncclGroupStart());
+  for (int q = 0; q < x->P; ++q)
+    for (int el = 0; el < x->El; ++el) {
+      FM_NCCL(ncclSend((const char*)send + ((size_t)q * x->El + el) * blk * x->es, blk, nccl_dt(x), q,
+                       x->comm_a2a, x->s_a2a));
+      FM_NCCL(ncclRecv((char*)recv + ((size_t)el * x->P + q) * blk * x->es, blk, nccl_dt(x), q,
+                       x->comm_a2a, x->s_a2a));
+    }
+  FM_NCCL(ncclGroupEnd());
+  return FLOWMOE_OK;
+}
+
+// send [El][P][C][M] (expert side) -> recv [E][C][M] (token-owner side)
+flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv) {
+  const size_t blk = (size_t)x->C * x->M;
+  FM_NCCL(ncclGroupStart());
+  for (int q = 0; q < x->P; ++q)
+    for (int el = 0; el < x->El; ++el) {
+      FM_NCCL(ncclSend((const char*)send + ((size_t)el * x->P + q) * blk * x->es, blk, nccl_dt(x), q,
+                       x->comm_a2a, x->s_a2a));
+      FM_NCCL(ncclRecv((char*)recv + ((size_t)q * x->El + el) * blk * x->es, blk, nccl_dt(x), q,
+                       x->comm_a2a, x->s_a2a));
+    }
+  FM_NCCL(ncclGroupEnd());
+  return FLOWMOE_OK;
+}
+
+template <typename P_>
+P_* at(void* base, size_t off) { return reinterpret_cast<P_*>(reinterpret_cast<char*>(base) + off); }
+template <typename P_>
+const P_* at(const void* base, size_t off) {
+  return reinterpret_cast<const P_*>(reinterpret_cast<const char*>(base) + off);
+}
+
+flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_bytes,
+                         cudaEvent_t ready) {
+  if (ready) FM_CUDA(cudaStreamWaitEvent(x->s_ar, ready, 0));
+  if (x->P == 1 || count == 0) return FLOWMOE_OK;
+  const size_t chunk = chunk_bytes / 4;
+  for (size_t off = 0; off < count; off += chunk) {
+    const size_t n = (count - off < chunk) ? count - off : chunk;
+    FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
+  }
+  return FLOWMOE_OK;
+}
+
+flowmoe_status new_ticket(flowmoe_ctx* x, flowmoe_ticket* out) {
+  const uint64_t t = x->next_ticket++;
+  FM_CUDA(cudaEventRecord(x->ticket_ev[t % NUM_TICKET_EVENTS], x->s_ar));
+  if (out) *out = t;
+  return FLOWMOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* flowmoe_status_string(flowmoe_status s) {
+  switch (s) {
+    case FLOWMOE_OK: return "ok";
+    case FLOWMOE_ERR_INVALID: return "invalid argument";
+    case FLOWMOE_ERR_CUDA: return "CUDA error";
+    case FLOWMOE_ERR_NCCL: return "NCCL error";
+    case FLOWMOE_ERR_OOM: return "out of device memory";
+    case FLOWMOE_ERR_UNSUPPORTED: return "unsupported";
+    case FLOWMOE_ERR_STATE: return "invalid state";
+  }
+  return "unknown status";
+}
+
+const char* flowmoe_last_error(void) { return g_err.c_str(); }
+
+uint64_t flowmoe_kernel_launches(void) { return g_launches.load(); }
+
+flowmoe_status flowmoe_debug_set(int key, int value) {
+  static int flags = 0;
+  if (key == 1) flags = (flags & ~1) | (value ? 1 : 0);
+  else if (key == 2) flags = (flags & ~2) | (value ? 2 : 0);
+  else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
+  gemm_tc_set_debug(flags);
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(FLOWMOE_ERR_INVALID, "id is NULL");
+  ncclUniqueId u;
+  FM_NCCL(ncclGetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id, &u, 128);
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], int device,
+                              flowmoe_ctx** out) {
+  if (!out) return fail(FLOWMOE_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (flowmoe_status s = validate(cfg)) return s;
+  if (cfg->world_size > 1 && !id) return fail(FLOWMOE_ERR_INVALID, "id is NULL with world_size > 1");
+  auto* x = new flowmoe_ctx();
+  x->cfg = *cfg;
+  x->dev = device;
+  x->T = cfg->B;
+  x->Tr = cfg->B / cfg->R;
+  x->N = cfg->seq_len;
+  x->S = cfg->B / cfg->seq_len;
+  x->M = cfg->M;
+  x->E = cfg->E;
+  x->k = cfg->top_k;
+  x->H = cfg->n_heads;
+  x->F = cfg->d_ffn;
+  x->P = cfg->world_size;
+  x->El = cfg->E / cfg->world_size;
+  x->C = capacity_of(cfg, x->Tr);
+  x->dt = cfg->dtype == FLOWMOE_BF16 ? DT_BF16 : DT_F32;
+  x->es = cfg->dtype == FLOWMOE_BF16 ? 2 : 4;
+  x->L = layout_of(x);
+  auto cleanup_fail = [&](flowmoe_status s) {
+    flowmoe_destroy(x);
+    return s;
+  };
+  if (cudaSetDevice(device) != cudaSuccess)
+    return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "cudaSetDevice failed"));
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = greatest priority (numerically lowest)
+  if (cudaStreamCreateWithPriority(&x->s_comp, cudaStreamNonBlocking, 0) ||
+      cudaStreamCreateWithPriority(&x->s_a2a, cudaStreamNonBlocking, hi) ||
+      cudaStreamCreateWithPriority(&x->s_ar, cudaStreamNonBlocking, lo))
+    return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
+  auto mk = [&](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
+  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba}) {
+    v->resize(cfg->R);
+    for (auto& e : *v)
+      if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  }
+  x->ticket_ev.resize(NUM_TICKET_EVENTS);
+  for (auto& e : x->ticket_ev)
+    if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  if (!mk(&x->ev_in) || !mk(&x->ev_done) || !mk(&x->ev_grads_a) || !mk(&x->ev_grads_b))
+    return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  // backward workspaces
+  auto alloc = [&](void** p, size_t bytes) {
+    if (cudaMalloc(p, bytes < 256 ? 256 : bytes) != cudaSuccess) return false;
+    x->allocs.push_back(*p);
+    return true;
+  };
+  const size_t es = x->es;
+  const int64_t R = cfg->R, ECM = x->E * x->C * x->M;
+  bool ok = alloc(&x->dyc, R * ECM * es) && alloc(&x->dxe, R * ECM * es) &&
+            alloc(&x->dz, (size_t)x->E * x->C * x->F * es) && alloc(&x->dA, x->T * x->M * es) &&
+            alloc(&x->dctx, x->T * x->M * es) && alloc(&x->dqkv, x->T * 3 * x->M * es) &&
+            alloc((void**)&x->dl, x->T * x->E * 4) && alloc((void**)&x->dw, x->T * x->k * 4) &&
+            alloc((void**)&x->Dbuf, x->T * x->H * 4) &&
+            alloc((void**)&x->wg_part, gate_wgrad_scratch_floats((int)x->T, (int)x->M, (int)x->E) * 4);
+  if (ok && x->P > 1) ok = alloc(&x->dye, R * ECM * es) && alloc(&x->dxc, R * ECM * es);
+  if (!ok) return cleanup_fail(fail(FLOWMOE_ERR_OOM, "workspace allocation failed"));
+  if (x->P == 1) { x->dye = x->dyc; x->dxc = x->dxe; }
+  if (x->dt == DT_BF16 && gemm_tc_init() != 0)
+    return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable"));
+  if (x->P > 1) {
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+    nc.blocking = 1;
+    if (ncclCommInitRankConfig(&x->comm_a2a, (int)x->P, u, cfg->rank, &nc) != ncclSuccess)
+      return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommInitRankConfig failed"));
+    ncclConfig_t nc2 = NCCL_CONFIG_INITIALIZER;
+    nc2.blocking = 1;
+    if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &x->comm_ar, &nc2) != ncclSuccess)
+      return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit failed"));
+  }
+  *out = x;
+  return FLOWMOE_OK;
+}
+
+size_t flowmoe_saved_bytes(const flowmoe_ctx* x) { return x ? x->L.total : 0; }
+
+size_t flowmoe_grad_flat_count(const flowmoe_ctx* x) {
+  return x ? (size_t)(4 * x->M * x->M + x->M * x->E) : 0;
+}
+
+flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* x, size_t* logits, size_t* idx,
+                                             size_t* w, size_t* pos, size_t* counts) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (logits) *logits = x->L.logits;
+  if (idx) *idx = x->L.idx;
+  if (w) *w = x->L.w;
+  if (pos) *pos = x->L.pos;
+  if (counts) *counts = x->L.counts;
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_set_forced_routing(flowmoe_ctx* x, const int32_t* idx) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  x->forced = idx;
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
+                                 void* y, void* saved, cudaStream_t stream) {
+  if (!x || !p || !xin || !y || !saved) return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL argument");
+  if (!p->wqkv || !p->wo || !p->wg || !p->w1 || !p->b1 || !p->w2 || !p->b2)
+    return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL parameter pointer");
+  const int dt = x->dt;
+  const size_t es = x->es;
+  const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
+  const int64_t ECM = E * C * M, ECF = E * C * F, PC = P * C;
+  const SavedLayout& L = x->L;
+  cudaStream_t sc = x->s_comp;
+  FM_CUDA(cudaEventRecord(x->ev_in, stream));
+  FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
+  // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer
+  for (int r = 0; r < x->cfg.R; ++r) {
+    const int64_t t0 = r * Tr;
+    const char* xr = (const char*)xin + t0 * M * es;
+    void* qkv = at<char>(saved, L.qkv + t0 * 3 * M * es);
+    void* ctxb = at<char>(saved, L.ctx + t0 * M * es);
+    void* a = at<char>(saved, L.a + t0 * M * es);
+    GemmArgs g;
+    g.M = (int)Tr; g.N = (int)(3 * M); g.K = (int)M;
+    g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
+    FM_K(1, gemm(g, dt, sc));
+    FM_K(1, attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N,
+                     (int)M, (int)x->H, x->cfg.causal, sc));
+    g = GemmArgs();
+    g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
+    g.A = ctxb; g.lda = M; g.B = p->wo; g.ldb = M; g.C = a; g.ldc = M;
+    if (x->cfg.residual) { g.resid = xr; g.ldr = M; }
+    FM_K(1, gemm(g, dt, sc));
+    FM_K(1, gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr,
+                      at<float>(saved, L.logits + t0 * E * 4), at<int32_t>(saved, L.idx + t0 * k * 4),
+                      at<float>(saved, L.w + t0 * k * 4), (int)Tr, (int)M, (int)E, (int)k, sc));
+    int32_t* src = at<int32_t>(saved, L.src + r * E * C * 4);
+    FM_K(1, route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+                       at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
+    FM_K(1, permute_pack(dt, a, src, at<char>(saved, L.send + r * ECM * es), (int)(E * C), (int)M,
+                         (int)k, sc));
+    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
+  }
+  // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
+  if (P > 1)
+    for (int r = 0; r < x->cfg.R; ++r) {
+      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_at[r], 0));
+      if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send + r * ECM * es),
+                                            at<char>(saved, L.xe + r * ECM * es)))
+        return s;
+      FM_CUDA(cudaEventRecord(x->ev_d[r], x->s_a2a));
+    }
+  // ---- E_1..E_R: batched expert FFN over [El][P*C] capacity rows
+  for (int r = 0; r < x->cfg.R; ++r) {
+    if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_d[r], 0));
+    void* xe = at<char>(saved, L.xe + r * ECM * es);
+    void* z = at<char>(saved, L.z + r * ECF * es);
+    void* h = at<char>(saved, L.h + r * ECF * es);
+    void* ye = at<char>(saved, L.ye + r * ECM * es);
+    GemmArgs g;
+    g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
+    g.A = xe; g.lda = M; g.sA = PC * M;
+    g.B = p->w1; g.ldb = F; g.sB = M * F;
+    g.C = h; g.ldc = F; g.sC = PC * F;
+    g.bias = p->b1; g.sBias = F;
+    g.aux = z; g.ldaux = F; g.sAux = PC * F;
+    g.epi = EPI_BIAS_GELU;
+    FM_K(1, gemm(g, dt, sc));
+    g = GemmArgs();
+    g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
+    g.A = h; g.lda = F; g.sA = PC * F;
+    g.B = p->w2; g.ldb = M; g.sB = F * M;
+    g.C = ye; g.ldc = M; g.sC = PC * M;
+    g.bias = p->b2; g.sBias = M;
+    FM_K(1, gemm(g, dt, sc));
+    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_e[r], sc));
+  }
+  // ---- C_1..C_R (Eq.(4))
+  if (P > 1)
+    for (int r = 0; r < x->cfg.R; ++r) {
+      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_e[r], 0));
+      if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye + r * ECM * es),
+                                           at<char>(saved, L.yc + r * ECM * es)))
+        return s;
+      FM_CUDA(cudaEventRecord(x->ev_c[r], x->s_a2a));
+    }
+  // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
+  for (int r = 0; r < x->cfg.R; ++r) {
+    if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_c[r], 0));
+    const int64_t t0 = r * Tr;
+    FM_K(1, unpermute_combine(dt, at<char>(saved, L.yc + r * ECM * es), at<int32_t>(saved, L.idx + t0 * k * 4),
+                              at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
+                              x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
+                              (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)C, sc));
+  }
+  FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
+                                 const void* saved, const void* dy, void* dx,
+                                 const flowmoe_grads* gr, size_t chunk_bytes, flowmoe_ticket* ar,
+                                 cudaStream_t stream) {
+  if (!x || !p || !xin || !saved || !dy || !gr)
+    return fail(FLOWMOE_ERR_INVALID, "block_bwd: NULL argument");
+  if (!gr->grad_flat || !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2)
+    return fail(FLOWMOE_ERR_INVALID, "block_bwd: NULL gradient pointer");
+  if (chunk_bytes == 0 || chunk_bytes % 16)
+    return fail(FLOWMOE_ERR_INVALID, "block_bwd: chunk_bytes (S_p) must be a positive multiple of 16");
+  const int dt = x->dt;
+  const size_t es = x->es;
+  const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
+  const int64_t ECM = E * C * M, ECF = E * C * F, PC = P * C;
+  const SavedLayout& L = x->L;
+  const int R = x->cfg.R;
+  cudaStream_t sc = x->s_comp;
+  FM_CUDA(cudaEventRecord(x->ev_in, stream));
+  FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
+  // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the combine-side buffer, dw = <dO, Y>
+  for (int r = R - 1; r >= 0; --r) {
+    const int64_t t0 = r * Tr;
+    FM_K(1, combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * ECM * es),
+                             at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+                             at<float>(saved, L.w + t0 * k * 4), at<int32_t>(saved, L.src + r * E * C * 4),
+                             (char*)x->dyc + r * ECM * es, x->dw + t0 * k, (int)Tr, (int)M, (int)k,
+                             (int)E, (int)C, sc));
+    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_cb[r], sc));
+  }
+  if (P > 1)
+    for (int r = R - 1; r >= 0; --r) {
+      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_cb[r], 0));
+      if (flowmoe_status s = a2a_to_experts(x, (char*)x->dyc + r * ECM * es, (char*)x->dye + r * ECM * es))
+        return s;
+      FM_CUDA(cudaEventRecord(x->ev_cba[r], x->s_a2a));
+    }
+  // ---- E_R^bwd .. E_1^bwd (Eq.(5))
+  for (int r = R - 1; r >= 0; --r) {
+    if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_cba[r], 0));
+    const void* dye = (char*)x->dye + r * ECM * es;
+    const void* xe = at<char>(saved, L.xe + r * ECM * es);
+    const void* z = at<char>(saved, L.z + r * ECF * es);
+    const void* h = at<char>(saved, L.h + r * ECF * es);
+    // dZ = (dY·W2ᵀ) ⊙ GELU'(Z)
+    GemmArgs g;
+    g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
+    g.A = dye; g.lda = M; g.sA = PC * M;
+    g.B = p->w2; g.ldb = M; g.sB = F * M; g.b_kmajor = 1;
+    g.C = x->dz; g.ldc = F; g.sC = PC * F;
+    g.aux = const_cast<void*>(z); g.ldaux = F; g.sAux = PC * F;
+    g.epi = EPI_DGELU;
+    FM_K(1, gemm(g, dt, sc));
+    // dW2 += Hᵀ·dY
+    g = GemmArgs();
+    g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)PC;
+    g.A = h; g.lda = F; g.sA = PC * F; g.a_mmajor = 1;
+    g.B = dye; g.ldb = M; g.sB = PC * M;
+    g.C = gr->dw2; g.ldc = M; g.sC = F * M;
+    g.epi = EPI_ACC_F32;
+    FM_K(1, gemm(g, dt, sc));
+    FM_K(1, colsum_acc(dt, dye, gr->db2, (int)El, (int)PC, (int)M, sc));
+    // dW1 += Xᵀ·dZ
+    g = GemmArgs();
+    g.batch = (int)El; g.M = (int)M; g.N = (int)F; g.K = (int)PC;
+    g.A = xe; g.lda = M; g.sA = PC * M; g.a_mmajor = 1;
+    g.B = x->dz; g.ldb = F; g.sB = PC * F;
+    g.C = gr->dw1; g.ldc = F; g.sC = M * F;
+    g.epi = EPI_ACC_F32;
+    FM_K(1, gemm(g, dt, sc));
+    FM_K(1, colsum_acc(dt, x->dz, gr->db1, (int)El, (int)PC, (int)F, sc));
+    // dX_e = dZ·W1ᵀ  -> dispatch-bwd send buffer [El][P][C][M]
+    g = GemmArgs();
+    g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
+    g.A = x->dz; g.lda = F; g.sA = PC * F;
+    g.B = p->w1; g.ldb = F; g.sB = M * F; g.b_kmajor = 1;
+    g.C = (char*)x->dxe + r * ECM * es; g.ldc = M; g.sC = PC * M;
+    FM_K(1, gemm(g, dt, sc));
+    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
+  }
+  if (P > 1)
+    for (int r = R - 1; r >= 0; --r) {
+      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_eb[r], 0));
+      if (flowmoe_status s = a2a_to_owners(x, (char*)x->dxe + r * ECM * es, (char*)x->dxc + r * ECM * es))
+        return s;
+      FM_CUDA(cudaEventRecord(x->ev_dba[r], x->s_a2a));
+    }
+  // ---- AT_R^bwd .. AT_1^bwd
+  for (int r = R - 1; r >= 0; --r) {
+    if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dba[r], 0));
+    const int64_t t0 = r * Tr;
+    void* dA = (char*)x->dA + t0 * M * es;
+    void* dctx = (char*)x->dctx + t0 * M * es;
+    void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
+    FM_K(1, gather_gate_bwd(dt, (char*)x->dxc + r * ECM * es, at<int32_t>(saved, L.idx + t0 * k * 4),
+                            at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
+                            x->dw + t0 * k, at<float>(saved, L.logits + t0 * E * 4), p->wg,
+                            x->cfg.residual ? (const char*)dy + t0 * M * es : nullptr, dA,
+                            x->dl + t0 * E, (int)Tr, (int)M, (int)E, (int)k, (int)C, sc));
+    GemmArgs g;
+    g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
+    g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
+    FM_K(1, gemm(g, dt, sc));
+    FM_K(3, attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
+                     at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf, (int)Tr, (int)x->N,
+                     (int)M, (int)x->H, x->cfg.causal, sc));
+    if (dx) {
+      g = GemmArgs();
+      g.M = (int)Tr; g.N = (int)M; g.K = (int)(3 * M);
+      g.A = dqkv; g.lda = 3 * M; g.B = p->wqkv; g.ldb = 3 * M; g.b_kmajor = 1;
+      g.C = (char*)dx + t0 * M * es; g.ldc = M;
+      if (x->cfg.residual) { g.resid = dA; g.ldr = M; }
+      FM_K(1, gemm(g, dt, sc));
+    }
+  }
+  // ---- deferred wgrads over all T tokens (one K=T GEMM each), in the order
+  // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
+  float* gf = gr->grad_flat;
+  FM_K(2, gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M,
+                     (int)E, sc));
+  GemmArgs g;
+  g.M = (int)M; g.N = (int)M; g.K = (int)x->T;
+  g.A = at<char>(saved, L.ctx); g.lda = M; g.a_mmajor = 1;
+  g.B = x->dA; g.ldb = M;
+  g.C = gf + 3 * M * M; g.ldc = M; g.epi = EPI_ACC_F32;
+  FM_K(1, gemm(g, dt, sc));
+  FM_CUDA(cudaEventRecord(x->ev_grads_a, sc));
+  g = GemmArgs();
+  g.M = (int)M; g.N = (int)(3 * M); g.K = (int)x->T;
+  g.A = xin; g.lda = M; g.a_mmajor = 1;
+  g.B = x->dqkv; g.ldb = 3 * M;
+  g.C = gf; g.ldc = 3 * M; g.epi = EPI_ACC_F32;
+  FM_K(1, gemm(g, dt, sc));
+  FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
+  // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2)
+  if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
+  if (flowmoe_status s = submit_ar(x, gf, (size_t)(3 * M * M), chunk_bytes, x->ev_grads_b)) return s;
+  if (flowmoe_status s = new_ticket(x, ar)) return s;
+  FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* x, float* buf, size_t count,
+                                        size_t chunk_bytes, int priority, cudaEvent_t ready,
+                                        flowmoe_ticket* out) {
+  if (!x || (!buf && count)) return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: NULL argument");
+  if (priority < 1) return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: priority must be >= 1 (0 is A2A)");
+  if (chunk_bytes == 0 || chunk_bytes % 16)
+    return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: chunk_bytes must be a positive multiple of 16");
+  if (!ready) {
+    FM_CUDA(cudaEventRecord(x->ev_grads_a, x->s_comp));
+    ready = x->ev_grads_a;
+  }
+  if (flowmoe_status s = submit_ar(x, buf, count, chunk_bytes, ready)) return s;
+  return new_ticket(x, out);
+}
+
+flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStream_t stream) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (t == 0 || t >= x->next_ticket || x->next_ticket - t > NUM_TICKET_EVENTS)
+    return fail(FLOWMOE_ERR_STATE, "allreduce_wait: unknown or expired ticket");
+  if (x->P > 1) {
+    ncclResult_t a = ncclSuccess, b = ncclSuccess;
+    ncclCommGetAsyncError(x->comm_a2a, &a);
+    ncclCommGetAsyncError(x->comm_ar, &b);
+    if (a != ncclSuccess || b != ncclSuccess)
+      return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
+  }
+  FM_CUDA(cudaStreamWaitEvent(stream, x->ticket_ev[t % NUM_TICKET_EVENTS], 0));
+  return FLOWMOE_OK;
+}
+
+void flowmoe_destroy(flowmoe_ctx* x) {
+  if (!x) return;
+  if (x->s_comp) cudaStreamSynchronize(x->s_comp);
+  if (x->s_a2a) cudaStreamSynchronize(x->s_a2a);
+  if (x->s_ar) cudaStreamSynchronize(x->s_ar);
+  if (x->comm_ar) ncclCommDestroy(x->comm_ar);
+  if (x->comm_a2a) ncclCommDestroy(x->comm_a2a);
+  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba})
+    for (auto e : *v) if (e) cudaEventDestroy(e);
+  for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
+  for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b}) if (e) cudaEventDestroy(e);
+  for (void* p : x->allocs) cudaFree(p);
+  if (x->s_comp) cudaStreamDestroy(x->s_comp);
+  if (x->s_a2a) cudaStreamDestroy(x->s_a2a);
+  if (x->s_ar) cudaStreamDestroy(x->s_ar);
+  delete x;
+}
+
+}  // extern "C"
+
+extern "C" flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch,
+                                            const void* A, int64_t lda, int64_t sA, int a_mmajor,
+                                            const void* B, int64_t ldb, int64_t sB, int b_kmajor,
+                                            void* C, int64_t ldc, int64_t sC, int epi,
+                                            const void* bias, const void* resid, void* aux,
+                                            cudaStream_t stream) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A = A; g.lda = lda; g.sA = sA; g.a_mmajor = a_mmajor;
+  g.B = B; g.ldb = ldb; g.sB = sB; g.b_kmajor = b_kmajor;
+  g.C = C; g.ldc = ldc; g.sC = sC; g.epi = epi;
+  g.bias = bias; g.sBias = N;
+  g.resid = resid; g.ldr = ldc; g.sR = sC;
+  g.aux = aux; g.ldaux = ldc; g.sAux = sC;
+  if (dtype != DT_F32 && dtype != DT_BF16) return fail(FLOWMOE_ERR_INVALID, "dtype");
+  FM_K(1, gemm(g, dtype, stream));
+  return FLOWMOE_OK;
+}

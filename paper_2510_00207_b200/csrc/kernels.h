@@ -1,0 +1,82 @@
+// Internal launcher interface between the FlowMoE scheduler (flowmoe.cu) and
+// the sm_100a kernels.  Not part of the public C ABI (include/flowmoe.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fm {
+
+enum DType { DT_F32 = 0, DT_BF16 = 1 };
+
+// ---------------------------------------------------------------- GEMM
+// C(m,n) = epilogue( alpha * sum_k A(m,k) B(k,n) ), batched over `batch`.
+//   A(m,k) = A[b*sA + m*lda + k]   (a_mmajor = 0, "K-major")
+//          = A[b*sA + k*lda + m]   (a_mmajor = 1, "M-major": A stored transposed)
+//   B(k,n) = B[b*sB + k*ldb + n]   (b_kmajor = 0: weights W[in][out], "N-major")
+//          = B[b*sB + n*ldb + k]   (b_kmajor = 1: B = W^T, "K-major")
+// Epilogues (all math in fp32):
+//   EPI_STORE     C = alpha*acc (+ bias[n]) (+ resid(m,n))          -> storage dtype
+//   EPI_BIAS_GELU aux = Z = acc + bias[n];  C = GELU(Z)             -> storage dtype
+//   EPI_DGELU     C = acc * GELU'(aux(m,n))                        -> storage dtype
+//   EPI_ACC_F32   Cf32(m,n) += alpha*acc                            -> fp32 (grads)
+enum GemmEpi { EPI_STORE = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_ACC_F32 = 3 };
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0, batch = 1;
+  const void* A = nullptr; int64_t lda = 0, sA = 0; int a_mmajor = 0;
+  const void* B = nullptr; int64_t ldb = 0, sB = 0; int b_kmajor = 0;
+  void* C = nullptr; int64_t ldc = 0, sC = 0;
+  const void* bias = nullptr; int64_t sBias = 0;
+  const void* resid = nullptr; int64_t ldr = 0, sR = 0;
+  void* aux = nullptr; int64_t ldaux = 0, sAux = 0;
+  int epi = EPI_STORE;
+  float alpha = 1.0f;
+};
+
+// Dispatches to the tcgen05 kernel for bf16 and the fp32 SIMT kernel (K10) for f32.
+int gemm(const GemmArgs& g, int dtype, cudaStream_t s);
+int gemm_simt(const GemmArgs& g, int dtype, cudaStream_t s);
+int gemm_tc(const GemmArgs& g, cudaStream_t s);  // bf16 only, tcgen05/TMEM/TMA
+int gemm_tc_init();                               // resolves cuTensorMapEncodeTiled
+void gemm_tc_set_debug(int flags);
+
+// ---------------------------------------------------------------- attention
+// qkv [T][3M] (per sequence of N rows; head h at columns h*dh of each of Q|K|V)
+// ctx [T][M], lse [T][H] fp32.  T must be a multiple of N.
+int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T, int N, int M, int H,
+             int causal, cudaStream_t s);
+// dctx [T][M] -> dqkv [T][3M]; Dbuf [T][H] fp32 scratch.
+int attn_bwd(int dtype, const void* qkv, const void* ctx, const float* lse, const void* dctx,
+             void* dqkv, float* Dbuf, int T, int N, int M, int H, int causal, cudaStream_t s);
+
+// ---------------------------------------------------------------- routing / data movement
+// K1: logits = a·Wg (fp32), top-k (ties -> lower index), gate weights.
+int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
+              int32_t* idx, float* w, int T, int M, int E, int k, cudaStream_t s);
+// K2: deterministic slot-major positions; counts[E]; src[E][C] = t*k+j or -1; pos[T][k] (-1 dropped)
+int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T, int E,
+               int k, int C, cudaStream_t s);
+// K3: send[e][c] = a[src/k] or zeros.  rows = E*C
+int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int rows, int M, int k,
+                 cudaStream_t s);
+// K7: out[t] = sum_j w_tj * y[idx][pos] (+ a[t] if resid)
+int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_t* pos,
+                      const float* w, const void* resid, void* out, int T, int M, int k, int C,
+                      cudaStream_t s);
+// K8: dy[e][pos] = w * dO[t]; dw[t][j] = <dO[t], y[e][pos]>; padding rows zeroed.
+int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* idx,
+                     const int32_t* pos, const float* w, const int32_t* src, void* dy, float* dw,
+                     int T, int M, int k, int E, int C, cudaStream_t s);
+// K9: dA[t] = sum_j dx[e][pos] + dlogits·Wg^T (+ dO[t] if resid); dlogits [T][E] fp32 out.
+int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t* pos,
+                    const float* w, const float* dw, const float* logits, const void* wg,
+                    const void* dout_resid, void* dA, float* dlogits, int T, int M, int E, int k,
+                    int C, cudaStream_t s);
+// dWg[M][E] += A^T · dlogits (deterministic split-T partials); part: scratch [nsplit][M][E]
+int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T,
+               int M, int E, cudaStream_t s);
+size_t gate_wgrad_scratch_floats(int T, int M, int E);
+// out[b][n] += sum_r X[b][r][n]   (bias gradients)
+int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, cudaStream_t s);
+
+}  // namespace fm

@@ -1,0 +1,262 @@
+"""Thin ctypes binding of libflowmoe.so (include/flowmoe.h).
+
+Argument marshalling only: every step of the block runs in the library's CUDA
+kernels.  PyTorch provides device memory, streams and process groups.  There is
+no fallback: if the shared library is missing or fails to load, importing the
+binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflowmoe.so")
+
+FLOWMOE_F32, FLOWMOE_BF16 = 0, 1
+
+EXPORTED = [
+    "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
+    "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
+    "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
+    "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
+]
+
+
+class FlowMoEError(RuntimeError):
+    pass
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("seq_len", ctypes.c_int32), ("M", ctypes.c_int32),
+                ("n_heads", ctypes.c_int32), ("E", ctypes.c_int32), ("top_k", ctypes.c_int32),
+                ("d_ffn", ctypes.c_int32), ("R", ctypes.c_int32),
+                ("capacity_factor", ctypes.c_float), ("causal", ctypes.c_int32),
+                ("residual", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("wqkv", "wo", "wg", "w1", "b1", "w2", "b2")]
+
+
+class Grads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("grad_flat", "dw1", "db1", "dw2", "db2")]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libflowmoe.so (built by paper_2510_00207_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FlowMoEError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+    L.flowmoe_get_unique_id.argtypes = [ctypes.c_char_p]
+    L.flowmoe_create.argtypes = [ctypes.POINTER(Config), ctypes.c_char_p, i32, ctypes.POINTER(vp)]
+    L.flowmoe_saved_bytes.argtypes = [vp]
+    L.flowmoe_saved_bytes.restype = sz
+    L.flowmoe_grad_flat_count.argtypes = [vp]
+    L.flowmoe_grad_flat_count.restype = sz
+    L.flowmoe_block_fwd.argtypes = [vp, ctypes.POINTER(Params), vp, vp, vp, vp]
+    L.flowmoe_block_bwd.argtypes = [vp, ctypes.POINTER(Params), vp, vp, vp, vp,
+                                    ctypes.POINTER(Grads), sz, ctypes.POINTER(u64), vp]
+    L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
+    L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
+    L.flowmoe_set_forced_routing.argtypes = [vp, vp]
+    L.flowmoe_saved_routing_offsets.argtypes = [vp] + [ctypes.POINTER(sz)] * 5
+    L.flowmoe_debug_set.argtypes = [i32, i32]
+    L.flowmoe_kernel_launches.restype = u64
+    i64 = ctypes.c_int64
+    L.flowmoe_test_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
+                                    vp, i64, i64, i32, vp, vp, vp, vp]
+    L.flowmoe_status_string.argtypes = [i32]
+    L.flowmoe_status_string.restype = ctypes.c_char_p
+    L.flowmoe_last_error.restype = ctypes.c_char_p
+    L.flowmoe_destroy.argtypes = [vp]
+    L.flowmoe_destroy.restype = None
+    _lib = L
+    if os.environ.get("FLOWMOE_DEBUG_SIMT"):  # debug knob: route bf16 GEMMs to the SIMT kernel
+        L.flowmoe_debug_set(1, 1)
+    if os.environ.get("FLOWMOE_DEBUG_SWAP"):  # debug knob: swap MN-major descriptor strides
+        L.flowmoe_debug_set(2, 1)
+    return L
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise FlowMoEError(f"{what}: {L.flowmoe_status_string(rc).decode()} "
+                           f"({L.flowmoe_last_error().decode()})")
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().flowmoe_get_unique_id(buf), "flowmoe_get_unique_id")
+    return buf.raw
+
+
+def debug_set(key: int, value: int):
+    _check(lib().flowmoe_debug_set(key, value), "flowmoe_debug_set")
+
+
+def kernel_launches() -> int:
+    return int(lib().flowmoe_kernel_launches())
+
+
+def test_gemm(dtype: str, A, B, C, *, M, N, K, batch=1, lda, sA=0, a_mmajor=0, ldb, sB=0,
+              b_kmajor=0, ldc, sC=0, epi=0, bias=None, resid=None, aux=None, stream=None):
+    """One GEMM through the library's GEMM kernels (include/flowmoe.h flowmoe_test_gemm)."""
+    _check(lib().flowmoe_test_gemm(FLOWMOE_BF16 if dtype == "bf16" else FLOWMOE_F32, M, N, K, batch,
+                                   _ptr(A), lda, sA, a_mmajor, _ptr(B), ldb, sB, b_kmajor, _ptr(C),
+                                   ldc, sC, epi, _ptr(bias), _ptr(resid), _ptr(aux),
+                                   _stream_handle(stream)), "flowmoe_test_gemm")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    return ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)
+
+
+@dataclass
+class BlockShape:
+    """Config fields of one rank (mirrors flowmoe_config)."""
+    B: int
+    seq_len: int
+    M: int
+    n_heads: int
+    E: int
+    top_k: int
+    d_ffn: int
+    R: int
+    capacity_factor: float = 1.0
+    causal: int = 0
+    residual: int = 0
+    dtype: str = "bf16"
+    world_size: int = 1
+    rank: int = 0
+
+    def to_c(self) -> Config:
+        return Config(self.B, self.seq_len, self.M, self.n_heads, self.E, self.top_k, self.d_ffn,
+                      self.R, self.capacity_factor, self.causal, self.residual,
+                      FLOWMOE_BF16 if self.dtype == "bf16" else FLOWMOE_F32, self.world_size,
+                      self.rank)
+
+
+class FlowMoE:
+    """One FlowMoE context (one rank): flowmoe_create ... flowmoe_destroy."""
+
+    def __init__(self, shape: BlockShape, device: int = 0, unique_id: bytes | None = None):
+        L = lib()
+        self.shape = shape
+        self._cfg = shape.to_c()
+        h = ctypes.c_void_p()
+        _check(L.flowmoe_create(ctypes.byref(self._cfg), unique_id, device, ctypes.byref(h)),
+               "flowmoe_create")
+        self.handle = h
+        self.saved_bytes = int(L.flowmoe_saved_bytes(h))
+        self.grad_flat_count = int(L.flowmoe_grad_flat_count(h))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().flowmoe_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def routing_offsets(self) -> dict:
+        vals = [ctypes.c_size_t() for _ in range(5)]
+        _check(lib().flowmoe_saved_routing_offsets(self.handle, *[ctypes.byref(v) for v in vals]),
+               "flowmoe_saved_routing_offsets")
+        return dict(zip(("logits", "idx", "w", "pos", "counts"), (v.value for v in vals)))
+
+    def set_forced_routing(self, idx):
+        _check(lib().flowmoe_set_forced_routing(self.handle, _ptr(idx)), "flowmoe_set_forced_routing")
+
+    def block_fwd(self, params: Params, x, y, saved, stream=None):
+        _check(lib().flowmoe_block_fwd(self.handle, ctypes.byref(params), _ptr(x), _ptr(y),
+                                       _ptr(saved), _stream_handle(stream)), "flowmoe_block_fwd")
+
+    def block_bwd(self, params: Params, x, saved, dy, dx, grads: Grads, chunk_bytes: int,
+                  stream=None) -> int:
+        t = ctypes.c_uint64()
+        _check(lib().flowmoe_block_bwd(self.handle, ctypes.byref(params), _ptr(x), _ptr(saved),
+                                       _ptr(dy), _ptr(dx), ctypes.byref(grads), chunk_bytes,
+                                       ctypes.byref(t), _stream_handle(stream)),
+               "flowmoe_block_bwd")
+        return t.value
+
+    def allreduce_submit(self, buf, count: int, chunk_bytes: int, priority: int = 1,
+                         ready_event=None) -> int:
+        t = ctypes.c_uint64()
+        ev = ctypes.c_void_p(ready_event.cuda_event) if ready_event is not None else None
+        _check(lib().flowmoe_allreduce_submit(self.handle, _ptr(buf), count, chunk_bytes, priority,
+                                              ev, ctypes.byref(t)), "flowmoe_allreduce_submit")
+        return t.value
+
+    def allreduce_wait(self, ticket: int, stream=None):
+        _check(lib().flowmoe_allreduce_wait(self.handle, ticket, _stream_handle(stream)),
+               "flowmoe_allreduce_wait")
+
+
+# ---------------------------------------------------------------- torch helpers
+def torch_dtype(dtype: str):
+    import torch
+    return torch.bfloat16 if dtype == "bf16" else torch.float32
+
+
+def to_device(a: np.ndarray, dtype: str, device):
+    """Upload an fp64 host array as the device storage dtype (bf16 bits or fp32)."""
+    import torch
+    if dtype == "bf16":
+        from synth import bf16_bits
+        return torch.from_numpy(bf16_bits(a).view(np.int16)).to(device).view(torch.bfloat16)
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device)
+
+
+def to_host_f64(t) -> np.ndarray:
+    import torch
+    return t.detach().to(torch.float32).cpu().numpy().astype(np.float64)
+
+
+class BlockTensors:
+    """Device weights + grads of one block for rank `rank` of `P` (local experts only)."""
+
+    def __init__(self, rep: dict, dtype: str, rank: int, P: int, device):
+        import torch
+        E = rep["w1"].shape[0]
+        El = E // P
+        sl = slice(rank * El, (rank + 1) * El)
+        self.t = {
+            "wqkv": to_device(rep["wqkv"], dtype, device), "wo": to_device(rep["wo"], dtype, device),
+            "wg": to_device(rep["wg"], dtype, device), "w1": to_device(rep["w1"][sl], dtype, device),
+            "b1": to_device(rep["b1"][sl], dtype, device), "w2": to_device(rep["w2"][sl], dtype, device),
+            "b2": to_device(rep["b2"][sl], dtype, device),
+        }
+        M, F = rep["w1"].shape[1], rep["w1"].shape[2]
+        f32 = dict(device=device, dtype=torch.float32)
+        self.g = {
+            "grad_flat": torch.zeros(4 * M * M + M * E, **f32),
+            "dw1": torch.zeros(El, M, F, **f32), "db1": torch.zeros(El, F, **f32),
+            "dw2": torch.zeros(El, F, M, **f32), "db2": torch.zeros(El, M, **f32),
+        }
+        self.params = Params(*[self.t[n].data_ptr() for n in ("wqkv", "wo", "wg", "w1", "b1", "w2", "b2")])
+        self.grads = Grads(*[self.g[n].data_ptr() for n in ("grad_flat", "dw1", "db1", "dw2", "db2")])
+
+    def zero_grads(self):
+        for v in self.g.values():
+            v.zero_()

@@ -1,0 +1,83 @@
+"""Helpers shared by the GPU parity tests: run one FlowMoE block through the
+C ABI on seeded synth inputs and return everything as fp64 numpy arrays."""
+from __future__ import annotations
+
+import numpy as np
+
+import paper_2510_00207_b200 as fm
+from synth import BlockConfig
+
+
+def rel(g: np.ndarray, r: np.ndarray) -> float:
+    """max |g - r| / max |r| (the north_star metric, per tensor)."""
+    den = float(np.max(np.abs(r)))
+    return float(np.max(np.abs(g - r))) / (den if den > 0 else 1.0)
+
+
+def shape_of(cfg: BlockConfig, P: int, rank: int) -> fm.BlockShape:
+    return fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,
+                         top_k=cfg.top_k, d_ffn=cfg.d_ffn, R=cfg.R,
+                         capacity_factor=cfg.capacity_factor, causal=cfg.causal,
+                         residual=cfg.residual, dtype=cfg.dtype, world_size=P, rank=rank)
+
+
+def run_block_gpu(cfg: BlockConfig, rep: dict, wk: dict, *, P: int = 1, rank: int = 0,
+                  forced: bool = True, chunk_bytes: int = 1 << 20, uid: bytes | None = None,
+                  device: int = 0) -> dict:
+    import torch
+    dev = torch.device("cuda", device)
+    torch.cuda.set_device(dev)
+    ctx = fm.FlowMoE(shape_of(cfg, P, rank), device, uid)
+    bt = fm.BlockTensors(rep, cfg.dtype, rank, P, dev)
+    x = fm.to_device(wk["x"], cfg.dtype, dev)
+    dy = fm.to_device(wk["dy"], cfg.dtype, dev)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    saved = torch.empty(ctx.saved_bytes, dtype=torch.uint8, device=dev)
+    fidx = None
+    if forced:
+        fidx = torch.from_numpy(np.ascontiguousarray(wk["forced_idx"], dtype=np.int32)).to(dev)
+        ctx.set_forced_routing(fidx)
+    s = torch.cuda.current_stream()
+    ctx.block_fwd(bt.params, x, y, saved, s)
+    t = ctx.block_bwd(bt.params, x, saved, dy, dx, bt.grads, chunk_bytes, s)
+    ctx.allreduce_wait(t, s)
+    torch.cuda.synchronize()
+    off = ctx.routing_offsets()
+    T, E, k, R = cfg.T, cfg.E, cfg.top_k, cfg.R
+
+    def view(o, n, dt):
+        nbytes = n * 4
+        return saved[o:o + nbytes].view(dt).cpu().numpy().copy()
+
+    out = {
+        "y": fm.to_host_f64(y), "dx": fm.to_host_f64(dx),
+        "grad_flat": bt.g["grad_flat"].cpu().numpy().astype(np.float64),
+        "dw1": bt.g["dw1"].cpu().numpy().astype(np.float64),
+        "db1": bt.g["db1"].cpu().numpy().astype(np.float64),
+        "dw2": bt.g["dw2"].cpu().numpy().astype(np.float64),
+        "db2": bt.g["db2"].cpu().numpy().astype(np.float64),
+        "logits": view(off["logits"], T * E, torch.float32).reshape(T, E),
+        "idx": view(off["idx"], T * k, torch.int32).reshape(T, k),
+        "w": view(off["w"], T * k, torch.float32).reshape(T, k),
+        "pos": view(off["pos"], T * k, torch.int32).reshape(T, k),
+        "counts": view(off["counts"], R * E, torch.int32).reshape(R, E),
+    }
+    ctx.close()
+    return out
+
+
+def oracle_block(cfg: BlockConfig, rep: dict, wks: list[dict], forced: bool = True):
+    """Oracle fwd+bwd over len(wks) workers (fp64)."""
+    import oracle as o
+    xs = [w["x"] for w in wks]
+    dys = [w["dy"] for w in wks]
+    fidx = [w["forced_idx"] for w in wks] if forced else None
+    ys, st = o.block_forward(cfg, rep, xs, fidx)
+    dxs, gflat, eg = o.block_backward(cfg, rep, st, dys)
+    return ys, dxs, gflat, eg, st
+
+
+def expert_grads(eg: dict, lo: int, hi: int):
+    return {name: np.stack([eg[e][i] for e in range(lo, hi)])
+            for i, name in enumerate(("dw1", "db1", "dw2", "db2"))}

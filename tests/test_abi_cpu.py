@@ -1,0 +1,72 @@
+"""CPU-side checks of the C-ABI boundary: libflowmoe.so loads, exports every
+symbol include/flowmoe.h declares, and validates configs synchronously (no GPU
+needed: validation happens before any CUDA call)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2510_00207_b200 as fm
+from paper_2510_00207_b200.flowmoe import EXPORTED, BlockShape, FlowMoE, FlowMoEError
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "flowmoe.h")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    return sorted(set(re.findall(r"\b(flowmoe_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    L = fm.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    out = os.popen(f"nm -D {fm.flowmoe.LIB_PATH}").read()
+    for name in declared_symbols():
+        assert re.search(rf" T {name}$", out, re.M), name
+
+
+def test_status_strings():
+    L = fm.lib()
+    assert L.flowmoe_status_string(0) == b"ok"
+    assert L.flowmoe_status_string(1) == b"invalid argument"
+
+
+GOOD = dict(B=256, seq_len=64, M=64, n_heads=4, E=4, top_k=2, d_ffn=128, R=2)
+
+
+@pytest.mark.parametrize("field,value,needle", [
+    ("B", 250, "config.B"), ("R", 3, "config.R"), ("top_k", 5, "config.top_k"),
+    ("n_heads", 3, "config.n_heads"), ("E", 6, "config.E"), ("M", 60, "config.M"),
+    ("capacity_factor", -1.0, "config.capacity_factor"), ("world_size", 3, "config.E"),
+    ("rank", 2, "config.rank"),
+])
+def test_create_rejects_invalid_config(field, value, needle):
+    kw = dict(GOOD)
+    if field in ("world_size", "rank"):
+        kw["world_size"] = 3 if field == "world_size" else 2
+        if field == "rank":
+            kw["rank"] = value
+    else:
+        kw[field] = value
+    with pytest.raises(FlowMoEError) as ei:
+        FlowMoE(BlockShape(**kw, dtype="f32"))
+    assert "invalid argument" in str(ei.value) and needle in str(ei.value)
+
+
+def test_debug_set_unknown_key():
+    with pytest.raises(FlowMoEError):
+        fm.debug_set(99, 1)
+
+
+def test_sass_has_tcgen05_and_tma():
+    """The bf16 GEMM is tcgen05 (UTCHMMA), fed by TMA (UTMALDG), read back via LDTM."""
+    out = os.popen(f"cuobjdump -sass {fm.flowmoe.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "UTCHMMA" in out and "UTMALDG" in out and "LDTM" in out

@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded synth inputs.  Tolerances (BASELINE.json north_star): routing
+indices / counts / positions bit-exact given identical logits; fp32 values
+rel <= 1e-4; bf16 with fp32 accumulation rel <= 2e-2, rel = max|g-r|/max|r|."""
+import numpy as np
+import pytest
+
+import oracle as o
+from synth import PRESETS, BlockConfig, gen_replicated, gen_worker
+from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+CASES = {
+    # configs[0] at P=1 (all 4 experts local), capacity drops (f=1.0)
+    "c1_f32": PRESETS["c1"].replace(P=1),
+    "c1_f32_dropless_causal_resid": PRESETS["c1_dropless"].replace(P=1, causal=1, residual=1),
+    "f32_k1": BlockConfig(T=256, seq_len=64, M=64, n_heads=2, E=8, top_k=1, d_ffn=96, R=4,
+                          capacity_factor=1.0, causal=1, residual=0, P=1, dtype="f32"),
+    # bf16, several tiles + ragged tails in every GEMM dimension
+    "bf16_small": BlockConfig(T=512, seq_len=128, M=256, n_heads=4, E=8, top_k=2, d_ffn=512, R=2,
+                              capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    "bf16_ragged": BlockConfig(T=384, seq_len=96, M=192, n_heads=3, E=4, top_k=2, d_ffn=328, R=2,
+                               capacity_factor=1.25, causal=0, residual=0, P=1, dtype="bf16"),
+    "bf16_k3_dh128": BlockConfig(T=256, seq_len=128, M=256, n_heads=2, E=16, top_k=3, d_ffn=256,
+                                 R=2, capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    # configs[1]: the bench workload (GPT2-Tiny-MoE-shaped, R=4), full size
+    "c2_bench": PRESETS["c2"],
+}
+
+
+def _check_block(cfg, forced=True):
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    g = run_block_gpu(cfg, rep, wk, forced=forced)
+    ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk], forced=forced)
+    tol = TOL[cfg.dtype]
+    res = {"y": rel(g["y"], ys[0]), "dx": rel(g["dx"], dxs[0]),
+           "grad_flat": rel(g["grad_flat"], gflat)}
+    ref_e = expert_grads(eg, 0, cfg.E)
+    for n in ("dw1", "db1", "dw2", "db2"):
+        res[n] = rel(g[n], ref_e[n])
+    M = cfg.M
+    res["dWqkv"] = rel(g["grad_flat"][:3 * M * M], gflat[:3 * M * M])
+    res["dWo"] = rel(g["grad_flat"][3 * M * M:4 * M * M], gflat[3 * M * M:4 * M * M])
+    res["dWg"] = rel(g["grad_flat"][4 * M * M:], gflat[4 * M * M:])
+    bad = {k: v for k, v in res.items() if not v <= tol}
+    assert not bad, f"rel errors above {tol}: {bad} (all: {res})"
+    # routing under forced indices: identical indices and positions
+    ro = st.route[0]
+    assert np.array_equal(g["idx"], ro.idx)
+    assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
+    assert np.array_equal(g["counts"], ro.counts)
+    return res
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_block_parity_forced_routing(name):
+    _check_block(CASES[name])
+
+
+@pytest.mark.parametrize("name", ["c1_f32", "bf16_small", "c2_bench", "bf16_k3_dh128", "f32_k1"])
+def test_routing_bitexact_given_gpu_logits(name):
+    """Natural routing: the oracle routes from the GPU's own fp32 logits; indices,
+    positions and per-chunk counts must match bit for bit, weights to fp32 rounding."""
+    cfg = CASES[name]
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    g = run_block_gpu(cfg, rep, wk, forced=False)
+    ro = o.route_worker(cfg, None, None, logits=g["logits"].astype(np.float64))
+    assert np.array_equal(g["idx"], ro.idx)
+    assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
+    assert np.array_equal(g["counts"], ro.counts)
+    assert np.max(np.abs(g["w"] - ro.w)) < 1e-6
+    # and the logits themselves match the oracle's A·Wg to the dtype tolerance
+    ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk], forced=False)
+    assert rel(g["logits"], st.route[0].logits) <= TOL[cfg.dtype]
+
+
+def test_skewed_routing_with_drops_bf16():
+    """Zipf-skewed expert popularity (input recipe 'skew'): uneven loads and drops."""
+    cfg = CASES["bf16_small"]
+    rep = gen_replicated(cfg, skew=True)
+    wk = gen_worker(cfg, 0, skew=True)
+    g = run_block_gpu(cfg, rep, wk, forced=False)
+    ro = o.route_worker(cfg, None, None, logits=g["logits"].astype(np.float64))
+    assert (~ro.kept).sum() > 0.1 * ro.kept.size, "skew must force capacity drops"
+    assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
+    assert np.array_equal(g["counts"], ro.counts)
+    wk2 = dict(wk, forced_idx=ro.idx)
+    g2 = run_block_gpu(cfg, rep, wk2, forced=True)
+    ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk2], forced=True)
+    assert rel(g2["y"], ys[0]) <= TOL["bf16"]
+    assert rel(g2["dx"], dxs[0]) <= TOL["bf16"]
+    assert rel(g2["grad_flat"], gflat) <= TOL["bf16"]
+
+
+def test_chunked_equals_unchunked_on_gpu():
+    """Pipelining (R chunks) does not change the result: GPU R=4 vs R=1, dropless."""
+    base = BlockConfig(T=256, seq_len=32, M=64, n_heads=4, E=4, top_k=2, d_ffn=128, R=1,
+                       capacity_factor=0.0, causal=1, residual=1, P=1, dtype="f32")
+    rep = gen_replicated(base)
+    wk = gen_worker(base, 0)
+    a = run_block_gpu(base, rep, wk)
+    b = run_block_gpu(base.replace(R=4), rep, wk)
+    for n in ("y", "dx"):
+        assert np.array_equal(a[n], b[n]), n
+    for n in ("grad_flat", "dw1", "db1", "dw2", "db2"):
+        assert rel(b[n], a[n]) <= 1e-5, n
+
+
+def test_empty_expert_and_all_tokens_one_expert():
+    """Degenerate routing: every token forced to experts {0,1}; experts 2..7 get
+    no rows (their grads stay exactly 0), most slots of 0/1 are dropped."""
+    cfg = CASES["bf16_small"].replace(capacity_factor=1.0)
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    wk["forced_idx"] = np.tile(np.array([[0, 1]], dtype=np.int32), (cfg.T, 1))
+    g = run_block_gpu(cfg, rep, wk)
+    ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk])
+    assert rel(g["y"], ys[0]) <= TOL["bf16"]
+    assert rel(g["dx"], dxs[0]) <= TOL["bf16"]
+    assert np.all(g["dw1"][2:] == 0) and np.all(g["db2"][2:] == 0)
+
+
+GEMM_SHAPES = [(200, 320, 136, 2), (128, 96, 64, 1), (296, 200, 520, 3), (64, 512, 256, 8)]  # rows, N, K multiple of 8 (TMA 16-B strides)
+
+
+@pytest.mark.parametrize("a_mmajor,b_kmajor", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape):
+    """tcgen05 GEMM (bf16 in, fp32 TMEM accum) against the fp64 product of the
+    same bf16 inputs; store epilogue (bf16 out) and fp32 accumulate epilogue."""
+    import torch
+    import paper_2510_00207_b200 as fm
+    Mr, N, K, batch = shape
+    rng = np.random.default_rng(sum(shape) + 7 * a_mmajor + 3 * b_kmajor)
+    A = rng.standard_normal((batch, Mr, K))
+    B = rng.standard_normal((batch, K, N))
+    dev = torch.device("cuda", 0)
+    a_store = A.transpose(0, 2, 1).copy() if a_mmajor else A
+    b_store = B.transpose(0, 2, 1).copy() if b_kmajor else B
+    At = fm.to_device(a_store, "bf16", dev)
+    Bt = fm.to_device(b_store, "bf16", dev)
+    Ar = fm.to_host_f64(At)
+    Br = fm.to_host_f64(Bt)
+    Ar = Ar.transpose(0, 2, 1) if a_mmajor else Ar
+    Br = Br.transpose(0, 2, 1) if b_kmajor else Br
+    ref = Ar @ Br
+    lda = Mr if a_mmajor else K
+    ldb = K if b_kmajor else N
+    C = torch.zeros((batch, Mr, N), dtype=torch.bfloat16, device=dev)
+    fm.test_gemm("bf16", At, Bt, C, M=Mr, N=N, K=K, batch=batch, lda=lda, sA=Mr * K,
+                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N)
+    C32 = torch.ones((batch, Mr, N), dtype=torch.float32, device=dev)
+    fm.test_gemm("bf16", At, Bt, C32, M=Mr, N=N, K=K, batch=batch, lda=lda, sA=Mr * K,
+                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N, epi=3)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref) <= 1e-2
+    assert rel(C32.cpu().numpy().astype(np.float64) - 1.0, ref) <= 1e-5
+
+
+def test_gemm_tc_epilogues():
+    import torch
+    import paper_2510_00207_b200 as fm
+    Mr, N, K, batch = 192, 384, 128, 2
+    rng = np.random.default_rng(3)
+    dev = torch.device("cuda", 0)
+    A = fm.to_device(rng.standard_normal((batch, Mr, K)) / 8, "bf16", dev)
+    B = fm.to_device(rng.standard_normal((batch, K, N)), "bf16", dev)
+    bias = fm.to_device(rng.standard_normal((batch, N)), "bf16", dev)
+    res = fm.to_device(rng.standard_normal((batch, Mr, N)), "bf16", dev)
+    ref = fm.to_host_f64(A) @ fm.to_host_f64(B)
+    kw = dict(M=Mr, N=N, K=K, batch=batch, lda=K, sA=Mr * K, ldb=N, sB=K * N, ldc=N, sC=Mr * N)
+    C = torch.empty((batch, Mr, N), dtype=torch.bfloat16, device=dev)
+    fm.test_gemm("bf16", A, B, C, epi=0, bias=bias, resid=res, **kw)
+    want = ref + fm.to_host_f64(bias)[:, None, :] + fm.to_host_f64(res)
+    assert rel(fm.to_host_f64(C), want) <= 1e-2
+    Z = torch.empty_like(C)
+    fm.test_gemm("bf16", A, B, C, epi=1, bias=bias, aux=Z, **kw)
+    z = ref + fm.to_host_f64(bias)[:, None, :]
+    assert rel(fm.to_host_f64(Z), z) <= 1e-2
+    assert rel(fm.to_host_f64(C), o.gelu(fm.to_host_f64(Z))) <= 1e-2
+    fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref * o.gelu_grad(fm.to_host_f64(Z))) <= 1e-2
