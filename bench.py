@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""FlowMoE block-stack training-iteration benchmark (B200, sm_100a).
+
+One step = one training iteration of an L-block transformer-MoE stack through
+the C ABI (libflowmoe.so): L × flowmoe_block_fwd, then L × flowmoe_block_bwd in
+reverse order (each auto-submitting the chunked S_p all-reduce of its MHA+gate
+grads), then flowmoe_allreduce_wait on every ticket (Alg. 1 lines 6-22, P:258-309;
+the optimizer update, line 23, is excluded as in SURVEY.md §8(d)).  Weights and
+inputs are synthetic (synth.gen_device_*), resident in HBM before the timed
+region.  The iteration is captured once into a CUDA graph and replayed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+N>1 is launched by torchrun (one rank per GPU, NCCL); weak scaling: T tokens per
+rank fixed, E experts fixed, E/P local experts per rank.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE block iteration ms & tokens/s at 1/2/4/8 B200; exposed comm %"  # BASELINE.json metric
+LAYERS = {"c1": 1, "c2": 12, "c3": 4, "c4": 4, "dsv2s": 4}   # Table 3 L for c2; §8(d) L in {1,4} else
+SP_DEFAULT = {"c1": 1 << 16, "c2": 1 << 20, "c3": 4 << 20, "c4": 4 << 20, "dsv2s": 4 << 20}
+CONFIG_NAMES = {
+    "c1": "configs[0] single fp32 MoE block (T=256, M=64, 4 heads, E=4 top-2, F=128, R=2)",
+    "c2": "configs[1] GPT2-Tiny-MoE-shaped block stack (M=256, 4 heads, E=8 top-2, F=512, R=4, L=12)",
+    "c3": "configs[2] BERT-Large-MoE-shaped (M=1024, 16 heads, E=16 top-2, F=2048, R=2)",
+    "c4": "configs[3] LLaMA2-MoE-shaped (M=4096, 32 heads, E=16 top-2, F=16384, R=2)",
+    "dsv2s": "configs[4] DeepSeek-V2-S-shaped (M=5120, 40 heads, E=16 top-8, F=1536, R=2)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="flowmoe", choices=["flowmoe", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(LAYERS))
+    ap.add_argument("--layers", type=int, default=0, help="blocks in the stack (default per config)")
+    ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
+    ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default="", help="write the per-kernel table here")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = os.path.join("/tmp", f"flowmoe_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        under_load = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+def cpu_oracle_baseline(cfg, L, budget_s=20.0):
+    """Time the fp64 oracle (as it stands) on this host: blocks fwd+bwd of the same
+    workload until ~budget_s, scaled to tokens/s of the L-block iteration."""
+    import numpy as np  # noqa: F401
+    import oracle as o
+    from synth import gen_replicated, gen_worker
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        cores = 1
+    one = cfg.replace(P=1)
+    n_blocks, t_total = 0, 0.0
+    while t_total < budget_s and n_blocks < L:
+        rep = gen_replicated(one, block=n_blocks)
+        wk = gen_worker(one, 0, block=n_blocks)
+        t0 = time.perf_counter()
+        ys, st = o.block_forward(one, rep, [wk["x"]])
+        o.block_backward(one, rep, st, [wk["dy"]])
+        t_total += time.perf_counter() - t0
+        n_blocks += 1
+    t_iter = t_total / n_blocks * L
+    return {"value": cfg.T / t_iter, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n_blocks} of {L} blocks fwd+bwd at full T={cfg.T} (P=1), scaled x{L}/{n_blocks}",
+            "s_per_iteration": t_iter}
+
+
+def run_reference(args, cfg, L, rank, world):
+    """--impl reference: the oracle on the host cores, each step a bounded sample
+    (one block, one chunk of T/R tokens) of the same workload."""
+    if rank != 0:
+        return
+    import oracle as o
+    from synth import gen_replicated, gen_worker
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        cores = 1
+    Tr = cfg.T // cfg.R
+    one = cfg.replace(P=1, T=Tr, R=1)
+    rep = gen_replicated(one)
+    wk = gen_worker(one, 0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ys, st = o.block_forward(one, rep, [wk["x"]])
+        o.block_backward(one, rep, st, [wk["dy"]])
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t_block = statistics.mean(times)
+    ms_iter = t_block * L * 1e3 * cfg.R          # the L-block iteration over all T tokens
+    value = Tr / (t_block * L)                   # tokens/s of the iteration (per rank) ...
+    value *= world                               # ... whole job (weak scaling: every rank has T tokens)
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": CONFIG_NAMES[args.config], "tokens_per_gpu": cfg.T, "layers": L,
+                       "R": cfg.R},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"per step: 1 block fwd+bwd over one chunk ({Tr} tokens), "
+                                       f"scaled to the {L}-block iteration"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from synth import PRESETS
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    L = args.layers or LAYERS[args.config]
+    cfg = PRESETS[args.config]
+    if args.R:
+        cfg = cfg.replace(R=args.R)
+    cfg = cfg.replace(P=world)
+    if args.impl == "reference":
+        run_reference(args, cfg, L, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2510_00207_b200 as fm
+    from synth import gen_device_block, gen_device_worker
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [fm.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    S_p = args.chunk_bytes or SP_DEFAULT[args.config]
+    shape = fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,
+                          top_k=cfg.top_k, d_ffn=cfg.d_ffn, R=cfg.R,
+                          capacity_factor=cfg.capacity_factor, causal=cfg.causal,
+                          residual=cfg.residual, dtype=cfg.dtype, world_size=world, rank=rank)
+    ctx = fm.FlowMoE(shape, local, uid)
+
+    # ---- resident synthetic state
+    blocks = []
+    for l in range(L):
+        w = gen_device_block(cfg, rank, world, l, dev)
+        f32 = dict(device=dev, dtype=torch.float32)
+        El = cfg.E // world
+        g = {"grad_flat": torch.zeros(ctx.grad_flat_count, **f32),
+             "dw1": torch.zeros(El, cfg.M, cfg.d_ffn, **f32), "db1": torch.zeros(El, cfg.d_ffn, **f32),
+             "dw2": torch.zeros(El, cfg.d_ffn, cfg.M, **f32), "db2": torch.zeros(El, cfg.M, **f32)}
+        params = fm.Params(*[w[n].data_ptr() for n in ("wqkv", "wo", "wg", "w1", "b1", "w2", "b2")])
+        grads = fm.Grads(*[g[n].data_ptr() for n in ("grad_flat", "dw1", "db1", "dw2", "db2")])
+        blocks.append(dict(w=w, g=g, params=params, grads=grads,
+                           saved=torch.empty(ctx.saved_bytes, dtype=torch.uint8, device=dev)))
+    x0, dy_top = gen_device_worker(cfg, rank, dev)
+    xs = [x0] + [torch.empty_like(x0) for _ in range(L)]
+    dxs = [torch.empty_like(x0) for _ in range(L)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def iteration(stream):
+        for l in range(L):  # Eq.(3)/(4) order, block after block
+            ctx.block_fwd(blocks[l]["params"], xs[l], xs[l + 1], blocks[l]["saved"], stream)
+        tickets = []
+        g_in = dy_top
+        for l in reversed(range(L)):  # Eq.(5)/(6): blocks L..1, AR of block l under block l-1
+            blocks[l]["g"]["grad_flat"].zero_()
+            tickets.append(ctx.block_bwd(blocks[l]["params"], xs[l], blocks[l]["saved"], g_in, dxs[l],
+                                         blocks[l]["grads"], S_p, stream))
+            g_in = dxs[l]
+        for t in tickets:  # Alg. 1 line 22: wait for all all-reduce before the update
+            ctx.allreduce_wait(t, stream)
+
+    stream = torch.cuda.current_stream()
+    # warm-up (eager) + launch count of one iteration
+    n0 = fm.kernel_launches()
+    iteration(stream)
+    launches_per_step = fm.kernel_launches() - n0
+    for _ in range(max(0, args.warmup - 1)):
+        iteration(stream)
+    torch.cuda.synchronize()
+
+    # per-kernel live timing (eager iteration, CUDA events on each kernel's own stream)
+    fm.profile_begin()
+    for _ in range(2):
+        iteration(stream)
+    prof = fm.profile_end()
+    for p in prof:
+        p["launches"] //= 2
+        p["ms"] /= 2
+        p["flops"] /= 2
+        p["bytes"] /= 2
+
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.graph(graph, stream=cap, capture_error_mode="thread_local"):
+            iteration(torch.cuda.current_stream())
+        run = graph.replay
+    else:
+        run = lambda: iteration(stream)  # noqa: E731
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps outside the events
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            run()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # ---- e2e: H2D of this step's inputs from pinned memory + the iteration + D2H of dx
+    K2 = min(args.steps, 20)
+    x_h = x0.cpu().pin_memory()
+    dy_h = dy_top.cpu().pin_memory()
+    dx_h = torch.empty_like(dxs[0], device="cpu").pin_memory()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K2):
+        xs[0].copy_(x_h, non_blocking=True)
+        dy_top.copy_(dy_h, non_blocking=True)
+        run()
+        dx_h.copy_(dxs[0], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / K2], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        tokens = cfg.T * world
+        compute = [p for p in prof if not p["name"].startswith(("a2a", "allreduce"))]
+        top = max(compute, key=lambda p: p["ms"])
+        total_ms = sum(p["ms"] for p in compute)
+        avg_ms = top["ms"] / top["launches"]
+        if top["name"].startswith("gemm"):
+            bound, unit = "tensor", "TFLOP/s"
+            achieved = top["flops"] / top["launches"] / (avg_ms * 1e-3) / 1e12
+            peak = peaks["bf16_tflops_sustained"]
+        elif top["name"].startswith("attn"):
+            bound, unit = "alu", "TFLOP/s"   # SIMT fp32 FMA: 148 SMs x 128 lanes x 2 x clock
+            achieved = top["flops"] / top["launches"] / (avg_ms * 1e-3) / 1e12
+            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        else:
+            bound, unit = "hbm", "GB/s"
+            achieved = top["bytes"] / top["launches"] / (avg_ms * 1e-3) / 1e9
+            peak = peaks["hbm_gbs"]
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tr.get(args.config, {}).get(top["name"])
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "tokens_per_gpu": cfg.T,
+                       "seq_len": cfg.seq_len, "M": cfg.M, "n_heads": cfg.n_heads, "E": cfg.E,
+                       "top_k": cfg.top_k, "d_ffn": cfg.d_ffn, "R": cfg.R, "layers": L,
+                       "capacity_factor": cfg.capacity_factor, "S_p_bytes": S_p,
+                       "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
+                       "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
+            "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
+                         "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src + (" sustained" if bound == "tensor" else ""),
+                         "share_of_compute": top["ms"] / total_ms,
+                         "per_launch_ms": avg_ms, "launches_per_step": top["launches"]},
+            "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": x0.numel() * x0.element_size() * 2,
+                    "d2h_bytes_per_step": dxs[0].numel() * dxs[0].element_size()},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "exposed_comm": None if world == 1 else "see profiles/",
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_oracle_baseline(cfg, L)
+        if args.profile_json:
+            json.dump({"config": args.config, "ms_per_step_eager_profiled": sum(p["ms"] for p in compute),
+                       "kernels": sorted(prof, key=lambda p: -p["ms"])}, open(args.profile_json, "w"), indent=1)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -159,6 +159,20 @@ flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch, cons
                                  int64_t sB, int b_kmajor, void* C, int64_t ldc, int64_t sC, int epi,
                                  const void* bias, const void* resid, void* aux, cudaStream_t stream);
 
+/* Per-kernel device timing (bench.py's live roofline).  Between begin and end,
+ * every kernel / NCCL call the library enqueues outside CUDA-graph capture is
+ * bracketed by timing events on its own stream.  end synchronises the device
+ * and writes one entry per kernel kind that ran: launches, summed device ms,
+ * summed algorithmic FLOPs and HBM (or bus) bytes.  Returns the number of
+ * entries written, or -1 on error. */
+typedef struct {
+  const char* name;   /* static string owned by the library */
+  int64_t launches;
+  double ms, flops, bytes;
+} flowmoe_prof_entry;
+flowmoe_status flowmoe_profile_begin(void);
+int flowmoe_profile_end(flowmoe_prof_entry* out, int max_entries);
+
 /* Number of kernels this library has launched in the calling process (bench accounting). */
 uint64_t flowmoe_kernel_launches(void);
 

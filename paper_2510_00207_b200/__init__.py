@@ -4,5 +4,5 @@ The compute lives in libflowmoe.so (C ABI: include/flowmoe.h, CUDA sm_100a);
 ``flowmoe`` is the thin ctypes binding.
 """
 from .flowmoe import (BlockShape, BlockTensors, FlowMoE, FlowMoEError, Grads, Params,  # noqa: F401
-                      debug_set, get_unique_id, kernel_launches, lib, test_gemm, to_device,
+                      debug_set, get_unique_id, kernel_launches, lib, profile_begin, profile_end, test_gemm, to_device,
                       to_host_f64, torch_dtype)

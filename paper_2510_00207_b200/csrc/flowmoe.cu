@@ -89,6 +89,68 @@ namespace {
                                         cudaGetErrorString((cudaError_t)e_));              \
   } while (0)
 
+// ---- per-kernel profiling (eager mode only; bench.py's live roofline) ----
+enum KKind {
+  KK_QKV, KK_ATTN_F, KK_OPROJ, KK_GATE, KK_ROUTE, KK_PACK, KK_E1, KK_E2, KK_COMBINE,
+  KK_CBPACK, KK_DGELU, KK_DW2, KK_DB2, KK_DW1, KK_DB1, KK_DXE, KK_GATHER, KK_DCTX, KK_ATTN_B,
+  KK_DX, KK_DWG, KK_DWO, KK_DWQKV, KK_A2A_D, KK_A2A_C, KK_A2A_CB, KK_A2A_DB, KK_AR, KK_TEST, KK_COUNT
+};
+const char* KK_NAMES[KK_COUNT] = {
+  "gemm_qkv", "attn_fwd", "gemm_oproj", "gate_topk", "route_scan", "permute_pack",
+  "gemm_expert1_gelu", "gemm_expert2", "unpermute_combine", "combine_bwd_pack", "gemm_expert_dgelu",
+  "gemm_expert_dw2", "colsum_db2", "gemm_expert_dw1", "colsum_db1", "gemm_expert_dx",
+  "gather_gate_bwd", "gemm_dctx", "attn_bwd", "gemm_dx", "gate_wgrad", "gemm_dwo", "gemm_dwqkv",
+  "a2a_dispatch", "a2a_combine", "a2a_combine_bwd", "a2a_dispatch_bwd", "allreduce_chunk", "test_gemm"};
+struct ProfRec { int kind; int ev; double flops, bytes; };
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<ProfRec> recs;
+} g_prof;
+
+int prof_start(cudaStream_t s) {
+  if (!g_prof.on) return -1;
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+  while (g_prof.pool.size() < g_prof.used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    g_prof.pool.push_back(e);
+  }
+  int i = (int)g_prof.used;
+  g_prof.used += 2;
+  cudaEventRecord(g_prof.pool[i], s);
+  return i;
+}
+void prof_stop(int i, int kind, double flops, double bytes, cudaStream_t s) {
+  if (i < 0) return;
+  cudaEventRecord(g_prof.pool[i + 1], s);
+  g_prof.recs.push_back({kind, i, flops, bytes});
+}
+#define FM_KP(kind, nk, fl, by, strm, call)            \
+  do {                                                  \
+    int pi_ = prof_start(strm);                         \
+    FM_K(nk, call);                                     \
+    prof_stop(pi_, kind, (double)(fl), (double)(by), strm); \
+  } while (0)
+
+// GEMM with its algorithmic work: 2·M·N·K flops; bytes = A + B + C (+C read for fp32 accumulate)
+flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStream_t s) {
+  const double b = g.batch;
+  const double flops = 2.0 * g.M * g.N * (double)g.K * b;
+  double bytes = ((double)g.M * g.K + (double)g.K * g.N) * es * b;
+  bytes += g.epi == EPI_ACC_F32 ? 8.0 * g.M * g.N * b : (double)g.M * g.N * es * b;
+  if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) bytes += (double)g.M * g.N * es * b;
+  if (g.resid) bytes += (double)g.M * g.N * es * b;
+  FM_KP(kind, 1, flops, bytes, s, gemm(g, dt, s));
+  return FLOWMOE_OK;
+}
+#define FM_GEMM(kind, g)                                                   \
+  do {                                                                     \
+    if (flowmoe_status st_ = run_gemm(kind, g, dt, es, sc)) return st_;   \
+  } while (0)
+
 flowmoe_status validate(const flowmoe_config* c) {
   if (!c) return fail(FLOWMOE_ERR_INVALID, "config is NULL");
   auto bad = [](const char* f, const std::string& why) {
@@ -200,7 +262,9 @@ flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_
   const size_t chunk = chunk_bytes / 4;
   for (size_t off = 0; off < count; off += chunk) {
     const size_t n = (count - off < chunk) ? count - off : chunk;
+    int pi = prof_start(x->s_ar);
     FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
+    prof_stop(pi, KK_AR, 0, 4.0 * n * 2.0 * (x->P - 1) / x->P, x->s_ar);
   }
   return FLOWMOE_OK;
 }
@@ -240,6 +304,37 @@ flowmoe_status flowmoe_debug_set(int key, int value) {
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   gemm_tc_set_debug(flags);
   return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_profile_begin(void) {
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  g_prof.on = true;
+  return FLOWMOE_OK;
+}
+
+int flowmoe_profile_end(flowmoe_prof_entry* out, int max_entries) {
+  g_prof.on = false;
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    fail(FLOWMOE_ERR_CUDA, "flowmoe_profile_end: device synchronize failed");
+    return -1;
+  }
+  std::vector<flowmoe_prof_entry> agg(KK_COUNT);
+  for (int i = 0; i < KK_COUNT; ++i) agg[i] = {KK_NAMES[i], 0, 0.0, 0.0, 0.0};
+  for (const ProfRec& r : g_prof.recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_prof.pool[r.ev], g_prof.pool[r.ev + 1]);
+    agg[r.kind].launches += 1;
+    agg[r.kind].ms += ms;
+    agg[r.kind].flops += r.flops;
+    agg[r.kind].bytes += r.bytes;
+  }
+  int n = 0;
+  for (int i = 0; i < KK_COUNT; ++i)
+    if (agg[i].launches > 0 && n < max_entries && out) out[n++] = agg[i];
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  return n;
 }
 
 flowmoe_status flowmoe_get_unique_id(uint8_t id[128]) {
@@ -379,21 +474,21 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     GemmArgs g;
     g.M = (int)Tr; g.N = (int)(3 * M); g.K = (int)M;
     g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
-    FM_K(1, gemm(g, dt, sc));
-    FM_K(1, attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N,
+    FM_GEMM(KK_QKV, g);
+    FM_KP(KK_ATTN_F, 1, 4.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 5 * M * es + Tr * x->H * 4.0, sc, attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N,
                      (int)M, (int)x->H, x->cfg.causal, sc));
     g = GemmArgs();
     g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
     g.A = ctxb; g.lda = M; g.B = p->wo; g.ldb = M; g.C = a; g.ldc = M;
     if (x->cfg.residual) { g.resid = xr; g.ldr = M; }
-    FM_K(1, gemm(g, dt, sc));
-    FM_K(1, gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr,
+    FM_GEMM(KK_OPROJ, g);
+    FM_KP(KK_GATE, 1, 2.0 * Tr * M * E, (double)Tr * M * es + M * E * es + Tr * E * 4.0 + Tr * k * 8.0, sc, gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr,
                       at<float>(saved, L.logits + t0 * E * 4), at<int32_t>(saved, L.idx + t0 * k * 4),
                       at<float>(saved, L.w + t0 * k * 4), (int)Tr, (int)M, (int)E, (int)k, sc));
     int32_t* src = at<int32_t>(saved, L.src + r * E * C * 4);
-    FM_K(1, route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+    FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc, route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
                        at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
-    FM_K(1, permute_pack(dt, a, src, at<char>(saved, L.send + r * ECM * es), (int)(E * C), (int)M,
+    FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc, permute_pack(dt, a, src, at<char>(saved, L.send + r * ECM * es), (int)(E * C), (int)M,
                          (int)k, sc));
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
   }
@@ -401,9 +496,11 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   if (P > 1)
     for (int r = 0; r < x->cfg.R; ++r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_at[r], 0));
+      int pi = prof_start(x->s_a2a);
       if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send + r * ECM * es),
                                             at<char>(saved, L.xe + r * ECM * es)))
         return s;
+      prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_d[r], x->s_a2a));
     }
   // ---- E_1..E_R: batched expert FFN over [El][P*C] capacity rows
@@ -421,30 +518,32 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.bias = p->b1; g.sBias = F;
     g.aux = z; g.ldaux = F; g.sAux = PC * F;
     g.epi = EPI_BIAS_GELU;
-    FM_K(1, gemm(g, dt, sc));
+    FM_GEMM(KK_E1, g);
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
     g.A = h; g.lda = F; g.sA = PC * F;
     g.B = p->w2; g.ldb = M; g.sB = F * M;
     g.C = ye; g.ldc = M; g.sC = PC * M;
     g.bias = p->b2; g.sBias = M;
-    FM_K(1, gemm(g, dt, sc));
+    FM_GEMM(KK_E2, g);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_e[r], sc));
   }
   // ---- C_1..C_R (Eq.(4))
   if (P > 1)
     for (int r = 0; r < x->cfg.R; ++r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_e[r], 0));
+      int pi = prof_start(x->s_a2a);
       if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye + r * ECM * es),
                                            at<char>(saved, L.yc + r * ECM * es)))
         return s;
+      prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_c[r], x->s_a2a));
     }
   // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
   for (int r = 0; r < x->cfg.R; ++r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_c[r], 0));
     const int64_t t0 = r * Tr;
-    FM_K(1, unpermute_combine(dt, at<char>(saved, L.yc + r * ECM * es), at<int32_t>(saved, L.idx + t0 * k * 4),
+    FM_KP(KK_COMBINE, 1, 2.0 * Tr * k * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0), sc, unpermute_combine(dt, at<char>(saved, L.yc + r * ECM * es), at<int32_t>(saved, L.idx + t0 * k * 4),
                               at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
                               x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
                               (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)C, sc));
@@ -476,7 +575,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the combine-side buffer, dw = <dO, Y>
   for (int r = R - 1; r >= 0; --r) {
     const int64_t t0 = r * Tr;
-    FM_K(1, combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * ECM * es),
+    FM_KP(KK_CBPACK, 1, 4.0 * Tr * k * M, (double)Tr * M * es + 2.0 * Tr * k * M * es, sc, combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * ECM * es),
                              at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
                              at<float>(saved, L.w + t0 * k * 4), at<int32_t>(saved, L.src + r * E * C * 4),
                              (char*)x->dyc + r * ECM * es, x->dw + t0 * k, (int)Tr, (int)M, (int)k,
@@ -486,8 +585,10 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_cb[r], 0));
+      int pi = prof_start(x->s_a2a);
       if (flowmoe_status s = a2a_to_experts(x, (char*)x->dyc + r * ECM * es, (char*)x->dye + r * ECM * es))
         return s;
+      prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], x->s_a2a));
     }
   // ---- E_R^bwd .. E_1^bwd (Eq.(5))
@@ -505,7 +606,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.C = x->dz; g.ldc = F; g.sC = PC * F;
     g.aux = const_cast<void*>(z); g.ldaux = F; g.sAux = PC * F;
     g.epi = EPI_DGELU;
-    FM_K(1, gemm(g, dt, sc));
+    FM_GEMM(KK_DGELU, g);
     // dW2 += Hᵀ·dY
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)PC;
@@ -513,8 +614,8 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.B = dye; g.ldb = M; g.sB = PC * M;
     g.C = gr->dw2; g.ldc = M; g.sC = F * M;
     g.epi = EPI_ACC_F32;
-    FM_K(1, gemm(g, dt, sc));
-    FM_K(1, colsum_acc(dt, dye, gr->db2, (int)El, (int)PC, (int)M, sc));
+    FM_GEMM(KK_DW2, g);
+    FM_KP(KK_DB2, 1, (double)El * PC * M, (double)El * PC * M * es + El * M * 8.0, sc, colsum_acc(dt, dye, gr->db2, (int)El, (int)PC, (int)M, sc));
     // dW1 += Xᵀ·dZ
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)M; g.N = (int)F; g.K = (int)PC;
@@ -522,22 +623,24 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.B = x->dz; g.ldb = F; g.sB = PC * F;
     g.C = gr->dw1; g.ldc = F; g.sC = M * F;
     g.epi = EPI_ACC_F32;
-    FM_K(1, gemm(g, dt, sc));
-    FM_K(1, colsum_acc(dt, x->dz, gr->db1, (int)El, (int)PC, (int)F, sc));
+    FM_GEMM(KK_DW1, g);
+    FM_KP(KK_DB1, 1, (double)El * PC * F, (double)El * PC * F * es + El * F * 8.0, sc, colsum_acc(dt, x->dz, gr->db1, (int)El, (int)PC, (int)F, sc));
     // dX_e = dZ·W1ᵀ  -> dispatch-bwd send buffer [El][P][C][M]
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
     g.A = x->dz; g.lda = F; g.sA = PC * F;
     g.B = p->w1; g.ldb = F; g.sB = M * F; g.b_kmajor = 1;
     g.C = (char*)x->dxe + r * ECM * es; g.ldc = M; g.sC = PC * M;
-    FM_K(1, gemm(g, dt, sc));
+    FM_GEMM(KK_DXE, g);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_eb[r], 0));
+      int pi = prof_start(x->s_a2a);
       if (flowmoe_status s = a2a_to_owners(x, (char*)x->dxe + r * ECM * es, (char*)x->dxc + r * ECM * es))
         return s;
+      prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], x->s_a2a));
     }
   // ---- AT_R^bwd .. AT_1^bwd
@@ -547,7 +650,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     void* dA = (char*)x->dA + t0 * M * es;
     void* dctx = (char*)x->dctx + t0 * M * es;
     void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
-    FM_K(1, gather_gate_bwd(dt, (char*)x->dxc + r * ECM * es, at<int32_t>(saved, L.idx + t0 * k * 4),
+    FM_KP(KK_GATHER, 1, 2.0 * Tr * E * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0) + M * E * es, sc, gather_gate_bwd(dt, (char*)x->dxc + r * ECM * es, at<int32_t>(saved, L.idx + t0 * k * 4),
                             at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
                             x->dw + t0 * k, at<float>(saved, L.logits + t0 * E * 4), p->wg,
                             x->cfg.residual ? (const char*)dy + t0 * M * es : nullptr, dA,
@@ -555,8 +658,8 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     GemmArgs g;
     g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
     g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
-    FM_K(1, gemm(g, dt, sc));
-    FM_K(3, attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
+    FM_GEMM(KK_DCTX, g);
+    FM_KP(KK_ATTN_B, 3, 10.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 8 * M * es, sc, attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
                      at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf, (int)Tr, (int)x->N,
                      (int)M, (int)x->H, x->cfg.causal, sc));
     if (dx) {
@@ -565,27 +668,27 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       g.A = dqkv; g.lda = 3 * M; g.B = p->wqkv; g.ldb = 3 * M; g.b_kmajor = 1;
       g.C = (char*)dx + t0 * M * es; g.ldc = M;
       if (x->cfg.residual) { g.resid = dA; g.ldr = M; }
-      FM_K(1, gemm(g, dt, sc));
+      FM_GEMM(KK_DX, g);
     }
   }
   // ---- deferred wgrads over all T tokens (one K=T GEMM each), in the order
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
   float* gf = gr->grad_flat;
-  FM_K(2, gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M,
+  FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc, gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M,
                      (int)E, sc));
   GemmArgs g;
   g.M = (int)M; g.N = (int)M; g.K = (int)x->T;
   g.A = at<char>(saved, L.ctx); g.lda = M; g.a_mmajor = 1;
   g.B = x->dA; g.ldb = M;
   g.C = gf + 3 * M * M; g.ldc = M; g.epi = EPI_ACC_F32;
-  FM_K(1, gemm(g, dt, sc));
+  FM_GEMM(KK_DWO, g);
   FM_CUDA(cudaEventRecord(x->ev_grads_a, sc));
   g = GemmArgs();
   g.M = (int)M; g.N = (int)(3 * M); g.K = (int)x->T;
   g.A = xin; g.lda = M; g.a_mmajor = 1;
   g.B = x->dqkv; g.ldb = 3 * M;
   g.C = gf; g.ldc = 3 * M; g.epi = EPI_ACC_F32;
-  FM_K(1, gemm(g, dt, sc));
+  FM_GEMM(KK_DWQKV, g);
   FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
   // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2)
   if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
@@ -661,6 +764,6 @@ extern "C" flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int 
   g.resid = resid; g.ldr = ldc; g.sR = sC;
   g.aux = aux; g.ldaux = ldc; g.sAux = sC;
   if (dtype != DT_F32 && dtype != DT_BF16) return fail(FLOWMOE_ERR_INVALID, "dtype");
-  FM_K(1, gemm(g, dtype, stream));
+  FM_KP(KK_TEST, 1, 2.0 * M * N * (double)K * batch, 0, stream, gemm(g, dtype, stream));
   return FLOWMOE_OK;
 }

@@ -307,7 +307,8 @@ static int attn_fwd_t(const void* qkv, void* ctx, float* lse, int T_, int N, int
                       int causal, cudaStream_t s) {
   size_t smem = (3 * AB * (DH + 1) + AB * (AB + 1)) * sizeof(float);
   auto k = attn_fwd_kernel<T, DH>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
   dim3 grid((N + AB - 1) / AB, H, T_ / N);
   k<<<grid, 256, smem, s>>>((const T*)qkv, (T*)ctx, lse, N, M, H, causal, 1.0f / sqrtf((float)DH));
   return (int)cudaGetLastError();
@@ -323,12 +324,14 @@ static int attn_bwd_t(const void* qkv, const void* ctx, const float* lse, const 
   dim3 grid((N + AB - 1) / AB, H, T_ / N);
   size_t smem1 = (4 * AB * (DH + 1) + 2 * AB * (AB + 1) + 2 * AB) * sizeof(float);
   auto k1 = attn_bwd_dkdv_kernel<T, DH>;
-  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), true);
+  (void)once1;
   k1<<<grid, 256, smem1, s>>>((const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
                               scale);
   size_t smem2 = (4 * AB * (DH + 1) + AB * (AB + 1)) * sizeof(float);
   auto k2 = attn_bwd_dq_kernel<T, DH>;
-  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), true);
+  (void)once2;
   k2<<<grid, 256, smem2, s>>>((const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
                               scale);
   return (int)cudaGetLastError();

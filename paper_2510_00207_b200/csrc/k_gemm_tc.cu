@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   __syncthreads();
   if (warp == 1) {
+    __syncwarp();
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"((uint32_t)BN));
@@ -318,18 +319,15 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
             ((uint32_t)(TC_BM >> 4) << 24);
   const size_t smem = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024 + 256;
   auto kern = gemm_tc_kernel<BN, STAGES>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)attr_set;
   dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, g.batch);
   kern<<<grid, TC_THREADS, smem, s>>>(ma, mb, p);
   return (int)cudaGetLastError();
 }
 
 int gemm_tc(const GemmArgs& g, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return 0;
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0 || g.K <= 0) return 0;
   if (g_tc_debug & 1) return gemm_simt(g, DT_BF16, s);
   if (int rc = gemm_tc_init()) return rc;
   if (g.N >= 256) return launch_tc<256, 4>(g, s);

@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(RS_THREADS) route_scan_kernel(const int32_t* i
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_, int E,
                int k, int C, cudaStream_t s) {
   size_t smem = (size_t)E * RS_THREADS * sizeof(int);
-  cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool once = (cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           64 * RS_THREADS * (int)sizeof(int)), true);
+  (void)once;
   route_scan_kernel<<<1, RS_THREADS, smem, s>>>(idx, pos, counts, src, T_, E, k, C);
   return (int)cudaGetLastError();
 }

@@ -22,7 +22,7 @@ EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
     "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
     "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
-    "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
+    "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
 ]
 
 
@@ -37,6 +37,11 @@ class Config(ctypes.Structure):
                 ("capacity_factor", ctypes.c_float), ("causal", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+class ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("launches", ctypes.c_int64), ("ms", ctypes.c_double),
+                ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
 class Params(ctypes.Structure):
@@ -77,6 +82,8 @@ def lib() -> ctypes.CDLL:
     i64 = ctypes.c_int64
     L.flowmoe_test_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
                                     vp, i64, i64, i32, vp, vp, vp, vp]
+    L.flowmoe_profile_end.argtypes = [ctypes.POINTER(ProfEntry), i32]
+    L.flowmoe_profile_end.restype = i32
     L.flowmoe_status_string.argtypes = [i32]
     L.flowmoe_status_string.restype = ctypes.c_char_p
     L.flowmoe_last_error.restype = ctypes.c_char_p
@@ -105,6 +112,20 @@ def get_unique_id() -> bytes:
 
 def debug_set(key: int, value: int):
     _check(lib().flowmoe_debug_set(key, value), "flowmoe_debug_set")
+
+
+def profile_begin():
+    _check(lib().flowmoe_profile_begin(), "flowmoe_profile_begin")
+
+
+def profile_end() -> list[dict]:
+    """Per-kernel-kind device time and algorithmic work since profile_begin()."""
+    buf = (ProfEntry * 64)()
+    n = lib().flowmoe_profile_end(buf, 64)
+    if n < 0:
+        raise FlowMoEError(f"flowmoe_profile_end: {lib().flowmoe_last_error().decode()}")
+    return [dict(name=buf[i].name.decode(), launches=buf[i].launches, ms=buf[i].ms,
+                 flops=buf[i].flops, bytes=buf[i].bytes) for i in range(n)]
 
 
 def kernel_launches() -> int:

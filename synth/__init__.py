@@ -157,3 +157,43 @@ def to_device_dtype(a: np.ndarray, dtype: str) -> np.ndarray:
     if dtype == "bf16":
         return bf16_bits(a)
     return np.asarray(a, dtype=np.float32)
+
+
+def gen_device_block(cfg: BlockConfig, rank: int, P: int, block: int, device):
+    """Device-side weights of one block for rank ``rank`` of ``P`` (local experts
+    only), same distributions as gen_replicated, drawn with a seeded torch
+    generator on the device.  Used by bench.py, where full-size configs are too
+    large for host fp64 generation; parity tests use gen_replicated."""
+    import torch
+    M, E, F = cfg.M, cfg.E, cfg.d_ffn
+    El = E // P
+    g = torch.Generator(device=device)
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+
+    def randn(shape, std, stream):
+        g.manual_seed(SEED_BASE * 1000003 + block * 7919 + stream)
+        return (torch.randn(shape, generator=g, device=device, dtype=torch.float32) * std).to(dt)
+
+    out = {"wqkv": randn((M, 3 * M), M ** -0.5, 1), "wo": randn((M, M), M ** -0.5, 2),
+           "wg": randn((M, E), M ** -0.5, 3)}
+    w1, b1, w2, b2 = [], [], [], []
+    for el in range(El):
+        e = rank * El + el
+        w1.append(randn((M, F), M ** -0.5, 100 + 4 * e))
+        b1.append(randn((F,), 0.02, 101 + 4 * e))
+        w2.append(randn((F, M), F ** -0.5, 102 + 4 * e))
+        b2.append(randn((M,), 0.02, 103 + 4 * e))
+    out.update(w1=torch.stack(w1), b1=torch.stack(b1), w2=torch.stack(w2), b2=torch.stack(b2))
+    return out
+
+
+def gen_device_worker(cfg: BlockConfig, rank: int, device):
+    """Device-side X [T,M] and dO [T,M] ~ N(0,1) for rank ``rank``."""
+    import torch
+    g = torch.Generator(device=device)
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    g.manual_seed(SEED_BASE * 31 + 2 * rank + 1)
+    x = torch.randn((cfg.T, cfg.M), generator=g, device=device).to(dt)
+    g.manual_seed(SEED_BASE * 31 + 2 * rank + 2)
+    dy = torch.randn((cfg.T, cfg.M), generator=g, device=device).to(dt)
+    return x, dy
