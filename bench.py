@@ -378,6 +378,10 @@ def main():
             json.dump({"config": args.config, "ms_per_step_eager_profiled": sum(p["ms"] for p in compute),
                        "kernels": sorted(prof, key=lambda p: -p["ms"])}, open(args.profile_json, "w"), indent=1)
         print(json.dumps(line), flush=True)
+    # a CUDA graph that captured NCCL calls must be destroyed before the communicators
+    if not args.no_graph:
+        del graph, run
+    torch.cuda.synchronize()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

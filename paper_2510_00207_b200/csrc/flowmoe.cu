@@ -208,7 +208,7 @@ SavedLayout layout_of(const flowmoe_ctx* x) {
   L.src = take(R * E * C * 4);
   L.send = take(R * E * C * M * es);
   L.xe = x->P > 1 ? take(R * E * C * M * es) : L.send;
-  L.z = take(R * E * C * F * es);  // [R][El][P*C][F] == R*E*C*F elements
+  L.z = take(R * E * C * F * es);  // [El][R][P*C][F] == R*E*C*F elements
   L.h = take(R * E * C * F * es);
   L.ye = take(R * E * C * M * es);
   L.yc = x->P > 1 ? take(R * E * C * M * es) : L.ye;
@@ -218,30 +218,40 @@ SavedLayout layout_of(const flowmoe_ctx* x) {
 
 ncclDataType_t nccl_dt(const flowmoe_ctx* x) { return x->dt == DT_BF16 ? ncclBfloat16 : ncclFloat; }
 
-// send [E][C][M] (experts grouped by owner) -> recv [El][P][C][M] (rows of one expert contiguous)
-flowmoe_status a2a_to_experts(flowmoe_ctx* x, const void* send, void* recv) {
+// Expert buffers are expert-major, chunk-minor so that one expert's rows over all
+// R chunks are contiguous (the expert wgrads then run as ONE K = R·P·C GEMM):
+//   owner side  [E][R][C][M]      (dispatch send, combine recv)
+//   expert side [E/P][R][P][C][M] (dispatch recv, expert GEMM rows, combine send)
+// Chunk r, destination/source rank q, local expert el: one C×M block each.
+size_t owner_blk(const flowmoe_ctx* x, int64_t e, int r) { return (size_t)(e * x->cfg.R + r) * x->C * x->M; }
+size_t expert_blk(const flowmoe_ctx* x, int64_t el, int r, int q) {
+  return (size_t)((el * x->cfg.R + r) * x->P + q) * x->C * x->M;
+}
+
+// owner side -> expert side for chunk r (dispatch D_r, and C_r^bwd of dY)
+flowmoe_status a2a_to_experts(flowmoe_ctx* x, const void* send, void* recv, int r) {
   const size_t blk = (size_t)x->C * x->M;
   FM_NCCL(ncclGroupStart());
   for (int q = 0; q < x->P; ++q)
     for (int el = 0; el < x->El; ++el) {
-      FM_NCCL(ncclSend((const char*)send + ((size_t)q * x->El + el) * blk * x->es, blk, nccl_dt(x), q,
+      FM_NCCL(ncclSend((const char*)send + owner_blk(x, q * x->El + el, r) * x->es, blk, nccl_dt(x), q,
                        x->comm_a2a, x->s_a2a));
-      FM_NCCL(ncclRecv((char*)recv + ((size_t)el * x->P + q) * blk * x->es, blk, nccl_dt(x), q,
+      FM_NCCL(ncclRecv((char*)recv + expert_blk(x, el, r, q) * x->es, blk, nccl_dt(x), q,
                        x->comm_a2a, x->s_a2a));
     }
   FM_NCCL(ncclGroupEnd());
   return FLOWMOE_OK;
 }
 
-// send [El][P][C][M] (expert side) -> recv [E][C][M] (token-owner side)
-flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv) {
+// expert side -> owner side for chunk r (combine C_r, and D_r^bwd of dX)
+flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv, int r) {
   const size_t blk = (size_t)x->C * x->M;
   FM_NCCL(ncclGroupStart());
   for (int q = 0; q < x->P; ++q)
     for (int el = 0; el < x->El; ++el) {
-      FM_NCCL(ncclSend((const char*)send + ((size_t)el * x->P + q) * blk * x->es, blk, nccl_dt(x), q,
+      FM_NCCL(ncclSend((const char*)send + expert_blk(x, el, r, q) * x->es, blk, nccl_dt(x), q,
                        x->comm_a2a, x->s_a2a));
-      FM_NCCL(ncclRecv((char*)recv + ((size_t)q * x->El + el) * blk * x->es, blk, nccl_dt(x), q,
+      FM_NCCL(ncclRecv((char*)recv + owner_blk(x, q * x->El + el, r) * x->es, blk, nccl_dt(x), q,
                        x->comm_a2a, x->s_a2a));
     }
   FM_NCCL(ncclGroupEnd());
@@ -402,7 +412,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   const size_t es = x->es;
   const int64_t R = cfg->R, ECM = x->E * x->C * x->M;
   bool ok = alloc(&x->dyc, R * ECM * es) && alloc(&x->dxe, R * ECM * es) &&
-            alloc(&x->dz, (size_t)x->E * x->C * x->F * es) && alloc(&x->dA, x->T * x->M * es) &&
+            alloc(&x->dz, (size_t)R * x->E * x->C * x->F * es) && alloc(&x->dA, x->T * x->M * es) &&
             alloc(&x->dctx, x->T * x->M * es) && alloc(&x->dqkv, x->T * 3 * x->M * es) &&
             alloc((void**)&x->dl, x->T * x->E * 4) && alloc((void**)&x->dw, x->T * x->k * 4) &&
             alloc((void**)&x->Dbuf, x->T * x->H * 4) &&
@@ -458,14 +468,15 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL parameter pointer");
   const int dt = x->dt;
   const size_t es = x->es;
+  const int R = x->cfg.R;
   const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
-  const int64_t ECM = E * C * M, ECF = E * C * F, PC = P * C;
+  const int64_t ECM = E * C * M, PC = P * C, ldE = R * C;
   const SavedLayout& L = x->L;
   cudaStream_t sc = x->s_comp;
   FM_CUDA(cudaEventRecord(x->ev_in, stream));
   FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer
-  for (int r = 0; r < x->cfg.R; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int64_t t0 = r * Tr;
     const char* xr = (const char*)xin + t0 * M * es;
     void* qkv = at<char>(saved, L.qkv + t0 * 3 * M * es);
@@ -475,78 +486,75 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.M = (int)Tr; g.N = (int)(3 * M); g.K = (int)M;
     g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
     FM_GEMM(KK_QKV, g);
-    FM_KP(KK_ATTN_F, 1, 4.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 5 * M * es + Tr * x->H * 4.0, sc, attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N,
-                     (int)M, (int)x->H, x->cfg.causal, sc));
+    FM_KP(KK_ATTN_F, 1, 4.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 5 * M * es + Tr * x->H * 4.0, sc,
+          attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N, (int)M,
+                   (int)x->H, x->cfg.causal, sc));
     g = GemmArgs();
     g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
     g.A = ctxb; g.lda = M; g.B = p->wo; g.ldb = M; g.C = a; g.ldc = M;
     if (x->cfg.residual) { g.resid = xr; g.ldr = M; }
     FM_GEMM(KK_OPROJ, g);
-    FM_KP(KK_GATE, 1, 2.0 * Tr * M * E, (double)Tr * M * es + M * E * es + Tr * E * 4.0 + Tr * k * 8.0, sc, gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr,
-                      at<float>(saved, L.logits + t0 * E * 4), at<int32_t>(saved, L.idx + t0 * k * 4),
-                      at<float>(saved, L.w + t0 * k * 4), (int)Tr, (int)M, (int)E, (int)k, sc));
+    FM_KP(KK_GATE, 1, 2.0 * Tr * M * E, (double)Tr * M * es + M * E * es + Tr * E * 4.0 + Tr * k * 8.0, sc,
+          gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr, at<float>(saved, L.logits + t0 * E * 4),
+                    at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4), (int)Tr, (int)M,
+                    (int)E, (int)k, sc));
     int32_t* src = at<int32_t>(saved, L.src + r * E * C * 4);
-    FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc, route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
-                       at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
-    FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc, permute_pack(dt, a, src, at<char>(saved, L.send + r * ECM * es), (int)(E * C), (int)M,
-                         (int)k, sc));
+    FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc,
+          route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+                     at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
+    FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc,
+          permute_pack(dt, a, src, at<char>(saved, L.send + r * C * M * es), (int)E, (int)C, (int)ldE, (int)M,
+                       (int)k, sc));
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
   }
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)
-    for (int r = 0; r < x->cfg.R; ++r) {
+    for (int r = 0; r < R; ++r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_at[r], 0));
       int pi = prof_start(x->s_a2a);
-      if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send + r * ECM * es),
-                                            at<char>(saved, L.xe + r * ECM * es)))
-        return s;
+      if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
       prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_d[r], x->s_a2a));
     }
-  // ---- E_1..E_R: batched expert FFN over [El][P*C] capacity rows
-  for (int r = 0; r < x->cfg.R; ++r) {
+  // ---- E_1..E_R: batched expert FFN over the [P*C] capacity rows of chunk r of each local expert
+  for (int r = 0; r < R; ++r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_d[r], 0));
-    void* xe = at<char>(saved, L.xe + r * ECM * es);
-    void* z = at<char>(saved, L.z + r * ECF * es);
-    void* h = at<char>(saved, L.h + r * ECF * es);
-    void* ye = at<char>(saved, L.ye + r * ECM * es);
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
-    g.A = xe; g.lda = M; g.sA = PC * M;
+    g.A = at<char>(saved, L.xe + r * PC * M * es); g.lda = M; g.sA = R * PC * M;
     g.B = p->w1; g.ldb = F; g.sB = M * F;
-    g.C = h; g.ldc = F; g.sC = PC * F;
+    g.C = at<char>(saved, L.h + r * PC * F * es); g.ldc = F; g.sC = R * PC * F;
     g.bias = p->b1; g.sBias = F;
-    g.aux = z; g.ldaux = F; g.sAux = PC * F;
+    g.aux = at<char>(saved, L.z + r * PC * F * es); g.ldaux = F; g.sAux = R * PC * F;
     g.epi = EPI_BIAS_GELU;
     FM_GEMM(KK_E1, g);
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
-    g.A = h; g.lda = F; g.sA = PC * F;
+    g.A = at<char>(saved, L.h + r * PC * F * es); g.lda = F; g.sA = R * PC * F;
     g.B = p->w2; g.ldb = M; g.sB = F * M;
-    g.C = ye; g.ldc = M; g.sC = PC * M;
+    g.C = at<char>(saved, L.ye + r * PC * M * es); g.ldc = M; g.sC = R * PC * M;
     g.bias = p->b2; g.sBias = M;
     FM_GEMM(KK_E2, g);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_e[r], sc));
   }
   // ---- C_1..C_R (Eq.(4))
   if (P > 1)
-    for (int r = 0; r < x->cfg.R; ++r) {
+    for (int r = 0; r < R; ++r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_e[r], 0));
       int pi = prof_start(x->s_a2a);
-      if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye + r * ECM * es),
-                                           at<char>(saved, L.yc + r * ECM * es)))
-        return s;
+      if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
       prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_c[r], x->s_a2a));
     }
   // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
-  for (int r = 0; r < x->cfg.R; ++r) {
+  for (int r = 0; r < R; ++r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_c[r], 0));
     const int64_t t0 = r * Tr;
-    FM_KP(KK_COMBINE, 1, 2.0 * Tr * k * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0), sc, unpermute_combine(dt, at<char>(saved, L.yc + r * ECM * es), at<int32_t>(saved, L.idx + t0 * k * 4),
-                              at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
-                              x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
-                              (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)C, sc));
+    FM_KP(KK_COMBINE, 1, 2.0 * Tr * k * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0), sc,
+          unpermute_combine(dt, at<char>(saved, L.yc + r * C * M * es), at<int32_t>(saved, L.idx + t0 * k * 4),
+                            at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
+                            x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
+                            (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)ldE, sc));
   }
   FM_CUDA(cudaEventRecord(x->ev_done, sc));
   FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
@@ -565,72 +573,50 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: chunk_bytes (S_p) must be a positive multiple of 16");
   const int dt = x->dt;
   const size_t es = x->es;
-  const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
-  const int64_t ECM = E * C * M, ECF = E * C * F, PC = P * C;
-  const SavedLayout& L = x->L;
   const int R = x->cfg.R;
+  const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
+  const int64_t ECM = E * C * M, PC = P * C, ldE = R * C;
+  const SavedLayout& L = x->L;
   cudaStream_t sc = x->s_comp;
   FM_CUDA(cudaEventRecord(x->ev_in, stream));
   FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
-  // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the combine-side buffer, dw = <dO, Y>
+  // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the owner-side buffer, dw = <dO, Y>
   for (int r = R - 1; r >= 0; --r) {
     const int64_t t0 = r * Tr;
-    FM_KP(KK_CBPACK, 1, 4.0 * Tr * k * M, (double)Tr * M * es + 2.0 * Tr * k * M * es, sc, combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * ECM * es),
-                             at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
-                             at<float>(saved, L.w + t0 * k * 4), at<int32_t>(saved, L.src + r * E * C * 4),
-                             (char*)x->dyc + r * ECM * es, x->dw + t0 * k, (int)Tr, (int)M, (int)k,
-                             (int)E, (int)C, sc));
+    FM_KP(KK_CBPACK, 1, 4.0 * Tr * k * M, (double)Tr * M * es + 2.0 * Tr * k * M * es, sc,
+          combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * C * M * es),
+                           at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+                           at<float>(saved, L.w + t0 * k * 4), at<int32_t>(saved, L.src + r * E * C * 4),
+                           (char*)x->dyc + r * C * M * es, x->dw + t0 * k, (int)Tr, (int)M, (int)k, (int)E,
+                           (int)C, (int)ldE, sc));
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_cb[r], sc));
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_cb[r], 0));
       int pi = prof_start(x->s_a2a);
-      if (flowmoe_status s = a2a_to_experts(x, (char*)x->dyc + r * ECM * es, (char*)x->dye + r * ECM * es))
-        return s;
+      if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
       prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], x->s_a2a));
     }
-  // ---- E_R^bwd .. E_1^bwd (Eq.(5))
+  // ---- E_R^bwd .. E_1^bwd (Eq.(5)): dgrads per chunk, so D_r^bwd can start early
   for (int r = R - 1; r >= 0; --r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_cba[r], 0));
-    const void* dye = (char*)x->dye + r * ECM * es;
-    const void* xe = at<char>(saved, L.xe + r * ECM * es);
-    const void* z = at<char>(saved, L.z + r * ECF * es);
-    const void* h = at<char>(saved, L.h + r * ECF * es);
     // dZ = (dY·W2ᵀ) ⊙ GELU'(Z)
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
-    g.A = dye; g.lda = M; g.sA = PC * M;
+    g.A = (char*)x->dye + r * PC * M * es; g.lda = M; g.sA = R * PC * M;
     g.B = p->w2; g.ldb = M; g.sB = F * M; g.b_kmajor = 1;
-    g.C = x->dz; g.ldc = F; g.sC = PC * F;
-    g.aux = const_cast<void*>(z); g.ldaux = F; g.sAux = PC * F;
+    g.C = (char*)x->dz + r * PC * F * es; g.ldc = F; g.sC = R * PC * F;
+    g.aux = const_cast<char*>(at<char>(saved, L.z + r * PC * F * es)); g.ldaux = F; g.sAux = R * PC * F;
     g.epi = EPI_DGELU;
     FM_GEMM(KK_DGELU, g);
-    // dW2 += Hᵀ·dY
-    g = GemmArgs();
-    g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)PC;
-    g.A = h; g.lda = F; g.sA = PC * F; g.a_mmajor = 1;
-    g.B = dye; g.ldb = M; g.sB = PC * M;
-    g.C = gr->dw2; g.ldc = M; g.sC = F * M;
-    g.epi = EPI_ACC_F32;
-    FM_GEMM(KK_DW2, g);
-    FM_KP(KK_DB2, 1, (double)El * PC * M, (double)El * PC * M * es + El * M * 8.0, sc, colsum_acc(dt, dye, gr->db2, (int)El, (int)PC, (int)M, sc));
-    // dW1 += Xᵀ·dZ
-    g = GemmArgs();
-    g.batch = (int)El; g.M = (int)M; g.N = (int)F; g.K = (int)PC;
-    g.A = xe; g.lda = M; g.sA = PC * M; g.a_mmajor = 1;
-    g.B = x->dz; g.ldb = F; g.sB = PC * F;
-    g.C = gr->dw1; g.ldc = F; g.sC = M * F;
-    g.epi = EPI_ACC_F32;
-    FM_GEMM(KK_DW1, g);
-    FM_KP(KK_DB1, 1, (double)El * PC * F, (double)El * PC * F * es + El * F * 8.0, sc, colsum_acc(dt, x->dz, gr->db1, (int)El, (int)PC, (int)F, sc));
-    // dX_e = dZ·W1ᵀ  -> dispatch-bwd send buffer [El][P][C][M]
+    // dX_e = dZ·W1ᵀ  -> dispatch-bwd send buffer (expert side)
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
-    g.A = x->dz; g.lda = F; g.sA = PC * F;
+    g.A = (char*)x->dz + r * PC * F * es; g.lda = F; g.sA = R * PC * F;
     g.B = p->w1; g.ldb = F; g.sB = M * F; g.b_kmajor = 1;
-    g.C = (char*)x->dxe + r * ECM * es; g.ldc = M; g.sC = PC * M;
+    g.C = (char*)x->dxe + r * PC * M * es; g.ldc = M; g.sC = R * PC * M;
     FM_GEMM(KK_DXE, g);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
   }
@@ -638,11 +624,32 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     for (int r = R - 1; r >= 0; --r) {
       FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_eb[r], 0));
       int pi = prof_start(x->s_a2a);
-      if (flowmoe_status s = a2a_to_owners(x, (char*)x->dxe + r * ECM * es, (char*)x->dxc + r * ECM * es))
-        return s;
+      if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
       prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], x->s_a2a));
     }
+  // ---- expert wgrads over all R chunks at once (K = R·P·C rows), overlapping the
+  // last D^bwd A2As; the sums are the chunk sums of P:1173 in a different order.
+  {
+    GemmArgs g;  // dW2 += Hᵀ·dY
+    g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)(R * PC);
+    g.A = at<char>(saved, L.h); g.lda = F; g.sA = R * PC * F; g.a_mmajor = 1;
+    g.B = x->dye; g.ldb = M; g.sB = R * PC * M;
+    g.C = gr->dw2; g.ldc = M; g.sC = F * M;
+    g.epi = EPI_ACC_F32;
+    FM_GEMM(KK_DW2, g);
+    FM_KP(KK_DB2, 1, (double)El * R * PC * M, (double)El * R * PC * M * es + El * M * 8.0, sc,
+          colsum_acc(dt, x->dye, gr->db2, (int)El, (int)(R * PC), (int)M, sc));
+    g = GemmArgs();  // dW1 += Xᵀ·dZ
+    g.batch = (int)El; g.M = (int)M; g.N = (int)F; g.K = (int)(R * PC);
+    g.A = at<char>(saved, L.xe); g.lda = M; g.sA = R * PC * M; g.a_mmajor = 1;
+    g.B = x->dz; g.ldb = F; g.sB = R * PC * F;
+    g.C = gr->dw1; g.ldc = F; g.sC = M * F;
+    g.epi = EPI_ACC_F32;
+    FM_GEMM(KK_DW1, g);
+    FM_KP(KK_DB1, 1, (double)El * R * PC * F, (double)El * R * PC * F * es + El * F * 8.0, sc,
+          colsum_acc(dt, x->dz, gr->db1, (int)El, (int)(R * PC), (int)F, sc));
+  }
   // ---- AT_R^bwd .. AT_1^bwd
   for (int r = R - 1; r >= 0; --r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dba[r], 0));
@@ -650,18 +657,20 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     void* dA = (char*)x->dA + t0 * M * es;
     void* dctx = (char*)x->dctx + t0 * M * es;
     void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
-    FM_KP(KK_GATHER, 1, 2.0 * Tr * E * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0) + M * E * es, sc, gather_gate_bwd(dt, (char*)x->dxc + r * ECM * es, at<int32_t>(saved, L.idx + t0 * k * 4),
-                            at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
-                            x->dw + t0 * k, at<float>(saved, L.logits + t0 * E * 4), p->wg,
-                            x->cfg.residual ? (const char*)dy + t0 * M * es : nullptr, dA,
-                            x->dl + t0 * E, (int)Tr, (int)M, (int)E, (int)k, (int)C, sc));
+    FM_KP(KK_GATHER, 1, 2.0 * Tr * E * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0) + M * E * es, sc,
+          gather_gate_bwd(dt, (char*)x->dxc + r * C * M * es, at<int32_t>(saved, L.idx + t0 * k * 4),
+                          at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
+                          x->dw + t0 * k, at<float>(saved, L.logits + t0 * E * 4), p->wg,
+                          x->cfg.residual ? (const char*)dy + t0 * M * es : nullptr, dA, x->dl + t0 * E,
+                          (int)Tr, (int)M, (int)E, (int)k, (int)ldE, sc));
     GemmArgs g;
     g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
     g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
     FM_GEMM(KK_DCTX, g);
-    FM_KP(KK_ATTN_B, 3, 10.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 8 * M * es, sc, attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
-                     at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf, (int)Tr, (int)x->N,
-                     (int)M, (int)x->H, x->cfg.causal, sc));
+    FM_KP(KK_ATTN_B, 3, 10.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 8 * M * es, sc,
+          attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
+                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf, (int)Tr, (int)x->N, (int)M,
+                   (int)x->H, x->cfg.causal, sc));
     if (dx) {
       g = GemmArgs();
       g.M = (int)Tr; g.N = (int)M; g.K = (int)(3 * M);
@@ -671,11 +680,11 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       FM_GEMM(KK_DX, g);
     }
   }
-  // ---- deferred wgrads over all T tokens (one K=T GEMM each), in the order
+  // ---- deferred MHA/gate wgrads over all T tokens (one K=T GEMM each), in the order
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
   float* gf = gr->grad_flat;
-  FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc, gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M,
-                     (int)E, sc));
+  FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc,
+        gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M, (int)E, sc));
   GemmArgs g;
   g.M = (int)M; g.N = (int)M; g.K = (int)x->T;
   g.A = at<char>(saved, L.ctx); g.lda = M; g.a_mmajor = 1;

@@ -18,84 +18,13 @@
 #include <stdio.h>
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace fm {
 
 constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 192;
 static int g_tc_debug = 0;  // bit0: force SIMT for bf16; bit1: swap LBO/SBO of MN-major descs
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
-
-// ------------------------------------------------------------ PTX wrappers
-FM_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-FM_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-FM_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-FM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-FM_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-FM_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-FM_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-FM_DEV void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-FM_DEV void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                   uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
-FM_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// UMMA shared-memory descriptor (SWIZZLE_128B, version 1 for sm_100).
-FM_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
-  return d;
-}
 
 // ------------------------------------------------------------ kernel
 struct TcArgs {
@@ -107,7 +36,9 @@ struct TcArgs {
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
-                   const __grid_constant__ CUtensorMap tma_b, const TcArgs p) {
+                   const __grid_constant__ CUtensorMap tma_b,
+                   const __grid_constant__ CUtensorMap tma_c,
+                   const __grid_constant__ CUtensorMap tma_aux, const TcArgs p) {
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   constexpr uint32_t B_BYTES = BN * TC_BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -190,70 +121,99 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_commit(tmem_full);
     }
   } else {
-    // ===== epilogue: TMEM -> registers -> global =====
+    // ===== epilogue: TMEM -> registers -> swizzled smem tile -> TMA store / reduce-add =====
+    // Each warp owns 32 rows (its TMEM lane quarter) and walks the BN columns in
+    // 32-column chunks.  A chunk is staged as a [32 rows][32 cols] box in smem with
+    // the TMA swizzle (128 B rows for fp32, 64 B rows for bf16: conflict-free
+    // 16-byte st.shared) and written by one TMA bulk store, or a TMA bulk
+    // reduce-add (fp32 grad accumulation C += acc, done in L2).  Two staging
+    // buffers per warp (4 KB each) overlap the next chunk with the in-flight store.
+    // The operand ring is free here (all MMAs, hence all TMA loads, completed).
     const int quarter = warp & 3;
-    const int row = m0 + quarter * 32 + lane;
+    const int r0 = quarter * 32;
+    const int row = m0 + r0 + lane;
+    uint8_t* stage = smem + quarter * 8192;
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const bool row_ok = row < g.M;
+    const bool f32out = g.epi == EPI_ACC_F32;
+    int buf = 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + c0, r);
       const int nb = n0 + c0;
-      if (!row_ok || nb >= g.N) continue;
+      if (nb >= g.N) break;  // warp-uniform
+      uint32_t r[32];
+      tmem_ld32(tmem_base + ((uint32_t)r0 << 16) + c0, r);
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
       const int nvalid = min(32, g.N - nb);
-      if (g.epi == EPI_ACC_F32) {
-        float* C = reinterpret_cast<float*>(g.C) + (int64_t)b * g.sC + (int64_t)row * g.ldc + nb;
-        if (nvalid == 32) {
+      if (!f32out) {
+        if (g.bias) {
+          const bf16* bias = reinterpret_cast<const bf16*>(g.bias) + (int64_t)b * g.sBias + nb;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 o = *reinterpret_cast<float4*>(C + i);
-            o.x += v[i]; o.y += v[i + 1]; o.z += v[i + 2]; o.w += v[i + 3];
-            *reinterpret_cast<float4*>(C + i) = o;
-          }
-        } else {
-          for (int i = 0; i < nvalid; ++i) C[i] += v[i];
+          for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? __bfloat162float(bias[i]) : 0.f;
         }
-        continue;
-      }
-      if (g.bias) {
-        const bf16* bias = reinterpret_cast<const bf16*>(g.bias) + (int64_t)b * g.sBias + nb;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? __bfloat162float(bias[i]) : 0.f;
-      }
-      bf16* C = reinterpret_cast<bf16*>(g.C) + (int64_t)b * g.sC + (int64_t)row * g.ldc + nb;
-      if (g.epi == EPI_STORE) {
-        if (g.resid) {
+        if (g.epi == EPI_STORE && g.resid && row_ok) {
           const bf16* R = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr + nb;
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? __bfloat162float(R[i]) : 0.f;
+        } else if (g.epi == EPI_DGELU && row_ok) {
+          const bf16* Z = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux + nb;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(__bfloat162float(Z[i])) : 0.f;
+        }
+      }
+      // staging buffer `buf` is free once the store issued two chunks ago has read it
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* sb = stage + buf * 4096;
+      if (f32out) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          *reinterpret_cast<float4*>(sb + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
         }
       } else if (g.epi == EPI_BIAS_GELU) {
-        bf16* Z = reinterpret_cast<bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux + nb;
-        if (nvalid == 32) {
+        // aux = Z (pre-activation), C = GELU(bf16(Z))
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) store16<bf16>(Z + i, v + i);
-        } else {
-          for (int i = 0; i < nvalid; ++i) Z[i] = __float2bfloat16_rn(v[i]);
+        for (int j = 0; j < 4; ++j) {
+          uint4 zq, hq;
+          float zz[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) zz[i] = __bfloat162float(__float2bfloat16_rn(v[8 * j + i]));
+          zq.x = pack_bf16x2(zz[0], zz[1]); zq.y = pack_bf16x2(zz[2], zz[3]);
+          zq.z = pack_bf16x2(zz[4], zz[5]); zq.w = pack_bf16x2(zz[6], zz[7]);
+          hq.x = pack_bf16x2(gelu_f(zz[0]), gelu_f(zz[1])); hq.y = pack_bf16x2(gelu_f(zz[2]), gelu_f(zz[3]));
+          hq.z = pack_bf16x2(gelu_f(zz[4]), gelu_f(zz[5])); hq.w = pack_bf16x2(gelu_f(zz[6]), gelu_f(zz[7]));
+          const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+          *reinterpret_cast<uint4*>(sb + off) = hq;
+          *reinterpret_cast<uint4*>(sb + 2048 + off) = zq;
         }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[i])));
-      } else {  // EPI_DGELU
-        const bf16* Z = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux + nb;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(__bfloat162float(Z[i])) : 0.f;
-      }
-      if (nvalid == 32) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) store16<bf16>(C + i, v + i);
       } else {
-        for (int i = 0; i < nvalid; ++i) C[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 q;
+          q.x = pack_bf16x2(v[8 * j], v[8 * j + 1]); q.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+          q.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]); q.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+          *reinterpret_cast<uint4*>(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = q;
+        }
       }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (f32out) {
+          tma_reduce_add_3d(&tma_c, sb, nb, m0 + r0, b);
+        } else {
+          tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
+          if (g.epi == EPI_BIAS_GELU) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
+        }
+        bulk_commit();
+      }
+      buf ^= 1;
     }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
     tc_fence_before();
   }
   __syncthreads();
@@ -282,18 +242,34 @@ int gemm_tc_init() {
   return 0;
 }
 
-// 3-D bf16 map {inner, outer, batch}; strides in elements; box {64, box_outer, 1}.
+// 3-D map {inner, outer, batch}; strides in elements; box {box_inner, box_outer, 1}.
 static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                    uint64_t batch, uint64_t ld, uint64_t bstride, uint32_t box_outer) {
+                    uint64_t batch, uint64_t ld, uint64_t bstride, uint32_t box_outer,
+                    uint32_t box_inner = 64, bool f32 = false,
+                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+  const uint64_t es = f32 ? 4 : 2;
   cuuint64_t dims[3] = {inner, outer, batch};
   if (batch <= 1) bstride = ld * outer;
-  cuuint64_t strides[2] = {ld * 2, bstride * 2};
-  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint64_t strides[2] = {ld * es, bstride * es};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                        const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                      uint32_t box_inner, uint32_t box_outer) {
+  if (int rc = gemm_tc_init()) return rc;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
@@ -307,6 +283,17 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   if (g.b_kmajor) rc = make_map(&mb, g.B, g.K, g.N, g.batch, g.ldb, g.sB, BN);
   else rc = make_map(&mb, g.B, g.N, g.K, g.batch, g.ldb, g.sB, TC_BK);
   if (rc) return rc;
+  // output tiles: [32 rows][32 cols] boxes, fp32 (reduce-add, SW128) or bf16 (store, SW64)
+  CUtensorMap mc, maux;
+  const bool f32 = g.epi == EPI_ACC_F32;
+  rc = make_map(&mc, g.C, g.N, g.M, g.batch, g.ldc, g.sC, 32, 32, f32,
+                f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  maux = mc;
+  if (g.epi == EPI_BIAS_GELU) {
+    rc = make_map(&maux, g.aux, g.N, g.M, g.batch, g.ldaux, g.sAux, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   TcArgs p;
   p.g = g;
   p.a_mmajor = g.a_mmajor;
@@ -322,7 +309,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)attr_set;
   dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, g.batch);
-  kern<<<grid, TC_THREADS, smem, s>>>(ma, mb, p);
+  kern<<<grid, TC_THREADS, smem, s>>>(ma, mb, mc, maux, p);
   return (int)cudaGetLastError();
 }
 
@@ -330,8 +317,12 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0 || g.K <= 0) return 0;
   if (g_tc_debug & 1) return gemm_simt(g, DT_BF16, s);
   if (int rc = gemm_tc_init()) return rc;
-  if (g.N >= 256) return launch_tc<256, 4>(g, s);
-  if (g.N >= 128) return launch_tc<128, 6>(g, s);
+  // Tile width: the widest BN that still fills one wave of the 148 SMs (wide tiles
+  // amortise A re-reads); small, latency-bound GEMMs get narrow tiles and more CTAs.
+  const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
+  auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
+  if (g.N >= 256 && tiles(256) >= 148) return launch_tc<256, 4>(g, s);
+  if (g.N >= 128 && tiles(128) >= 148) return launch_tc<128, 6>(g, s);
   return launch_tc<64, 8>(g, s);
 }
 

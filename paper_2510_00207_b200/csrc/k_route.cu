@@ -201,12 +201,14 @@ int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, 
 // ------------------------------------------------------------------ K3
 template <typename T>
 __global__ void __launch_bounds__(256) permute_pack_kernel(const T* a, const int32_t* src,
-                                                           T* send, int rows, int M, int k) {
+                                                           T* send, int rows, int C, int ldE,
+                                                           int M, int k) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const int sl = src[warp];
   constexpr int V = 16 / sizeof(T);
-  uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)warp * M);
+  const int64_t drow = (int64_t)(warp / C) * ldE + warp % C;
+  uint4* dst = reinterpret_cast<uint4*>(send + drow * M);
   const int nv = M / V;
   if (sl < 0) {
     for (int i = lane; i < nv; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
@@ -216,14 +218,15 @@ __global__ void __launch_bounds__(256) permute_pack_kernel(const T* a, const int
   }
 }
 
-int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int rows, int M, int k,
-                 cudaStream_t s) {
+int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E, int C, int ldE,
+                 int M, int k, cudaStream_t s) {
+  const int rows = E * C;
   if (rows <= 0) return 0;
   dim3 grid((rows * 32 + 255) / 256);
   if (dtype == DT_F32)
-    permute_pack_kernel<float><<<grid, 256, 0, s>>>((const float*)a, src, (float*)send, rows, M, k);
+    permute_pack_kernel<float><<<grid, 256, 0, s>>>((const float*)a, src, (float*)send, rows, C, ldE, M, k);
   else
-    permute_pack_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)a, src, (bf16*)send, rows, M, k);
+    permute_pack_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)a, src, (bf16*)send, rows, C, ldE, M, k);
   return (int)cudaGetLastError();
 }
 
@@ -232,7 +235,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, const int32_t* idx,
                                                                 const int32_t* pos, const float* w,
                                                                 const T* resid, T* out, int T_,
-                                                                int M, int k, int C) {
+                                                                int M, int k, int ldE) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T_) return;
   constexpr int V = 16 / sizeof(T);
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, cons
   for (int j = 0; j < k; ++j) {
     int p = pos[(int64_t)t * k + j];
     if (p >= 0) {
-      rows[nk] = y + ((int64_t)idx[(int64_t)t * k + j] * C + p) * M;
+      rows[nk] = y + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M;
       ws[nk] = w[(int64_t)t * k + j];
       ++nk;
     }
@@ -266,16 +269,16 @@ __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, cons
 }
 
 int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_t* pos,
-                      const float* w, const void* resid, void* out, int T_, int M, int k, int C,
+                      const float* w, const void* resid, void* out, int T_, int M, int k, int ldE,
                       cudaStream_t s) {
   if (T_ <= 0) return 0;
   dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
     unpermute_combine_kernel<float><<<grid, 256, 0, s>>>((const float*)y, idx, pos, w,
-                                                        (const float*)resid, (float*)out, T_, M, k, C);
+                                                        (const float*)resid, (float*)out, T_, M, k, ldE);
   else
     unpermute_combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)y, idx, pos, w,
-                                                       (const bf16*)resid, (bf16*)out, T_, M, k, C);
+                                                       (const bf16*)resid, (bf16*)out, T_, M, k, ldE);
   return (int)cudaGetLastError();
 }
 
@@ -287,13 +290,13 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
                                                                const int32_t* pos, const float* w,
                                                                const int32_t* src, T* dy,
                                                                float* dw, int T_, int M, int k,
-                                                               int rows, int C) {
+                                                               int rows, int C, int ldE) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   constexpr int V = 16 / sizeof(T);
   if (warp >= T_) {
     const int r = warp - T_;
     if (r >= rows || src[r] >= 0) return;
-    uint4* dst = reinterpret_cast<uint4*>(dy + (int64_t)r * M);
+    uint4* dst = reinterpret_cast<uint4*>(dy + ((int64_t)(r / C) * ldE + r % C) * M);
     for (int i = lane; i < M / V; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
     return;
   }
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
       if (lane == 0) dw[(int64_t)t * k + j] = 0.f;
       continue;
     }
-    const int64_t row = (int64_t)idx[(int64_t)t * k + j] * C + p;
+    const int64_t row = (int64_t)idx[(int64_t)t * k + j] * ldE + p;
     const float wj = w[(int64_t)t * k + j];
     float dot = 0.f;
     for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
@@ -323,15 +326,15 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
 
 int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* idx,
                      const int32_t* pos, const float* w, const int32_t* src, void* dy, float* dw,
-                     int T_, int M, int k, int E, int C, cudaStream_t s) {
+                     int T_, int M, int k, int E, int C, int ldE, cudaStream_t s) {
   const int rows = E * C;
   dim3 grid(((T_ + rows) * 32 + 255) / 256);
   if (dtype == DT_F32)
     combine_bwd_pack_kernel<float><<<grid, 256, 0, s>>>((const float*)dout, (const float*)y, idx,
-                                                       pos, w, src, (float*)dy, dw, T_, M, k, rows, C);
+                                                       pos, w, src, (float*)dy, dw, T_, M, k, rows, C, ldE);
   else
     combine_bwd_pack_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dout, (const bf16*)y, idx,
-                                                      pos, w, src, (bf16*)dy, dw, T_, M, k, rows, C);
+                                                      pos, w, src, (bf16*)dy, dw, T_, M, k, rows, C, ldE);
   return (int)cudaGetLastError();
 }
 
@@ -340,7 +343,7 @@ template <typename T, int E>
 __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
     const T* dx, const int32_t* idx, const int32_t* pos, const float* w, const float* dw,
     const float* logits, const T* wg, const T* dres, T* dA, float* dlogits, int T_, int M, int k,
-    int C) {
+    int ldE) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T_) return;
   constexpr int V = 16 / sizeof(T);
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
   int nk = 0;
   for (int j = 0; j < k; ++j) {
     const int p = pos[(int64_t)t * k + j];
-    if (p >= 0) rows[nk++] = dx + ((int64_t)idx[(int64_t)t * k + j] * C + p) * M;
+    if (p >= 0) rows[nk++] = dx + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M;
   }
   for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -416,25 +419,25 @@ template <int E>
 static void gather_gate_bwd_launch(int dtype, const void* dx, const int32_t* idx,
                                    const int32_t* pos, const float* w, const float* dw,
                                    const float* logits, const void* wg, const void* dres, void* dA,
-                                   float* dlogits, int T_, int M, int k, int C, cudaStream_t s) {
+                                   float* dlogits, int T_, int M, int k, int ldE, cudaStream_t s) {
   dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
     gather_gate_bwd_kernel<float, E><<<grid, 256, 0, s>>>(
         (const float*)dx, idx, pos, w, dw, logits, (const float*)wg, (const float*)dres,
-        (float*)dA, dlogits, T_, M, k, C);
+        (float*)dA, dlogits, T_, M, k, ldE);
   else
     gather_gate_bwd_kernel<bf16, E><<<grid, 256, 0, s>>>(
         (const bf16*)dx, idx, pos, w, dw, logits, (const bf16*)wg, (const bf16*)dres, (bf16*)dA,
-        dlogits, T_, M, k, C);
+        dlogits, T_, M, k, ldE);
 }
 
 int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t* pos,
                     const float* w, const float* dw, const float* logits, const void* wg,
-                    const void* dres, void* dA, float* dlogits, int T_, int M, int E, int k, int C,
+                    const void* dres, void* dA, float* dlogits, int T_, int M, int E, int k, int ldE,
                     cudaStream_t s) {
   if (T_ <= 0) return 0;
   FM_E_SWITCH(E, gather_gate_bwd_launch, dtype, dx, idx, pos, w, dw, logits, wg, dres, dA,
-              dlogits, T_, M, k, C, s)
+              dlogits, T_, M, k, ldE, s)
   return (int)cudaGetLastError();
 }
 

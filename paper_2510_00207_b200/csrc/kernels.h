@@ -56,22 +56,24 @@ int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, f
 // K2: deterministic slot-major positions; counts[E]; src[E][C] = t*k+j or -1; pos[T][k] (-1 dropped)
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T, int E,
                int k, int C, cudaStream_t s);
-// K3: send[e][c] = a[src/k] or zeros.  rows = E*C
-int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int rows, int M, int k,
-                 cudaStream_t s);
+// Owner-side expert buffers are [E][R][C][M] (expert-major, chunk-minor); a chunk's
+// view starts at r*C rows and consecutive experts are ldE = R*C rows apart.
+// K3: send[e*ldE + c] = a[src/k] or zeros, for (e, c) in [E) x [C).
+int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E, int C, int ldE,
+                 int M, int k, cudaStream_t s);
 // K7: out[t] = sum_j w_tj * y[idx][pos] (+ a[t] if resid)
 int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_t* pos,
-                      const float* w, const void* resid, void* out, int T, int M, int k, int C,
+                      const float* w, const void* resid, void* out, int T, int M, int k, int ldE,
                       cudaStream_t s);
 // K8: dy[e][pos] = w * dO[t]; dw[t][j] = <dO[t], y[e][pos]>; padding rows zeroed.
 int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* idx,
                      const int32_t* pos, const float* w, const int32_t* src, void* dy, float* dw,
-                     int T, int M, int k, int E, int C, cudaStream_t s);
+                     int T, int M, int k, int E, int C, int ldE, cudaStream_t s);
 // K9: dA[t] = sum_j dx[e][pos] + dlogits·Wg^T (+ dO[t] if resid); dlogits [T][E] fp32 out.
 int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t* pos,
                     const float* w, const float* dw, const float* logits, const void* wg,
                     const void* dout_resid, void* dA, float* dlogits, int T, int M, int E, int k,
-                    int C, cudaStream_t s);
+                    int ldE, cudaStream_t s);
 // dWg[M][E] += A^T · dlogits (deterministic split-T partials); part: scratch [nsplit][M][E]
 int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T,
                int M, int E, cudaStream_t s);

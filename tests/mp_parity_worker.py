@@ -1,0 +1,62 @@
+"""One rank of the multi-GPU parity check (launched by tests/test_gpu_multi.py via
+torchrun).  Every rank runs its block through the C ABI with world_size = P and
+compares its own outputs with the oracle's P simulated workers."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2510_00207_b200 as fm  # noqa: E402
+from synth import PRESETS, BlockConfig, gen_replicated, gen_worker  # noqa: E402
+from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu  # noqa: E402
+
+CASES = {
+    "c1_f32": PRESETS["c1"],
+    "bf16_p": BlockConfig(T=512, seq_len=128, M=256, n_heads=4, E=8, top_k=2, d_ffn=512, R=2,
+                          capacity_factor=1.0, causal=1, residual=1, dtype="bf16"),
+}
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    P = int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    results = {}
+    for name, base in CASES.items():
+        cfg = base.replace(P=P)
+        obj = [fm.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rep = gen_replicated(cfg)
+        wks = [gen_worker(cfg, p) for p in range(P)]
+        # tiny S_p so the all-reduce is cut into many chunks incl. a remainder
+        g = run_block_gpu(cfg, rep, wks[rank], P=P, rank=rank, uid=obj[0], device=dev.index,
+                          chunk_bytes=4096 + 16)
+        ys, dxs, gflat, eg, st = oracle_block(cfg, rep, wks)
+        El = cfg.E // P
+        ref_e = expert_grads(eg, rank * El, (rank + 1) * El)
+        r = {"y": rel(g["y"], ys[rank]), "dx": rel(g["dx"], dxs[rank]),
+             "grad_flat": rel(g["grad_flat"], gflat)}
+        for n in ("dw1", "db1", "dw2", "db2"):
+            r[n] = rel(g[n], ref_e[n])
+        ro = st.route[rank]
+        r["routing_exact"] = bool(np.array_equal(g["idx"], ro.idx) and
+                                  np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1)) and
+                                  np.array_equal(g["counts"], ro.counts))
+        results[name] = r
+    out = [None] * P
+    dist.all_gather_object(out, results)
+    if rank == 0:
+        print("MP_RESULTS " + json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

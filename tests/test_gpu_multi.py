@@ -1,0 +1,36 @@
+"""Multi-GPU parity (P = 2 or 4 ranks, NCCL A2A + chunked AR) against the oracle's
+P simulated workers.  Needs >= 2 GPUs (gpurun --gpus 2|4)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = {"c1_f32": 1e-4, "bf16_p": 2e-2}
+
+
+def _ngpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_gpu_parity(P):
+    if _ngpus() < P:
+        pytest.skip(f"needs {P} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + P),
+           os.path.join(ROOT, "tests", "mp_parity_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("MP_RESULTS ")]
+    assert line, out.stdout[-3000:]
+    per_rank = json.loads(line[0][len("MP_RESULTS "):])
+    for rank, res in enumerate(per_rank):
+        for case, r in res.items():
+            assert r["routing_exact"], (rank, case)
+            bad = {k: v for k, v in r.items() if k != "routing_exact" and not v <= TOL[case]}
+            assert not bad, (rank, case, bad)
