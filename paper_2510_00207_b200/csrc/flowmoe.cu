@@ -311,6 +311,7 @@ flowmoe_status flowmoe_debug_set(int key, int value) {
   static int flags = 0;
   if (key == 1) flags = (flags & ~1) | (value ? 1 : 0);
   else if (key == 2) flags = (flags & ~2) | (value ? 2 : 0);
+  else if (key == 3) flags = (flags & ~4) | (value ? 4 : 0);
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   gemm_tc_set_debug(flags);
   return FLOWMOE_OK;

@@ -353,6 +353,7 @@ template <int DH> static int bwd_bf16(const void* a, const void* b, const float*
 
 int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H,
              int causal, cudaStream_t s) {
+  if (attn_tc_supported(dtype, M, H)) return attn_fwd_tc(qkv, ctx, lse, T_, N, M, H, causal, s);
   const int dh = M / H;
   if (dtype == DT_F32) { FM_DH_SWITCH(dh, fwd_f32, qkv, ctx, lse, T_, N, M, H, causal, s) }
   FM_DH_SWITCH(dh, fwd_bf16, qkv, ctx, lse, T_, N, M, H, causal, s)
@@ -360,6 +361,7 @@ int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T_, int N, i
 
 int attn_bwd(int dtype, const void* qkv, const void* ctx, const float* lse, const void* dctx,
              void* dqkv, float* D, int T_, int N, int M, int H, int causal, cudaStream_t s) {
+  if (attn_tc_supported(dtype, M, H)) return attn_bwd_tc(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
   const int dh = M / H;
   if (dtype == DT_F32) { FM_DH_SWITCH(dh, bwd_f32, qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s) }
   FM_DH_SWITCH(dh, bwd_bf16, qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s)

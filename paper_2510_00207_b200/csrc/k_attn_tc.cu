@@ -1,0 +1,629 @@
+// K6 on the 5th-generation tensor cores: flash attention forward and backward
+// (S2 AT-attn and its backward in B5) for bf16, d_h in {64, 128}.
+//
+// Math per sequence s and head h (P:75 MHA; reading Q7: scale 1/sqrt(d_h), optional
+// causal mask):  S = Q K^T * scale, P = softmax(S), ctx = P V, lse = log sum exp(S);
+// backward: D = rowsum(dO ⊙ O), P = exp(S - lse), dP = dO V^T, dS = P ⊙ (dP - D),
+// dV = P^T dO, dK = dS^T Q * scale, dQ = dS K * scale.
+//
+// Every product is a tcgen05.mma (cta_group::1, M = 128) with fp32 accumulators in
+// TMEM; Q/K/V/dO tiles arrive by TMA (boxes {64 cols, 128 rows}, 128-byte swizzle);
+// P, P^T and dS^T are written by the softmax warps straight into shared memory in
+// the UMMA K-major swizzled layout and consumed as the A operand of the next MMA.
+// The same smem tile of K (or V, Q, dO) serves as a K-major operand (contracting
+// over d) and as an MN-major operand (contracting over rows), so no transposes.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + single-thread
+// MMA issuer, warps 2..5 softmax / epilogue, one query (or key) row per thread.
+#include <cuda.h>
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace fm {
+
+constexpr int AT_THREADS = 192;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+// Operand built from TMA boxes of {64 cols, 128 rows} (16 KB each, SW128):
+// K-major (contract over the 64-col dim): k-step kk of 16 -> box kk/4, +32 B*(kk%4).
+FM_DEV uint64_t kdesc(uint32_t base, int kk) {
+  return umma_desc(base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+}
+// MN-major (contract over the 128 rows): k-step kk of 16 rows -> +2048 B; 64-col blocks 16 KB apart.
+FM_DEV uint64_t mdesc(uint32_t base, int kk) { return umma_desc(base + kk * 2048, 16384, 1024); }
+
+FM_DEV uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Write 32 fp32 values of row `row` (keys/queries c0..c0+31 of a 128-wide tile) as bf16
+// into a K-major SW128 tile made of two {64, 128} boxes.
+FM_DEV void st_row32_bf16(uint8_t* tile, int row, int c0, const float* v) {
+  uint8_t* box = tile + (c0 >> 6) * 16384 + row * 128;
+  const int cbase = (c0 & 63) >> 3;  // 16-byte chunk index of c0 within the 128-byte row
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 q;
+    q.x = pack_bf16x2(v[8 * j], v[8 * j + 1]);
+    q.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+    q.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+    q.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+    *reinterpret_cast<uint4*>(box + (((cbase + j) ^ (row & 7)) << 4)) = q;
+  }
+}
+
+FM_DEV void store_row_bf16(bf16* dst, const float* v, int n) {  // n multiple of 8
+#pragma unroll
+  for (int i = 0; i < 32; i += 8)
+    if (i < n) store16<bf16>(dst + i, v + i);
+}
+
+// ============================================================== forward
+// grid (ceil(N/128), H, n_seq_in_chunk); qkv map over the chunk [T_r][3M].
+template <int DH>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, bf16* ctx, float* lse, int N, int M,
+                       int H, int causal, float scale_log2) {
+  constexpr int NB = DH / 64;
+  constexpr uint32_t TILE = 128 * DH * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sK0 = smem + TILE;
+  uint8_t* sV0 = smem + 2 * TILE;
+  uint8_t* sK1 = smem + 3 * TILE;
+  uint8_t* sV1 = smem + 4 * TILE;
+  uint8_t* sP = smem + 5 * TILE;  // 32 KB: [2 boxes][128 q][64 keys]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 32768);
+  uint64_t* bar_q = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
+  const int q0 = qt * 128, row_base = sq * N;
+  int nkv = (N + 127) / 128;
+  if (causal) nkv = min(nkv, qt + 1);
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); mbar_init(&s_full[i], 1); }
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, TILE);
+      for (int i = 0; i < NB; ++i) tma_load_2d(sQ + i * 16384, &tq, bar_q, h * DH + 64 * i, row_base + q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        uint8_t* sK = st ? sK1 : sK0;
+        uint8_t* sV = st ? sV1 : sV0;
+        mbar_expect_tx(&kv_full[st], 2 * TILE);
+        for (int i = 0; i < NB; ++i) {
+          tma_load_2d(sK + i * 16384, &tq, &kv_full[st], M + h * DH + 64 * i, row_base + j * 128);
+          tma_load_2d(sV + i * 16384, &tq, &kv_full[st], 2 * M + h * DH + 64 * i, row_base + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+      constexpr uint32_t id_o = idesc_bf16(128, DH, 0, 1);   // P (K-major) x V (MN-major)
+      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+      mbar_wait(bar_q, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(st ? sK1 : sK0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tmem + st * 128, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+        tc_commit(&s_full[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const uint32_t aV = smem_u32((j & 1) ? sV1 : sV0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tO, kdesc(aP, kk), mdesc(aV, kk), id_o, (j > 0 || kk > 0));
+        tc_commit(o_done);
+        tc_commit(&kv_empty[j & 1]);
+      }
+    }
+  } else {
+    // ===== softmax warps: thread = query row
+    const int quarter = warp & 3;
+    const int rloc = quarter * 32 + lane;
+    const int qrow = q0 + rloc;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tS = tmem + lane_off + (j & 1) * 128;
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tS + c * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = j * 128 + c * 32 + i;
+          const bool ok = key < N && (!causal || key <= qrow);
+          if (ok) mx = fmaxf(mx, __uint_as_float(r[i]) * scale_log2);
+        }
+      }
+      const float m_new = fmaxf(m, mx);
+      const float corr = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+      const float msub = (m_new == -INFINITY) ? 0.f : m_new;
+      if (j > 0) {
+        mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O is stable and P smem is free
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tO + lane_off + c * 32, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st32(tO + lane_off + c * 32, r);
+          }
+        }
+      }
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tS + c * 32, r);
+        float p[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = j * 128 + c * 32 + i;
+          const bool ok = key < N && (!causal || key <= qrow);
+          p[i] = ok ? exp2f(__uint_as_float(r[i]) * scale_log2 - msub) : 0.f;
+          rs += p[i];
+        }
+        st_row32_bf16(sP, rloc, c * 32, p);
+      }
+      l = l * corr + rs;
+      m = m_new;
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_done, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    bf16* dst = ctx + (int64_t)(row_base + qrow) * M + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tO + lane_off + c * 32, r);
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
+      if (qrow < N) store_row_bf16(dst + c * 32, v, 32);
+    }
+    if (qrow < N) lse[(int64_t)(row_base + qrow) * H + h] = (m + log2f(l)) * LN2;
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ============================================================== backward: dK, dV
+// grid (ceil(N/128) key tiles, H, n_seq).  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
+template <int DH>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
+                            const float* lse, const float* Dv, bf16* dqkv, int N, int M, int H,
+                            int causal, float scale_log2, float scale) {
+  constexpr int NB = DH / 64;
+  constexpr uint32_t TILE = 128 * DH * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE;
+  uint8_t* sQ = smem + 2 * TILE;
+  uint8_t* sdO = smem + 3 * TILE;
+  uint8_t* sP = smem + 4 * TILE;      // P^T  [keys][queries], 32 KB
+  uint8_t* sdS = sP + 32768;          // dS^T [keys][queries], 32 KB
+  float* sL = reinterpret_cast<float*>(sdS + 32768);  // lse (log2 units) of the q tile
+  float* sD = sL + 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 128);
+  uint64_t* kv_bar = bars;
+  uint64_t* q_full = bars + 1;
+  uint64_t* q_empty = bars + 2;
+  uint64_t* s_full = bars + 3;
+  uint64_t* p_full = bars + 4;
+  uint64_t* mm_done = bars + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
+  const int k0 = kt * 128, row_base = sq * N;
+  const int nq_tiles = (N + 127) / 128;
+  const int qt0 = causal ? kt : 0;
+  const int niter = nq_tiles - qt0;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(kv_bar, 1);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(mm_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tST = tmem, tdPT = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_bar, 2 * TILE);
+      for (int i = 0; i < NB; ++i) {
+        tma_load_2d(sK + i * 16384, &tq, kv_bar, M + h * DH + 64 * i, row_base + k0);
+        tma_load_2d(sV + i * 16384, &tq, kv_bar, 2 * M + h * DH + 64 * i, row_base + k0);
+      }
+      for (int it = 0; it < niter; ++it) {
+        const int qr = row_base + (qt0 + it) * 128;
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
+        mbar_expect_tx(q_full, 2 * TILE);
+        for (int i = 0; i < NB; ++i) {
+          tma_load_2d(sQ + i * 16384, &tq, q_full, h * DH + 64 * i, qr);
+          tma_load_2d(sdO + i * 16384, &tdo, q_full, h * DH + 64 * i, qr);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
+      const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
+      mbar_wait(kv_bar, 0);
+      for (int it = 0; it < niter; ++it) {
+        mbar_wait(q_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tST, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdPT, kdesc(aV, kk), kdesc(adO, kk), id_s, kk > 0);
+        tc_commit(s_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdV, kdesc(aP, kk), mdesc(adO, kk), id_g, (it > 0 || kk > 0));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdK, kdesc(adS, kk), mdesc(aQ, kk), id_g, (it > 0 || kk > 0));
+        tc_commit(q_empty);
+        tc_commit(mm_done);
+      }
+    }
+  } else {
+    // ===== thread = key row
+    const int quarter = warp & 3;
+    const int kloc = quarter * 32 + lane;
+    const int key = k0 + kloc;
+    const int t128 = threadIdx.x - 64;  // 0..127
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    for (int it = 0; it < niter; ++it) {
+      const int qbase = (qt0 + it) * 128;
+      named_bar_sync(1, 128);  // everyone is done reading sL/sD of the previous tile
+      {
+        const int qi = qbase + t128;
+        sL[t128] = qi < N ? lse[(int64_t)(row_base + qi) * H + h] * LOG2E : 0.f;
+        sD[t128] = qi < N ? Dv[(int64_t)(row_base + qi) * H + h] : 0.f;
+      }
+      named_bar_sync(1, 128);
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      if (it > 0) {
+        mbar_wait(mm_done, (it - 1) & 1);  // previous dV/dK MMAs finished reading P^T, dS^T
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tST + lane_off + c * 32, rs);
+        tmem_ld32(tdPT + lane_off + c * 32, rp);
+        float p[32], ds[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int ql = c * 32 + i;
+          const int qi = qbase + ql;
+          const bool ok = qi < N && key < N && (!causal || key <= qi);
+          const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - sL[ql]) : 0.f;
+          p[i] = pv;
+          ds[i] = pv * (__uint_as_float(rp[i]) - sD[ql]);
+        }
+        st_row32_bf16(sP, kloc, c * 32, p);
+        st_row32_bf16(sdS, kloc, c * 32, ds);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(mm_done, (niter - 1) & 1);
+    tc_fence_after();
+    bf16* row = dqkv + (int64_t)(row_base + key) * 3 * M;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t r[32];
+      float v[32];
+      tmem_ld32(tdV + lane_off + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = niter > 0 ? __uint_as_float(r[i]) : 0.f;
+      if (key < N) store_row_bf16(row + 2 * M + h * DH + c * 32, v, 32);
+      tmem_ld32(tdK + lane_off + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = niter > 0 ? __uint_as_float(r[i]) * scale : 0.f;
+      if (key < N) store_row_bf16(row + M + h * DH + c * 32, v, 32);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ============================================================== backward: dQ
+// grid (ceil(N/128) query tiles, H, n_seq).  TMEM: S [0,128), dP [128,256), dQ [256, 256+DH).
+template <int DH, int STAGES>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
+                          const float* lse, const float* Dv, bf16* dqkv, int N, int M, int H,
+                          int causal, float scale_log2, float scale) {
+  constexpr int NB = DH / 64;
+  constexpr uint32_t TILE = 128 * DH * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + TILE;
+  uint8_t* sKV = smem + 2 * TILE;                  // STAGES x {K, V}
+  uint8_t* sdS = smem + (2 + 2 * STAGES) * TILE;   // 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 32768);
+  uint64_t* q_bar = bars;
+  uint64_t* kv_full = bars + 1;            // [STAGES]
+  uint64_t* kv_empty = bars + 1 + STAGES;  // [STAGES]
+  uint64_t* s_full = bars + 1 + 2 * STAGES;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* mm_done = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
+  const int q0 = qt * 128, row_base = sq * N;
+  int nkv = (N + 127) / 128;
+  if (causal) nkv = min(nkv, qt + 1);
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_bar, 1);
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(mm_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_bar, 2 * TILE);
+      for (int i = 0; i < NB; ++i) {
+        tma_load_2d(sQ + i * 16384, &tq, q_bar, h * DH + 64 * i, row_base + q0);
+        tma_load_2d(sdO + i * 16384, &tdo, q_bar, h * DH + 64 * i, row_base + q0);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % STAGES;
+        if (j >= STAGES) mbar_wait(&kv_empty[st], ((j / STAGES) - 1) & 1);
+        uint8_t* sK = sKV + st * 2 * TILE;
+        uint8_t* sV = sK + TILE;
+        mbar_expect_tx(&kv_full[st], 2 * TILE);
+        for (int i = 0; i < NB; ++i) {
+          tma_load_2d(sK + i * 16384, &tq, &kv_full[st], M + h * DH + 64 * i, row_base + j * 128);
+          tma_load_2d(sV + i * 16384, &tq, &kv_full[st], 2 * M + h * DH + 64 * i, row_base + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
+      const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), adS = smem_u32(sdS);
+      mbar_wait(q_bar, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_full[st], (j / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sKV + st * 2 * TILE), aV = aK + TILE;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tS, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdP, kdesc(adO, kk), kdesc(aV, kk), id_s, kk > 0);
+        tc_commit(s_full);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdQ, kdesc(adS, kk), mdesc(aK, kk), id_g, (j > 0 || kk > 0));
+        tc_commit(&kv_empty[st]);
+        tc_commit(mm_done);
+      }
+    }
+  } else {
+    // ===== thread = query row
+    const int quarter = warp & 3;
+    const int rloc = quarter * 32 + lane;
+    const int qrow = q0 + rloc;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float L2 = qrow < N ? lse[(int64_t)(row_base + qrow) * H + h] * LOG2E : 0.f;
+    const float Dq = qrow < N ? Dv[(int64_t)(row_base + qrow) * H + h] : 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      if (j > 0) {
+        mbar_wait(mm_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tS + lane_off + c * 32, rs);
+        tmem_ld32(tdP + lane_off + c * 32, rp);
+        float ds[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int kj = j * 128 + c * 32 + i;
+          const bool ok = qrow < N && kj < N && (!causal || kj <= qrow);
+          const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - L2) : 0.f;
+          ds[i] = pv * (__uint_as_float(rp[i]) - Dq);
+        }
+        st_row32_bf16(sdS, rloc, c * 32, ds);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(mm_done, (nkv - 1) & 1);
+    tc_fence_after();
+    bf16* row = dqkv + (int64_t)(row_base + qrow) * 3 * M + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t r[32];
+      float v[32];
+      tmem_ld32(tdQ + lane_off + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * scale;
+      if (qrow < N) store_row_bf16(row + c * 32, v, 32);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]: one warp per token, lanes over heads' columns
+__global__ void attn_bwd_pre_tc_kernel(const bf16* ctx, const bf16* dctx, float* D, int T_, int M,
+                                       int H) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= T_) return;
+  const int dh = M / H;
+  const bf16* o = ctx + (int64_t)t * M;
+  const bf16* g = dctx + (int64_t)t * M;
+  // each lane handles 8 consecutive columns per step; heads are dh-aligned (dh % 8 == 0)
+  for (int h0 = 0; h0 < H; h0 += 1) {
+    float acc = 0.f;
+    for (int c = lane * 8; c < dh; c += 256) {
+      float a[8], b[8];
+      load16<bf16>(o + h0 * dh + c, a);
+      load16<bf16>(g + h0 * dh + c, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(a[i], b[i], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) D[(int64_t)t * H + h0] = acc;
+  }
+}
+
+// ------------------------------------------------------------ host
+template <int DH>
+static size_t fwd_smem() { return 5 * 128 * DH * 2 + 32768 + 1024 + 256; }
+template <int DH>
+static size_t dkdv_smem() { return 4 * 128 * DH * 2 + 65536 + 1024 + 1024 + 256; }
+template <int DH, int ST>
+static size_t dq_smem() { return (2 + 2 * ST) * 128 * DH * 2 + 32768 + 1024 + 256; }
+
+template <int DH>
+static int attn_fwd_tc_t(const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H, int causal,
+                         cudaStream_t s) {
+  CUtensorMap tq;
+  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
+  auto k = attn_fwd_tc_kernel<DH>;
+  const size_t smem = fwd_smem<DH>();
+  static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
+  dim3 grid((N + 127) / 128, H, T_ / N);
+  k<<<grid, AT_THREADS, smem, s>>>(tq, (bf16*)ctx, lse, N, M, H, causal, LOG2E / sqrtf((float)DH));
+  return (int)cudaGetLastError();
+}
+
+template <int DH>
+static int attn_bwd_tc_t(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv,
+                         float* D, int T_, int N, int M, int H, int causal, cudaStream_t s) {
+  CUtensorMap tq, tdo;
+  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
+  if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, T_, M, 64, 128)) return rc;
+  attn_bwd_pre_tc_kernel<<<(T_ * 32 + 255) / 256, 256, 0, s>>>((const bf16*)ctx, (const bf16*)dctx, D, T_, M, H);
+  const float scale = 1.0f / sqrtf((float)DH), sl2 = LOG2E * scale;
+  dim3 grid((N + 127) / 128, H, T_ / N);
+  auto k1 = attn_bwd_dkdv_tc_kernel<DH>;
+  const size_t sm1 = dkdv_smem<DH>();
+  static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1), true);
+  (void)once1;
+  k1<<<grid, AT_THREADS, sm1, s>>>(tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  constexpr int ST = DH == 128 ? 1 : 2;
+  auto k2 = attn_bwd_dq_tc_kernel<DH, ST>;
+  const size_t sm2 = dq_smem<DH, ST>();
+  static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2), true);
+  (void)once2;
+  k2<<<grid, AT_THREADS, sm2, s>>>(tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  return (int)cudaGetLastError();
+}
+
+bool attn_tc_supported(int dtype, int M, int H) {
+  const int dh = M / H;
+  return dtype == DT_BF16 && (dh == 64 || dh == 128) && !(attn_tc_debug_off());
+}
+
+int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H, int causal,
+                cudaStream_t s) {
+  if (M / H == 64) return attn_fwd_tc_t<64>(qkv, ctx, lse, T_, N, M, H, causal, s);
+  return attn_fwd_tc_t<128>(qkv, ctx, lse, T_, N, M, H, causal, s);
+}
+
+int attn_bwd_tc(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv, float* D,
+                int T_, int N, int M, int H, int causal, cudaStream_t s) {
+  if (M / H == 64) return attn_bwd_tc_t<64>(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
+  return attn_bwd_tc_t<128>(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
+}
+
+}  // namespace fm

@@ -25,6 +25,7 @@ namespace fm {
 constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 192;
 static int g_tc_debug = 0;  // bit0: force SIMT for bf16; bit1: swap LBO/SBO of MN-major descs
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
+int attn_tc_debug_off() { return g_tc_debug & 4; }  // bit2: force the SIMT attention kernels
 
 // ------------------------------------------------------------ kernel
 struct TcArgs {

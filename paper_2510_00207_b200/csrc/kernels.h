@@ -49,6 +49,14 @@ int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T, int N, in
 int attn_bwd(int dtype, const void* qkv, const void* ctx, const float* lse, const void* dctx,
              void* dqkv, float* Dbuf, int T, int N, int M, int H, int causal, cudaStream_t s);
 
+// tcgen05 flash attention (bf16, d_h in {64,128}); attn_fwd/attn_bwd dispatch to these.
+bool attn_tc_supported(int dtype, int M, int H);
+int attn_tc_debug_off();
+int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int T, int N, int M, int H, int causal,
+                cudaStream_t s);
+int attn_bwd_tc(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv,
+                float* D, int T, int N, int M, int H, int causal, cudaStream_t s);
+
 // ---------------------------------------------------------------- routing / data movement
 // K1: logits = a·Wg (fp32), top-k (ties -> lower index), gate weights.
 int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,

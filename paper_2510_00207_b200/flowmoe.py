@@ -92,6 +92,8 @@ def lib() -> ctypes.CDLL:
     _lib = L
     if os.environ.get("FLOWMOE_DEBUG_SIMT"):  # debug knob: route bf16 GEMMs to the SIMT kernel
         L.flowmoe_debug_set(1, 1)
+    if os.environ.get("FLOWMOE_DEBUG_SIMT_ATTN"):  # debug knob: SIMT attention for bf16
+        L.flowmoe_debug_set(3, 1)
     if os.environ.get("FLOWMOE_DEBUG_SWAP"):  # debug knob: swap MN-major descriptor strides
         L.flowmoe_debug_set(2, 1)
     return L

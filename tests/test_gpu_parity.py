@@ -28,6 +28,16 @@ CASES = {
                                  R=2, capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
     # configs[1]: the bench workload (GPT2-Tiny-MoE-shaped, R=4), full size
     "c2_bench": PRESETS["c2"],
+    # long sequences: several 128-row attention tiles, causal diagonal tiles, d_h 128 / 64
+    "bf16_long_causal_dh128": BlockConfig(T=1024, seq_len=512, M=256, n_heads=2, E=4, top_k=2,
+                                          d_ffn=256, R=2, capacity_factor=1.0, causal=1, residual=1,
+                                          P=1, dtype="bf16"),
+    "bf16_long_dh64_ragged": BlockConfig(T=768, seq_len=384, M=256, n_heads=4, E=4, top_k=2,
+                                         d_ffn=256, R=2, capacity_factor=1.0, causal=0, residual=0,
+                                         P=1, dtype="bf16"),
+    "bf16_ragged_seq_causal": BlockConfig(T=400, seq_len=200, M=128, n_heads=2, E=4, top_k=2,
+                                          d_ffn=256, R=2, capacity_factor=1.0, causal=1, residual=1,
+                                          P=1, dtype="bf16"),
 }
 
 
