@@ -42,7 +42,7 @@ CONFIG_NAMES = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="flowmoe", choices=["flowmoe", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(LAYERS))
@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -332,8 +332,9 @@ def main():
         top = max(compute, key=lambda p: p["ms"])
         total_ms = sum(p["ms"] for p in compute)
         avg_ms = top["ms"] / top["launches"]
-        if top["name"].startswith("gemm"):
-            bound, unit = "tensor", "TFLOP/s"
+        tc_attn = cfg.dtype == "bf16" and (cfg.M // cfg.n_heads) in (64, 128)
+        if top["name"].startswith("gemm") or (top["name"].startswith("attn") and tc_attn):
+            bound, unit = "tensor", "TFLOP/s"   # tcgen05 kernels (GEMM, flash attention)
             achieved = top["flops"] / top["launches"] / (avg_ms * 1e-3) / 1e12
             peak = peaks["bf16_tflops_sustained"]
         elif top["name"].startswith("attn"):

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <utility>
 
 #define FM_DEV __device__ __forceinline__
 
@@ -72,6 +73,39 @@ FM_DEV float gelu_f(float z) { return 0.5f * z * (1.0f + erff(z * 0.707106781186
 FM_DEV float gelu_grad_f(float z) {
   return 0.5f * (1.0f + erff(z * 0.70710678118654752f)) +
          z * __expf(-0.5f * z * z) * 0.39894228040143268f;
+}
+
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel is launched with programmatic stream serialization, so it may be
+// scheduled while its predecessor on the stream is still running.  Each kernel
+// therefore calls griddep_wait() before its first global-memory access (after its
+// smem/TMEM/barrier prologue in the tensor-core kernels), which blocks until the
+// predecessor grid has completed and flushed; it then calls griddep_launch() so
+// the successor's prologue can overlap this kernel's body.
+FM_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FM_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+#define FM_PDL_ENTRY() \
+  do {                 \
+    fm::griddep_wait();  \
+    fm::griddep_launch(); \
+  } while (0)
+
+extern int g_pdl_enabled;  // flowmoe_debug_set(4, 0) turns PDL off (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl_enabled;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 }  // namespace fm

@@ -24,6 +24,10 @@
 
 using namespace fm;
 
+namespace fm {
+int g_pdl_enabled = 1;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -312,6 +316,7 @@ flowmoe_status flowmoe_debug_set(int key, int value) {
   if (key == 1) flags = (flags & ~1) | (value ? 1 : 0);
   else if (key == 2) flags = (flags & ~2) | (value ? 2 : 0);
   else if (key == 3) flags = (flags & ~4) | (value ? 4 : 0);
+  else if (key == 4) { g_pdl_enabled = value ? 1 : 0; return FLOWMOE_OK; }
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   gemm_tc_set_debug(flags);
   return FLOWMOE_OK;

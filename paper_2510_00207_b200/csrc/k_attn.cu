@@ -36,6 +36,7 @@ __device__ void load_tile(float* dst, const T* src, int64_t ld, int row0, int nr
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, float* lse, int N,
                                                        int M, int H, int causal, float scale) {
+  FM_PDL_ENTRY();
   extern __shared__ float sm[];
   float* Qs = sm;
   float* Ks = Qs + AB * (DH + 1);
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, flo
 // D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]
 template <typename T>
 __global__ void attn_bwd_pre_kernel(const T* ctx, const T* dctx, float* D, int T_, int M, int H) {
+  FM_PDL_ENTRY();
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (int64_t)T_ * H) return;
   const int t = id / H, h = id % H, dh = M / H;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const 
                                                             const float* lse, const float* D,
                                                             T* dqkv, int N, int M, int H,
                                                             int causal, float scale) {
+  FM_PDL_ENTRY();
   extern __shared__ float sm[];
   float* Ks = sm;
   float* Vs = Ks + AB * (DH + 1);
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T*
                                                           const float* lse, const float* D,
                                                           T* dqkv, int N, int M, int H,
                                                           int causal, float scale) {
+  FM_PDL_ENTRY();
   extern __shared__ float sm[];
   float* Qs = sm;
   float* dOs = Qs + AB * (DH + 1);
@@ -310,7 +314,7 @@ static int attn_fwd_t(const void* qkv, void* ctx, float* lse, int T_, int N, int
   static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)once;
   dim3 grid((N + AB - 1) / AB, H, T_ / N);
-  k<<<grid, 256, smem, s>>>((const T*)qkv, (T*)ctx, lse, N, M, H, causal, 1.0f / sqrtf((float)DH));
+  launch_k(k, grid, 256, smem, s, (const T*)qkv, (T*)ctx, lse, N, M, H, causal, 1.0f / sqrtf((float)DH));
   return (int)cudaGetLastError();
 }
 
@@ -319,20 +323,20 @@ static int attn_bwd_t(const void* qkv, const void* ctx, const float* lse, const 
                       void* dqkv, float* D, int T_, int N, int M, int H, int causal,
                       cudaStream_t s) {
   const float scale = 1.0f / sqrtf((float)DH);
-  attn_bwd_pre_kernel<T><<<(T_ * H + 255) / 256, 256, 0, s>>>((const T*)ctx, (const T*)dctx, D,
+  launch_k(attn_bwd_pre_kernel<T>, (T_ * H + 255) / 256, 256, 0, s, (const T*)ctx, (const T*)dctx, D,
                                                               T_, M, H);
   dim3 grid((N + AB - 1) / AB, H, T_ / N);
   size_t smem1 = (4 * AB * (DH + 1) + 2 * AB * (AB + 1) + 2 * AB) * sizeof(float);
   auto k1 = attn_bwd_dkdv_kernel<T, DH>;
   static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), true);
   (void)once1;
-  k1<<<grid, 256, smem1, s>>>((const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
+  launch_k(k1, grid, 256, smem1, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
                               scale);
   size_t smem2 = (4 * AB * (DH + 1) + AB * (AB + 1)) * sizeof(float);
   auto k2 = attn_bwd_dq_kernel<T, DH>;
   static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), true);
   (void)once2;
-  k2<<<grid, 256, smem2, s>>>((const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
+  launch_k(k2, grid, 256, smem2, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
                               scale);
   return (int)cudaGetLastError();
 }

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  FM_PDL_ENTRY();
   const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  FM_PDL_ENTRY();
   const uint32_t tST = tmem, tdPT = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
 
   if (warp == 0) {
@@ -440,6 +442,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  FM_PDL_ENTRY();
   const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
 
   if (warp == 0) {
@@ -541,26 +544,27 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
 }
 
-// D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]: one warp per token, lanes over heads' columns
+// D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]: one warp per token, 16-byte loads;
+// lane groups of dh/8 lanes reduce one head each (segmented shuffle reduction).
 __global__ void attn_bwd_pre_tc_kernel(const bf16* ctx, const bf16* dctx, float* D, int T_, int M,
                                        int H) {
+  FM_PDL_ENTRY();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T_) return;
-  const int dh = M / H;
+  const int dh = M / H, G = dh / 8;  // lanes per head (8 or 16)
   const bf16* o = ctx + (int64_t)t * M;
   const bf16* g = dctx + (int64_t)t * M;
-  // each lane handles 8 consecutive columns per step; heads are dh-aligned (dh % 8 == 0)
-  for (int h0 = 0; h0 < H; h0 += 1) {
+  for (int m0 = lane * 8; m0 - lane * 8 < M; m0 += 256) {
     float acc = 0.f;
-    for (int c = lane * 8; c < dh; c += 256) {
+    if (m0 < M) {
       float a[8], b[8];
-      load16<bf16>(o + h0 * dh + c, a);
-      load16<bf16>(g + h0 * dh + c, b);
+      load16<bf16>(o + m0, a);
+      load16<bf16>(g + m0, b);
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc = fmaf(a[i], b[i], acc);
     }
-    acc = warp_sum(acc);
-    if (lane == 0) D[(int64_t)t * H + h0] = acc;
+    for (int off = 1; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (m0 < M && (lane % G) == 0) D[(int64_t)t * H + m0 / dh] = acc;
   }
 }
 
@@ -582,7 +586,7 @@ static int attn_fwd_tc_t(const void* qkv, void* ctx, float* lse, int T_, int N, 
   static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)once;
   dim3 grid((N + 127) / 128, H, T_ / N);
-  k<<<grid, AT_THREADS, smem, s>>>(tq, (bf16*)ctx, lse, N, M, H, causal, LOG2E / sqrtf((float)DH));
+  launch_k(k, grid, AT_THREADS, smem, s, tq, (bf16*)ctx, lse, N, M, H, causal, LOG2E / sqrtf((float)DH));
   return (int)cudaGetLastError();
 }
 
@@ -592,20 +596,20 @@ static int attn_bwd_tc_t(const void* qkv, const void* ctx, const float* lse, con
   CUtensorMap tq, tdo;
   if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
   if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, T_, M, 64, 128)) return rc;
-  attn_bwd_pre_tc_kernel<<<(T_ * 32 + 255) / 256, 256, 0, s>>>((const bf16*)ctx, (const bf16*)dctx, D, T_, M, H);
+  launch_k(attn_bwd_pre_tc_kernel, (T_ * 32 + 255) / 256, 256, 0, s, (const bf16*)ctx, (const bf16*)dctx, D, T_, M, H);
   const float scale = 1.0f / sqrtf((float)DH), sl2 = LOG2E * scale;
   dim3 grid((N + 127) / 128, H, T_ / N);
   auto k1 = attn_bwd_dkdv_tc_kernel<DH>;
   const size_t sm1 = dkdv_smem<DH>();
   static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1), true);
   (void)once1;
-  k1<<<grid, AT_THREADS, sm1, s>>>(tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
   constexpr int ST = DH == 128 ? 1 : 2;
   auto k2 = attn_bwd_dq_tc_kernel<DH, ST>;
   const size_t sm2 = dq_smem<DH, ST>();
   static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2), true);
   (void)once2;
-  k2<<<grid, AT_THREADS, sm2, s>>>(tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
   return (int)cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@ constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+  FM_PDL_ENTRY();
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const int b = blockIdx.z;
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 int gemm_simt(const GemmArgs& g, int dtype, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return 0;
   dim3 grid((g.N + SB_N - 1) / SB_N, (g.M + SB_M - 1) / SB_M, g.batch);
-  if (dtype == DT_F32) gemm_simt_kernel<float><<<grid, 256, 0, s>>>(g);
-  else gemm_simt_kernel<bf16><<<grid, 256, 0, s>>>(g);
+  if (dtype == DT_F32) launch_k(gemm_simt_kernel<float>, grid, 256, 0, s, g);
+  else launch_k(gemm_simt_kernel<bf16>, grid, 256, 0, s, g);
   return (int)cudaGetLastError();
 }
 

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  FM_PDL_ENTRY();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -310,7 +311,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)attr_set;
   dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, g.batch);
-  kern<<<grid, TC_THREADS, smem, s>>>(ma, mb, mc, maux, p);
+  launch_k(kern, grid, TC_THREADS, smem, s, ma, mb, mc, maux, p);
   return (int)cudaGetLastError();
 }
 

@@ -16,6 +16,19 @@
 
 namespace fm {
 
+// E contiguous storage elements -> fp32 (16-byte vector loads when the row allows)
+template <typename T, int E>
+FM_DEV void load_row(const T* p, float* out) {
+  constexpr int V = 16 / sizeof(T);
+  if constexpr (E % V == 0) {
+#pragma unroll
+    for (int i = 0; i < E; i += V) load16<T>(p + i, out + i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) out[i] = to_f<T>(p[i]);
+  }
+}
+
 // ------------------------------------------------------------------ K1
 // One warp per token.  Lane l owns row elements [8l + 256i, 8l + 256i + 8) (bf16)
 // or [4l + 128i, ...) (f32) and keeps E partial dot products; xor-reduce gives
@@ -26,6 +39,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
                                                         const int32_t* forced, float* logits,
                                                         int32_t* idx, float* w, int T_, int M,
                                                         int k) {
+  FM_PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= T_) return;
   constexpr int V = 16 / sizeof(T);
@@ -38,9 +52,10 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
     load16<T>(row + m0, x);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const T* wr = wg + (int64_t)(m0 + i) * E;
+      float wr[E];
+      load_row<T, E>(wg + (int64_t)(m0 + i) * E, wr);
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = fmaf(x[i], to_f<T>(wr[e]), acc[e]);
+      for (int e = 0; e < E; ++e) acc[e] = fmaf(x[i], wr[e], acc[e]);
     }
   }
 #pragma unroll
@@ -108,10 +123,10 @@ static void gate_topk_launch(int dtype, const void* a, const void* wg, const int
                              cudaStream_t s) {
   dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
-    gate_topk_kernel<float, E><<<grid, 256, 0, s>>>((const float*)a, (const float*)wg, forced,
+    launch_k(gate_topk_kernel<float, E>, grid, 256, 0, s, (const float*)a, (const float*)wg, forced,
                                                    logits, idx, w, T_, M, k);
   else
-    gate_topk_kernel<bf16, E><<<grid, 256, 0, s>>>((const bf16*)a, (const bf16*)wg, forced,
+    launch_k(gate_topk_kernel<bf16, E>, grid, 256, 0, s, (const bf16*)a, (const bf16*)wg, forced,
                                                   logits, idx, w, T_, M, k);
 }
 
@@ -158,6 +173,7 @@ __device__ int block_excl_scan(int v, int* warp_tot) {
 __global__ void __launch_bounds__(RS_THREADS) route_scan_kernel(const int32_t* idx, int32_t* pos,
                                                                 int32_t* counts, int32_t* src,
                                                                 int T_, int E, int k, int C) {
+  FM_PDL_ENTRY();
   extern __shared__ int hist[];  // [E][RS_THREADS]
   __shared__ int warp_tot[32];
   const int tid = threadIdx.x;
@@ -194,7 +210,7 @@ int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, 
   static bool once = (cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            64 * RS_THREADS * (int)sizeof(int)), true);
   (void)once;
-  route_scan_kernel<<<1, RS_THREADS, smem, s>>>(idx, pos, counts, src, T_, E, k, C);
+  launch_k(route_scan_kernel, 1, RS_THREADS, smem, s, idx, pos, counts, src, T_, E, k, C);
   return (int)cudaGetLastError();
 }
 
@@ -203,6 +219,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) permute_pack_kernel(const T* a, const int32_t* src,
                                                            T* send, int rows, int C, int ldE,
                                                            int M, int k) {
+  FM_PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const int sl = src[warp];
@@ -224,9 +241,9 @@ int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E
   if (rows <= 0) return 0;
   dim3 grid((rows * 32 + 255) / 256);
   if (dtype == DT_F32)
-    permute_pack_kernel<float><<<grid, 256, 0, s>>>((const float*)a, src, (float*)send, rows, C, ldE, M, k);
+    launch_k(permute_pack_kernel<float>, grid, 256, 0, s, (const float*)a, src, (float*)send, rows, C, ldE, M, k);
   else
-    permute_pack_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)a, src, (bf16*)send, rows, C, ldE, M, k);
+    launch_k(permute_pack_kernel<bf16>, grid, 256, 0, s, (const bf16*)a, src, (bf16*)send, rows, C, ldE, M, k);
   return (int)cudaGetLastError();
 }
 
@@ -236,6 +253,7 @@ __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, cons
                                                                 const int32_t* pos, const float* w,
                                                                 const T* resid, T* out, int T_,
                                                                 int M, int k, int ldE) {
+  FM_PDL_ENTRY();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T_) return;
   constexpr int V = 16 / sizeof(T);
@@ -274,10 +292,10 @@ int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_
   if (T_ <= 0) return 0;
   dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
-    unpermute_combine_kernel<float><<<grid, 256, 0, s>>>((const float*)y, idx, pos, w,
+    launch_k(unpermute_combine_kernel<float>, grid, 256, 0, s, (const float*)y, idx, pos, w,
                                                         (const float*)resid, (float*)out, T_, M, k, ldE);
   else
-    unpermute_combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)y, idx, pos, w,
+    launch_k(unpermute_combine_kernel<bf16>, grid, 256, 0, s, (const bf16*)y, idx, pos, w,
                                                        (const bf16*)resid, (bf16*)out, T_, M, k, ldE);
   return (int)cudaGetLastError();
 }
@@ -291,6 +309,7 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
                                                                const int32_t* src, T* dy,
                                                                float* dw, int T_, int M, int k,
                                                                int rows, int C, int ldE) {
+  FM_PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   constexpr int V = 16 / sizeof(T);
   if (warp >= T_) {
@@ -330,10 +349,10 @@ int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* 
   const int rows = E * C;
   dim3 grid(((T_ + rows) * 32 + 255) / 256);
   if (dtype == DT_F32)
-    combine_bwd_pack_kernel<float><<<grid, 256, 0, s>>>((const float*)dout, (const float*)y, idx,
+    launch_k(combine_bwd_pack_kernel<float>, grid, 256, 0, s, (const float*)dout, (const float*)y, idx,
                                                        pos, w, src, (float*)dy, dw, T_, M, k, rows, C, ldE);
   else
-    combine_bwd_pack_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dout, (const bf16*)y, idx,
+    launch_k(combine_bwd_pack_kernel<bf16>, grid, 256, 0, s, (const bf16*)dout, (const bf16*)y, idx,
                                                       pos, w, src, (bf16*)dy, dw, T_, M, k, rows, C, ldE);
   return (int)cudaGetLastError();
 }
@@ -344,6 +363,7 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
     const T* dx, const int32_t* idx, const int32_t* pos, const float* w, const float* dw,
     const float* logits, const T* wg, const T* dres, T* dA, float* dlogits, int T_, int M, int k,
     int ldE) {
+  FM_PDL_ENTRY();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T_) return;
   constexpr int V = 16 / sizeof(T);
@@ -399,10 +419,11 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
     }
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const T* wr = wg + (int64_t)(m0 + i) * E;
+      float wr[E];
+      load_row<T, E>(wg + (int64_t)(m0 + i) * E, wr);
       float s = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) s = fmaf(dl[e], to_f<T>(wr[e]), s);
+      for (int e = 0; e < E; ++e) s = fmaf(dl[e], wr[e], s);
       acc[i] += s;
     }
     if (dres) {
@@ -422,11 +443,11 @@ static void gather_gate_bwd_launch(int dtype, const void* dx, const int32_t* idx
                                    float* dlogits, int T_, int M, int k, int ldE, cudaStream_t s) {
   dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
-    gather_gate_bwd_kernel<float, E><<<grid, 256, 0, s>>>(
+    launch_k(gather_gate_bwd_kernel<float, E>, grid, 256, 0, s, 
         (const float*)dx, idx, pos, w, dw, logits, (const float*)wg, (const float*)dres,
         (float*)dA, dlogits, T_, M, k, ldE);
   else
-    gather_gate_bwd_kernel<bf16, E><<<grid, 256, 0, s>>>(
+    launch_k(gather_gate_bwd_kernel<bf16, E>, grid, 256, 0, s, 
         (const bf16*)dx, idx, pos, w, dw, logits, (const bf16*)wg, (const bf16*)dres, (bf16*)dA,
         dlogits, T_, M, k, ldE);
 }
@@ -448,6 +469,7 @@ constexpr int GW_SPLIT_T = 128;
 template <typename T, int E>
 __global__ void __launch_bounds__(128) gate_wgrad_part_kernel(const T* a, const float* dl,
                                                               float* part, int T_, int M) {
+  FM_PDL_ENTRY();
   __shared__ float dls[GW_SPLIT_T][E];
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   const int t0 = blockIdx.y * GW_SPLIT_T;
@@ -469,6 +491,7 @@ __global__ void __launch_bounds__(128) gate_wgrad_part_kernel(const T* a, const 
 }
 
 __global__ void gate_wgrad_reduce_kernel(const float* part, float* dwg, int nsplit, int n) {
+  FM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s = 0.f;
@@ -485,9 +508,9 @@ static void gate_wgrad_launch(int dtype, const void* a, const float* dl, float* 
                               int M, cudaStream_t s) {
   dim3 grid((M + 127) / 128, (T_ + GW_SPLIT_T - 1) / GW_SPLIT_T);
   if (dtype == DT_F32)
-    gate_wgrad_part_kernel<float, E><<<grid, 128, 0, s>>>((const float*)a, dl, part, T_, M);
+    launch_k(gate_wgrad_part_kernel<float, E>, grid, 128, 0, s, (const float*)a, dl, part, T_, M);
   else
-    gate_wgrad_part_kernel<bf16, E><<<grid, 128, 0, s>>>((const bf16*)a, dl, part, T_, M);
+    launch_k(gate_wgrad_part_kernel<bf16, E>, grid, 128, 0, s, (const bf16*)a, dl, part, T_, M);
 }
 
 int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T_,
@@ -495,13 +518,14 @@ int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float
   if (T_ <= 0) return 0;
   FM_E_SWITCH(E, gate_wgrad_launch, dtype, a, dlogits, part, T_, M, s)
   const int nsplit = (T_ + GW_SPLIT_T - 1) / GW_SPLIT_T;
-  gate_wgrad_reduce_kernel<<<(M * E + 255) / 256, 256, 0, s>>>(part, dwg, nsplit, M * E);
+  launch_k(gate_wgrad_reduce_kernel, (M * E + 255) / 256, 256, 0, s, part, dwg, nsplit, M * E);
   return (int)cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ bias grads
 template <typename T>
 __global__ void colsum_acc_kernel(const T* x, float* out, int rows, int N) {
+  FM_PDL_ENTRY();
   const int n = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
   if (n >= N) return;
   const T* xb = x + (int64_t)b * rows * N;
@@ -512,8 +536,8 @@ __global__ void colsum_acc_kernel(const T* x, float* out, int rows, int N) {
 
 int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, cudaStream_t s) {
   dim3 grid((N + 255) / 256, batch);
-  if (dtype == DT_F32) colsum_acc_kernel<float><<<grid, 256, 0, s>>>((const float*)x, out, rows, N);
-  else colsum_acc_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)x, out, rows, N);
+  if (dtype == DT_F32) launch_k(colsum_acc_kernel<float>, grid, 256, 0, s, (const float*)x, out, rows, N);
+  else launch_k(colsum_acc_kernel<bf16>, grid, 256, 0, s, (const bf16*)x, out, rows, N);
   return (int)cudaGetLastError();
 }
 

@@ -94,6 +94,8 @@ def lib() -> ctypes.CDLL:
         L.flowmoe_debug_set(1, 1)
     if os.environ.get("FLOWMOE_DEBUG_SIMT_ATTN"):  # debug knob: SIMT attention for bf16
         L.flowmoe_debug_set(3, 1)
+    if os.environ.get("FLOWMOE_NO_PDL"):  # A/B knob: plain stream-ordered launches
+        L.flowmoe_debug_set(4, 0)
     if os.environ.get("FLOWMOE_DEBUG_SWAP"):  # debug knob: swap MN-major descriptor strides
         L.flowmoe_debug_set(2, 1)
     return L
