@@ -49,6 +49,11 @@ typedef enum {
 
 typedef enum { FLOWMOE_F32 = 0, FLOWMOE_BF16 = 1 } flowmoe_dtype;
 
+/* How flowmoe_block_bwd writes weight gradients: ACCUMULATE adds into the
+ * buffers (gradient accumulation across backward calls), OVERWRITE stores them
+ * (the buffers need no zeroing; like zero_grad(set_to_none) + backward). */
+typedef enum { FLOWMOE_GRAD_ACCUMULATE = 0, FLOWMOE_GRAD_OVERWRITE = 1 } flowmoe_grad_mode;
+
 typedef struct {
   int64_t B;               /* tokens on this rank (paper B·N); B % seq_len == 0; (B/seq_len) % R == 0 */
   int32_t seq_len;         /* N, tokens per sequence (attention span) */
@@ -64,6 +69,7 @@ typedef struct {
   int32_t dtype;           /* flowmoe_dtype */
   int32_t world_size;      /* P */
   int32_t rank;            /* p; experts [p·E/P, (p+1)·E/P) are local (reading Q12) */
+  int32_t grad_mode;       /* flowmoe_grad_mode */
 } flowmoe_config;
 
 /* Weights of one block (dtype of the config).  Replicated: wqkv [M][3M] (columns
@@ -73,9 +79,10 @@ typedef struct {
   const void *wqkv, *wo, *wg, *w1, *b1, *w2, *b2;
 } flowmoe_params;
 
-/* Gradients, fp32, ACCUMULATED (+=).  grad_flat = [dWqkv (M×3M) | dWo (M×M) |
- * dWg (M×E)], 4M²+M·E floats, all-reduced (sum over ranks) by the AR that
- * flowmoe_block_bwd submits; zero it before an iteration for a plain sum.
+/* Gradients, fp32, accumulated (+=) or overwritten per config.grad_mode.
+ * grad_flat = [dWqkv (M×3M) | dWo (M×M) | dWg (M×E)], 4M²+M·E floats,
+ * all-reduced (sum over ranks) by the AR that flowmoe_block_bwd submits (in
+ * ACCUMULATE mode the previous contents are summed over ranks too).
  * dw1 [E/P][M][F], db1 [E/P][F], dw2 [E/P][F][M], db2 [E/P][M] are the local
  * experts' grads summed over all source ranks (no AR: experts are sharded). */
 typedef struct {

@@ -144,7 +144,8 @@ flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStre
   const double b = g.batch;
   const double flops = 2.0 * g.M * g.N * (double)g.K * b;
   double bytes = ((double)g.M * g.K + (double)g.K * g.N) * es * b;
-  bytes += g.epi == EPI_ACC_F32 ? 8.0 * g.M * g.N * b : (double)g.M * g.N * es * b;
+  bytes += g.epi == EPI_ACC_F32 ? 8.0 * g.M * g.N * b
+                                 : (double)g.M * g.N * (g.epi == EPI_STORE_F32 ? 4 : es) * b;
   if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) bytes += (double)g.M * g.N * es * b;
   if (g.resid) bytes += (double)g.M * g.N * es * b;
   FM_KP(kind, 1, flops, bytes, s, gemm(g, dt, s));
@@ -178,6 +179,8 @@ flowmoe_status validate(const flowmoe_config* c) {
   if (c->causal != 0 && c->causal != 1) return bad("causal", "must be 0 or 1");
   if (c->residual != 0 && c->residual != 1) return bad("residual", "must be 0 or 1");
   if (c->dtype != FLOWMOE_F32 && c->dtype != FLOWMOE_BF16) return bad("dtype", "must be FLOWMOE_F32 or FLOWMOE_BF16");
+  if (c->grad_mode != FLOWMOE_GRAD_ACCUMULATE && c->grad_mode != FLOWMOE_GRAD_OVERWRITE)
+    return bad("grad_mode", "must be FLOWMOE_GRAD_ACCUMULATE or FLOWMOE_GRAD_OVERWRITE");
   if (c->world_size < 1) return bad("world_size", "must be >= 1");
   if (c->rank < 0 || c->rank >= c->world_size) return bad("rank", "must be in [0, world_size)");
   if (c->E % c->world_size) return bad("E", "must be a multiple of world_size (experts sharded evenly)");
@@ -584,6 +587,11 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   const int64_t ECM = E * C * M, PC = P * C, ldE = R * C;
   const SavedLayout& L = x->L;
   cudaStream_t sc = x->s_comp;
+  // grad_mode: every weight grad of a block is produced by exactly one kernel (the
+  // expert wgrads over all chunks, the deferred K=T MHA/gate wgrads), so "overwrite"
+  // is a plain store and "accumulate" a TMA reduce-add / read-modify-write.
+  const int gacc = x->cfg.grad_mode == FLOWMOE_GRAD_ACCUMULATE;
+  const int gepi = gacc ? EPI_ACC_F32 : EPI_STORE_F32;
   FM_CUDA(cudaEventRecord(x->ev_in, stream));
   FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
   // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the owner-side buffer, dw = <dO, Y>
@@ -642,19 +650,19 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.A = at<char>(saved, L.h); g.lda = F; g.sA = R * PC * F; g.a_mmajor = 1;
     g.B = x->dye; g.ldb = M; g.sB = R * PC * M;
     g.C = gr->dw2; g.ldc = M; g.sC = F * M;
-    g.epi = EPI_ACC_F32;
+    g.epi = gepi;
     FM_GEMM(KK_DW2, g);
     FM_KP(KK_DB2, 1, (double)El * R * PC * M, (double)El * R * PC * M * es + El * M * 8.0, sc,
-          colsum_acc(dt, x->dye, gr->db2, (int)El, (int)(R * PC), (int)M, sc));
+          colsum_acc(dt, x->dye, gr->db2, (int)El, (int)(R * PC), (int)M, gacc, sc));
     g = GemmArgs();  // dW1 += Xᵀ·dZ
     g.batch = (int)El; g.M = (int)M; g.N = (int)F; g.K = (int)(R * PC);
     g.A = at<char>(saved, L.xe); g.lda = M; g.sA = R * PC * M; g.a_mmajor = 1;
     g.B = x->dz; g.ldb = F; g.sB = R * PC * F;
     g.C = gr->dw1; g.ldc = F; g.sC = M * F;
-    g.epi = EPI_ACC_F32;
+    g.epi = gepi;
     FM_GEMM(KK_DW1, g);
     FM_KP(KK_DB1, 1, (double)El * R * PC * F, (double)El * R * PC * F * es + El * F * 8.0, sc,
-          colsum_acc(dt, x->dz, gr->db1, (int)El, (int)(R * PC), (int)F, sc));
+          colsum_acc(dt, x->dz, gr->db1, (int)El, (int)(R * PC), (int)F, gacc, sc));
   }
   // ---- AT_R^bwd .. AT_1^bwd
   for (int r = R - 1; r >= 0; --r) {
@@ -690,19 +698,19 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
   float* gf = gr->grad_flat;
   FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc,
-        gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M, (int)E, sc));
+        gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M, (int)E, gacc, sc));
   GemmArgs g;
   g.M = (int)M; g.N = (int)M; g.K = (int)x->T;
   g.A = at<char>(saved, L.ctx); g.lda = M; g.a_mmajor = 1;
   g.B = x->dA; g.ldb = M;
-  g.C = gf + 3 * M * M; g.ldc = M; g.epi = EPI_ACC_F32;
+  g.C = gf + 3 * M * M; g.ldc = M; g.epi = gepi;
   FM_GEMM(KK_DWO, g);
   FM_CUDA(cudaEventRecord(x->ev_grads_a, sc));
   g = GemmArgs();
   g.M = (int)M; g.N = (int)(3 * M); g.K = (int)x->T;
   g.A = xin; g.lda = M; g.a_mmajor = 1;
   g.B = x->dqkv; g.ldb = 3 * M;
-  g.C = gf; g.ldc = 3 * M; g.epi = EPI_ACC_F32;
+  g.C = gf; g.ldc = 3 * M; g.epi = gepi;
   FM_GEMM(KK_DWQKV, g);
   FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
   // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2)

@@ -65,9 +65,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
       int n = n0 + tx + 16 * j;
       if (n >= g.N) continue;
       float v = acc[i][j] * g.alpha;
-      if (g.epi == EPI_ACC_F32) {
+      if (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32) {
         float* C = reinterpret_cast<float*>(g.C) + (int64_t)b * g.sC;
-        C[(int64_t)m * g.ldc + n] += v;
+        if (g.epi == EPI_ACC_F32) C[(int64_t)m * g.ldc + n] += v;
+        else C[(int64_t)m * g.ldc + n] = v;
         continue;
       }
       T* C = reinterpret_cast<T*>(g.C) + (int64_t)b * g.sC;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const bool row_ok = row < g.M;
-    const bool f32out = g.epi == EPI_ACC_F32;
+    const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
     int buf = 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -204,8 +204,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (f32out) {
+        if (g.epi == EPI_ACC_F32) {
           tma_reduce_add_3d(&tma_c, sb, nb, m0 + r0, b);
+        } else if (g.epi == EPI_STORE_F32) {
+          tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
         } else {
           tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
           if (g.epi == EPI_BIAS_GELU) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
@@ -287,7 +289,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   if (rc) return rc;
   // output tiles: [32 rows][32 cols] boxes, fp32 (reduce-add, SW128) or bf16 (store, SW64)
   CUtensorMap mc, maux;
-  const bool f32 = g.epi == EPI_ACC_F32;
+  const bool f32 = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
   rc = make_map(&mc, g.C, g.N, g.M, g.batch, g.ldc, g.sC, 32, 32, f32,
                 f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;

@@ -490,13 +490,13 @@ __global__ void __launch_bounds__(128) gate_wgrad_part_kernel(const T* a, const 
   for (int e = 0; e < E; ++e) dst[e] = acc[e];
 }
 
-__global__ void gate_wgrad_reduce_kernel(const float* part, float* dwg, int nsplit, int n) {
+__global__ void gate_wgrad_reduce_kernel(const float* part, float* dwg, int nsplit, int n, int accumulate) {
   FM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s = 0.f;
   for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * n + i];
-  dwg[i] += s;
+  dwg[i] = accumulate ? dwg[i] + s : s;
 }
 
 size_t gate_wgrad_scratch_floats(int T_, int M, int E) {
@@ -514,30 +514,31 @@ static void gate_wgrad_launch(int dtype, const void* a, const float* dl, float* 
 }
 
 int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T_,
-               int M, int E, cudaStream_t s) {
+               int M, int E, int accumulate, cudaStream_t s) {
   if (T_ <= 0) return 0;
   FM_E_SWITCH(E, gate_wgrad_launch, dtype, a, dlogits, part, T_, M, s)
   const int nsplit = (T_ + GW_SPLIT_T - 1) / GW_SPLIT_T;
-  launch_k(gate_wgrad_reduce_kernel, (M * E + 255) / 256, 256, 0, s, part, dwg, nsplit, M * E);
+  launch_k(gate_wgrad_reduce_kernel, (M * E + 255) / 256, 256, 0, s, part, dwg, nsplit, M * E, accumulate);
   return (int)cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ bias grads
 template <typename T>
-__global__ void colsum_acc_kernel(const T* x, float* out, int rows, int N) {
+__global__ void colsum_acc_kernel(const T* x, float* out, int rows, int N, int accumulate) {
   FM_PDL_ENTRY();
   const int n = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
   if (n >= N) return;
   const T* xb = x + (int64_t)b * rows * N;
   float s = 0.f;
   for (int r = 0; r < rows; ++r) s += to_f<T>(xb[(int64_t)r * N + n]);
-  out[(int64_t)b * N + n] += s;
+  out[(int64_t)b * N + n] = accumulate ? out[(int64_t)b * N + n] + s : s;
 }
 
-int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, cudaStream_t s) {
+int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
+               cudaStream_t s) {
   dim3 grid((N + 255) / 256, batch);
-  if (dtype == DT_F32) launch_k(colsum_acc_kernel<float>, grid, 256, 0, s, (const float*)x, out, rows, N);
-  else launch_k(colsum_acc_kernel<bf16>, grid, 256, 0, s, (const bf16*)x, out, rows, N);
+  if (dtype == DT_F32) launch_k(colsum_acc_kernel<float>, grid, 256, 0, s, (const float*)x, out, rows, N, accumulate);
+  else launch_k(colsum_acc_kernel<bf16>, grid, 256, 0, s, (const bf16*)x, out, rows, N, accumulate);
   return (int)cudaGetLastError();
 }
 

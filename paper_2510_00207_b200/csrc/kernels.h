@@ -18,8 +18,9 @@ enum DType { DT_F32 = 0, DT_BF16 = 1 };
 //   EPI_STORE     C = alpha*acc (+ bias[n]) (+ resid(m,n))          -> storage dtype
 //   EPI_BIAS_GELU aux = Z = acc + bias[n];  C = GELU(Z)             -> storage dtype
 //   EPI_DGELU     C = acc * GELU'(aux(m,n))                        -> storage dtype
-//   EPI_ACC_F32   Cf32(m,n) += alpha*acc                            -> fp32 (grads)
-enum GemmEpi { EPI_STORE = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_ACC_F32 = 3 };
+//   EPI_ACC_F32   Cf32(m,n) += alpha*acc                            -> fp32 (grads, accumulate)
+//   EPI_STORE_F32 Cf32(m,n)  = alpha*acc                            -> fp32 (grads, overwrite)
+enum GemmEpi { EPI_STORE = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_ACC_F32 = 3, EPI_STORE_F32 = 4 };
 
 struct GemmArgs {
   int M = 0, N = 0, K = 0, batch = 1;
@@ -82,11 +83,12 @@ int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t
                     const float* w, const float* dw, const float* logits, const void* wg,
                     const void* dout_resid, void* dA, float* dlogits, int T, int M, int E, int k,
                     int ldE, cudaStream_t s);
-// dWg[M][E] += A^T · dlogits (deterministic split-T partials); part: scratch [nsplit][M][E]
+// dWg[M][E] (+)= A^T · dlogits (deterministic split-T partials); part: scratch [nsplit][M][E]
 int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T,
-               int M, int E, cudaStream_t s);
+               int M, int E, int accumulate, cudaStream_t s);
 size_t gate_wgrad_scratch_floats(int T, int M, int E);
-// out[b][n] += sum_r X[b][r][n]   (bias gradients)
-int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, cudaStream_t s);
+// out[b][n] (+)= sum_r X[b][r][n]   (bias gradients)
+int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
+               cudaStream_t s);
 
 }  // namespace fm

@@ -1,0 +1,108 @@
+"""Kernel timeline analysis from a CUPTI trace (torch.profiler chrome trace).
+
+Measurement plumbing for bench.py (not part of the hot path):
+  - per-kernel device time in the steady state (CUDA-graph replays),
+  - idle time (no kernel on any stream of the GPU),
+  - exposed communication: |∪ comm-kernel intervals \\ ∪ compute-kernel
+    intervals|, reported as a fraction of total comm time and of the iteration time.
+NCCL kernels are the comm kernels (A2A send/recv groups and AR chunks); everything else
+on the device is compute.
+"""
+from __future__ import annotations
+
+import collections
+import json
+import re
+
+
+def _union(intervals):
+    out = []
+    for a, b in sorted(intervals):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def _length(iv):
+    return sum(b - a for a, b in iv)
+
+
+def _subtract(a_iv, b_iv):
+    """|A \\ B| for two sorted disjoint interval lists."""
+    total, j = 0.0, 0
+    for a0, a1 in a_iv:
+        cur = a0
+        while j < len(b_iv) and b_iv[j][1] <= cur:
+            j += 1
+        k = j
+        while k < len(b_iv) and b_iv[k][0] < a1:
+            b0, b1 = b_iv[k]
+            if b0 > cur:
+                total += b0 - cur
+            cur = max(cur, b1)
+            if cur >= a1:
+                break
+            k += 1
+        if cur < a1:
+            total += a1 - cur
+    return total
+
+
+def is_comm(name: str) -> bool:
+    return name.startswith("nccl") or "ncclDevKernel" in name or "ncclKernel" in name
+
+
+def short_name(name: str) -> str:
+    n = re.sub(r"^void ", "", name)
+    m = re.match(r"([\w:]+(?:<[^()]*?>)?)", n)
+    return (m.group(1) if m else n)[:80]
+
+
+def analyze(trace_path: str, n_iters: int) -> dict:
+    ev = json.load(open(trace_path))
+    ev = ev["traceEvents"] if isinstance(ev, dict) else ev
+    kern = [e for e in ev if e.get("cat") == "kernel" and "dur" in e]
+    if not kern:
+        return {"error": "no kernel events in trace"}
+    comm = [(e["ts"], e["ts"] + e["dur"]) for e in kern if is_comm(e["name"])]
+    comp = [(e["ts"], e["ts"] + e["dur"]) for e in kern if not is_comm(e["name"])]
+    uc, up = _union(comm), _union(comp)
+    t0 = min(e["ts"] for e in kern)
+    t1 = max(e["ts"] + e["dur"] for e in kern)
+    busy = _union(comm + comp)
+    per = collections.defaultdict(lambda: [0, 0.0])
+    for e in kern:
+        k = short_name(e["name"])
+        per[k][0] += 1
+        per[k][1] += e["dur"]
+    comm_us = _length(uc)
+    exposed_us = _subtract(uc, up)
+    span_us = t1 - t0
+    return {
+        "iterations": n_iters,
+        "span_us_per_iter": span_us / n_iters,
+        "compute_busy_us_per_iter": _length(up) / n_iters,
+        "comm_busy_us_per_iter": comm_us / n_iters,
+        "exposed_comm_us_per_iter": exposed_us / n_iters,
+        "exposed_comm_frac_of_comm": (exposed_us / comm_us) if comm_us > 0 else None,
+        "exposed_comm_frac_of_iter": exposed_us / span_us if span_us > 0 else None,
+        "idle_us_per_iter": (span_us - _length(busy)) / n_iters,
+        "kernels_per_iter": len(kern) / n_iters,
+        "top_kernels": sorted(([k, c // n_iters, d / n_iters] for k, (c, d) in per.items()),
+                              key=lambda x: -x[2])[:25],
+    }
+
+
+def trace_replays(run, n_iters: int, path: str):
+    """Run `run()` n_iters times under torch.profiler (CUDA activities) and write a chrome trace."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(n_iters):
+            run()
+        torch.cuda.synchronize()
+    prof.export_chrome_trace(path)
+    return analyze(path, n_iters)

@@ -196,3 +196,22 @@ def test_gemm_tc_epilogues():
     fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw)
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref * o.gelu_grad(fm.to_host_f64(Z))) <= 1e-2
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_grad_modes_overwrite_and_accumulate(dtype):
+    """OVERWRITE ignores (garbage) buffer contents; ACCUMULATE adds: two backward
+    calls give twice the grads (P=1, so the AR is the identity)."""
+    cfg = (CASES["c1_f32"] if dtype == "f32" else CASES["bf16_small"])
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk])
+    ref_e = expert_grads(eg, 0, cfg.E)
+    g = run_block_gpu(cfg, rep, wk, grad_mode="overwrite", grad_fill=1e6)
+    assert rel(g["grad_flat"], gflat) <= TOL[dtype]
+    for n in ("dw1", "db1", "dw2", "db2"):
+        assert rel(g[n], ref_e[n]) <= TOL[dtype], n
+    g1 = run_block_gpu(cfg, rep, wk, grad_mode="accumulate")
+    g2 = run_block_gpu(cfg, rep, wk, grad_mode="accumulate", repeat_bwd=2)
+    for n in ("grad_flat", "dw1", "db1", "dw2", "db2"):
+        assert rel(g2[n], 2.0 * g1[n]) <= 1e-6, n
