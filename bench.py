@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
     ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--compute-streams", type=int, default=-1,
+                    help="compute lanes (1 = paper's single compute stream; default R)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the per-kernel table here")
     ap.add_argument("--trace-iters", type=int, default=10,
@@ -213,11 +215,14 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     S_p = args.chunk_bytes or SP_DEFAULT[args.config]
+    if args.compute_streams < 0:
+        args.compute_streams = cfg.R
     shape = fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,
                           top_k=cfg.top_k, d_ffn=cfg.d_ffn, R=cfg.R,
                           capacity_factor=cfg.capacity_factor, causal=cfg.causal,
                           residual=cfg.residual, dtype=cfg.dtype, world_size=world, rank=rank,
-                          grad_mode="overwrite")  # fresh grads each iteration (zero_grad + backward)
+                          grad_mode="overwrite",  # fresh grads each iteration (zero_grad + backward)
+                          compute_streams=args.compute_streams)
     ctx = fm.FlowMoE(shape, local, uid)
 
     # ---- resident synthetic state
@@ -375,6 +380,7 @@ def main():
                        "top_k": cfg.top_k, "d_ffn": cfg.d_ffn, "R": cfg.R, "layers": L,
                        "capacity_factor": cfg.capacity_factor, "S_p_bytes": S_p,
                        "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
+                       "compute_streams": args.compute_streams,
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,

@@ -70,6 +70,10 @@ typedef struct {
   int32_t world_size;      /* P */
   int32_t rank;            /* p; experts [p·E/P, (p+1)·E/P) are local (reading Q12) */
   int32_t grad_mode;       /* flowmoe_grad_mode */
+  int32_t compute_streams; /* 0/1: the compute tasks of all chunks run in Eq.(3)/(5) order on ONE
+                              stream (the paper's single compute resource); n > 1: chunk r's
+                              compute tasks run in that order on stream r % min(n, R), so chunks
+                              whose kernels do not fill the 148 SMs co-run (same results) */
 } flowmoe_config;
 
 /* Weights of one block (dtype of the config).  Replicated: wqkv [M][3M] (columns
@@ -172,8 +176,9 @@ flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch, cons
  * every kernel / NCCL call the library enqueues outside CUDA-graph capture is
  * bracketed by timing events on its own stream.  end synchronises the device
  * and writes one entry per kernel kind that ran: launches, summed device ms,
- * summed algorithmic FLOPs and HBM (or bus) bytes.  Returns the number of
- * entries written, or -1 on error. */
+ * summed algorithmic FLOPs and HBM (or bus) bytes.  While profiling, the
+ * compute lanes are collapsed onto one stream so every duration is the
+ * kernel's own.  Returns the number of entries written, or -1 on error. */
 typedef struct {
   const char* name;   /* static string owned by the library */
   int64_t launches;

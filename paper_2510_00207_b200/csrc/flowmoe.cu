@@ -55,6 +55,9 @@ struct flowmoe_ctx {
   size_t es = 2;
   int dt = DT_BF16;
   cudaStream_t s_comp = nullptr, s_a2a = nullptr, s_ar = nullptr;
+  // compute lanes: lanes[0] == s_comp; chunk r's compute tasks run on lanes[r % n_lanes]
+  std::vector<cudaStream_t> lanes;
+  std::vector<cudaEvent_t> ev_lane;
   ncclComm_t comm_a2a = nullptr, comm_ar = nullptr;
   // per-chunk events
   std::vector<cudaEvent_t> ev_at, ev_d, ev_e, ev_c, ev_cb, ev_cba, ev_eb, ev_dba;
@@ -181,6 +184,7 @@ flowmoe_status validate(const flowmoe_config* c) {
   if (c->dtype != FLOWMOE_F32 && c->dtype != FLOWMOE_BF16) return bad("dtype", "must be FLOWMOE_F32 or FLOWMOE_BF16");
   if (c->grad_mode != FLOWMOE_GRAD_ACCUMULATE && c->grad_mode != FLOWMOE_GRAD_OVERWRITE)
     return bad("grad_mode", "must be FLOWMOE_GRAD_ACCUMULATE or FLOWMOE_GRAD_OVERWRITE");
+  if (c->compute_streams < 0) return bad("compute_streams", "must be >= 0 (0 or 1 = one compute stream)");
   if (c->world_size < 1) return bad("world_size", "must be >= 1");
   if (c->rank < 0 || c->rank >= c->world_size) return bad("rank", "must be in [0, world_size)");
   if (c->E % c->world_size) return bad("E", "must be a multiple of world_size (experts sharded evenly)");
@@ -262,6 +266,22 @@ flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv, int r
                        x->comm_a2a, x->s_a2a));
     }
   FM_NCCL(ncclGroupEnd());
+  return FLOWMOE_OK;
+}
+
+// fork: every compute lane waits for the caller's stream
+flowmoe_status fork_lanes(flowmoe_ctx* x, cudaStream_t stream) {
+  FM_CUDA(cudaEventRecord(x->ev_in, stream));
+  for (cudaStream_t l : x->lanes) FM_CUDA(cudaStreamWaitEvent(l, x->ev_in, 0));
+  return FLOWMOE_OK;
+}
+// join: `dst` waits for every compute lane other than itself
+flowmoe_status join_lanes(flowmoe_ctx* x, cudaStream_t dst) {
+  for (size_t l = 0; l < x->lanes.size(); ++l) {
+    if (x->lanes[l] == dst) continue;
+    FM_CUDA(cudaEventRecord(x->ev_lane[l], x->lanes[l]));
+    FM_CUDA(cudaStreamWaitEvent(dst, x->ev_lane[l], 0));
+  }
   return FLOWMOE_OK;
 }
 
@@ -402,6 +422,19 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
       cudaStreamCreateWithPriority(&x->s_ar, cudaStreamNonBlocking, lo))
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
   auto mk = [&](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
+  {
+    const int nl = cfg->compute_streams < 1 ? 1 : (cfg->compute_streams > cfg->R ? cfg->R : cfg->compute_streams);
+    x->lanes.push_back(x->s_comp);
+    for (int l = 1; l < nl; ++l) {
+      cudaStream_t st = nullptr;
+      if (cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, 0))
+        return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
+      x->lanes.push_back(st);
+    }
+    x->ev_lane.resize(nl);
+    for (auto& e : x->ev_lane)
+      if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  }
   for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba}) {
     v->resize(cfg->R);
     for (auto& e : *v)
@@ -481,11 +514,13 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
   const int64_t ECM = E * C * M, PC = P * C, ldE = R * C;
   const SavedLayout& L = x->L;
-  cudaStream_t sc = x->s_comp;
-  FM_CUDA(cudaEventRecord(x->ev_in, stream));
-  FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
+  // the per-kernel profile (flowmoe_profile_begin) collapses the lanes so that each
+  // kernel's event-timed duration is its own, not shared with co-running chunks
+  const int nl = g_prof.on ? 1 : (int)x->lanes.size();
+  if (flowmoe_status st = fork_lanes(x, stream)) return st;
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer
   for (int r = 0; r < R; ++r) {
+    cudaStream_t sc = x->lanes[r % nl];
     const int64_t t0 = r * Tr;
     const char* xr = (const char*)xin + t0 * M * es;
     void* qkv = at<char>(saved, L.qkv + t0 * 3 * M * es);
@@ -527,6 +562,7 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     }
   // ---- E_1..E_R: batched expert FFN over the [P*C] capacity rows of chunk r of each local expert
   for (int r = 0; r < R; ++r) {
+    cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_d[r], 0));
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
@@ -557,6 +593,7 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     }
   // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
   for (int r = 0; r < R; ++r) {
+    cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_c[r], 0));
     const int64_t t0 = r * Tr;
     FM_KP(KK_COMBINE, 1, 2.0 * Tr * k * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0), sc,
@@ -565,7 +602,8 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
                             x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
                             (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)ldE, sc));
   }
-  FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
+  FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
   FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
   return FLOWMOE_OK;
 }
@@ -586,16 +624,18 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   const int64_t M = x->M, E = x->E, k = x->k, C = x->C, F = x->F, Tr = x->Tr, El = x->El, P = x->P;
   const int64_t ECM = E * C * M, PC = P * C, ldE = R * C;
   const SavedLayout& L = x->L;
-  cudaStream_t sc = x->s_comp;
+  // the per-kernel profile (flowmoe_profile_begin) collapses the lanes so that each
+  // kernel's event-timed duration is its own, not shared with co-running chunks
+  const int nl = g_prof.on ? 1 : (int)x->lanes.size();
   // grad_mode: every weight grad of a block is produced by exactly one kernel (the
   // expert wgrads over all chunks, the deferred K=T MHA/gate wgrads), so "overwrite"
   // is a plain store and "accumulate" a TMA reduce-add / read-modify-write.
   const int gacc = x->cfg.grad_mode == FLOWMOE_GRAD_ACCUMULATE;
   const int gepi = gacc ? EPI_ACC_F32 : EPI_STORE_F32;
-  FM_CUDA(cudaEventRecord(x->ev_in, stream));
-  FM_CUDA(cudaStreamWaitEvent(sc, x->ev_in, 0));
+  if (flowmoe_status st = fork_lanes(x, stream)) return st;
   // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the owner-side buffer, dw = <dO, Y>
   for (int r = R - 1; r >= 0; --r) {
+    cudaStream_t sc = x->lanes[r % nl];
     const int64_t t0 = r * Tr;
     FM_KP(KK_CBPACK, 1, 4.0 * Tr * k * M, (double)Tr * M * es + 2.0 * Tr * k * M * es, sc,
           combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * C * M * es),
@@ -615,6 +655,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     }
   // ---- E_R^bwd .. E_1^bwd (Eq.(5)): dgrads per chunk, so D_r^bwd can start early
   for (int r = R - 1; r >= 0; --r) {
+    cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_cba[r], 0));
     // dZ = (dY·W2ᵀ) ⊙ GELU'(Z)
     GemmArgs g;
@@ -632,7 +673,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.B = p->w1; g.ldb = F; g.sB = M * F; g.b_kmajor = 1;
     g.C = (char*)x->dxe + r * PC * M * es; g.ldc = M; g.sC = R * PC * M;
     FM_GEMM(KK_DXE, g);
-    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
+    FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
@@ -645,6 +686,9 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // ---- expert wgrads over all R chunks at once (K = R·P·C rows), overlapping the
   // last D^bwd A2As; the sums are the chunk sums of P:1173 in a different order.
   {
+    cudaStream_t sc = x->lanes[0];
+    for (int r = 0; r < R; ++r)
+      if (r % nl) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
     GemmArgs g;  // dW2 += Hᵀ·dY
     g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)(R * PC);
     g.A = at<char>(saved, L.h); g.lda = F; g.sA = R * PC * F; g.a_mmajor = 1;
@@ -666,6 +710,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   }
   // ---- AT_R^bwd .. AT_1^bwd
   for (int r = R - 1; r >= 0; --r) {
+    cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dba[r], 0));
     const int64_t t0 = r * Tr;
     void* dA = (char*)x->dA + t0 * M * es;
@@ -683,7 +728,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     FM_GEMM(KK_DCTX, g);
     FM_KP(KK_ATTN_B, 3, 10.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 8 * M * es, sc,
           attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
-                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf, (int)Tr, (int)x->N, (int)M,
+                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf + t0 * x->H, (int)Tr, (int)x->N, (int)M,
                    (int)x->H, x->cfg.causal, sc));
     if (dx) {
       g = GemmArgs();
@@ -696,6 +741,8 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   }
   // ---- deferred MHA/gate wgrads over all T tokens (one K=T GEMM each), in the order
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
+  cudaStream_t sc = x->lanes[0];
+  if (flowmoe_status st = join_lanes(x, sc)) return st;
   float* gf = gr->grad_flat;
   FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc,
         gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M, (int)E, gacc, sc));
@@ -730,6 +777,7 @@ flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* x, float* buf, size_t count
   if (chunk_bytes == 0 || chunk_bytes % 16)
     return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: chunk_bytes must be a positive multiple of 16");
   if (!ready) {
+    if (flowmoe_status st = join_lanes(x, x->s_comp)) return st;
     FM_CUDA(cudaEventRecord(x->ev_grads_a, x->s_comp));
     ready = x->ev_grads_a;
   }
@@ -754,6 +802,7 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
 
 void flowmoe_destroy(flowmoe_ctx* x) {
   if (!x) return;
+  for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamSynchronize(x->lanes[l]);
   if (x->s_comp) cudaStreamSynchronize(x->s_comp);
   if (x->s_a2a) cudaStreamSynchronize(x->s_a2a);
   if (x->s_ar) cudaStreamSynchronize(x->s_ar);
@@ -762,6 +811,8 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba})
     for (auto e : *v) if (e) cudaEventDestroy(e);
   for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
+  for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);
+  for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b}) if (e) cudaEventDestroy(e);
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);

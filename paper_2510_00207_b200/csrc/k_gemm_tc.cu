@@ -154,16 +154,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (g.bias) {
           const bf16* bias = reinterpret_cast<const bf16*>(g.bias) + (int64_t)b * g.sBias + nb;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? __bfloat162float(bias[i]) : 0.f;
+          for (int i = 0; i < 32; i += 8) {  // 16-byte loads (N % 8 == 0, so i < nvalid covers the group)
+            float t[8];
+            if (i < nvalid) load16<bf16>(bias + i, t);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[i + q] += (i < nvalid) ? t[q] : 0.f;
+          }
         }
         if (g.epi == EPI_STORE && g.resid && row_ok) {
           const bf16* R = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr + nb;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? __bfloat162float(R[i]) : 0.f;
+          for (int i = 0; i < 32; i += 8) {
+            float t[8];
+            if (i < nvalid) load16<bf16>(R + i, t);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[i + q] += (i < nvalid) ? t[q] : 0.f;
+          }
         } else if (g.epi == EPI_DGELU && row_ok) {
           const bf16* Z = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux + nb;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(__bfloat162float(Z[i])) : 0.f;
+          for (int i = 0; i < 32; i += 8) {
+            float t[8];
+            if (i < nvalid) load16<bf16>(Z + i, t);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[i + q] *= (i < nvalid) ? gelu_grad_f(t[q]) : 0.f;
+          }
         }
       }
       // staging buffer `buf` is free once the store issued two chunks ago has read it

@@ -37,7 +37,7 @@ class Config(ctypes.Structure):
                 ("capacity_factor", ctypes.c_float), ("causal", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("grad_mode", ctypes.c_int32)]
+                ("grad_mode", ctypes.c_int32), ("compute_streams", ctypes.c_int32)]
 
 
 class ProfEntry(ctypes.Structure):
@@ -172,12 +172,13 @@ class BlockShape:
     world_size: int = 1
     rank: int = 0
     grad_mode: str = "accumulate"  # or "overwrite"
+    compute_streams: int = 1
 
     def to_c(self) -> Config:
         return Config(self.B, self.seq_len, self.M, self.n_heads, self.E, self.top_k, self.d_ffn,
                       self.R, self.capacity_factor, self.causal, self.residual,
                       FLOWMOE_BF16 if self.dtype == "bf16" else FLOWMOE_F32, self.world_size,
-                      self.rank, 1 if self.grad_mode == "overwrite" else 0)
+                      self.rank, 1 if self.grad_mode == "overwrite" else 0, self.compute_streams)
 
 
 class FlowMoE:

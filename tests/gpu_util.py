@@ -14,22 +14,23 @@ def rel(g: np.ndarray, r: np.ndarray) -> float:
     return float(np.max(np.abs(g - r))) / (den if den > 0 else 1.0)
 
 
-def shape_of(cfg: BlockConfig, P: int, rank: int, grad_mode: str = "accumulate") -> fm.BlockShape:
+def shape_of(cfg: BlockConfig, P: int, rank: int, grad_mode: str = "accumulate",
+             compute_streams: int = 1) -> fm.BlockShape:
     return fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,
                          top_k=cfg.top_k, d_ffn=cfg.d_ffn, R=cfg.R,
                          capacity_factor=cfg.capacity_factor, causal=cfg.causal,
                          residual=cfg.residual, dtype=cfg.dtype, world_size=P, rank=rank,
-                         grad_mode=grad_mode)
+                         grad_mode=grad_mode, compute_streams=compute_streams)
 
 
 def run_block_gpu(cfg: BlockConfig, rep: dict, wk: dict, *, P: int = 1, rank: int = 0,
                   forced: bool = True, chunk_bytes: int = 1 << 20, uid: bytes | None = None,
                   device: int = 0, grad_mode: str = "accumulate", repeat_bwd: int = 1,
-                  grad_fill: float = 0.0) -> dict:
+                  grad_fill: float = 0.0, compute_streams: int = 1) -> dict:
     import torch
     dev = torch.device("cuda", device)
     torch.cuda.set_device(dev)
-    ctx = fm.FlowMoE(shape_of(cfg, P, rank, grad_mode), device, uid)
+    ctx = fm.FlowMoE(shape_of(cfg, P, rank, grad_mode, compute_streams), device, uid)
     bt = fm.BlockTensors(rep, cfg.dtype, rank, P, dev)
     if grad_fill:
         for v in bt.g.values():

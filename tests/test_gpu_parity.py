@@ -215,3 +215,16 @@ def test_grad_modes_overwrite_and_accumulate(dtype):
     g2 = run_block_gpu(cfg, rep, wk, grad_mode="accumulate", repeat_bwd=2)
     for n in ("grad_flat", "dw1", "db1", "dw2", "db2"):
         assert rel(g2[n], 2.0 * g1[n]) <= 1e-6, n
+
+
+@pytest.mark.parametrize("name", ["c2_bench", "c1_f32", "bf16_long_dh64_ragged"])
+def test_compute_lanes_bitwise_identical(name):
+    """Chunks' compute tasks on min(n, R) streams give bit-identical results to the
+    single compute stream (no atomics; every output has one writer)."""
+    cfg = CASES[name]
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    a = run_block_gpu(cfg, rep, wk, compute_streams=1)
+    b = run_block_gpu(cfg, rep, wk, compute_streams=cfg.R)
+    for n in ("y", "dx", "grad_flat", "dw1", "db1", "dw2", "db2", "logits", "idx", "pos", "counts"):
+        assert np.array_equal(a[n], b[n]), n
