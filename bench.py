@@ -54,7 +54,7 @@ def parse():
                     help="compute lanes (1 = paper's single compute stream; default R)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the per-kernel table here")
-    ap.add_argument("--trace-iters", type=int, default=10,
+    ap.add_argument("--trace-iters", type=int, default=20,
                     help="CUDA-graph replays traced with CUPTI (timeline, exposed comm); 0 = off")
     return ap.parse_args()
 
@@ -337,7 +337,11 @@ def main():
     if args.trace_iters > 0:
         from paper_2510_00207_b200.timeline import trace_replays
         try:
-            tl = trace_replays(run, args.trace_iters, f"/tmp/flowmoe_trace_r{rank}.json")
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            tl = trace_replays(run, args.trace_iters, f"/tmp/flowmoe_trace_r{rank}.json",
+                               trim=max(0, min(3, (args.trace_iters - 2) // 4)))
         except Exception as e:  # the timeline is diagnostics, never the measurement
             tl = {"error": repr(e)}
         if world > 1:
@@ -404,8 +408,8 @@ def main():
                     "frac_of_iteration": worst["exposed_comm_frac_of_iter"],
                     "exposed_ms": worst["exposed_comm_us_per_iter"] / 1e3,
                     "comm_busy_ms": worst["comm_busy_us_per_iter"] / 1e3,
-                    "method": f"CUPTI trace of {args.trace_iters} graph replays; worst rank; "
-                              "|union(NCCL kernels) minus union(compute kernels)|"}
+                    "method": f"CUPTI trace of {args.trace_iters} graph replays (edge iterations "
+                              "trimmed); worst rank; |union(NCCL kernels) minus union(compute kernels)|"}
             if ok:
                 r0 = ok[0]
                 line["timeline"] = {"span_ms": r0["span_us_per_iter"] / 1e3,

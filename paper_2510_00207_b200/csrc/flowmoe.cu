@@ -58,6 +58,10 @@ struct flowmoe_ctx {
   // compute lanes: lanes[0] == s_comp; chunk r's compute tasks run on lanes[r % n_lanes]
   std::vector<cudaStream_t> lanes;
   std::vector<cudaEvent_t> ev_lane;
+  // A2A lanes (P > 1): chunk r's A2As use a2a_comm[r % n] on a2a_stream[r % n]
+  // (index 0 = comm_a2a / s_a2a); each communicator sees a static op order.
+  std::vector<ncclComm_t> a2a_comm;
+  std::vector<cudaStream_t> a2a_stream;
   ncclComm_t comm_a2a = nullptr, comm_ar = nullptr;
   // per-chunk events
   std::vector<cudaEvent_t> ev_at, ev_d, ev_e, ev_c, ev_cb, ev_cba, ev_eb, ev_dba;
@@ -242,13 +246,16 @@ size_t expert_blk(const flowmoe_ctx* x, int64_t el, int r, int q) {
 // owner side -> expert side for chunk r (dispatch D_r, and C_r^bwd of dY)
 flowmoe_status a2a_to_experts(flowmoe_ctx* x, const void* send, void* recv, int r) {
   const size_t blk = (size_t)x->C * x->M;
+  const int ln = r % (int)x->a2a_comm.size();
+  ncclComm_t comm = x->a2a_comm[ln];
+  cudaStream_t st = x->a2a_stream[ln];
   FM_NCCL(ncclGroupStart());
   for (int q = 0; q < x->P; ++q)
     for (int el = 0; el < x->El; ++el) {
       FM_NCCL(ncclSend((const char*)send + owner_blk(x, q * x->El + el, r) * x->es, blk, nccl_dt(x), q,
-                       x->comm_a2a, x->s_a2a));
+                       comm, st));
       FM_NCCL(ncclRecv((char*)recv + expert_blk(x, el, r, q) * x->es, blk, nccl_dt(x), q,
-                       x->comm_a2a, x->s_a2a));
+                       comm, st));
     }
   FM_NCCL(ncclGroupEnd());
   return FLOWMOE_OK;
@@ -257,13 +264,16 @@ flowmoe_status a2a_to_experts(flowmoe_ctx* x, const void* send, void* recv, int 
 // expert side -> owner side for chunk r (combine C_r, and D_r^bwd of dX)
 flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv, int r) {
   const size_t blk = (size_t)x->C * x->M;
+  const int ln = r % (int)x->a2a_comm.size();
+  ncclComm_t comm = x->a2a_comm[ln];
+  cudaStream_t st = x->a2a_stream[ln];
   FM_NCCL(ncclGroupStart());
   for (int q = 0; q < x->P; ++q)
     for (int el = 0; el < x->El; ++el) {
       FM_NCCL(ncclSend((const char*)send + expert_blk(x, el, r, q) * x->es, blk, nccl_dt(x), q,
-                       x->comm_a2a, x->s_a2a));
+                       comm, st));
       FM_NCCL(ncclRecv((char*)recv + owner_blk(x, q * x->El + el, r) * x->es, blk, nccl_dt(x), q,
-                       x->comm_a2a, x->s_a2a));
+                       comm, st));
     }
   FM_NCCL(ncclGroupEnd());
   return FLOWMOE_OK;
@@ -475,6 +485,20 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     nc2.blocking = 1;
     if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &x->comm_ar, &nc2) != ncclSuccess)
       return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit failed"));
+    x->a2a_comm.push_back(x->comm_a2a);
+    x->a2a_stream.push_back(x->s_a2a);
+    for (size_t l = 1; l < x->lanes.size(); ++l) {
+      ncclConfig_t nc3 = NCCL_CONFIG_INITIALIZER;
+      nc3.blocking = 1;
+      ncclComm_t c2 = nullptr;
+      cudaStream_t s2 = nullptr;
+      if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &c2, &nc3) != ncclSuccess)
+        return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit (A2A lane) failed"));
+      x->a2a_comm.push_back(c2);
+      if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))
+        return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
+      x->a2a_stream.push_back(s2);
+    }
   }
   *out = x;
   return FLOWMOE_OK;
@@ -554,11 +578,12 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)
     for (int r = 0; r < R; ++r) {
-      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_at[r], 0));
-      int pi = prof_start(x->s_a2a);
+      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      FM_CUDA(cudaStreamWaitEvent(sa, x->ev_at[r], 0));
+      int pi = prof_start(sa);
       if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
-      prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
-      FM_CUDA(cudaEventRecord(x->ev_d[r], x->s_a2a));
+      prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, sa);
+      FM_CUDA(cudaEventRecord(x->ev_d[r], sa));
     }
   // ---- E_1..E_R: batched expert FFN over the [P*C] capacity rows of chunk r of each local expert
   for (int r = 0; r < R; ++r) {
@@ -585,11 +610,12 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // ---- C_1..C_R (Eq.(4))
   if (P > 1)
     for (int r = 0; r < R; ++r) {
-      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_e[r], 0));
-      int pi = prof_start(x->s_a2a);
+      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      FM_CUDA(cudaStreamWaitEvent(sa, x->ev_e[r], 0));
+      int pi = prof_start(sa);
       if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
-      prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
-      FM_CUDA(cudaEventRecord(x->ev_c[r], x->s_a2a));
+      prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, sa);
+      FM_CUDA(cudaEventRecord(x->ev_c[r], sa));
     }
   // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
   for (int r = 0; r < R; ++r) {
@@ -647,11 +673,12 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
-      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_cb[r], 0));
-      int pi = prof_start(x->s_a2a);
+      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      FM_CUDA(cudaStreamWaitEvent(sa, x->ev_cb[r], 0));
+      int pi = prof_start(sa);
       if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
-      prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
-      FM_CUDA(cudaEventRecord(x->ev_cba[r], x->s_a2a));
+      prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, sa);
+      FM_CUDA(cudaEventRecord(x->ev_cba[r], sa));
     }
   // ---- E_R^bwd .. E_1^bwd (Eq.(5)): dgrads per chunk, so D_r^bwd can start early
   for (int r = R - 1; r >= 0; --r) {
@@ -677,11 +704,12 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
-      FM_CUDA(cudaStreamWaitEvent(x->s_a2a, x->ev_eb[r], 0));
-      int pi = prof_start(x->s_a2a);
+      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      FM_CUDA(cudaStreamWaitEvent(sa, x->ev_eb[r], 0));
+      int pi = prof_start(sa);
       if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
-      prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, x->s_a2a);
-      FM_CUDA(cudaEventRecord(x->ev_dba[r], x->s_a2a));
+      prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, sa);
+      FM_CUDA(cudaEventRecord(x->ev_dba[r], sa));
     }
   // ---- expert wgrads over all R chunks at once (K = R·P·C rows), overlapping the
   // last D^bwd A2As; the sums are the chunk sums of P:1173 in a different order.
@@ -791,7 +819,11 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
     return fail(FLOWMOE_ERR_STATE, "allreduce_wait: unknown or expired ticket");
   if (x->P > 1) {
     ncclResult_t a = ncclSuccess, b = ncclSuccess;
-    ncclCommGetAsyncError(x->comm_a2a, &a);
+    for (ncclComm_t c : x->a2a_comm) {
+      ncclResult_t e = ncclSuccess;
+      ncclCommGetAsyncError(c, &e);
+      if (e != ncclSuccess) a = e;
+    }
     ncclCommGetAsyncError(x->comm_ar, &b);
     if (a != ncclSuccess || b != ncclSuccess)
       return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
@@ -806,6 +838,9 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   if (x->s_comp) cudaStreamSynchronize(x->s_comp);
   if (x->s_a2a) cudaStreamSynchronize(x->s_a2a);
   if (x->s_ar) cudaStreamSynchronize(x->s_ar);
+  for (size_t l = 1; l < x->a2a_stream.size(); ++l) cudaStreamSynchronize(x->a2a_stream[l]);
+  for (size_t l = 1; l < x->a2a_comm.size(); ++l) ncclCommDestroy(x->a2a_comm[l]);
+  for (size_t l = 1; l < x->a2a_stream.size(); ++l) cudaStreamDestroy(x->a2a_stream[l]);
   if (x->comm_ar) ncclCommDestroy(x->comm_ar);
   if (x->comm_a2a) ncclCommDestroy(x->comm_a2a);
   for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba})

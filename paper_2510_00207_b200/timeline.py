@@ -60,12 +60,28 @@ def short_name(name: str) -> str:
     return (m.group(1) if m else n)[:80]
 
 
-def analyze(trace_path: str, n_iters: int) -> dict:
+def analyze(trace_path: str, n_iters: int, trim: int = 0) -> dict:
+    """Interval statistics of the traced kernels.  With trim > 0 the first and last
+    `trim` iterations' worth of time are cut off (kernel intervals clipped to the
+    middle window), so rank skew at the edges of the trace (NCCL kernels spinning
+    on a late peer) does not count as exposed communication."""
     ev = json.load(open(trace_path))
     ev = ev["traceEvents"] if isinstance(ev, dict) else ev
     kern = [e for e in ev if e.get("cat") == "kernel" and "dur" in e]
     if not kern:
         return {"error": "no kernel events in trace"}
+    if trim > 0 and n_iters > 2 * trim:
+        a = min(e["ts"] for e in kern)
+        b = max(e["ts"] + e["dur"] for e in kern)
+        it = (b - a) / n_iters
+        lo, hi = a + trim * it, b - trim * it
+        clipped = []
+        for e in kern:
+            s0, s1 = max(e["ts"], lo), min(e["ts"] + e["dur"], hi)
+            if s1 > s0:
+                clipped.append(dict(e, ts=s0, dur=s1 - s0))
+        kern = clipped
+        n_iters -= 2 * trim
     comm = [(e["ts"], e["ts"] + e["dur"]) for e in kern if is_comm(e["name"])]
     comp = [(e["ts"], e["ts"] + e["dur"]) for e in kern if not is_comm(e["name"])]
     uc, up = _union(comm), _union(comp)
@@ -95,7 +111,7 @@ def analyze(trace_path: str, n_iters: int) -> dict:
     }
 
 
-def trace_replays(run, n_iters: int, path: str):
+def trace_replays(run, n_iters: int, path: str, trim: int = 0):
     """Run `run()` n_iters times under torch.profiler (CUDA activities) and write a chrome trace."""
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -105,4 +121,4 @@ def trace_replays(run, n_iters: int, path: str):
             run()
         torch.cuda.synchronize()
     prof.export_chrome_trace(path)
-    return analyze(path, n_iters)
+    return analyze(path, n_iters, trim)
