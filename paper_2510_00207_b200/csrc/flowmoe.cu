@@ -58,6 +58,9 @@ struct flowmoe_ctx {
   // compute lanes: lanes[0] == s_comp; chunk r's compute tasks run on lanes[r % n_lanes]
   std::vector<cudaStream_t> lanes;
   std::vector<cudaEvent_t> ev_lane;
+  // per-block weight-grad stream (expert wgrads over all chunks, deferred MHA/gate
+  // wgrads); == s_comp with one lane, its own stream with several
+  cudaStream_t s_wg = nullptr;
   // A2A lanes (P > 1): chunk r's A2As use a2a_comm[r % n] on a2a_stream[r % n]
   // (index 0 = comm_a2a / s_a2a); each communicator sees a static op order.
   std::vector<ncclComm_t> a2a_comm;
@@ -441,6 +444,12 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
         return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
       x->lanes.push_back(st);
     }
+    if (nl > 1) {
+      if (cudaStreamCreateWithPriority(&x->s_wg, cudaStreamNonBlocking, 0))
+        return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
+    } else {
+      x->s_wg = x->s_comp;
+    }
     x->ev_lane.resize(nl);
     for (auto& e : x->ev_lane)
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
@@ -714,9 +723,9 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // ---- expert wgrads over all R chunks at once (K = R·P·C rows), overlapping the
   // last D^bwd A2As; the sums are the chunk sums of P:1173 in a different order.
   {
-    cudaStream_t sc = x->lanes[0];
+    cudaStream_t sc = nl > 1 ? x->s_wg : x->lanes[0];
     for (int r = 0; r < R; ++r)
-      if (r % nl) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
+      if (sc != x->lanes[r % nl]) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
     GemmArgs g;  // dW2 += Hᵀ·dY
     g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)(R * PC);
     g.A = at<char>(saved, L.h); g.lda = F; g.sA = R * PC * F; g.a_mmajor = 1;
@@ -769,7 +778,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   }
   // ---- deferred MHA/gate wgrads over all T tokens (one K=T GEMM each), in the order
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
-  cudaStream_t sc = x->lanes[0];
+  cudaStream_t sc = nl > 1 ? x->s_wg : x->lanes[0];
   if (flowmoe_status st = join_lanes(x, sc)) return st;
   float* gf = gr->grad_flat;
   FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc,
@@ -835,6 +844,7 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
 void flowmoe_destroy(flowmoe_ctx* x) {
   if (!x) return;
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamSynchronize(x->lanes[l]);
+  if (x->s_wg && x->s_wg != x->s_comp) cudaStreamSynchronize(x->s_wg);
   if (x->s_comp) cudaStreamSynchronize(x->s_comp);
   if (x->s_a2a) cudaStreamSynchronize(x->s_a2a);
   if (x->s_ar) cudaStreamSynchronize(x->s_ar);
@@ -848,6 +858,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
   for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);
+  if (x->s_wg && x->s_wg != x->s_comp) cudaStreamDestroy(x->s_wg);
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b}) if (e) cudaEventDestroy(e);
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);
