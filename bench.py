@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
     ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--schedule", default="flowmoe",
+                    choices=["flowmoe", "flowmoe_ar", "flowmoe_at", "pipe_moe", "vanilla_ep"],
+                    help="scheduling policy (the paper's Table 6 ablation)")
     ap.add_argument("--compute-streams", type=int, default=-1,
                     help="compute lanes (1 = paper's single compute stream; default R)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -222,7 +225,7 @@ def main():
                           capacity_factor=cfg.capacity_factor, causal=cfg.causal,
                           residual=cfg.residual, dtype=cfg.dtype, world_size=world, rank=rank,
                           grad_mode="overwrite",  # fresh grads each iteration (zero_grad + backward)
-                          compute_streams=args.compute_streams)
+                          compute_streams=args.compute_streams, schedule=args.schedule)
     ctx = fm.FlowMoE(shape, local, uid)
 
     # ---- resident synthetic state
@@ -392,7 +395,7 @@ def main():
                        "top_k": cfg.top_k, "d_ffn": cfg.d_ffn, "R": cfg.R, "layers": L,
                        "capacity_factor": cfg.capacity_factor, "S_p_bytes": S_p,
                        "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
-                       "compute_streams": args.compute_streams,
+                       "compute_streams": args.compute_streams, "schedule": args.schedule,
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,

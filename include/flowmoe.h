@@ -54,6 +54,18 @@ typedef enum { FLOWMOE_F32 = 0, FLOWMOE_BF16 = 1 } flowmoe_dtype;
  * (the buffers need no zeroing; like zero_grad(set_to_none) + backward). */
 typedef enum { FLOWMOE_GRAD_ACCUMULATE = 0, FLOWMOE_GRAD_OVERWRITE = 1 } flowmoe_grad_mode;
 
+/* Scheduling policy — the paper's ablation (Table 6), all on
+ * the same kernels and with identical results for the same effective R:
+ *   FLOWMOE     AT, D, E, C split into R subtasks (Eqs.(3)-(6)) + chunked AR per block
+ *   FLOWMOE_AR  MoE part split (experts + A2A), AT unsplit, chunked AR per block
+ *   FLOWMOE_AT  AT and MoE part split, AR centralized after the backward pass
+ *   PIPE_MOE    MoE part split only (Tutel-like), AT unsplit, AR centralized
+ *   VANILLA_EP  no pipelining (R treated as 1), AR centralized */
+typedef enum {
+  FLOWMOE_SCHED_FLOWMOE = 0, FLOWMOE_SCHED_FLOWMOE_AR = 1, FLOWMOE_SCHED_FLOWMOE_AT = 2,
+  FLOWMOE_SCHED_PIPE_MOE = 3, FLOWMOE_SCHED_VANILLA_EP = 4
+} flowmoe_schedule;
+
 typedef struct {
   int64_t B;               /* tokens on this rank (paper B·N); B % seq_len == 0; (B/seq_len) % R == 0 */
   int32_t seq_len;         /* N, tokens per sequence (attention span) */
@@ -74,6 +86,7 @@ typedef struct {
                               stream (the paper's single compute resource); n > 1: chunk r's
                               compute tasks run in that order on stream r % min(n, R), so chunks
                               whose kernels do not fill the 148 SMs co-run (same results) */
+  int32_t schedule;        /* a flowmoe_schedule value; default FLOWMOE */
 } flowmoe_config;
 
 /* Weights of one block (dtype of the config).  Replicated: wqkv [M][3M] (columns

@@ -69,6 +69,7 @@ struct flowmoe_ctx {
   // per-chunk events
   std::vector<cudaEvent_t> ev_at, ev_d, ev_e, ev_c, ev_cb, ev_cba, ev_eb, ev_dba;
   cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_grads_a = nullptr, ev_grads_b = nullptr;
+  cudaEvent_t ev_bwd_done = nullptr;  // end of the latest block_bwd (centralized AR starts after it)
   std::vector<cudaEvent_t> ticket_ev;
   uint64_t next_ticket = 1;
   SavedLayout L{};
@@ -78,6 +79,10 @@ struct flowmoe_ctx {
   float *dl = nullptr, *dw = nullptr, *Dbuf = nullptr, *wg_part = nullptr;
   std::vector<void*> allocs;
   const int32_t* forced = nullptr;
+  // scheduling policy (flowmoe_schedule): AT split into R subtasks? AR chunked per block?
+  bool at_split = true, ar_pipelined = true;
+  struct PendingAR { float* buf; size_t count; uint64_t ticket; };
+  std::vector<PendingAR> pending_ar;  // centralized-AR policies: flushed at allreduce_wait
 };
 
 namespace {
@@ -191,6 +196,8 @@ flowmoe_status validate(const flowmoe_config* c) {
   if (c->dtype != FLOWMOE_F32 && c->dtype != FLOWMOE_BF16) return bad("dtype", "must be FLOWMOE_F32 or FLOWMOE_BF16");
   if (c->grad_mode != FLOWMOE_GRAD_ACCUMULATE && c->grad_mode != FLOWMOE_GRAD_OVERWRITE)
     return bad("grad_mode", "must be FLOWMOE_GRAD_ACCUMULATE or FLOWMOE_GRAD_OVERWRITE");
+  if (c->schedule < FLOWMOE_SCHED_FLOWMOE || c->schedule > FLOWMOE_SCHED_VANILLA_EP)
+    return bad("schedule", "must be a flowmoe_schedule value");
   if (c->compute_streams < 0) return bad("compute_streams", "must be >= 0 (0 or 1 = one compute stream)");
   if (c->world_size < 1) return bad("world_size", "must be >= 1");
   if (c->rank < 0 || c->rank >= c->world_size) return bad("rank", "must be in [0, world_size)");
@@ -406,9 +413,14 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   if (cfg->world_size > 1 && !id) return fail(FLOWMOE_ERR_INVALID, "id is NULL with world_size > 1");
   auto* x = new flowmoe_ctx();
   x->cfg = *cfg;
+  // VANILLA_EP treats the block as one chunk (R = 1); PIPE_MOE and FLOWMOE_AR keep the
+  // MHA+gate task AT unsplit; only FLOWMOE_AR and FLOWMOE pipeline the AR (Table 6)
+  if (cfg->schedule == FLOWMOE_SCHED_VANILLA_EP) x->cfg.R = 1;
+  x->at_split = cfg->schedule == FLOWMOE_SCHED_FLOWMOE || cfg->schedule == FLOWMOE_SCHED_FLOWMOE_AT;
+  x->ar_pipelined = cfg->schedule == FLOWMOE_SCHED_FLOWMOE || cfg->schedule == FLOWMOE_SCHED_FLOWMOE_AR;
   x->dev = device;
   x->T = cfg->B;
-  x->Tr = cfg->B / cfg->R;
+  x->Tr = cfg->B / x->cfg.R;
   x->N = cfg->seq_len;
   x->S = cfg->B / cfg->seq_len;
   x->M = cfg->M;
@@ -418,7 +430,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   x->F = cfg->d_ffn;
   x->P = cfg->world_size;
   x->El = cfg->E / cfg->world_size;
-  x->C = capacity_of(cfg, x->Tr);
+  x->C = capacity_of(&x->cfg, x->Tr);
   x->dt = cfg->dtype == FLOWMOE_BF16 ? DT_BF16 : DT_F32;
   x->es = cfg->dtype == FLOWMOE_BF16 ? 2 : 4;
   x->L = layout_of(x);
@@ -436,7 +448,8 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
   auto mk = [&](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
   {
-    const int nl = cfg->compute_streams < 1 ? 1 : (cfg->compute_streams > cfg->R ? cfg->R : cfg->compute_streams);
+    const int R_ = x->cfg.R;
+    const int nl = cfg->compute_streams < 1 ? 1 : (cfg->compute_streams > R_ ? R_ : cfg->compute_streams);
     x->lanes.push_back(x->s_comp);
     for (int l = 1; l < nl; ++l) {
       cudaStream_t st = nullptr;
@@ -455,14 +468,15 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   }
   for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba}) {
-    v->resize(cfg->R);
+    v->resize(x->cfg.R);
     for (auto& e : *v)
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   }
   x->ticket_ev.resize(NUM_TICKET_EVENTS);
   for (auto& e : x->ticket_ev)
     if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
-  if (!mk(&x->ev_in) || !mk(&x->ev_done) || !mk(&x->ev_grads_a) || !mk(&x->ev_grads_b))
+  if (!mk(&x->ev_in) || !mk(&x->ev_done) || !mk(&x->ev_grads_a) || !mk(&x->ev_grads_b) ||
+      !mk(&x->ev_bwd_done))
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   // backward workspaces
   auto alloc = [&](void** p, size_t bytes) {
@@ -471,7 +485,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     return true;
   };
   const size_t es = x->es;
-  const int64_t R = cfg->R, ECM = x->E * x->C * x->M;
+  const int64_t R = x->cfg.R, ECM = x->E * x->C * x->M;
   bool ok = alloc(&x->dyc, R * ECM * es) && alloc(&x->dxe, R * ECM * es) &&
             alloc(&x->dz, (size_t)R * x->E * x->C * x->F * es) && alloc(&x->dA, x->T * x->M * es) &&
             alloc(&x->dctx, x->T * x->M * es) && alloc(&x->dqkv, x->T * 3 * x->M * es) &&
@@ -551,30 +565,37 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // kernel's event-timed duration is its own, not shared with co-running chunks
   const int nl = g_prof.on ? 1 : (int)x->lanes.size();
   if (flowmoe_status st = fork_lanes(x, stream)) return st;
-  // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer
-  for (int r = 0; r < R; ++r) {
-    cudaStream_t sc = x->lanes[r % nl];
-    const int64_t t0 = r * Tr;
+  // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer.
+  // Policies that keep AT unsplit (PIPE_MOE, FLOWMOE_AR) run MHA + gate once over all
+  // tokens, then route/pack per chunk (capacity is per chunk in every policy).
+  const int n_at = x->at_split ? R : 1;
+  const int64_t Ta = x->at_split ? Tr : x->T;
+  for (int ai = 0; ai < n_at; ++ai) {
+    cudaStream_t sc = x->lanes[ai % nl];
+    const int64_t t0 = ai * Ta;
     const char* xr = (const char*)xin + t0 * M * es;
     void* qkv = at<char>(saved, L.qkv + t0 * 3 * M * es);
     void* ctxb = at<char>(saved, L.ctx + t0 * M * es);
     void* a = at<char>(saved, L.a + t0 * M * es);
     GemmArgs g;
-    g.M = (int)Tr; g.N = (int)(3 * M); g.K = (int)M;
+    g.M = (int)Ta; g.N = (int)(3 * M); g.K = (int)M;
     g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
     FM_GEMM(KK_QKV, g);
-    FM_KP(KK_ATTN_F, 1, 4.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 5 * M * es + Tr * x->H * 4.0, sc,
-          attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Tr, (int)x->N, (int)M,
+    FM_KP(KK_ATTN_F, 1, 4.0 * Ta * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Ta * 5 * M * es + Ta * x->H * 4.0, sc,
+          attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Ta, (int)x->N, (int)M,
                    (int)x->H, x->cfg.causal, sc));
     g = GemmArgs();
-    g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
+    g.M = (int)Ta; g.N = (int)M; g.K = (int)M;
     g.A = ctxb; g.lda = M; g.B = p->wo; g.ldb = M; g.C = a; g.ldc = M;
     if (x->cfg.residual) { g.resid = xr; g.ldr = M; }
     FM_GEMM(KK_OPROJ, g);
-    FM_KP(KK_GATE, 1, 2.0 * Tr * M * E, (double)Tr * M * es + M * E * es + Tr * E * 4.0 + Tr * k * 8.0, sc,
+    FM_KP(KK_GATE, 1, 2.0 * Ta * M * E, (double)Ta * M * es + M * E * es + Ta * E * 4.0 + Ta * k * 8.0, sc,
           gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr, at<float>(saved, L.logits + t0 * E * 4),
-                    at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4), (int)Tr, (int)M,
+                    at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4), (int)Ta, (int)M,
                     (int)E, (int)k, sc));
+   for (int r = x->at_split ? ai : 0; r < (x->at_split ? ai + 1 : R); ++r) {
+    const int64_t t0 = r * Tr;
+    void* a = at<char>(saved, L.a + t0 * M * es);
     int32_t* src = at<int32_t>(saved, L.src + r * E * C * 4);
     FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc,
           route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
@@ -582,7 +603,8 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc,
           permute_pack(dt, a, src, at<char>(saved, L.send + r * C * M * es), (int)E, (int)C, (int)ldE, (int)M,
                        (int)k, sc));
-    if (P > 1) FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
+    FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
+   }
   }
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)
@@ -598,6 +620,7 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   for (int r = 0; r < R; ++r) {
     cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_d[r], 0));
+    else if (!x->at_split && sc != x->lanes[0]) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_at[r], 0));
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
     g.A = at<char>(saved, L.xe + r * PC * M * es); g.lda = M; g.sA = R * PC * M;
@@ -745,31 +768,39 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     FM_KP(KK_DB1, 1, (double)El * R * PC * F, (double)El * R * PC * F * es + El * F * 8.0, sc,
           colsum_acc(dt, x->dz, gr->db1, (int)El, (int)(R * PC), (int)F, gacc, sc));
   }
-  // ---- AT_R^bwd .. AT_1^bwd
-  for (int r = R - 1; r >= 0; --r) {
-    cudaStream_t sc = x->lanes[r % nl];
+  // ---- AT_R^bwd .. AT_1^bwd (unsplit policies: gathers per chunk, then MHA backward
+  // once over all tokens)
+  const int n_atb = x->at_split ? R : 1;
+  const int64_t Tb = x->at_split ? Tr : x->T;
+  for (int ai = n_atb - 1; ai >= 0; --ai) {
+    cudaStream_t sc = x->lanes[ai % nl];
+   for (int r = x->at_split ? ai : R - 1; r >= (x->at_split ? ai : 0); --r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dba[r], 0));
+    else if (sc != x->lanes[r % nl] || !x->at_split) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
     const int64_t t0 = r * Tr;
     void* dA = (char*)x->dA + t0 * M * es;
-    void* dctx = (char*)x->dctx + t0 * M * es;
-    void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
     FM_KP(KK_GATHER, 1, 2.0 * Tr * E * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0) + M * E * es, sc,
           gather_gate_bwd(dt, (char*)x->dxc + r * C * M * es, at<int32_t>(saved, L.idx + t0 * k * 4),
                           at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
                           x->dw + t0 * k, at<float>(saved, L.logits + t0 * E * 4), p->wg,
                           x->cfg.residual ? (const char*)dy + t0 * M * es : nullptr, dA, x->dl + t0 * E,
                           (int)Tr, (int)M, (int)E, (int)k, (int)ldE, sc));
+   }
+    const int64_t t0 = ai * Tb;
+    void* dA = (char*)x->dA + t0 * M * es;
+    void* dctx = (char*)x->dctx + t0 * M * es;
+    void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
     GemmArgs g;
-    g.M = (int)Tr; g.N = (int)M; g.K = (int)M;
+    g.M = (int)Tb; g.N = (int)M; g.K = (int)M;
     g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
     FM_GEMM(KK_DCTX, g);
-    FM_KP(KK_ATTN_B, 3, 10.0 * Tr * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tr * 8 * M * es, sc,
+    FM_KP(KK_ATTN_B, 3, 10.0 * Tb * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tb * 8 * M * es, sc,
           attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
-                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf + t0 * x->H, (int)Tr, (int)x->N, (int)M,
+                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf + t0 * x->H, (int)Tb, (int)x->N, (int)M,
                    (int)x->H, x->cfg.causal, sc));
     if (dx) {
       g = GemmArgs();
-      g.M = (int)Tr; g.N = (int)M; g.K = (int)(3 * M);
+      g.M = (int)Tb; g.N = (int)M; g.K = (int)(3 * M);
       g.A = dqkv; g.lda = 3 * M; g.B = p->wqkv; g.ldb = 3 * M; g.b_kmajor = 1;
       g.C = (char*)dx + t0 * M * es; g.ldc = M;
       if (x->cfg.residual) { g.resid = dA; g.ldr = M; }
@@ -797,11 +828,19 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   g.C = gf; g.ldc = 3 * M; g.epi = gepi;
   FM_GEMM(KK_DWQKV, g);
   FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
-  // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2)
-  if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
-  if (flowmoe_status s = submit_ar(x, gf, (size_t)(3 * M * M), chunk_bytes, x->ev_grads_b)) return s;
-  if (flowmoe_status s = new_ticket(x, ar)) return s;
+  // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2); centralized
+  // policies defer every block's AR until the backward pass is over (allreduce_wait).
   FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  FM_CUDA(cudaEventRecord(x->ev_bwd_done, sc));
+  if (x->ar_pipelined) {
+    if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
+    if (flowmoe_status s = submit_ar(x, gf, (size_t)(3 * M * M), chunk_bytes, x->ev_grads_b)) return s;
+    if (flowmoe_status s = new_ticket(x, ar)) return s;
+  } else {
+    const uint64_t t = x->next_ticket++;
+    x->pending_ar.push_back({gf, (size_t)(4 * M * M + M * E), t});
+    if (ar) *ar = t;
+  }
   FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
   return FLOWMOE_OK;
 }
@@ -837,6 +876,15 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
     if (a != ncclSuccess || b != ncclSuccess)
       return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
   }
+  if (!x->pending_ar.empty()) {
+    // centralized AR: every pending block AR, whole tensors, after the last backward
+    FM_CUDA(cudaStreamWaitEvent(x->s_ar, x->ev_bwd_done, 0));
+    for (const auto& pa : x->pending_ar)
+      if (flowmoe_status s = submit_ar(x, pa.buf, pa.count, pa.count * 4, nullptr)) return s;
+    for (const auto& pa : x->pending_ar)
+      FM_CUDA(cudaEventRecord(x->ticket_ev[pa.ticket % NUM_TICKET_EVENTS], x->s_ar));
+    x->pending_ar.clear();
+  }
   FM_CUDA(cudaStreamWaitEvent(stream, x->ticket_ev[t % NUM_TICKET_EVENTS], 0));
   return FLOWMOE_OK;
 }
@@ -859,7 +907,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);
   if (x->s_wg && x->s_wg != x->s_comp) cudaStreamDestroy(x->s_wg);
-  for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b}) if (e) cudaEventDestroy(e);
+  for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b, x->ev_bwd_done}) if (e) cudaEventDestroy(e);
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);
   if (x->s_a2a) cudaStreamDestroy(x->s_a2a);

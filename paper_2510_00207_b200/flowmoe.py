@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libflowmoe.so")
 
 FLOWMOE_F32, FLOWMOE_BF16 = 0, 1
+SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "vanilla_ep": 4}
 
 EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
@@ -37,7 +38,8 @@ class Config(ctypes.Structure):
                 ("capacity_factor", ctypes.c_float), ("causal", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("grad_mode", ctypes.c_int32), ("compute_streams", ctypes.c_int32)]
+                ("grad_mode", ctypes.c_int32), ("compute_streams", ctypes.c_int32),
+                ("schedule", ctypes.c_int32)]
 
 
 class ProfEntry(ctypes.Structure):
@@ -173,12 +175,14 @@ class BlockShape:
     rank: int = 0
     grad_mode: str = "accumulate"  # or "overwrite"
     compute_streams: int = 1
+    schedule: str = "flowmoe"
 
     def to_c(self) -> Config:
         return Config(self.B, self.seq_len, self.M, self.n_heads, self.E, self.top_k, self.d_ffn,
                       self.R, self.capacity_factor, self.causal, self.residual,
                       FLOWMOE_BF16 if self.dtype == "bf16" else FLOWMOE_F32, self.world_size,
-                      self.rank, 1 if self.grad_mode == "overwrite" else 0, self.compute_streams)
+                      self.rank, 1 if self.grad_mode == "overwrite" else 0, self.compute_streams,
+                      SCHEDULES[self.schedule])
 
 
 class FlowMoE:

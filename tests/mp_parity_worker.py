@@ -30,7 +30,10 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     results = {}
-    for name, base in CASES.items():
+    runs = [(n, c, "flowmoe", 1) for n, c in CASES.items()]
+    runs += [("bf16_p_" + sch, CASES["bf16_p"], sch, lanes)
+             for sch, lanes in (("flowmoe", 2), ("flowmoe_ar", 1), ("pipe_moe", 2), ("vanilla_ep", 1))]
+    for name, base, schedule, lanes in runs:
         cfg = base.replace(P=P)
         obj = [fm.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -38,8 +41,9 @@ def main():
         wks = [gen_worker(cfg, p) for p in range(P)]
         # tiny S_p so the all-reduce is cut into many chunks incl. a remainder
         g = run_block_gpu(cfg, rep, wks[rank], P=P, rank=rank, uid=obj[0], device=dev.index,
-                          chunk_bytes=4096 + 16)
-        ys, dxs, gflat, eg, st = oracle_block(cfg, rep, wks)
+                          chunk_bytes=4096 + 16, schedule=schedule, compute_streams=lanes)
+        ocfg = cfg.replace(R=1) if schedule == "vanilla_ep" else cfg
+        ys, dxs, gflat, eg, st = oracle_block(ocfg, rep, wks)
         El = cfg.E // P
         ref_e = expert_grads(eg, rank * El, (rank + 1) * El)
         r = {"y": rel(g["y"], ys[rank]), "dx": rel(g["dx"], dxs[rank]),

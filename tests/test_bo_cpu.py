@@ -1,0 +1,61 @@
+"""BO S_p tuner (FlowMoE §4.1, Appendix D) — closed forms and properties."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2510_00207_b200.bo import (GP, bo_tune, expected_improvement, grid_tune, random_tune,
+                                      retune_trigger)
+
+
+def test_ei_closed_forms():
+    assert expected_improvement(np.array([1.0]), np.array([0.0]), 1.0, 0.1)[0] == 0.0
+    assert abs(expected_improvement(np.array([1.0 - 0.1 - 1.0]), np.array([0.0]), 1.0, 0.1)[0] - 1.0) < 1e-15
+    v = expected_improvement(np.array([1.0 - 0.1]), np.array([1.0]), 1.0, 0.1)[0]
+    assert abs(v - 1.0 / math.sqrt(2 * math.pi)) < 1e-12  # phi(0) = 0.39894...
+    rng = np.random.default_rng(0)
+    m, s2 = rng.normal(size=100), rng.uniform(0, 2, 100)
+    assert np.all(expected_improvement(m, s2, 0.0, 0.1) >= 0)
+
+
+def test_gp_interpolation_decay_symmetry():
+    gp = GP(length=1.0, signal_var=2.0, noise_var=1e-12, mean0=0.5).fit([0.0, 1.0, 3.0], [1.0, -1.0, 2.0])
+    mu, var = gp.posterior([1.0])
+    assert abs(mu[0] + 1.0) < 1e-6 and var[0] < 1e-6
+    mu, var = gp.posterior([1e4])
+    assert abs(mu[0] - 0.5) < 1e-9 and abs(var[0] - 2.0) < 1e-9
+    gp = GP(length=1.0, signal_var=1.0, noise_var=1e-12, mean0=0.5).fit([-1.0, 1.0], [0.0, 1.0])
+    mu, var = gp.posterior([0.0])
+    assert abs(mu[0] - 0.5) < 1e-12
+    _, var = gp.posterior(np.linspace(-5, 5, 101))
+    assert np.all(var >= 0) and np.all(var <= 1.0 + 1e-12)
+
+
+def test_bo_finds_interior_minimum_of_quadratic():
+    lo, hi = 0.0, 10.0
+    f = lambda x: (x - 2.5) ** 2 + 3.0  # interior optimum (Fig. 5's 2.5 MB shape)
+    fine = min(f(x) for x in np.linspace(lo + 1e-3, hi, 20001))
+    good = 0
+    for seed in range(20):
+        r = bo_tune(f, lo, hi, budget=8, seed=seed, quantum=1e-3)
+        assert r.best_time == min(y for _, _, y, _ in r.log)          # monotone incumbent
+        assert all(lo < x <= hi for _, x, _, _ in r.log)
+        good += r.best_time <= 1.02 * fine
+    assert good >= 16
+
+
+def test_grid_random_constant_and_monotone():
+    r = grid_tune(lambda x: 5.0, 0.0, 8.0)
+    assert r.best_sp == 1.0 and r.best_time == 5.0
+    r = grid_tune(lambda x: -x, 0.0, 8.0)
+    assert r.best_sp == 8.0
+    r = random_tune(lambda x: 7.0, 0.0, 8.0, draws=1, seed=3)
+    assert r.best_time == 7.0 and len(r.log) == 1
+
+
+def test_retune_trigger_examples():
+    assert not retune_trigger(1.0, 1.0, 0.1)
+    assert retune_trigger(1.2, 1.0, 0.1)
+    assert not retune_trigger(1.05, 1.0, 0.1)
+    with pytest.raises(ValueError):
+        retune_trigger(1.0, 0.0, 0.1)

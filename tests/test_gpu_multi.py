@@ -9,7 +9,7 @@ import pytest
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TOL = {"c1_f32": 1e-4, "bf16_p": 2e-2}
+TOL = {"c1_f32": 1e-4, "bf16_p": 2e-2}  # bf16_p_<schedule> variants use the bf16 tolerance
 
 
 def _ngpus():
@@ -32,5 +32,6 @@ def test_multi_gpu_parity(P):
     for rank, res in enumerate(per_rank):
         for case, r in res.items():
             assert r["routing_exact"], (rank, case)
-            bad = {k: v for k, v in r.items() if k != "routing_exact" and not v <= TOL[case]}
+            tol = TOL.get(case, TOL["bf16_p"])
+            bad = {k: v for k, v in r.items() if k != "routing_exact" and not v <= tol}
             assert not bad, (rank, case, bad)

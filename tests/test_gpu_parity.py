@@ -228,3 +228,30 @@ def test_compute_lanes_bitwise_identical(name):
     b = run_block_gpu(cfg, rep, wk, compute_streams=cfg.R)
     for n in ("y", "dx", "grad_flat", "dw1", "db1", "dw2", "db2", "logits", "idx", "pos", "counts"):
         assert np.array_equal(a[n], b[n]), n
+
+
+@pytest.mark.parametrize("schedule", ["flowmoe_ar", "flowmoe_at", "pipe_moe"])
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_schedule_policies_bitwise_identical(schedule, lanes):
+    """The Table 6 policies change only the schedule (AT split or not, AR pipelined or
+    centralized): same effective R gives bit-identical results (P=1)."""
+    cfg = CASES["c2_bench"]
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    a = run_block_gpu(cfg, rep, wk, compute_streams=lanes)
+    b = run_block_gpu(cfg, rep, wk, compute_streams=lanes, schedule=schedule)
+    for n in ("y", "dx", "grad_flat", "dw1", "db1", "dw2", "db2", "idx", "pos", "counts"):
+        assert np.array_equal(a[n], b[n]), n
+
+
+def test_vanilla_ep_is_the_unchunked_block():
+    """VANILLA_EP runs the block as one chunk (R = 1, capacity over all tokens)."""
+    cfg = CASES["bf16_small"]
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    g = run_block_gpu(cfg, rep, wk, schedule="vanilla_ep")
+    ys, dxs, gflat, eg, st = oracle_block(cfg.replace(R=1), rep, [wk])
+    assert rel(g["y"], ys[0]) <= TOL["bf16"]
+    assert rel(g["dx"], dxs[0]) <= TOL["bf16"]
+    assert rel(g["grad_flat"], gflat) <= TOL["bf16"]
+    assert np.array_equal(g["counts"], st.route[0].counts)
