@@ -75,6 +75,14 @@ struct flowmoe_ctx {
   SavedLayout L{};
   // backward workspaces (ctx-owned, reused by every block)
   void *dyc = nullptr, *dye = nullptr, *dz = nullptr, *dxe = nullptr, *dxc = nullptr;
+  // workspaces read by the weight-grad stream come in two sets when that stream is
+  // separate, so block l's wgrads overlap block l-1's backward (set = call parity)
+  void *ws_dyc[2] = {}, *ws_dye[2] = {}, *ws_dz[2] = {}, *ws_dA[2] = {}, *ws_dqkv[2] = {};
+  float* ws_dl[2] = {};
+  cudaEvent_t ev_wg_done[2] = {};
+  unsigned long long wg_cap_id[2] = {};  // capture id at record time (0 = eager)
+  bool wg_recorded[2] = {false, false};
+  uint64_t bwd_calls = 0;
   void *dA = nullptr, *dctx = nullptr, *dqkv = nullptr;
   float *dl = nullptr, *dw = nullptr, *Dbuf = nullptr, *wg_part = nullptr;
   std::vector<void*> allocs;
@@ -290,6 +298,13 @@ flowmoe_status a2a_to_owners(flowmoe_ctx* x, const void* send, void* recv, int r
 }
 
 // fork: every compute lane waits for the caller's stream
+unsigned long long capture_id(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &id) != cudaSuccess || st != cudaStreamCaptureStatusActive) return 0;
+  return id;
+}
+
 flowmoe_status fork_lanes(flowmoe_ctx* x, cudaStream_t stream) {
   FM_CUDA(cudaEventRecord(x->ev_in, stream));
   for (cudaStream_t l : x->lanes) FM_CUDA(cudaStreamWaitEvent(l, x->ev_in, 0));
@@ -486,15 +501,25 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   };
   const size_t es = x->es;
   const int64_t R = x->cfg.R, ECM = x->E * x->C * x->M;
-  bool ok = alloc(&x->dyc, R * ECM * es) && alloc(&x->dxe, R * ECM * es) &&
-            alloc(&x->dz, (size_t)R * x->E * x->C * x->F * es) && alloc(&x->dA, x->T * x->M * es) &&
-            alloc(&x->dctx, x->T * x->M * es) && alloc(&x->dqkv, x->T * 3 * x->M * es) &&
-            alloc((void**)&x->dl, x->T * x->E * 4) && alloc((void**)&x->dw, x->T * x->k * 4) &&
-            alloc((void**)&x->Dbuf, x->T * x->H * 4) &&
+  bool ok = alloc(&x->dxe, R * ECM * es) && alloc(&x->dctx, x->T * x->M * es) &&
+            alloc((void**)&x->dw, x->T * x->k * 4) && alloc((void**)&x->Dbuf, x->T * x->H * 4) &&
             alloc((void**)&x->wg_part, gate_wgrad_scratch_floats((int)x->T, (int)x->M, (int)x->E) * 4);
-  if (ok && x->P > 1) ok = alloc(&x->dye, R * ECM * es) && alloc(&x->dxc, R * ECM * es);
+  const int nsets = x->s_wg != x->s_comp ? 2 : 1;
+  for (int st = 0; st < nsets && ok; ++st) {
+    ok = alloc(&x->ws_dyc[st], R * ECM * es) && alloc(&x->ws_dz[st], (size_t)R * x->E * x->C * x->F * es) &&
+         alloc(&x->ws_dA[st], x->T * x->M * es) && alloc(&x->ws_dqkv[st], x->T * 3 * x->M * es) &&
+         alloc((void**)&x->ws_dl[st], x->T * x->E * 4);
+    if (ok && x->P > 1) ok = alloc(&x->ws_dye[st], R * ECM * es);
+    if (x->P == 1) x->ws_dye[st] = x->ws_dyc[st];
+    if (ok && !mk(&x->ev_wg_done[st])) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  }
+  for (int st = nsets; st < 2; ++st) {
+    x->ws_dyc[st] = x->ws_dyc[0]; x->ws_dye[st] = x->ws_dye[0]; x->ws_dz[st] = x->ws_dz[0];
+    x->ws_dA[st] = x->ws_dA[0]; x->ws_dqkv[st] = x->ws_dqkv[0]; x->ws_dl[st] = x->ws_dl[0];
+  }
+  if (ok && x->P > 1) ok = alloc(&x->dxc, R * ECM * es);
   if (!ok) return cleanup_fail(fail(FLOWMOE_ERR_OOM, "workspace allocation failed"));
-  if (x->P == 1) { x->dye = x->dyc; x->dxc = x->dxe; }
+  if (x->P == 1) x->dxc = x->dxe;
   if (x->dt == DT_BF16 && gemm_tc_init() != 0)
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable"));
   if (x->P > 1) {
@@ -691,6 +716,14 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   const int gacc = x->cfg.grad_mode == FLOWMOE_GRAD_ACCUMULATE;
   const int gepi = gacc ? EPI_ACC_F32 : EPI_STORE_F32;
   if (flowmoe_status st = fork_lanes(x, stream)) return st;
+  const int wset = x->ev_wg_done[1] ? (int)(x->bwd_calls++ & 1) : 0;
+  x->dyc = x->ws_dyc[wset]; x->dye = x->ws_dye[wset]; x->dz = x->ws_dz[wset];
+  x->dA = x->ws_dA[wset]; x->dqkv = x->ws_dqkv[wset]; x->dl = x->ws_dl[wset];
+  // the wgrads that last read this workspace set must be done; an event recorded in
+  // another capture (or outside the current one) is already ordered by the graph /
+  // stream boundary, and waiting on it would break the capture
+  if (x->ev_wg_done[1] && x->wg_recorded[wset] && x->wg_cap_id[wset] == capture_id(stream))
+    for (cudaStream_t l : x->lanes) FM_CUDA(cudaStreamWaitEvent(l, x->ev_wg_done[wset], 0));
   // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the owner-side buffer, dw = <dO, Y>
   for (int r = R - 1; r >= 0; --r) {
     cudaStream_t sc = x->lanes[r % nl];
@@ -830,8 +863,21 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
   // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2); centralized
   // policies defer every block's AR until the backward pass is over (allreduce_wait).
-  FM_CUDA(cudaEventRecord(x->ev_done, sc));
   FM_CUDA(cudaEventRecord(x->ev_bwd_done, sc));
+  if (x->ev_wg_done[1]) {
+    FM_CUDA(cudaEventRecord(x->ev_wg_done[wset], sc));
+    x->wg_recorded[wset] = true;
+    x->wg_cap_id[wset] = capture_id(sc);
+  }
+  // dx is ready once the lanes are done; with a separate wgrad stream the caller does
+  // not wait for the wgrads (they finish under the next block's backward, and every
+  // AR ticket / allreduce_wait orders after them)
+  if (sc != x->lanes[0]) {
+    if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
+    FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
+  } else {
+    FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  }
   if (x->ar_pipelined) {
     if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
     if (flowmoe_status s = submit_ar(x, gf, (size_t)(3 * M * M), chunk_bytes, x->ev_grads_b)) return s;
@@ -905,6 +951,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
     for (auto e : *v) if (e) cudaEventDestroy(e);
   for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
   for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);
+  for (auto e : x->ev_wg_done) if (e) cudaEventDestroy(e);
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);
   if (x->s_wg && x->s_wg != x->s_comp) cudaStreamDestroy(x->s_wg);
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b, x->ev_bwd_done}) if (e) cudaEventDestroy(e);

@@ -464,7 +464,7 @@ int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t
 
 // ------------------------------------------------------------------ dWg
 // part[sp][m][e] = Σ_{t in split sp} A[t][m] dl[t][e]; then dwg[m][e] += Σ_sp part (in order).
-constexpr int GW_SPLIT_T = 128;
+constexpr int GW_SPLIT_T = 32;
 
 template <typename T, int E>
 __global__ void __launch_bounds__(128) gate_wgrad_part_kernel(const T* a, const float* dl,
@@ -523,20 +523,31 @@ int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float
 }
 
 // ------------------------------------------------------------------ bias grads
+// out[b][n] (+)= Σ_r x[b][r][n].  Block (32 columns x 8 row groups): thread (tx, ty)
+// sums rows ty, ty+8, ...; the 8 partials are added in a fixed order (deterministic).
 template <typename T>
-__global__ void colsum_acc_kernel(const T* x, float* out, int rows, int N, int accumulate) {
+__global__ void __launch_bounds__(256) colsum_acc_kernel(const T* x, float* out, int rows, int N, int accumulate) {
   FM_PDL_ENTRY();
-  const int n = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
-  if (n >= N) return;
+  __shared__ float part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + tx, b = blockIdx.y;
   const T* xb = x + (int64_t)b * rows * N;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += to_f<T>(xb[(int64_t)r * N + n]);
-  out[(int64_t)b * N + n] = accumulate ? out[(int64_t)b * N + n] + s : s;
+  if (n < N)
+    for (int r = ty; r < rows; r += 8) s += to_f<T>(xb[(int64_t)r * N + n]);
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += part[i][tx];
+    out[(int64_t)b * N + n] = accumulate ? out[(int64_t)b * N + n] + t : t;
+  }
 }
 
 int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
                cudaStream_t s) {
-  dim3 grid((N + 255) / 256, batch);
+  dim3 grid((N + 31) / 32, batch);
   if (dtype == DT_F32) launch_k(colsum_acc_kernel<float>, grid, 256, 0, s, (const float*)x, out, rows, N, accumulate);
   else launch_k(colsum_acc_kernel<bf16>, grid, 256, 0, s, (const bf16*)x, out, rows, N, accumulate);
   return (int)cudaGetLastError();

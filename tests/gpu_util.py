@@ -89,3 +89,56 @@ def oracle_block(cfg: BlockConfig, rep: dict, wks: list[dict], forced: bool = Tr
 def expert_grads(eg: dict, lo: int, hi: int):
     return {name: np.stack([eg[e][i] for e in range(lo, hi)])
             for i, name in enumerate(("dw1", "db1", "dw2", "db2"))}
+
+
+def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: int = 1,
+                  schedule: str = "flowmoe", graph: bool = False, device: int = 0) -> dict:
+    """L = len(reps) blocks chained through the C ABI on one rank (forced routing per
+    block from wk['forced'][l]): forward x -> y_L, backward from wk['dy'] to dx_0."""
+    import torch
+    dev = torch.device("cuda", device)
+    torch.cuda.set_device(dev)
+    ctx = fm.FlowMoE(shape_of(cfg, 1, 0, "overwrite", compute_streams, schedule), device, None)
+    L = len(reps)
+    bts = [fm.BlockTensors(r, cfg.dtype, 0, 1, dev) for r in reps]
+    xs = [fm.to_device(wk["x"], cfg.dtype, dev)] + [None] * L
+    for l in range(L):
+        xs[l + 1] = torch.empty_like(xs[0])
+    dxs = [torch.empty_like(xs[0]) for _ in range(L)]
+    dy = fm.to_device(wk["dy"], cfg.dtype, dev)
+    saved = [torch.empty(ctx.saved_bytes, dtype=torch.uint8, device=dev) for _ in range(L)]
+    forced = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.int32)).to(dev) for f in wk["forced"]]
+
+    def iteration(s):
+        for l in range(L):
+            ctx.set_forced_routing(forced[l])
+            ctx.block_fwd(bts[l].params, xs[l], xs[l + 1], saved[l], s)
+        g, tickets = dy, []
+        for l in reversed(range(L)):
+            tickets.append(ctx.block_bwd(bts[l].params, xs[l], saved[l], g, dxs[l], bts[l].grads, 1 << 20, s))
+            g = dxs[l]
+        for t in tickets:
+            ctx.allreduce_wait(t, s)
+
+    s = torch.cuda.current_stream()
+    iteration(s)
+    if graph:  # capture the same iteration and replay it twice (overwrite grads -> same values)
+        for bt in bts:
+            for v in bt.g.values():
+                v.fill_(7.0)
+        gr = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(s)
+        with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
+            iteration(torch.cuda.current_stream())
+        gr.replay()
+        gr.replay()
+    torch.cuda.synchronize()
+    out = {"y": fm.to_host_f64(xs[L]), "dx": fm.to_host_f64(dxs[0]),
+           "grad_flat": [bt.g["grad_flat"].cpu().numpy().astype(np.float64) for bt in bts],
+           "dw1": [bt.g["dw1"].cpu().numpy().astype(np.float64) for bt in bts]}
+    if graph:
+        del gr
+        torch.cuda.synchronize()
+    ctx.close()
+    return out

@@ -255,3 +255,43 @@ def test_vanilla_ep_is_the_unchunked_block():
     assert rel(g["dx"], dxs[0]) <= TOL["bf16"]
     assert rel(g["grad_flat"], gflat) <= TOL["bf16"]
     assert np.array_equal(g["counts"], st.route[0].counts)
+
+
+@pytest.mark.parametrize("dtype,lanes,graph", [("f32", 1, False), ("bf16", 4, False), ("bf16", 4, True),
+                                               ("f32", 2, True)])
+def test_block_stack_chain_parity(dtype, lanes, graph):
+    """3 chained blocks (different weights, forced routing): forward y_3 and backward dx_0
+    plus every block's grads vs the oracle chain; exercises cross-block reuse of the
+    ctx workspaces, compute lanes, the overlapped weight-grad stream, CUDA-graph replay."""
+    from tests.gpu_util import run_stack_gpu
+    base = CASES["c2_bench"] if dtype == "bf16" else CASES["c1_f32"].replace(R=4, residual=1, causal=1)
+    cfg = base
+    L = 3
+    reps = [gen_replicated(cfg, block=l) for l in range(L)]
+    wk = gen_worker(cfg, 0)
+    wk["forced"] = [gen_worker(cfg, 0, block=l)["forced_idx"] for l in range(L)]
+    g = run_stack_gpu(cfg, reps, wk, compute_streams=lanes, graph=graph)
+    xs, sts = [wk["x"]], []
+    for l in range(L):
+        ys, st = o.block_forward(cfg, reps[l], [xs[-1]], [wk["forced"][l]])
+        xs.append(ys[0])
+        sts.append(st)
+    dy, grads = wk["dy"], [None] * L
+    for l in reversed(range(L)):
+        dxs, gflat, eg = o.block_backward(cfg, reps[l], sts[l], [dy])
+        grads[l] = (gflat, np.stack([eg[e][0] for e in range(cfg.E)]))
+        dy = dxs[0]
+    # bf16 rounding of every activation compounds through the chain: the tolerance
+    # scales with depth; the f32 cases and the bitwise lanes==1 check prove the logic
+    tol = TOL[dtype] * (L if dtype == "bf16" else 1)
+    if dtype == "bf16":
+        ref = run_stack_gpu(cfg, reps, wk, compute_streams=1, graph=False)
+        for n in ("y", "dx"):
+            assert np.array_equal(g[n], ref[n]), n
+        for l in range(L):
+            assert np.array_equal(g["grad_flat"][l], ref["grad_flat"][l]) and np.array_equal(g["dw1"][l], ref["dw1"][l])
+    assert rel(g["y"], xs[-1]) <= tol
+    assert rel(g["dx"], dy) <= tol
+    for l in range(L):
+        assert rel(g["grad_flat"][l], grads[l][0]) <= tol, l
+        assert rel(g["dw1"][l], grads[l][1]) <= tol, l
