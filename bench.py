@@ -29,7 +29,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "MoE block iteration ms & tokens/s at 1/2/4/8 B200; exposed comm %"  # BASELINE.json metric
 LAYERS = {"c1": 1, "c2": 12, "c3": 4, "c4": 4, "dsv2s": 4}   # Table 3 L for c2; §8(d) L in {1,4} else
-SP_DEFAULT = {"c1": 1 << 16, "c2": 1 << 20, "c3": 4 << 20, "c4": 4 << 20, "dsv2s": 4 << 20}
+# S_p defaults from BO on 2x B200 (profiles/r01/tune/): NCCL's per-call cost on NVLink puts the
+# optimum at (or near) the whole per-block tensor; 0 = whole tensor
+SP_DEFAULT = {"c1": 0, "c2": 0, "c3": 16 << 20, "c4": 0, "dsv2s": 0}
 CONFIG_NAMES = {
     "c1": "configs[0] single fp32 MoE block (T=256, M=64, 4 heads, E=4 top-2, F=128, R=2)",
     "c2": "configs[1] GPT2-Tiny-MoE-shaped block stack (M=256, 4 heads, E=8 top-2, F=512, R=4, L=12)",
@@ -218,6 +220,9 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     S_p = args.chunk_bytes or SP_DEFAULT[args.config]
+    if S_p <= 0:  # whole per-block AR tensor in one chunk
+        S_p = 4 * (4 * cfg.M * cfg.M + cfg.M * cfg.E)
+    S_p = (S_p + 15) // 16 * 16
     if args.compute_streams < 0:
         args.compute_streams = cfg.R
     shape = fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,

@@ -85,6 +85,7 @@ struct flowmoe_ctx {
   uint64_t bwd_calls = 0;
   void *dA = nullptr, *dctx = nullptr, *dqkv = nullptr;
   float *dl = nullptr, *dw = nullptr, *Dbuf = nullptr, *wg_part = nullptr;
+  unsigned int* route_done = nullptr;  // [R] last-CTA counters of the fused gate+route kernel
   std::vector<void*> allocs;
   const int32_t* forced = nullptr;
   // scheduling policy (flowmoe_schedule): AT split into R subtasks? AR chunked per block?
@@ -501,7 +502,9 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   };
   const size_t es = x->es;
   const int64_t R = x->cfg.R, ECM = x->E * x->C * x->M;
-  bool ok = alloc(&x->dxe, R * ECM * es) && alloc(&x->dctx, x->T * x->M * es) &&
+  bool ok = alloc((void**)&x->route_done, R * sizeof(unsigned int)) &&
+            cudaMemset(x->route_done, 0, R * sizeof(unsigned int)) == cudaSuccess &&
+            alloc(&x->dxe, R * ECM * es) && alloc(&x->dctx, x->T * x->M * es) &&
             alloc((void**)&x->dw, x->T * x->k * 4) && alloc((void**)&x->Dbuf, x->T * x->H * 4) &&
             alloc((void**)&x->wg_part, gate_wgrad_scratch_floats((int)x->T, (int)x->M, (int)x->E) * 4);
   const int nsets = x->s_wg != x->s_comp ? 2 : 1;
@@ -614,17 +617,27 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.A = ctxb; g.lda = M; g.B = p->wo; g.ldb = M; g.C = a; g.ldc = M;
     if (x->cfg.residual) { g.resid = xr; g.ldr = M; }
     FM_GEMM(KK_OPROJ, g);
-    FM_KP(KK_GATE, 1, 2.0 * Ta * M * E, (double)Ta * M * es + M * E * es + Ta * E * 4.0 + Ta * k * 8.0, sc,
-          gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr, at<float>(saved, L.logits + t0 * E * 4),
-                    at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4), (int)Ta, (int)M,
-                    (int)E, (int)k, sc));
+    if (x->at_split) {  // gate + routing scan of chunk ai in one launch (last-CTA scan)
+      FM_KP(KK_GATE, 1, 2.0 * Ta * M * E, (double)Ta * M * es + M * E * es + Ta * E * 4.0 + Ta * k * 20.0, sc,
+            gate_route(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr, at<float>(saved, L.logits + t0 * E * 4),
+                       at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
+                       at<int32_t>(saved, L.pos + t0 * k * 4), at<int32_t>(saved, L.counts + ai * E * 4),
+                       at<int32_t>(saved, L.src + ai * E * C * 4), x->route_done + ai, (int)Ta, (int)M, (int)E,
+                       (int)k, (int)C, sc));
+    } else {
+      FM_KP(KK_GATE, 1, 2.0 * Ta * M * E, (double)Ta * M * es + M * E * es + Ta * E * 4.0 + Ta * k * 8.0, sc,
+            gate_topk(dt, a, p->wg, x->forced ? x->forced + t0 * k : nullptr, at<float>(saved, L.logits + t0 * E * 4),
+                      at<int32_t>(saved, L.idx + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4), (int)Ta, (int)M,
+                      (int)E, (int)k, sc));
+    }
    for (int r = x->at_split ? ai : 0; r < (x->at_split ? ai + 1 : R); ++r) {
     const int64_t t0 = r * Tr;
     void* a = at<char>(saved, L.a + t0 * M * es);
     int32_t* src = at<int32_t>(saved, L.src + r * E * C * 4);
-    FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc,
-          route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
-                     at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
+    if (!x->at_split)
+      FM_KP(KK_ROUTE, 1, 0, Tr * k * 12.0 + E * C * 4.0 + E * 4.0, sc,
+            route_scan(at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
+                       at<int32_t>(saved, L.counts + r * E * 4), src, (int)Tr, (int)E, (int)k, (int)C, sc));
     FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc,
           permute_pack(dt, a, src, at<char>(saved, L.send + r * C * M * es), (int)E, (int)C, (int)ldE, (int)M,
                        (int)k, sc));
@@ -827,7 +840,7 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     g.M = (int)Tb; g.N = (int)M; g.K = (int)M;
     g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
     FM_GEMM(KK_DCTX, g);
-    FM_KP(KK_ATTN_B, 3, 10.0 * Tb * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tb * 8 * M * es, sc,
+    FM_KP(KK_ATTN_B, attn_tc_supported(dt, (int)M, (int)x->H) ? 2 : 3, 10.0 * Tb * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tb * 8 * M * es, sc,
           attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
                    at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf + t0 * x->H, (int)Tb, (int)x->N, (int)M,
                    (int)x->H, x->cfg.causal, sc));

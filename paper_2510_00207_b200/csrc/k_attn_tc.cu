@@ -60,6 +60,21 @@ FM_DEV void store_row_bf16(bf16* dst, const float* v, int n) {  // n multiple of
     if (i < n) store16<bf16>(dst + i, v + i);
 }
 
+// D = <O_row, dO_row> over one head's DH columns (16-byte loads)
+template <int DH>
+FM_DEV float row_dot_bf16(const bf16* o, const bf16* g) {
+  float acc = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < DH; c += 8) {
+    float a[8], b[8];
+    load16<bf16>(o + c, a);
+    load16<bf16>(g + c, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc = fmaf(a[i], b[i], acc);
+  }
+  return acc;
+}
+
 // ============================================================== forward
 // grid (ceil(N/128), H, n_seq_in_chunk); qkv map over the chunk [T_r][3M].
 template <int DH>
@@ -240,8 +255,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 template <int DH>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                            const float* lse, const float* Dv, bf16* dqkv, int N, int M, int H,
-                            int causal, float scale_log2, float scale) {
+                            const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int M,
+                            int H, int causal, float scale_log2, float scale) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -342,7 +357,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       {
         const int qi = qbase + t128;
         sL[t128] = qi < N ? lse[(int64_t)(row_base + qi) * H + h] * LOG2E : 0.f;
-        sD[t128] = qi < N ? Dv[(int64_t)(row_base + qi) * H + h] : 0.f;
+        const int64_t ro = (int64_t)(row_base + qi) * M + h * DH;
+        sD[t128] = qi < N ? row_dot_bf16<DH>(ctxO + ro, dctx + ro) : 0.f;
       }
       named_bar_sync(1, 128);
       mbar_wait(s_full, it & 1);
@@ -404,8 +420,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 template <int DH, int STAGES>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                          const float* lse, const float* Dv, bf16* dqkv, int N, int M, int H,
-                          int causal, float scale_log2, float scale) {
+                          const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int M,
+                          int H, int causal, float scale_log2, float scale) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -495,7 +511,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int qrow = q0 + rloc;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float L2 = qrow < N ? lse[(int64_t)(row_base + qrow) * H + h] * LOG2E : 0.f;
-    const float Dq = qrow < N ? Dv[(int64_t)(row_base + qrow) * H + h] : 0.f;
+    const float Dq = qrow < N ? row_dot_bf16<DH>(ctxO + (int64_t)(row_base + qrow) * M + h * DH,
+                                                 dctx + (int64_t)(row_base + qrow) * M + h * DH) : 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
@@ -596,20 +613,22 @@ static int attn_bwd_tc_t(const void* qkv, const void* ctx, const float* lse, con
   CUtensorMap tq, tdo;
   if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
   if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, T_, M, 64, 128)) return rc;
-  launch_k(attn_bwd_pre_tc_kernel, (T_ * 32 + 255) / 256, 256, 0, s, (const bf16*)ctx, (const bf16*)dctx, D, T_, M, H);
+  (void)D;  // D = rowsum(dO ⊙ O) is computed inside the two kernels
   const float scale = 1.0f / sqrtf((float)DH), sl2 = LOG2E * scale;
   dim3 grid((N + 127) / 128, H, T_ / N);
   auto k1 = attn_bwd_dkdv_tc_kernel<DH>;
   const size_t sm1 = dkdv_smem<DH>();
   static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1), true);
   (void)once1;
-  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, M,
+           H, causal, sl2, scale);
   constexpr int ST = DH == 128 ? 1 : 2;
   auto k2 = attn_bwd_dq_tc_kernel<DH, ST>;
   const size_t sm2 = dq_smem<DH, ST>();
   static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2), true);
   (void)once2;
-  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, D, (bf16*)dqkv, N, M, H, causal, sl2, scale);
+  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, M,
+           H, causal, sl2, scale);
   return (int)cudaGetLastError();
 }
 

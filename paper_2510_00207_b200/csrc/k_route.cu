@@ -29,19 +29,29 @@ FM_DEV void load_row(const T* p, float* out) {
   }
 }
 
+__device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
+                                int E, int k, int C, int* hist, int* warp_tot);
+
 // ------------------------------------------------------------------ K1
 // One warp per token.  Lane l owns row elements [8l + 256i, 8l + 256i + 8) (bf16)
 // or [4l + 128i, ...) (f32) and keeps E partial dot products; xor-reduce gives
 // every lane all E logits, then top-k by repeated argmax (strictly greater ->
 // lower index wins ties).
+// With `done` != nullptr the kernel also runs K2: the CTA that finishes last (atomic
+// ticket on done[0], reset afterwards) performs the deterministic routing scan of the
+// whole chunk, saving a launch.
 template <typename T, int E>
 __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
                                                         const int32_t* forced, float* logits,
                                                         int32_t* idx, float* w, int T_, int M,
-                                                        int k) {
+                                                        int k, int32_t* pos, int32_t* counts,
+                                                        int32_t* src, int C, unsigned int* done) {
   FM_PDL_ENTRY();
+  extern __shared__ int hist[];  // [E][blockDim.x] for the fused scan
+  __shared__ int warp_tot[32];
+  __shared__ unsigned int ticket;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= T_) return;
+  if (warp < T_) {
   constexpr int V = 16 / sizeof(T);
   float acc[E];
 #pragma unroll
@@ -66,7 +76,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
     for (int e = 0; e < E; ++e) if (e == lane) mine = acc[e];
     logits[(int64_t)warp * E + lane] = mine;
   }
-  if (lane != 0) return;
+  if (lane == 0) {
   // top-k selection on logits
   uint64_t taken = 0;
   int sel[8];
@@ -104,6 +114,17 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
     for (int j = 0; j < k; ++j) { ex[j] = expf(lsel[j] - mx); den += ex[j]; }
     for (int j = 0; j < k; ++j) w[(int64_t)warp * k + j] = ex[j] / den;
   }
+  }  // lane 0
+  }  // warp < T_
+  if (done == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(done, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();  // every CTA's idx is visible
+  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, warp_tot);
+  if (threadIdx.x == 0) *done = 0u;  // ready for the next use (stream-ordered)
 }
 
 #define FM_E_SWITCH(E_, F, ...)                                 \
@@ -120,20 +141,39 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
 template <int E>
 static void gate_topk_launch(int dtype, const void* a, const void* wg, const int32_t* forced,
                              float* logits, int32_t* idx, float* w, int T_, int M, int k,
+                             int32_t* pos, int32_t* counts, int32_t* src, int C, unsigned int* done,
                              cudaStream_t s) {
   dim3 grid((T_ * 32 + 255) / 256);
-  if (dtype == DT_F32)
-    launch_k(gate_topk_kernel<float, E>, grid, 256, 0, s, (const float*)a, (const float*)wg, forced,
-                                                   logits, idx, w, T_, M, k);
-  else
-    launch_k(gate_topk_kernel<bf16, E>, grid, 256, 0, s, (const bf16*)a, (const bf16*)wg, forced,
-                                                  logits, idx, w, T_, M, k);
+  const size_t smem = done ? (size_t)E * 256 * sizeof(int) : 0;
+  if (dtype == DT_F32) {
+    static bool once = (cudaFuncSetAttribute(gate_topk_kernel<float, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             E * 256 * (int)sizeof(int)), true);
+    (void)once;
+    launch_k(gate_topk_kernel<float, E>, grid, 256, smem, s, (const float*)a, (const float*)wg, forced,
+             logits, idx, w, T_, M, k, pos, counts, src, C, done);
+  } else {
+    static bool once = (cudaFuncSetAttribute(gate_topk_kernel<bf16, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             E * 256 * (int)sizeof(int)), true);
+    (void)once;
+    launch_k(gate_topk_kernel<bf16, E>, grid, 256, smem, s, (const bf16*)a, (const bf16*)wg, forced,
+             logits, idx, w, T_, M, k, pos, counts, src, C, done);
+  }
 }
 
 int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
               int32_t* idx, float* w, int T_, int M, int E, int k, cudaStream_t s) {
   if (T_ <= 0) return 0;
-  FM_E_SWITCH(E, gate_topk_launch, dtype, a, wg, forced, logits, idx, w, T_, M, k, s)
+  FM_E_SWITCH(E, gate_topk_launch, dtype, a, wg, forced, logits, idx, w, T_, M, k, nullptr, nullptr,
+              nullptr, 0, nullptr, s)
+  return (int)cudaGetLastError();
+}
+
+int gate_route(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
+               int32_t* idx, float* w, int32_t* pos, int32_t* counts, int32_t* src, unsigned int* done,
+               int T_, int M, int E, int k, int C, cudaStream_t s) {
+  if (T_ <= 0) return 0;
+  FM_E_SWITCH(E, gate_topk_launch, dtype, a, wg, forced, logits, idx, w, T_, M, k, pos, counts, src,
+              C, done, s)
   return (int)cudaGetLastError();
 }
 
@@ -170,38 +210,45 @@ __device__ int block_excl_scan(int v, int* warp_tot) {
   return res;
 }
 
+// Block-wide deterministic routing scan (one CTA, any block size <= 1024): hist is
+// [E][blockDim.x] ints of dynamic shared memory.
+__device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
+                                int E, int k, int C, int* hist, int* warp_tot) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int n = T_ * k;
+  const int seg = (n + nt - 1) / nt;
+  const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
+  for (int e = 0; e < E; ++e) hist[e * nt + tid] = 0;
+  for (int i = tid; i < E * C; i += nt) src[i] = -1;
+  for (int s = s0; s < s1; ++s) {
+    const int j = s / T_, t = s % T_;
+    hist[idx[(int64_t)t * k + j] * nt + tid] += 1;
+  }
+  __syncthreads();
+  for (int e = 0; e < E; ++e) {
+    int v = hist[e * nt + tid];
+    int ex = block_excl_scan(v, warp_tot);
+    hist[e * nt + tid] = ex;
+    if (tid == nt - 1) counts[e] = ex + v;
+  }
+  __syncthreads();
+  for (int s = s0; s < s1; ++s) {
+    const int j = s / T_, t = s % T_;
+    const int e = idx[(int64_t)t * k + j];
+    const int p = hist[e * nt + tid]++;
+    const bool kept = p < C;
+    pos[(int64_t)t * k + j] = kept ? p : -1;
+    if (kept) src[e * C + p] = t * k + j;
+  }
+}
+
 __global__ void __launch_bounds__(RS_THREADS) route_scan_kernel(const int32_t* idx, int32_t* pos,
                                                                 int32_t* counts, int32_t* src,
                                                                 int T_, int E, int k, int C) {
   FM_PDL_ENTRY();
   extern __shared__ int hist[];  // [E][RS_THREADS]
   __shared__ int warp_tot[32];
-  const int tid = threadIdx.x;
-  const int n = T_ * k;
-  const int seg = (n + RS_THREADS - 1) / RS_THREADS;
-  const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
-  for (int e = 0; e < E; ++e) hist[e * RS_THREADS + tid] = 0;
-  for (int i = tid; i < E * C; i += RS_THREADS) src[i] = -1;
-  for (int s = s0; s < s1; ++s) {
-    const int j = s / T_, t = s % T_;
-    hist[idx[(int64_t)t * k + j] * RS_THREADS + tid] += 1;
-  }
-  __syncthreads();
-  for (int e = 0; e < E; ++e) {
-    int v = hist[e * RS_THREADS + tid];
-    int ex = block_excl_scan(v, warp_tot);
-    hist[e * RS_THREADS + tid] = ex;
-    if (tid == RS_THREADS - 1) counts[e] = ex + v;
-  }
-  __syncthreads();
-  for (int s = s0; s < s1; ++s) {
-    const int j = s / T_, t = s % T_;
-    const int e = idx[(int64_t)t * k + j];
-    const int p = hist[e * RS_THREADS + tid]++;
-    const bool kept = p < C;
-    pos[(int64_t)t * k + j] = kept ? p : -1;
-    if (kept) src[e * C + p] = t * k + j;
-  }
+  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, warp_tot);
 }
 
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_, int E,

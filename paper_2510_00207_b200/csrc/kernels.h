@@ -62,6 +62,11 @@ int attn_bwd_tc(const void* qkv, const void* ctx, const float* lse, const void* 
 // K1: logits = a·Wg (fp32), top-k (ties -> lower index), gate weights.
 int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
               int32_t* idx, float* w, int T, int M, int E, int k, cudaStream_t s);
+// K1+K2 fused: the last CTA of the gate kernel runs the routing scan of the chunk.
+// done: one zero-initialised counter per concurrently running chunk (reset in-kernel).
+int gate_route(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
+               int32_t* idx, float* w, int32_t* pos, int32_t* counts, int32_t* src, unsigned int* done,
+               int T, int M, int E, int k, int C, cudaStream_t s);
 // K2: deterministic slot-major positions; counts[E]; src[E][C] = t*k+j or -1; pos[T][k] (-1 dropped)
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T, int E,
                int k, int C, cudaStream_t s);
