@@ -376,6 +376,7 @@ flowmoe_status flowmoe_debug_set(int key, int value) {
   else if (key == 2) flags = (flags & ~2) | (value ? 2 : 0);
   else if (key == 3) flags = (flags & ~4) | (value ? 4 : 0);
   else if (key == 4) { g_pdl_enabled = value ? 1 : 0; return FLOWMOE_OK; }
+  else if (key == 5) { gemm_tc_force_bn(value); return FLOWMOE_OK; }
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   gemm_tc_set_debug(flags);
   return FLOWMOE_OK;

@@ -8,7 +8,9 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // single-thread MMA issuer, warps 2..5 = epilogue (warp w reads TMEM lanes
-// 32*(w%4) .. +31, one output row per thread).
+// 32*(w%4) .. +31, one output row per thread).  Persistent: grid = min(#tiles,
+// #SMs), the smem ring runs across a CTA's tiles and the accumulator is double-
+// buffered in TMEM so tile i's epilogue overlaps tile i+1's mainloop.
 //
 // Operand layouts (see kernels.h): A K-major [rows][K] or M-major [K][rows];
 // B N-major [K][N] (weights W[in][out]) or K-major [N][K].  All tensors are
@@ -24,6 +26,8 @@ namespace fm {
 
 constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 192;
 static int g_tc_debug = 0;  // bit0: force SIMT for bf16; bit1: swap LBO/SBO of MN-major descs
+static int g_force_bn = 0;  // 0 = wave-aware choice; 64/128/256 = forced tile width (benchmarks)
+void gemm_tc_force_bn(int bn) { g_force_bn = bn; }
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
 int attn_tc_debug_off() { return g_tc_debug & 4; }  // bit2: force the SIMT attention kernels
 
@@ -34,6 +38,10 @@ struct TcArgs {
   int a_mmajor, b_kmajor, nk, dbg;
 };
 
+// Persistent: grid = min(#tiles, #SMs); CTA i walks tiles i, i + grid, ... (n fastest,
+// then m, then batch).  The smem operand ring runs continuously across tiles, and the
+// accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
+// overlaps the TMA loads + MMAs of tile i+1.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
@@ -43,30 +51,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   constexpr uint32_t B_BYTES = BN * TC_BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t RING = STAGES * STAGE_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const int ntn = (p.g.N + BN - 1) / BN, ntm = (p.g.M + TC_BM - 1) / TC_BM;
+  const int num_tiles = ntn * ntm * p.g.batch;
+  // one tile per CTA: the operand ring is free when the epilogue runs, so it doubles
+  // as the staging area and a single TMEM accumulator suffices (smaller footprint)
+  const bool single = num_tiles <= (int)gridDim.x;
+  uint8_t* epi_smem = single ? smem : smem + RING;  // 4 epilogue warps x 2 x 4 KB staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : 32768));
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * TC_BM, b = blockIdx.z;
   const GemmArgs& g = p.g;
+  const uint32_t tmem_cols = single ? BN : 2 * BN;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"((uint32_t)BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -75,25 +86,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
-      for (int kb = 0; kb < p.nk; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) + 1) & 1);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        const int k0 = kb * TC_BK;
-        if (!p.a_mmajor) {
-          tma_load_3d(sa, &tma_a, &full[s], k0, m0, b);
-        } else {
+      // ===== TMA producer: one ring across all tiles of this CTA =====
+      int gk = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
+        for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+          const int s = gk % STAGES;
+          if (gk >= STAGES) mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = kb * TC_BK;
+          if (!p.a_mmajor) {
+            tma_load_3d(sa, &tma_a, &full[s], k0, m0, b);
+          } else {
 #pragma unroll
-          for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d(sa + i * 8192, &tma_a, &full[s], m0 + 64 * i, k0, b);
-        }
-        if (p.b_kmajor) {
-          tma_load_3d(sb, &tma_b, &full[s], k0, n0, b);
-        } else {
+            for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d(sa + i * 8192, &tma_a, &full[s], m0 + 64 * i, k0, b);
+          }
+          if (p.b_kmajor) {
+            tma_load_3d(sb, &tma_b, &full[s], k0, n0, b);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0, b);
+            for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0, b);
+          }
         }
       }
     }
@@ -102,25 +117,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ===== MMA issuer (one thread) =====
       const bool swap = (p.dbg & 2) != 0;
       const uint32_t mn_lbo = swap ? 1024u : 8192u, mn_sbo = swap ? 8192u : 1024u;
-      for (int kb = 0; kb < p.nk; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&full[s], (kb / STAGES) & 1);
+      int gk = 0, it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1, use = it >> 1;
+        if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained this buffer
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+          const int s = gk % STAGES;
+          mbar_wait(&full[s], (gk / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / 16; ++kk) {
-          // K-major: +32 B per UMMA_K=16 inside the 128-B swizzle row; SBO = 8 rows * 128 B.
-          // MN-major: +16 K-rows * 128 B; LBO = 64-element MN block stride (one TMA box).
-          const uint64_t ad = p.a_mmajor ? umma_desc(sa + kk * 2048, mn_lbo, mn_sbo)
-                                         : umma_desc(sa + kk * 32, 16, 1024);
-          const uint64_t bd = p.b_kmajor ? umma_desc(sb + kk * 32, 16, 1024)
-                                         : umma_desc(sb + kk * 2048, mn_lbo, mn_sbo);
-          tc_mma(tmem_base, ad, bd, p.idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            // K-major: +32 B per UMMA_K=16 inside the 128-B swizzle row; SBO = 8 rows * 128 B.
+            // MN-major: +16 K-rows * 128 B; LBO = 64-element MN block stride (one TMA box).
+            const uint64_t ad = p.a_mmajor ? umma_desc(sa + kk * 2048, mn_lbo, mn_sbo)
+                                           : umma_desc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = p.b_kmajor ? umma_desc(sb + kk * 32, 16, 1024)
+                                           : umma_desc(sb + kk * 2048, mn_lbo, mn_sbo);
+            tc_mma(tmem_d, ad, bd, p.idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
         }
-        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);
       }
-      tc_commit(tmem_full);
     }
   } else {
     // ===== epilogue: TMEM -> registers -> swizzled smem tile -> TMA store / reduce-add =====
@@ -130,22 +152,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // 16-byte st.shared) and written by one TMA bulk store, or a TMA bulk
     // reduce-add (fp32 grad accumulation C += acc, done in L2).  Two staging
     // buffers per warp (4 KB each) overlap the next chunk with the in-flight store.
-    // The operand ring is free here (all MMAs, hence all TMA loads, completed).
     const int quarter = warp & 3;
     const int r0 = quarter * 32;
-    const int row = m0 + r0 + lane;
-    uint8_t* stage = smem + quarter * 8192;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const bool row_ok = row < g.M;
+    uint8_t* stage = epi_smem + quarter * 8192;
     const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
-    int buf = 0;
+    int buf = 0, it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
+      const int acc = it & 1, use = it >> 1;
+      const uint32_t tmem_acc = tmem_base + acc * BN;
+      const int row = m0 + r0 + lane;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+    const bool row_ok = row < g.M;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       const int nb = n0 + c0;
       if (nb >= g.N) break;  // warp-uniform
       uint32_t r[32];
-      tmem_ld32(tmem_base + ((uint32_t)r0 << 16) + c0, r);
+      tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
@@ -231,6 +256,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       buf ^= 1;
     }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM reads of this tile are complete
+    }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
     tc_fence_before();
@@ -239,8 +268,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)BN));
+    tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 
@@ -323,12 +351,21 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.a_mmajor ? 1 : 0) << 15) |
             ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
             ((uint32_t)(TC_BM >> 4) << 24);
-  const size_t smem = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024 + 256;
+  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 32768 + 1024 + 256;
   auto kern = gemm_tc_kernel<BN, STAGES>;
-  static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max), true);
   (void)attr_set;
-  dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, g.batch);
-  launch_k(kern, grid, TC_THREADS, smem, s, ma, mb, mc, maux, p);
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM - 1) / TC_BM) * g.batch;
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  const size_t smem = tiles <= grid ? smem_max - 32768 : smem_max;
+  launch_k(kern, dim3(grid), TC_THREADS, smem, s, ma, mb, mc, maux, p);
   return (int)cudaGetLastError();
 }
 
@@ -336,12 +373,16 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0 || g.K <= 0) return 0;
   if (g_tc_debug & 1) return gemm_simt(g, DT_BF16, s);
   if (int rc = gemm_tc_init()) return rc;
-  // Tile width: the widest BN that still fills one wave of the 148 SMs (wide tiles
-  // amortise A re-reads); small, latency-bound GEMMs get narrow tiles and more CTAs.
+  // Tile width (measured, tools/gemm_microbench.py): BN=256 (best MMA/operand efficiency)
+  // whenever it still yields >= 48 tiles; small, latency-bound GEMMs get narrower tiles
+  // and more CTAs.
+  if (g_force_bn == 256) return launch_tc<256, 4>(g, s);
+  if (g_force_bn == 128) return launch_tc<128, 6>(g, s);
+  if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
-  if (g.N >= 256 && tiles(256) >= 148) return launch_tc<256, 4>(g, s);
-  if (g.N >= 128 && tiles(128) >= 148) return launch_tc<128, 6>(g, s);
+  if (g.N >= 256 && tiles(256) >= 48) return launch_tc<256, 4>(g, s);
+  if (g.N >= 128 && tiles(128) >= 48) return launch_tc<128, 6>(g, s);
   return launch_tc<64, 8>(g, s);
 }
 

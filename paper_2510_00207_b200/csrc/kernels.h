@@ -40,6 +40,7 @@ int gemm_simt(const GemmArgs& g, int dtype, cudaStream_t s);
 int gemm_tc(const GemmArgs& g, cudaStream_t s);  // bf16 only, tcgen05/TMEM/TMA
 int gemm_tc_init();                               // resolves cuTensorMapEncodeTiled
 void gemm_tc_set_debug(int flags);
+void gemm_tc_force_bn(int bn);
 
 // ---------------------------------------------------------------- attention
 // qkv [T][3M] (per sequence of N rows; head h at columns h*dh of each of Q|K|V)

@@ -1,0 +1,69 @@
+"""Per-launch device time of the tcgen05 GEMM at the block's shapes, measured inside a
+CUDA graph of `reps` back-to-back launches (so host launch cost is excluded), with
+PDL on/off and forced tile widths.  Prints one JSON line per case."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2510_00207_b200 as fm  # noqa: E402
+
+SHAPES = {  # name: (M rows, N, K, batch, a_mmajor, b_kmajor, epi)
+    "c2_qkv": (256, 768, 256, 1, 0, 0, 0),
+    "c2_oproj": (256, 256, 256, 1, 0, 0, 0),
+    "c2_e1": (64, 512, 256, 8, 0, 0, 0),
+    "c2_e2": (64, 256, 512, 8, 0, 0, 0),
+    "c2_dwqkv": (256, 768, 1024, 1, 1, 0, 4),
+    "c3_e1": (128, 2048, 1024, 16, 0, 0, 0),
+    "c3_qkv": (1024, 3072, 1024, 1, 0, 0, 0),
+    "c4_e1": (128, 16384, 4096, 16, 0, 0, 0),
+    "c4_qkv": (1024, 12288, 4096, 1, 0, 0, 0),
+    "c4_dw1": (4096, 16384, 256, 16, 1, 0, 4),
+}
+
+
+def run(name, reps, bn, pdl):
+    Mr, N, K, batch, am, bk, epi = SHAPES[name]
+    dev = torch.device("cuda", 0)
+    A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
+    B = torch.randn(batch, (N if bk else K), (K if bk else N), device=dev).to(torch.bfloat16) * 0.05
+    C = torch.zeros(batch, Mr, N, device=dev, dtype=torch.float32 if epi == 4 else torch.bfloat16)
+    fm.debug_set(5, bn)
+    fm.debug_set(4, pdl)
+    kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
+              ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi)
+    s = torch.cuda.current_stream()
+    fm.test_gemm("bf16", A, B, C, stream=s, **kw)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(s)
+    with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+        for _ in range(reps):
+            fm.test_gemm("bf16", A, B, C, stream=torch.cuda.current_stream(), **kw)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+    flops = 2.0 * Mr * N * K * batch
+    print(json.dumps({"shape": name, "bn": bn, "pdl": pdl, "us_per_launch": round(us, 3),
+                      "tflops": round(flops / us / 1e6, 1)}), flush=True)
+    del g
+
+
+if __name__ == "__main__":
+    for name in SHAPES:
+        reps = 200 if name.startswith("c2") else (50 if name.startswith("c3") else 10)
+        for bn in (0, 64, 128, 256):
+            for pdl in (1, 0):
+                if bn and pdl == 0:
+                    continue
+                run(name, reps, bn, pdl)
