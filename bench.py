@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--schedule", default="flowmoe",
                     choices=["flowmoe", "flowmoe_ar", "flowmoe_at", "pipe_moe", "vanilla_ep"],
                     help="scheduling policy (the paper's Table 6 ablation)")
+    ap.add_argument("--a2a", default="p2p", choices=["nccl", "p2p"],
+                    help="A2A: NCCL send/recv groups or peer-memory kernels over NVLink")
     ap.add_argument("--compute-streams", type=int, default=-1,
                     help="compute lanes (1 = paper's single compute stream; default R)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -230,7 +232,8 @@ def main():
                           capacity_factor=cfg.capacity_factor, causal=cfg.causal,
                           residual=cfg.residual, dtype=cfg.dtype, world_size=world, rank=rank,
                           grad_mode="overwrite",  # fresh grads each iteration (zero_grad + backward)
-                          compute_streams=args.compute_streams, schedule=args.schedule)
+                          compute_streams=args.compute_streams, schedule=args.schedule,
+                          a2a_impl=args.a2a)
     ctx = fm.FlowMoE(shape, local, uid)
 
     # ---- resident synthetic state
@@ -401,6 +404,7 @@ def main():
                        "capacity_factor": cfg.capacity_factor, "S_p_bytes": S_p,
                        "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
                        "compute_streams": args.compute_streams, "schedule": args.schedule,
+                       "a2a": args.a2a,
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,

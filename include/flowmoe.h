@@ -66,6 +66,12 @@ typedef enum {
   FLOWMOE_SCHED_PIPE_MOE = 3, FLOWMOE_SCHED_VANILLA_EP = 4
 } flowmoe_schedule;
 
+/* A2A implementation: NCCL grouped send/recv, or peer-memory kernels over NVLink
+ * (buffers mapped with CUDA IPC at create / first use of a `saved` stash — the first
+ * flowmoe_block_fwd of each stash must run outside CUDA-graph capture on every rank,
+ * otherwise that stash falls back to NCCL). */
+typedef enum { FLOWMOE_A2A_NCCL = 0, FLOWMOE_A2A_P2P = 1 } flowmoe_a2a_impl;
+
 typedef struct {
   int64_t B;               /* tokens on this rank (paper B·N); B % seq_len == 0; (B/seq_len) % R == 0 */
   int32_t seq_len;         /* N, tokens per sequence (attention span) */
@@ -87,6 +93,9 @@ typedef struct {
                               compute tasks run in that order on stream r % min(n, R), so chunks
                               whose kernels do not fill the 148 SMs co-run (same results) */
   int32_t schedule;        /* a flowmoe_schedule value; default FLOWMOE */
+  int32_t a2a_impl;        /* a flowmoe_a2a_impl value: NCCL send/recv groups (default) or
+                              stores from this library's kernels into CUDA-IPC-mapped peer
+                              buffers on NVLink (world_size <= 8; results identical) */
 } flowmoe_config;
 
 /* Weights of one block (dtype of the config).  Replicated: wqkv [M][3M] (columns

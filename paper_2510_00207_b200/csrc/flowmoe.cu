@@ -17,7 +17,9 @@
 #include <string.h>
 #include <atomic>
 #include <string>
+#include <map>
 #include <vector>
+#include <cuda.h>
 
 #include "../../include/flowmoe.h"
 #include "kernels.h"
@@ -41,7 +43,7 @@ flowmoe_status fail(flowmoe_status s, const std::string& msg) {
 constexpr int NUM_TICKET_EVENTS = 4096;
 
 struct SavedLayout {
-  size_t qkv, ctx, lse, a, logits, idx, w, pos, counts, src, send, xe, z, h, ye, yc, total;
+  size_t qkv, ctx, lse, a, logits, idx, w, pos, counts, src, send, xe, z, h, ye, yc, dye, total;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -88,6 +90,14 @@ struct flowmoe_ctx {
   unsigned int* route_done = nullptr;  // [R] last-CTA counters of the fused gate+route kernel
   std::vector<void*> allocs;
   const int32_t* forced = nullptr;
+  // ---- A2A over NVLink peer memory (a2a_impl = FLOWMOE_A2A_P2P)
+  bool p2p = false;
+  void* p2p_arena = nullptr;            // [flags 4*R*P | piece counters 4*R*P | seen 4*R | err]
+  unsigned int *flags = nullptr, *piece_cnt = nullptr, *seen = nullptr, *p2p_err = nullptr;
+  std::vector<unsigned int*> peer_flags; // per rank: its flags array (mapped)
+  std::vector<void*> peer_dxc;           // per rank: its dispatch-bwd receive buffer (mapped)
+  std::map<const void*, std::vector<void*>> peer_saved;  // my saved ptr -> each rank's saved ptr
+  std::vector<void*> ipc_opened;         // peer mappings to close at destroy
   // scheduling policy (flowmoe_schedule): AT split into R subtasks? AR chunked per block?
   bool at_split = true, ar_pipelined = true;
   struct PendingAR { float* buf; size_t count; uint64_t ticket; };
@@ -207,6 +217,10 @@ flowmoe_status validate(const flowmoe_config* c) {
     return bad("grad_mode", "must be FLOWMOE_GRAD_ACCUMULATE or FLOWMOE_GRAD_OVERWRITE");
   if (c->schedule < FLOWMOE_SCHED_FLOWMOE || c->schedule > FLOWMOE_SCHED_VANILLA_EP)
     return bad("schedule", "must be a flowmoe_schedule value");
+  if (c->a2a_impl != FLOWMOE_A2A_NCCL && c->a2a_impl != FLOWMOE_A2A_P2P)
+    return bad("a2a_impl", "must be FLOWMOE_A2A_NCCL or FLOWMOE_A2A_P2P");
+  if (c->a2a_impl == FLOWMOE_A2A_P2P && c->world_size > 8)
+    return bad("a2a_impl", "peer-memory A2A supports world_size <= 8 (one NVLink domain)");
   if (c->compute_streams < 0) return bad("compute_streams", "must be >= 0 (0 or 1 = one compute stream)");
   if (c->world_size < 1) return bad("world_size", "must be >= 1");
   if (c->rank < 0 || c->rank >= c->world_size) return bad("rank", "must be in [0, world_size)");
@@ -246,6 +260,9 @@ SavedLayout layout_of(const flowmoe_ctx* x) {
   L.h = take(R * E * C * F * es);
   L.ye = take(R * E * C * M * es);
   L.yc = x->P > 1 ? take(R * E * C * M * es) : L.ye;
+  // P > 1: receive buffer of the backward combine A2A (dY on the expert side), per block so
+  // that peers writing block l-1's dY can never race the wgrads still reading block l's
+  L.dye = x->P > 1 ? take(R * E * C * M * es) : 0;
   L.total = off;
   return L;
 }
@@ -319,6 +336,69 @@ flowmoe_status join_lanes(flowmoe_ctx* x, cudaStream_t dst) {
     FM_CUDA(cudaStreamWaitEvent(dst, x->ev_lane[l], 0));
   }
   return FLOWMOE_OK;
+}
+
+// ---- CUDA-IPC exchange over the A2A communicator (outside graph capture only)
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+struct IpcRec {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+};
+
+// every rank publishes (handle of the allocation containing `ptr`, offset of ptr in it);
+// returns each rank's view pointer (own = ptr)
+flowmoe_status ipc_exchange(flowmoe_ctx* x, void* ptr, std::vector<void*>* out) {
+  static PFN_getAddressRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(FLOWMOE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<PFN_getAddressRange>(fn);
+  }
+  // quiesce: earlier NCCL work of this communicator (any stream) must be done on every
+  // rank before the exchange collective (eager path, once per registered buffer)
+  FM_CUDA(cudaDeviceSynchronize());
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return fail(FLOWMOE_ERR_CUDA, "cuMemGetAddressRange failed");
+  IpcRec mine;
+  FM_CUDA(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)));
+  mine.offset = (uint64_t)((CUdeviceptr)ptr - base);
+  const int P = (int)x->P;
+  IpcRec* d = nullptr;
+  FM_CUDA(cudaMalloc(&d, sizeof(IpcRec) * (P + 1)));
+  FM_CUDA(cudaMemcpy(d + P, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice));
+  FM_NCCL(ncclAllGather(d + P, d, sizeof(IpcRec), ncclUint8, x->comm_a2a, x->s_comp));
+  FM_CUDA(cudaStreamSynchronize(x->s_comp));
+  std::vector<IpcRec> all(P);
+  FM_CUDA(cudaMemcpy(all.data(), d, sizeof(IpcRec) * P, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  out->assign(P, nullptr);
+  for (int q = 0; q < P; ++q) {
+    if (q == x->cfg.rank) { (*out)[q] = ptr; continue; }
+    void* pb = nullptr;
+    FM_CUDA(cudaIpcOpenMemHandle(&pb, all[q].h, cudaIpcMemLazyEnablePeerAccess));
+    x->ipc_opened.push_back(pb);
+    (*out)[q] = reinterpret_cast<char*>(pb) + all[q].offset;
+  }
+  return FLOWMOE_OK;
+}
+
+// P2P usable for this `saved` buffer?  Registers it (collectively) on first sight; a buffer
+// first seen during graph capture uses NCCL (every rank sees the same sequence of calls).
+bool p2p_ready(flowmoe_ctx* x, const void* saved, cudaStream_t stream) {
+  if (!x->p2p) return false;
+  if (x->peer_saved.count(saved)) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return false;
+  std::vector<void*> v;
+  if (ipc_exchange(x, const_cast<void*>(saved), &v) != FLOWMOE_OK) return false;
+  x->peer_saved[saved] = v;
+  return true;
 }
 
 template <typename P_>
@@ -513,8 +593,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     ok = alloc(&x->ws_dyc[st], R * ECM * es) && alloc(&x->ws_dz[st], (size_t)R * x->E * x->C * x->F * es) &&
          alloc(&x->ws_dA[st], x->T * x->M * es) && alloc(&x->ws_dqkv[st], x->T * 3 * x->M * es) &&
          alloc((void**)&x->ws_dl[st], x->T * x->E * 4);
-    if (ok && x->P > 1) ok = alloc(&x->ws_dye[st], R * ECM * es);
-    if (x->P == 1) x->ws_dye[st] = x->ws_dyc[st];
+    x->ws_dye[st] = x->ws_dyc[st];  // P > 1 receives dY into the per-block saved stash
     if (ok && !mk(&x->ev_wg_done[st])) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   }
   for (int st = nsets; st < 2; ++st) {
@@ -539,6 +618,23 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
       return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit failed"));
     x->a2a_comm.push_back(x->comm_a2a);
     x->a2a_stream.push_back(x->s_a2a);
+    if (cfg->a2a_impl == FLOWMOE_A2A_P2P) {
+      const size_t nfl = (size_t)4 * x->cfg.R * x->P;
+      const size_t bytes = (2 * nfl + 4 * x->cfg.R + 1) * sizeof(unsigned int);
+      if (!alloc(&x->p2p_arena, bytes) || cudaMemset(x->p2p_arena, 0, bytes) != cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess)
+        return cleanup_fail(fail(FLOWMOE_ERR_OOM, "p2p arena allocation failed"));
+      x->flags = reinterpret_cast<unsigned int*>(x->p2p_arena);
+      x->piece_cnt = x->flags + nfl;
+      x->seen = x->piece_cnt + nfl;
+      x->p2p_err = x->seen + 4 * x->cfg.R;
+      std::vector<void*> v;
+      if (ipc_exchange(x, x->p2p_arena, &v) != FLOWMOE_OK)
+        return cleanup_fail(FLOWMOE_ERR_CUDA);
+      for (void* q : v) x->peer_flags.push_back(reinterpret_cast<unsigned int*>(q));
+      if (ipc_exchange(x, x->dxc, &x->peer_dxc) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
+      x->p2p = true;
+    }
     for (size_t l = 1; l < x->lanes.size(); ++l) {
       ncclConfig_t nc3 = NCCL_CONFIG_INITIALIZER;
       nc3.blocking = 1;
@@ -593,6 +689,7 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // the per-kernel profile (flowmoe_profile_begin) collapses the lanes so that each
   // kernel's event-timed duration is its own, not shared with co-running chunks
   const int nl = g_prof.on ? 1 : (int)x->lanes.size();
+  const bool use_p2p = P > 1 && p2p_ready(x, saved, stream);
   if (flowmoe_status st = fork_lanes(x, stream)) return st;
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer.
   // Policies that keep AT unsplit (PIPE_MOE, FLOWMOE_AR) run MHA + gate once over all
@@ -651,7 +748,12 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_at[r], 0));
       int pi = prof_start(sa);
-      if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
+      if (use_p2p) {
+        std::vector<void*> dst(P);
+        for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.xe;
+        FM_K(2, a2a_p2p(at<char>(saved, L.send), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
+                        x->p2p_err, 0, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true));
+      } else if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
       prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_d[r], sa));
     }
@@ -684,7 +786,12 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_e[r], 0));
       int pi = prof_start(sa);
-      if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
+      if (use_p2p) {
+        std::vector<void*> dst(P);
+        for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.yc;
+        FM_K(2, a2a_p2p(at<char>(saved, L.ye), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
+                        x->p2p_err, 1, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true));
+      } else if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
       prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_c[r], sa));
     }
@@ -732,6 +839,8 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   if (flowmoe_status st = fork_lanes(x, stream)) return st;
   const int wset = x->ev_wg_done[1] ? (int)(x->bwd_calls++ & 1) : 0;
   x->dyc = x->ws_dyc[wset]; x->dye = x->ws_dye[wset]; x->dz = x->ws_dz[wset];
+  if (P > 1) x->dye = const_cast<char*>(at<char>(saved, L.dye));  // per-block landing buffer
+  const bool use_p2p = P > 1 && p2p_ready(x, saved, stream);
   x->dA = x->ws_dA[wset]; x->dqkv = x->ws_dqkv[wset]; x->dl = x->ws_dl[wset];
   // the wgrads that last read this workspace set must be done; an event recorded in
   // another capture (or outside the current one) is already ordered by the graph /
@@ -755,7 +864,12 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_cb[r], 0));
       int pi = prof_start(sa);
-      if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
+      if (use_p2p) {
+        std::vector<void*> dst(P);
+        for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.dye;
+        FM_K(2, a2a_p2p(x->dyc, dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
+                        x->p2p_err, 2, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true));
+      } else if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
       prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], sa));
     }
@@ -786,7 +900,10 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
       cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_eb[r], 0));
       int pi = prof_start(sa);
-      if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
+      if (use_p2p) {
+        FM_K(2, a2a_p2p(x->dxe, x->peer_dxc.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
+                        x->p2p_err, 3, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true));
+      } else if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
       prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], sa));
     }
@@ -933,6 +1050,11 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
       if (e != ncclSuccess) a = e;
     }
     ncclCommGetAsyncError(x->comm_ar, &b);
+    if (x->p2p) {
+      unsigned int e = 0;
+      cudaMemcpy(&e, x->p2p_err, sizeof(e), cudaMemcpyDeviceToHost);
+      if (e) return fail(FLOWMOE_ERR_STATE, "peer-memory A2A timed out waiting for a peer");
+    }
     if (a != ncclSuccess || b != ncclSuccess)
       return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
   }
@@ -969,6 +1091,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);
   if (x->s_wg && x->s_wg != x->s_comp) cudaStreamDestroy(x->s_wg);
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b, x->ev_bwd_done}) if (e) cudaEventDestroy(e);
+  for (void* p : x->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);
   if (x->s_a2a) cudaStreamDestroy(x->s_a2a);

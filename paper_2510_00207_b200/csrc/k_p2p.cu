@@ -1,0 +1,117 @@
+// A2A over NVLink peer memory: the dispatch / combine exchanges
+// (S6, S8, B1, B3) as stores from this GPU's SMs straight into the peers' receive
+// buffers (CUDA-IPC-mapped), completed by system-scope release counters.
+//
+// Protocol per (kind, chunk) use — no host involvement, CUDA-graph capturable:
+//   sender  : CTAs copy 16-byte vectors of each C×M block to the destination rank's
+//             buffer; each CTA fences (system scope) and bumps a local per-destination
+//             piece counter; the CTA completing a destination fences again and atomically
+//             increments that destination's arrival counter flags[kind][r][me] (remote
+//             atomic over NVLink), then resets the piece counter.
+//   receiver: one CTA waits (acquire loads) until flags[kind][r][src] >= seen + 1 for
+//             every source, then seen += 1.  Counters are monotonic, so graph replays
+//             and repeated blocks need no resets.  A spin bounded by ~10 s sets an error
+//             word instead of hanging (checked by flowmoe_allreduce_wait).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fm {
+
+struct P2PArgs {
+  const uint8_t* src;       // local source buffer (owner or expert side)
+  uint8_t* dst[8];          // per-destination-rank receive buffer (mapped peer pointer or local)
+  unsigned int* peer_flags[8];  // per-destination-rank arrival counters, indexed [kind][R][P]
+  unsigned int* piece_cnt;  // local [kind][R][P] piece counters
+  int kind, r, R, P, El, me;
+  int to_experts;           // 1: owner [E][R][C] -> expert [El][R][P][C]; 0: the reverse
+  int64_t blk_bytes;        // C*M*es
+  int pieces;               // CTAs per (destination, local expert) block
+};
+
+FM_DEV int64_t owner_off(int e, int r, int R, int64_t blk) { return ((int64_t)e * R + r) * blk; }
+FM_DEV int64_t expert_off(int el, int r, int q, int R, int P, int64_t blk) {
+  return (((int64_t)el * R + r) * P + q) * blk;
+}
+
+// grid (pieces, El, P): x = piece of the block, y = local expert, z = destination rank
+__global__ void __launch_bounds__(256) a2a_p2p_send_kernel(P2PArgs a) {
+  FM_PDL_ENTRY();
+  const int piece = blockIdx.x, el = blockIdx.y, q = blockIdx.z;
+  int64_t soff, doff;
+  if (a.to_experts) {  // my owner-side block of expert (q, el) -> q's expert side slot (el, r, me)
+    soff = owner_off(q * a.El + el, a.r, a.R, a.blk_bytes);
+    doff = expert_off(el, a.r, a.me, a.R, a.P, a.blk_bytes);
+  } else {  // my expert-side block (el, r, q) -> q's owner side slot (me*El + el, r)
+    soff = expert_off(el, a.r, q, a.R, a.P, a.blk_bytes);
+    doff = owner_off(a.me * a.El + el, a.r, a.R, a.blk_bytes);
+  }
+  const int64_t per = (a.blk_bytes / 16 + a.pieces - 1) / a.pieces;  // uint4 per piece
+  const int64_t v0 = piece * per, v1 = min(a.blk_bytes / 16, v0 + per);
+  const uint4* s = reinterpret_cast<const uint4*>(a.src + soff);
+  uint4* d = reinterpret_cast<uint4*>(a.dst[q] + doff);
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) d[i] = __ldg(s + i);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* cnt = a.piece_cnt + ((int64_t)a.kind * a.R + a.r) * a.P + q;
+    const unsigned int total = (unsigned int)(a.pieces * a.El);
+    if (atomicAdd(cnt, 1u) == total - 1) {  // every piece for destination q has landed
+      __threadfence_system();
+      atomicAdd_system(a.peer_flags[q] + ((int64_t)a.kind * a.R + a.r) * a.P + a.me, 1u);
+      *cnt = 0u;
+    }
+  }
+}
+
+// one CTA of P threads: wait for all sources of (kind, r)
+__global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* seen, unsigned int* err,
+                                    int kind, int r, int R, int P) {
+  FM_PDL_ENTRY();
+  __shared__ unsigned int expect;
+  if (threadIdx.x == 0) expect = seen[kind * R + r] + 1u;
+  __syncthreads();
+  const int q = threadIdx.x;
+  if (q < P) {
+    const unsigned int* f = flags + ((int64_t)kind * R + r) * P + q;
+    const long long t0 = clock64();
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if ((int)(v - expect) >= 0) break;
+      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: report instead of hanging
+        atomicExch(err, 1u);
+        break;
+      }
+      __nanosleep(64);
+    } while (true);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) seen[kind * R + r] = expect;
+}
+
+int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
+            unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,
+            int El, int me, int to_experts, int64_t blk_bytes, cudaStream_t send_stream,
+            cudaStream_t wait_stream, bool do_send, bool do_wait) {
+  if (P > 8) return (int)cudaErrorInvalidValue;
+  if (do_send) {
+    P2PArgs a;
+    a.src = reinterpret_cast<const uint8_t*>(src);
+    for (int q = 0; q < 8; ++q) {
+      a.dst[q] = q < P ? reinterpret_cast<uint8_t*>(dst[q]) : nullptr;
+      a.peer_flags[q] = q < P ? peer_flags[q] : nullptr;
+    }
+    a.piece_cnt = piece_cnt;
+    a.kind = kind; a.r = r; a.R = R; a.P = P; a.El = El; a.me = me; a.to_experts = to_experts;
+    a.blk_bytes = blk_bytes;
+    a.pieces = (int)((blk_bytes + 32767) / 32768);  // ~32 KB per CTA
+    launch_k(a2a_p2p_send_kernel, dim3(a.pieces, El, P), 256, 0, send_stream, a);
+    if (cudaError_t e = cudaGetLastError()) return (int)e;
+  }
+  if (do_wait) {
+    launch_k(a2a_p2p_wait_kernel, 1, 32, 0, wait_stream, (const unsigned int*)my_flags, seen, err, kind, r, R, P);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace fm

@@ -97,4 +97,10 @@ size_t gate_wgrad_scratch_floats(int T, int M, int E);
 int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
                cudaStream_t s);
 
+// A2A over NVLink peer memory (k_p2p.cu): send (copy + publish) and/or wait for (kind, r).
+int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
+            unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,
+            int El, int me, int to_experts, int64_t blk_bytes, cudaStream_t send_stream,
+            cudaStream_t wait_stream, bool do_send, bool do_wait);
+
 }  // namespace fm

@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
                 ("residual", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("grad_mode", ctypes.c_int32), ("compute_streams", ctypes.c_int32),
-                ("schedule", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32), ("a2a_impl", ctypes.c_int32)]
 
 
 class ProfEntry(ctypes.Structure):
@@ -176,13 +176,14 @@ class BlockShape:
     grad_mode: str = "accumulate"  # or "overwrite"
     compute_streams: int = 1
     schedule: str = "flowmoe"
+    a2a_impl: str = "nccl"  # or "p2p"
 
     def to_c(self) -> Config:
         return Config(self.B, self.seq_len, self.M, self.n_heads, self.E, self.top_k, self.d_ffn,
                       self.R, self.capacity_factor, self.causal, self.residual,
                       FLOWMOE_BF16 if self.dtype == "bf16" else FLOWMOE_F32, self.world_size,
                       self.rank, 1 if self.grad_mode == "overwrite" else 0, self.compute_streams,
-                      SCHEDULES[self.schedule])
+                      SCHEDULES[self.schedule], 1 if self.a2a_impl == "p2p" else 0)
 
 
 class FlowMoE:

@@ -51,7 +51,8 @@ def _subtract(a_iv, b_iv):
 
 
 def is_comm(name: str) -> bool:
-    return name.startswith("nccl") or "ncclDevKernel" in name or "ncclKernel" in name
+    return (name.startswith("nccl") or "ncclDevKernel" in name or "ncclKernel" in name
+            or "a2a_p2p" in name)
 
 
 def short_name(name: str) -> str:

@@ -15,23 +15,24 @@ def rel(g: np.ndarray, r: np.ndarray) -> float:
 
 
 def shape_of(cfg: BlockConfig, P: int, rank: int, grad_mode: str = "accumulate",
-             compute_streams: int = 1, schedule: str = "flowmoe") -> fm.BlockShape:
+             compute_streams: int = 1, schedule: str = "flowmoe", a2a_impl: str = "nccl") -> fm.BlockShape:
     return fm.BlockShape(B=cfg.T, seq_len=cfg.seq_len, M=cfg.M, n_heads=cfg.n_heads, E=cfg.E,
                          top_k=cfg.top_k, d_ffn=cfg.d_ffn, R=cfg.R,
                          capacity_factor=cfg.capacity_factor, causal=cfg.causal,
                          residual=cfg.residual, dtype=cfg.dtype, world_size=P, rank=rank,
-                         grad_mode=grad_mode, compute_streams=compute_streams, schedule=schedule)
+                         grad_mode=grad_mode, compute_streams=compute_streams, schedule=schedule,
+                         a2a_impl=a2a_impl)
 
 
 def run_block_gpu(cfg: BlockConfig, rep: dict, wk: dict, *, P: int = 1, rank: int = 0,
                   forced: bool = True, chunk_bytes: int = 1 << 20, uid: bytes | None = None,
                   device: int = 0, grad_mode: str = "accumulate", repeat_bwd: int = 1,
                   grad_fill: float = 0.0, compute_streams: int = 1,
-                  schedule: str = "flowmoe") -> dict:
+                  schedule: str = "flowmoe", a2a_impl: str = "nccl", repeat: int = 1) -> dict:
     import torch
     dev = torch.device("cuda", device)
     torch.cuda.set_device(dev)
-    ctx = fm.FlowMoE(shape_of(cfg, P, rank, grad_mode, compute_streams, schedule), device, uid)
+    ctx = fm.FlowMoE(shape_of(cfg, P, rank, grad_mode, compute_streams, schedule, a2a_impl), device, uid)
     bt = fm.BlockTensors(rep, cfg.dtype, rank, P, dev)
     if grad_fill:
         for v in bt.g.values():
@@ -46,10 +47,14 @@ def run_block_gpu(cfg: BlockConfig, rep: dict, wk: dict, *, P: int = 1, rank: in
         fidx = torch.from_numpy(np.ascontiguousarray(wk["forced_idx"], dtype=np.int32)).to(dev)
         ctx.set_forced_routing(fidx)
     s = torch.cuda.current_stream()
-    ctx.block_fwd(bt.params, x, y, saved, s)
-    for _ in range(repeat_bwd):
-        t = ctx.block_bwd(bt.params, x, saved, dy, dx, bt.grads, chunk_bytes, s)
-        ctx.allreduce_wait(t, s)
+    for it in range(repeat):  # repeat > 1 re-runs the iteration (A2A counters/epochs advance)
+        if it:
+            for v in bt.g.values():
+                v.zero_()
+        ctx.block_fwd(bt.params, x, y, saved, s)
+        for _ in range(repeat_bwd):
+            t = ctx.block_bwd(bt.params, x, saved, dy, dx, bt.grads, chunk_bytes, s)
+            ctx.allreduce_wait(t, s)
     torch.cuda.synchronize()
     off = ctx.routing_offsets()
     T, E, k, R = cfg.T, cfg.E, cfg.top_k, (1 if schedule == "vanilla_ep" else cfg.R)

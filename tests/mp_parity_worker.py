@@ -30,10 +30,15 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     results = {}
-    runs = [(n, c, "flowmoe", 1) for n, c in CASES.items()]
-    runs += [("bf16_p_" + sch, CASES["bf16_p"], sch, lanes)
+    runs = [(n, c, "flowmoe", 1) for n, c in CASES.items()]  # (name, cfg, schedule, lanes)
+    runs = [(n, c, s, l, "nccl") for n, c, s, l in runs]
+    runs += [("bf16_p_" + sch, CASES["bf16_p"], sch, lanes, "nccl")
              for sch, lanes in (("flowmoe", 2), ("flowmoe_ar", 1), ("pipe_moe", 2), ("vanilla_ep", 1))]
-    for name, base, schedule, lanes in runs:
+    # peer-memory A2A (NVLink stores from our kernels) — same results as NCCL
+    runs += [("c1_f32_p2p", CASES["c1_f32"], "flowmoe", 2, "p2p"),
+             ("bf16_p_p2p", CASES["bf16_p"], "flowmoe", 2, "p2p"),
+             ("bf16_p_p2p_vanilla", CASES["bf16_p"], "vanilla_ep", 1, "p2p")]
+    for name, base, schedule, lanes, a2a in runs:
         cfg = base.replace(P=P)
         obj = [fm.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -41,7 +46,8 @@ def main():
         wks = [gen_worker(cfg, p) for p in range(P)]
         # tiny S_p so the all-reduce is cut into many chunks incl. a remainder
         g = run_block_gpu(cfg, rep, wks[rank], P=P, rank=rank, uid=obj[0], device=dev.index,
-                          chunk_bytes=4096 + 16, schedule=schedule, compute_streams=lanes)
+                          chunk_bytes=4096 + 16, schedule=schedule, compute_streams=lanes, a2a_impl=a2a,
+                          repeat=(2 if a2a == "p2p" else 1))
         ocfg = cfg.replace(R=1) if schedule == "vanilla_ep" else cfg
         ys, dxs, gflat, eg, st = oracle_block(ocfg, rep, wks)
         El = cfg.E // P
