@@ -2,9 +2,9 @@
 """FlowMoE block-stack training-iteration benchmark (B200, sm_100a).
 
 One step = one training iteration of an L-block transformer-MoE stack through
-the C ABI (libflowmoe.so): L × flowmoe_block_fwd, then L × flowmoe_block_bwd in
-reverse order (each auto-submitting the chunked S_p all-reduce of its MHA+gate
-grads), then flowmoe_allreduce_wait on every ticket (Alg. 1 lines 6-22, P:258-309;
+the C ABI (libflowmoe.so): flowmoe_stack_fwd over the L blocks, then
+flowmoe_stack_bwd in reverse order (each block auto-submitting the chunked S_p
+all-reduce of its MHA+gate grads), then flowmoe_allreduce_wait on every ticket (Alg. 1 lines 6-22, P:258-309;
 the optimizer update, line 23, is excluded as in SURVEY.md §8(d)).  Weights and
 inputs are synthetic (synth.gen_device_*), resident in HBM before the timed
 region.  The iteration is captured once into a CUDA graph and replayed.
@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
     ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--per-block", action="store_true",
+                    help="L block_fwd/block_bwd calls (lanes joined per block) instead of the stack API")
     ap.add_argument("--schedule", default="flowmoe",
                     choices=["flowmoe", "flowmoe_ar", "flowmoe_at", "pipe_moe", "vanilla_ep"],
                     help="scheduling policy (the paper's Table 6 ablation)")
@@ -254,7 +256,16 @@ def main():
     dxs = [torch.empty_like(x0) for _ in range(L)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    plist = [b["params"] for b in blocks]
+    glist = [b["grads"] for b in blocks]
+    slist = [b["saved"] for b in blocks]
+
     def iteration(stream):
+        if not args.per_block:  # lanes forked once per direction, chunk r chains across blocks
+            ctx.stack_fwd(plist, x0, xs[1:], slist, stream)
+            for t in ctx.stack_bwd(plist, x0, xs[1:], slist, dy_top, dxs, glist, S_p, stream):
+                ctx.allreduce_wait(t, stream)
+            return
         for l in range(L):  # Eq.(3)/(4) order, block after block
             ctx.block_fwd(blocks[l]["params"], xs[l], xs[l + 1], blocks[l]["saved"], stream)
         tickets = []
@@ -352,7 +363,8 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             tl = trace_replays(run, args.trace_iters, f"/tmp/flowmoe_trace_r{rank}.json",
-                               trim=max(0, min(3, (args.trace_iters - 2) // 4)))
+                               trim=max(0, min(3, (args.trace_iters - 2) // 4)),
+                               sync=(dist.barrier if world > 1 else None))
         except Exception as e:  # the timeline is diagnostics, never the measurement
             tl = {"error": repr(e)}
         if world > 1:
@@ -404,7 +416,7 @@ def main():
                        "capacity_factor": cfg.capacity_factor, "S_p_bytes": S_p,
                        "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
                        "compute_streams": args.compute_streams, "schedule": args.schedule,
-                       "a2a": args.a2a,
+                       "a2a": args.a2a, "api": "per_block" if args.per_block else "stack",
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,

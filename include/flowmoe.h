@@ -154,6 +154,20 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* ctx, const flowmoe_params* params,
                                  const flowmoe_grads* grads, size_t chunk_bytes,
                                  flowmoe_ticket* ar, cudaStream_t stream);
 
+/* The L-block stack (Alg. 1 lines 6-21) in one call each way.  Same results
+ * as L block_fwd / block_bwd calls; the lanes are forked once, so chunk r of block l+1
+ * starts as soon as chunk r of block l is done (no block-boundary barrier).
+ *   stack_fwd: block l maps ys[l-1] (x0 for l = 0) -> ys[l], stash saved[l].
+ *   stack_bwd: blocks L-1..0; block l gets dy (l = L-1) or dxs[l+1], writes dxs[l]
+ *              (dxs[0] nullable), grads[l], and returns its AR ticket in tickets[l]
+ *              (nullable).  params/grads/ys/saved/dxs/tickets are arrays of length L. */
+flowmoe_status flowmoe_stack_fwd(flowmoe_ctx* ctx, int L, const flowmoe_params* params, const void* x0,
+                                 void* const* ys, void* const* saved, cudaStream_t stream);
+flowmoe_status flowmoe_stack_bwd(flowmoe_ctx* ctx, int L, const flowmoe_params* params, const void* x0,
+                                 void* const* ys, void* const* saved, const void* dy, void* const* dxs,
+                                 const flowmoe_grads* grads, size_t chunk_bytes, flowmoe_ticket* tickets,
+                                 cudaStream_t stream);
+
 /* Chunked in-place sum all-reduce of buf[count] fp32 over the world on the
  * low-priority AR stream (Alg. 2 PARTITION + ARQueue).  Starts after `ready`
  * (nullable: after work already enqueued on the ctx compute stream).

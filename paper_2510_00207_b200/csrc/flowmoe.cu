@@ -675,8 +675,14 @@ flowmoe_status flowmoe_set_forced_routing(flowmoe_ctx* x, const int32_t* idx) {
   return FLOWMOE_OK;
 }
 
-flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
-                                 void* y, void* saved, cudaStream_t stream) {
+}  // extern "C"
+
+namespace {
+// One block's forward.  fork: lanes first wait for `stream`; join: `stream` then waits for
+// every lane.  The stack API forks once and joins once, so chunk r of block l+1 follows
+// chunk r of block l on lane r % n without a block-boundary barrier.
+flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin, void* y, void* saved,
+                           cudaStream_t stream, bool fork, bool join) {
   if (!x || !p || !xin || !y || !saved) return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL argument");
   if (!p->wqkv || !p->wo || !p->wg || !p->w1 || !p->b1 || !p->w2 || !p->b2)
     return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL parameter pointer");
@@ -690,7 +696,8 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // kernel's event-timed duration is its own, not shared with co-running chunks
   const int nl = g_prof.on ? 1 : (int)x->lanes.size();
   const bool use_p2p = P > 1 && p2p_ready(x, saved, stream);
-  if (flowmoe_status st = fork_lanes(x, stream)) return st;
+  if (fork)
+    if (flowmoe_status st = fork_lanes(x, stream)) return st;
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer.
   // Policies that keep AT unsplit (PIPE_MOE, FLOWMOE_AR) run MHA + gate once over all
   // tokens, then route/pack per chunk (capacity is per chunk in every policy).
@@ -806,16 +813,17 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const 
                             x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
                             (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)ldE, sc));
   }
-  if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
-  FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
-  FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  if (join) {
+    if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
+    FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
+    FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  }
   return FLOWMOE_OK;
 }
 
-flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
-                                 const void* saved, const void* dy, void* dx,
-                                 const flowmoe_grads* gr, size_t chunk_bytes, flowmoe_ticket* ar,
-                                 cudaStream_t stream) {
+flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin, const void* saved,
+                           const void* dy, void* dx, const flowmoe_grads* gr, size_t chunk_bytes,
+                           flowmoe_ticket* ar, cudaStream_t stream, bool fork, bool join) {
   if (!x || !p || !xin || !saved || !dy || !gr)
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: NULL argument");
   if (!gr->grad_flat || !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2)
@@ -836,7 +844,8 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // is a plain store and "accumulate" a TMA reduce-add / read-modify-write.
   const int gacc = x->cfg.grad_mode == FLOWMOE_GRAD_ACCUMULATE;
   const int gepi = gacc ? EPI_ACC_F32 : EPI_STORE_F32;
-  if (flowmoe_status st = fork_lanes(x, stream)) return st;
+  if (fork)
+    if (flowmoe_status st = fork_lanes(x, stream)) return st;
   const int wset = x->ev_wg_done[1] ? (int)(x->bwd_calls++ & 1) : 0;
   x->dyc = x->ws_dyc[wset]; x->dye = x->ws_dye[wset]; x->dz = x->ws_dz[wset];
   if (P > 1) x->dye = const_cast<char*>(at<char>(saved, L.dye));  // per-block landing buffer
@@ -1003,11 +1012,13 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
   // dx is ready once the lanes are done; with a separate wgrad stream the caller does
   // not wait for the wgrads (they finish under the next block's backward, and every
   // AR ticket / allreduce_wait orders after them)
-  if (sc != x->lanes[0]) {
-    if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
-    FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
-  } else {
-    FM_CUDA(cudaEventRecord(x->ev_done, sc));
+  if (join) {
+    if (sc != x->lanes[0]) {
+      if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
+      FM_CUDA(cudaEventRecord(x->ev_done, x->lanes[0]));
+    } else {
+      FM_CUDA(cudaEventRecord(x->ev_done, sc));
+    }
   }
   if (x->ar_pipelined) {
     if (flowmoe_status s = submit_ar(x, gf + 3 * M * M, (size_t)(M * M + M * E), chunk_bytes, x->ev_grads_a)) return s;
@@ -1018,7 +1029,46 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
     x->pending_ar.push_back({gf, (size_t)(4 * M * M + M * E), t});
     if (ar) *ar = t;
   }
-  FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  if (join) FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  return FLOWMOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
+                                 void* y, void* saved, cudaStream_t stream) {
+  return enqueue_fwd(x, p, xin, y, saved, stream, true, true);
+}
+
+flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
+                                 const void* saved, const void* dy, void* dx,
+                                 const flowmoe_grads* gr, size_t chunk_bytes, flowmoe_ticket* ar,
+                                 cudaStream_t stream) {
+  return enqueue_bwd(x, p, xin, saved, dy, dx, gr, chunk_bytes, ar, stream, true, true);
+}
+
+flowmoe_status flowmoe_stack_fwd(flowmoe_ctx* x, int L, const flowmoe_params* params, const void* x0,
+                                 void* const* ys, void* const* saved, cudaStream_t stream) {
+  if (!x || L < 1 || !params || !x0 || !ys || !saved) return fail(FLOWMOE_ERR_INVALID, "stack_fwd: bad argument");
+  for (int l = 0; l < L; ++l)
+    if (flowmoe_status s = enqueue_fwd(x, &params[l], l ? ys[l - 1] : x0, ys[l], saved[l], stream, l == 0,
+                                       l == L - 1))
+      return s;
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_stack_bwd(flowmoe_ctx* x, int L, const flowmoe_params* params, const void* x0,
+                                 void* const* ys, void* const* saved, const void* dy, void* const* dxs,
+                                 const flowmoe_grads* grads, size_t chunk_bytes, flowmoe_ticket* tickets,
+                                 cudaStream_t stream) {
+  if (!x || L < 1 || !params || !x0 || !ys || !saved || !dy || !dxs || !grads)
+    return fail(FLOWMOE_ERR_INVALID, "stack_bwd: bad argument");
+  for (int l = L - 1; l >= 0; --l)
+    if (flowmoe_status s = enqueue_bwd(x, &params[l], l ? ys[l - 1] : x0, saved[l], l == L - 1 ? dy : dxs[l + 1],
+                                       dxs[l], &grads[l], chunk_bytes, tickets ? &tickets[l] : nullptr, stream,
+                                       l == L - 1, l == 0))
+      return s;
   return FLOWMOE_OK;
 }
 

@@ -21,7 +21,7 @@ SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "van
 
 EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
-    "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
+    "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
     "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
     "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
 ]
@@ -76,6 +76,11 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_block_fwd.argtypes = [vp, ctypes.POINTER(Params), vp, vp, vp, vp]
     L.flowmoe_block_bwd.argtypes = [vp, ctypes.POINTER(Params), vp, vp, vp, vp,
                                     ctypes.POINTER(Grads), sz, ctypes.POINTER(u64), vp]
+    L.flowmoe_stack_fwd.argtypes = [vp, i32, ctypes.POINTER(Params), vp, ctypes.POINTER(vp),
+                                    ctypes.POINTER(vp), vp]
+    L.flowmoe_stack_bwd.argtypes = [vp, i32, ctypes.POINTER(Params), vp, ctypes.POINTER(vp),
+                                    ctypes.POINTER(vp), vp, ctypes.POINTER(vp), ctypes.POINTER(Grads), sz,
+                                    ctypes.POINTER(u64), vp]
     L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
     L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
@@ -232,6 +237,27 @@ class FlowMoE:
                                        ctypes.byref(t), _stream_handle(stream)),
                "flowmoe_block_bwd")
         return t.value
+
+    def stack_fwd(self, params: list, x0, ys: list, saved: list, stream=None):
+        L = len(params)
+        pa = (Params * L)(*params)
+        yv = (ctypes.c_void_p * L)(*[t.data_ptr() for t in ys])
+        sv = (ctypes.c_void_p * L)(*[t.data_ptr() for t in saved])
+        _check(lib().flowmoe_stack_fwd(self.handle, L, pa, _ptr(x0), yv, sv, _stream_handle(stream)),
+               "flowmoe_stack_fwd")
+
+    def stack_bwd(self, params: list, x0, ys: list, saved: list, dy, dxs: list, grads: list,
+                  chunk_bytes: int, stream=None) -> list:
+        L = len(params)
+        pa = (Params * L)(*params)
+        yv = (ctypes.c_void_p * L)(*[t.data_ptr() for t in ys])
+        sv = (ctypes.c_void_p * L)(*[t.data_ptr() for t in saved])
+        dv = (ctypes.c_void_p * L)(*[(t.data_ptr() if t is not None else None) for t in dxs])
+        gv = (Grads * L)(*grads)
+        tk = (ctypes.c_uint64 * L)()
+        _check(lib().flowmoe_stack_bwd(self.handle, L, pa, _ptr(x0), yv, sv, _ptr(dy), dv, gv, chunk_bytes,
+                                       tk, _stream_handle(stream)), "flowmoe_stack_bwd")
+        return list(tk)
 
     def allreduce_submit(self, buf, count: int, chunk_bytes: int, priority: int = 1,
                          ready_event=None) -> int:

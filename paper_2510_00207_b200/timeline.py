@@ -112,12 +112,17 @@ def analyze(trace_path: str, n_iters: int, trim: int = 0) -> dict:
     }
 
 
-def trace_replays(run, n_iters: int, path: str, trim: int = 0):
-    """Run `run()` n_iters times under torch.profiler (CUDA activities) and write a chrome trace."""
+def trace_replays(run, n_iters: int, path: str, trim: int = 0, sync=None):
+    """Run `run()` n_iters times under torch.profiler (CUDA activities) and write a chrome trace.
+    `sync()` (e.g. a process-group barrier) runs once the profiler is live, so ranks whose
+    CUPTI start-up took different times still enter the traced replays together."""
     import torch
     from torch.profiler import ProfilerActivity, profile
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        if sync is not None:
+            sync()
+            torch.cuda.synchronize()
         for _ in range(n_iters):
             run()
         torch.cuda.synchronize()

@@ -97,30 +97,43 @@ def expert_grads(eg: dict, lo: int, hi: int):
 
 
 def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: int = 1,
-                  schedule: str = "flowmoe", graph: bool = False, device: int = 0) -> dict:
+                  schedule: str = "flowmoe", graph: bool = False, device: int = 0,
+                  api: str = "per_block", P: int = 1, rank: int = 0, uid: bytes | None = None,
+                  a2a_impl: str = "nccl", chunk_bytes: int = 1 << 20) -> dict:
     """L = len(reps) blocks chained through the C ABI on one rank (forced routing per
-    block from wk['forced'][l]): forward x -> y_L, backward from wk['dy'] to dx_0."""
+    block from wk['forced'][l], or the gate's own routing when wk['forced'] is None):
+    forward x -> y_L, backward from wk['dy'] to dx_0.  api='stack' drives the same
+    iteration through flowmoe_stack_fwd / flowmoe_stack_bwd."""
     import torch
     dev = torch.device("cuda", device)
     torch.cuda.set_device(dev)
-    ctx = fm.FlowMoE(shape_of(cfg, 1, 0, "overwrite", compute_streams, schedule), device, None)
+    ctx = fm.FlowMoE(shape_of(cfg, P, rank, "overwrite", compute_streams, schedule, a2a_impl), device, uid)
     L = len(reps)
-    bts = [fm.BlockTensors(r, cfg.dtype, 0, 1, dev) for r in reps]
+    bts = [fm.BlockTensors(r, cfg.dtype, rank, P, dev) for r in reps]
     xs = [fm.to_device(wk["x"], cfg.dtype, dev)] + [None] * L
     for l in range(L):
         xs[l + 1] = torch.empty_like(xs[0])
     dxs = [torch.empty_like(xs[0]) for _ in range(L)]
     dy = fm.to_device(wk["dy"], cfg.dtype, dev)
     saved = [torch.empty(ctx.saved_bytes, dtype=torch.uint8, device=dev) for _ in range(L)]
-    forced = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.int32)).to(dev) for f in wk["forced"]]
+    forced = None if wk.get("forced") is None else \
+        [torch.from_numpy(np.ascontiguousarray(f, dtype=np.int32)).to(dev) for f in wk["forced"]]
+    assert api == "per_block" or forced is None, "stack API runs the gate's own routing"
 
     def iteration(s):
+        if api == "stack":
+            ctx.stack_fwd([b.params for b in bts], xs[0], xs[1:], saved, s)
+            for t in ctx.stack_bwd([b.params for b in bts], xs[0], xs[1:], saved, dy, dxs,
+                                   [b.grads for b in bts], chunk_bytes, s):
+                ctx.allreduce_wait(t, s)
+            return
         for l in range(L):
-            ctx.set_forced_routing(forced[l])
+            if forced is not None:
+                ctx.set_forced_routing(forced[l])
             ctx.block_fwd(bts[l].params, xs[l], xs[l + 1], saved[l], s)
         g, tickets = dy, []
         for l in reversed(range(L)):
-            tickets.append(ctx.block_bwd(bts[l].params, xs[l], saved[l], g, dxs[l], bts[l].grads, 1 << 20, s))
+            tickets.append(ctx.block_bwd(bts[l].params, xs[l], saved[l], g, dxs[l], bts[l].grads, chunk_bytes, s))
             g = dxs[l]
         for t in tickets:
             ctx.allreduce_wait(t, s)

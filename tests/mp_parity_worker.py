@@ -12,9 +12,10 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import oracle as o  # noqa: E402
 import paper_2510_00207_b200 as fm  # noqa: E402
 from synth import PRESETS, BlockConfig, gen_replicated, gen_worker  # noqa: E402
-from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu  # noqa: E402
+from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu, run_stack_gpu  # noqa: E402
 
 CASES = {
     "c1_f32": PRESETS["c1"],
@@ -60,6 +61,47 @@ def main():
         r["routing_exact"] = bool(np.array_equal(g["idx"], ro.idx) and
                                   np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1)) and
                                   np.array_equal(g["counts"], ro.counts))
+        results[name] = r
+    # 3-block stack: per-block calls (forced routing) vs the oracle chain over P workers,
+    # and the stack API (lanes forked once) vs per-block calls bit for bit
+    L = 3
+    for name, base, a2a in (("stack_f32", CASES["c1_f32"].replace(R=4, causal=1, residual=1), "nccl"),
+                            ("stack_bf16_p2p", CASES["bf16_p"], "p2p"),
+                            ("stack_bf16_nccl", CASES["bf16_p"], "nccl")):
+        cfg = base.replace(P=P)
+        reps = [gen_replicated(cfg, block=l) for l in range(L)]
+        wks = [gen_worker(cfg, p) for p in range(P)]
+        forced = [[gen_worker(cfg, p, block=l)["forced_idx"] for p in range(P)] for l in range(L)]
+        r = {}
+        runs_api = {}
+        for api, fr in (("per_block", True), ("per_block_free", False), ("stack", False)):
+            obj = [fm.get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            wk = dict(wks[rank])
+            wk["forced"] = [forced[l][rank] for l in range(L)] if fr else None
+            runs_api[api] = run_stack_gpu(cfg, reps, wk, compute_streams=cfg.R, device=dev.index,
+                                          api="stack" if api == "stack" else "per_block", P=P, rank=rank,
+                                          uid=obj[0], a2a_impl=a2a, chunk_bytes=4096 + 16,
+                                          graph=(api == "stack"))
+        xs, sts = [[w["x"] for w in wks]], []
+        for l in range(L):
+            ys, st = o.block_forward(cfg, reps[l], xs[-1], forced[l])
+            xs.append(ys)
+            sts.append(st)
+        dys, ref_g = [w["dy"] for w in wks], [None] * L
+        for l in reversed(range(L)):
+            dxl, gflat, eg = o.block_backward(cfg, reps[l], sts[l], dys)
+            ref_g[l] = (gflat, expert_grads(eg, rank * (cfg.E // P), (rank + 1) * (cfg.E // P))["dw1"])
+            dys = dxl
+        g = runs_api["per_block"]
+        r["y"] = rel(g["y"], xs[-1][rank])
+        r["dx"] = rel(g["dx"], dys[rank])
+        r["grad_flat"] = max(rel(g["grad_flat"][l], ref_g[l][0]) for l in range(L))
+        r["dw1"] = max(rel(g["dw1"][l], ref_g[l][1]) for l in range(L))
+        a, b = runs_api["stack"], runs_api["per_block_free"]
+        r["stack_bitwise"] = bool(all(np.array_equal(a[n], b[n]) for n in ("y", "dx")) and all(
+            np.array_equal(a[n][l], b[n][l]) for n in ("grad_flat", "dw1") for l in range(L)))
+        r["depth"] = L
         results[name] = r
     out = [None] * P
     dist.all_gather_object(out, results)

@@ -31,7 +31,12 @@ def test_multi_gpu_parity(P):
     per_rank = json.loads(line[0][len("MP_RESULTS "):])
     for rank, res in enumerate(per_rank):
         for case, r in res.items():
-            assert r["routing_exact"], (rank, case)
-            tol = TOL.get(case, TOL["bf16_p"])
-            bad = {k: v for k, v in r.items() if k != "routing_exact" and not v <= tol}
+            if case.startswith("stack_"):  # 3-block chain: bf16 rounding compounds with depth
+                assert r.pop("stack_bitwise"), (rank, case)
+                depth = r.pop("depth")
+                tol = 1e-4 if "f32" in case else 2e-2 * depth
+            else:
+                assert r.pop("routing_exact"), (rank, case)
+                tol = TOL.get(case, TOL["bf16_p"])
+            bad = {k: v for k, v in r.items() if not v <= tol}
             assert not bad, (rank, case, bad)

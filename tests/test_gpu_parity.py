@@ -295,3 +295,23 @@ def test_block_stack_chain_parity(dtype, lanes, graph):
     for l in range(L):
         assert rel(g["grad_flat"][l], grads[l][0]) <= tol, l
         assert rel(g["dw1"][l], grads[l][1]) <= tol, l
+
+
+@pytest.mark.parametrize("dtype,graph", [("bf16", False), ("bf16", True), ("float32", False)])
+def test_stack_api_matches_per_block(dtype, graph):
+    """flowmoe_stack_fwd/bwd (lanes forked once, chunks chained across blocks) gives
+    bit-identical activations and grads to L block_fwd/block_bwd calls: the same kernels
+    run on the same lane per chunk, only the block-boundary joins are gone."""
+    from tests.gpu_util import run_stack_gpu
+    cfg = CASES["c2_bench"] if dtype == "bf16" else CASES["c1_f32"].replace(R=4, residual=1, causal=1)
+    L = 3
+    reps = [gen_replicated(cfg, block=l) for l in range(L)]
+    wk = gen_worker(cfg, 0)
+    wk["forced"] = None
+    ref = run_stack_gpu(cfg, reps, wk, compute_streams=cfg.R, api="per_block")
+    g = run_stack_gpu(cfg, reps, wk, compute_streams=cfg.R, graph=graph, api="stack")
+    for n in ("y", "dx"):
+        assert np.array_equal(g[n], ref[n]), n
+    for l in range(L):
+        assert np.array_equal(g["grad_flat"][l], ref["grad_flat"][l]), l
+        assert np.array_equal(g["dw1"][l], ref["dw1"][l]), l
