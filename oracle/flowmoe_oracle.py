@@ -17,7 +17,10 @@ unchunked block's result, so this is the plain definition evaluated directly.
 The chunk index matters only through the per-chunk capacity (reading Q2).
 
 Readings of silent/garbled points:
-Q1 chunks are whole sequences; Q2 capacity ceil per (worker, chunk);
+Q1 chunks are whole sequences, or (Q1', causal only) contiguous slices of one
+sequence when R exceeds the number of sequences — chunked prefill, whose
+attention result is the causal attention's, so only the per-chunk capacity
+depends on the chunking; Q2 capacity ceil per (worker, chunk);
 Q3 slot-major-then-token position order, drop if pos >= C, f=0 dropless;
 Q4 top-k on logits, ties -> lower expert index; Q5 renormalised top-k weights
 for k>=2, raw softmax prob for k=1; Q6 gate has no bias; Q7 MHA has no biases,

@@ -70,6 +70,14 @@ struct flowmoe_ctx {
   ncclComm_t comm_a2a = nullptr, comm_ar = nullptr;
   // per-chunk events
   std::vector<cudaEvent_t> ev_at, ev_d, ev_e, ev_c, ev_cb, ev_cba, ev_eb, ev_dba;
+  // token chunks (chunk = causal slice of one sequence, reading Q1'): chunk r's attention
+  // reads Q/K/V of the earlier chunks of its sequence (ev_qkv) and, backward, the dctx
+  // of the later ones (ev_dctx); a chunk's dctx rows may be rewritten by the next
+  // block's backward only after the earlier chunks' attention backward read them (ev_atb)
+  bool tok = false;
+  std::vector<cudaEvent_t> ev_qkv, ev_dctx, ev_atb;
+  std::vector<unsigned long long> atb_cap;  // capture id at record time
+  std::vector<char> atb_rec;
   cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_grads_a = nullptr, ev_grads_b = nullptr;
   cudaEvent_t ev_bwd_done = nullptr;  // end of the latest block_bwd (centralized AR starts after it)
   std::vector<cudaEvent_t> ticket_ev;
@@ -199,8 +207,13 @@ flowmoe_status validate(const flowmoe_config* c) {
   if (c->seq_len <= 0) return bad("seq_len", "must be > 0");
   if (c->B % c->seq_len) return bad("B", "must be a multiple of seq_len (whole sequences)");
   if (c->R <= 0) return bad("R", "must be >= 1");
-  if ((c->B / c->seq_len) % c->R)
-    return bad("R", "must divide the number of sequences B/seq_len (chunks are whole sequences, reading Q1)");
+  if (c->B % c->R) return bad("R", "must divide B (chunks of B/R tokens)");
+  {
+    const int64_t Tr = c->B / c->R;
+    if (Tr % c->seq_len && (c->seq_len % Tr || !c->causal))
+      return bad("R", "chunks of B/R tokens must be whole sequences (reading Q1) or, with causal = 1, "
+                      "slices of one sequence (B/R dividing seq_len, reading Q1')");
+  }
   if (c->M <= 0 || c->M % 8) return bad("M", "must be a positive multiple of 8");
   if (c->n_heads <= 0 || c->M % c->n_heads) return bad("n_heads", "must divide M");
   int dh = c->M / c->n_heads;
@@ -528,6 +541,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   x->P = cfg->world_size;
   x->El = cfg->E / cfg->world_size;
   x->C = capacity_of(&x->cfg, x->Tr);
+  x->tok = x->at_split && x->Tr < x->N;
   x->dt = cfg->dtype == FLOWMOE_BF16 ? DT_BF16 : DT_F32;
   x->es = cfg->dtype == FLOWMOE_BF16 ? 2 : 4;
   x->L = layout_of(x);
@@ -564,7 +578,10 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     for (auto& e : x->ev_lane)
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   }
-  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba}) {
+  x->atb_cap.assign(x->cfg.R, 0);
+  x->atb_rec.assign(x->cfg.R, 0);
+  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba,
+                  &x->ev_qkv, &x->ev_dctx, &x->ev_atb}) {
     v->resize(x->cfg.R);
     for (auto& e : *v)
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
@@ -714,8 +731,20 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     g.M = (int)Ta; g.N = (int)(3 * M); g.K = (int)M;
     g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
     FM_GEMM(KK_QKV, g);
-    FM_KP(KK_ATTN_F, 1, 4.0 * Ta * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Ta * 5 * M * es + Ta * x->H * 4.0, sc,
-          attn_fwd(dt, qkv, ctxb, at<float>(saved, L.lse + t0 * x->H * 4), (int)Ta, (int)x->N, (int)M,
+    // attention rows: whole sequences of the chunk, or (token chunk) positions
+    // [p0, p0+Ta) of sequence t0/N attending to that sequence's keys before them
+    int64_t a0 = t0, nseq = Ta / x->N, p0 = 0, np = x->N;
+    double attn_flops = 4.0 * Ta * x->N * M * (x->cfg.causal ? 0.5 : 1.0);
+    if (x->tok) {
+      a0 = t0 / x->N * x->N; nseq = 1; p0 = t0 - a0; np = Ta;
+      attn_flops = 4.0 * M * ((double)Ta * p0 + 0.5 * Ta * Ta);
+      FM_CUDA(cudaEventRecord(x->ev_qkv[ai], sc));
+      for (int64_t q = a0 / Ta; q < ai; ++q)  // earlier chunks of the sequence
+        if (x->lanes[q % nl] != sc) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_qkv[q], 0));
+    }
+    FM_KP(KK_ATTN_F, 1, attn_flops, (double)Ta * 5 * M * es + Ta * x->H * 4.0, sc,
+          attn_fwd(dt, at<char>(saved, L.qkv + a0 * 3 * M * es), at<char>(saved, L.ctx + a0 * M * es),
+                   at<float>(saved, L.lse + a0 * x->H * 4), (int)nseq, (int)x->N, (int)p0, (int)np, (int)M,
                    (int)x->H, x->cfg.causal, sc));
     g = GemmArgs();
     g.M = (int)Ta; g.N = (int)M; g.K = (int)M;
@@ -963,14 +992,37 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     void* dA = (char*)x->dA + t0 * M * es;
     void* dctx = (char*)x->dctx + t0 * M * es;
     void* dqkv = (char*)x->dqkv + t0 * 3 * M * es;
+    int64_t a0 = t0, nseq = Tb / x->N, p0 = 0, np = x->N;
+    double attn_flops = 10.0 * Tb * x->N * M * (x->cfg.causal ? 0.5 : 1.0);
+    if (x->tok) {
+      a0 = t0 / x->N * x->N; nseq = 1; p0 = t0 - a0; np = Tb;
+      attn_flops = 10.0 * M * ((double)Tb * p0 + 0.5 * Tb * Tb);
+      // the previous block's attention backward of this sequence's earlier chunks read
+      // these dctx / D rows (same stack or capture only: otherwise already ordered)
+      const unsigned long long cid = capture_id(sc);
+      for (int64_t q = a0 / Tb; q < ai; ++q)
+        if (x->atb_rec[q] && x->atb_cap[q] == cid && x->lanes[q % nl] != sc)
+          FM_CUDA(cudaStreamWaitEvent(sc, x->ev_atb[q], 0));
+    }
     GemmArgs g;
     g.M = (int)Tb; g.N = (int)M; g.K = (int)M;
     g.A = dA; g.lda = M; g.B = p->wo; g.ldb = M; g.b_kmajor = 1; g.C = dctx; g.ldc = M;
     FM_GEMM(KK_DCTX, g);
-    FM_KP(KK_ATTN_B, attn_tc_supported(dt, (int)M, (int)x->H) ? 2 : 3, 10.0 * Tb * x->N * M * (x->cfg.causal ? 0.5 : 1.0), (double)Tb * 8 * M * es, sc,
-          attn_bwd(dt, at<char>(saved, L.qkv + t0 * 3 * M * es), at<char>(saved, L.ctx + t0 * M * es),
-                   at<float>(saved, L.lse + t0 * x->H * 4), dctx, dqkv, x->Dbuf + t0 * x->H, (int)Tb, (int)x->N, (int)M,
-                   (int)x->H, x->cfg.causal, sc));
+    if (x->tok) {  // dK/dV of this chunk's keys take the later chunks' queries (their dctx)
+      FM_CUDA(cudaEventRecord(x->ev_dctx[ai], sc));
+      for (int64_t q = ai + 1; q < (a0 + x->N) / Tb; ++q)
+        if (x->lanes[q % nl] != sc) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dctx[q], 0));
+    }
+    FM_KP(KK_ATTN_B, attn_tc_supported(dt, (int)M, (int)x->H) ? 2 : 3, attn_flops, (double)Tb * 8 * M * es, sc,
+          attn_bwd(dt, at<char>(saved, L.qkv + a0 * 3 * M * es), at<char>(saved, L.ctx + a0 * M * es),
+                   at<float>(saved, L.lse + a0 * x->H * 4), (char*)x->dctx + a0 * M * es,
+                   (char*)x->dqkv + a0 * 3 * M * es, x->Dbuf + a0 * x->H, (int)nseq, (int)x->N, (int)p0, (int)np,
+                   (int)M, (int)x->H, x->cfg.causal, sc));
+    if (x->tok) {
+      FM_CUDA(cudaEventRecord(x->ev_atb[ai], sc));
+      x->atb_rec[ai] = 1;
+      x->atb_cap[ai] = capture_id(sc);
+    }
     if (dx) {
       g = GemmArgs();
       g.M = (int)Tb; g.N = (int)M; g.K = (int)(3 * M);
@@ -1133,7 +1185,8 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (size_t l = 1; l < x->a2a_stream.size(); ++l) cudaStreamDestroy(x->a2a_stream[l]);
   if (x->comm_ar) ncclCommDestroy(x->comm_ar);
   if (x->comm_a2a) ncclCommDestroy(x->comm_a2a);
-  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba})
+  for (auto* v : {&x->ev_at, &x->ev_d, &x->ev_e, &x->ev_c, &x->ev_cb, &x->ev_cba, &x->ev_eb, &x->ev_dba,
+                  &x->ev_qkv, &x->ev_dctx, &x->ev_atb})
     for (auto e : *v) if (e) cudaEventDestroy(e);
   for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
   for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);

@@ -31,11 +31,14 @@ __device__ void load_tile(float* dst, const T* src, int64_t ld, int row0, int nr
   }
 }
 
-// grid (ceil(N/AB), H, n_seq); 256 threads; thread (ty,tx): rows ty+16a (a<4),
+// Row ranges as in k_attn_tc.cu: own rows (queries for fwd / dQ, keys for dK/dV) are the
+// positions [p0, p0 + np) of each of the n_seq sequences (N rows apart); whole sequences
+// have p0 = 0, np = N; a token chunk is a slice of one sequence (causal).
+// grid (ceil(np/AB), H, n_seq); 256 threads; thread (ty,tx): rows ty+16a (a<4),
 // key cols tx+16b (b<4), output cols tx+16c (c<dh/16).
 template <typename T, int DH>
-__global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, float* lse, int N,
-                                                       int M, int H, int causal, float scale) {
+__global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, float* lse, int N, int p0,
+                                                       int np, int M, int H, int causal, float scale) {
   FM_PDL_ENTRY();
   extern __shared__ float sm[];
   float* Qs = sm;
@@ -46,17 +49,18 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, flo
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int64_t ld = 3 * (int64_t)M;
   const T* base = qkv + (int64_t)s * N * ld;
-  load_tile<T>(Qs, base + h * DH, ld, qb * AB, N, DH);
+  const int pe = p0 + np;  // rows at or past pe are not read (not yet computed in a token chunk)
+  load_tile<T>(Qs, base + h * DH, ld, p0 + qb * AB, pe, DH);
   constexpr int NC = DH / 16;
   float o[4][NC] = {};
   float mrow[4], lrow[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) { mrow[a] = -INFINITY; lrow[a] = 0.f; }
-  const int nkb = causal ? qb + 1 : (N + AB - 1) / AB;
+  const int nkb = causal ? (min(pe, p0 + (qb + 1) * AB) + AB - 1) / AB : (N + AB - 1) / AB;
   for (int kb = 0; kb < nkb; ++kb) {
     __syncthreads();
-    load_tile<T>(Ks, base + M + h * DH, ld, kb * AB, N, DH);
-    load_tile<T>(Vs, base + 2 * M + h * DH, ld, kb * AB, N, DH);
+    load_tile<T>(Ks, base + M + h * DH, ld, kb * AB, pe, DH);
+    load_tile<T>(Vs, base + 2 * M + h * DH, ld, kb * AB, pe, DH);
     __syncthreads();
     float sc[4][4] = {};
     for (int d = 0; d < DH; ++d) {
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, flo
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const int i = qb * AB + ty + 16 * a;
+      const int i = p0 + qb * AB + ty + 16 * a;
       float mx = -INFINITY;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -114,8 +118,8 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const T* qkv, T* ctx, flo
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int i = qb * AB + ty + 16 * a;
-    if (i >= N) continue;
+    const int i = p0 + qb * AB + ty + 16 * a;
+    if (i >= pe) continue;
     const float inv = 1.f / lrow[a];
     T* dst = ctx + ((int64_t)s * N + i) * M + h * DH;
 #pragma unroll
@@ -138,12 +142,12 @@ __global__ void attn_bwd_pre_kernel(const T* ctx, const T* dctx, float* D, int T
   D[id] = acc;
 }
 
-// dK, dV for one key block; grid (ceil(N/AB), H, n_seq).
+// dK, dV for one own key block; grid (ceil(np/AB), H, n_seq); queries up to N.
 // thread: keys ty+16a (a<4) x queries tx+16b (b<4); dK/dV rows ty+16a x cols tx+16c.
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const T* dctx,
                                                             const float* lse, const float* D,
-                                                            T* dqkv, int N, int M, int H,
+                                                            T* dqkv, int N, int p0, int np, int M, int H,
                                                             int causal, float scale) {
   FM_PDL_ENTRY();
   extern __shared__ float sm[];
@@ -160,12 +164,13 @@ __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const 
   const int64_t ld = 3 * (int64_t)M;
   const T* base = qkv + (int64_t)s * N * ld;
   const T* dob = dctx + (int64_t)s * N * M;
-  load_tile<T>(Ks, base + M + h * DH, ld, kb * AB, N, DH);
-  load_tile<T>(Vs, base + 2 * M + h * DH, ld, kb * AB, N, DH);
+  const int pe = p0 + np, k0 = p0 + kb * AB;
+  load_tile<T>(Ks, base + M + h * DH, ld, k0, pe, DH);
+  load_tile<T>(Vs, base + 2 * M + h * DH, ld, k0, pe, DH);
   constexpr int NC = DH / 16;
   float dk[4][NC] = {}, dv[4][NC] = {};
   const int nqb = (N + AB - 1) / AB;
-  for (int qb = causal ? kb : 0; qb < nqb; ++qb) {
+  for (int qb = causal ? k0 / AB : 0; qb < nqb; ++qb) {
     __syncthreads();
     load_tile<T>(Qs, base + h * DH, ld, qb * AB, N, DH);
     load_tile<T>(dOs, dob + h * DH, M, qb * AB, N, DH);
@@ -189,14 +194,14 @@ __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const 
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const int j = kb * AB + ty + 16 * a;
+      const int j = k0 + ty + 16 * a;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int il = tx + 16 * b, i = qb * AB + il;
-        bool valid = i < N && j < N && (!causal || j <= i);
+        bool valid = i < N && j < pe && (!causal || j <= i);
         float p = valid ? expf(sc[a][b] * scale - Ls[il]) : 0.f;
         Ps[(ty + 16 * a) * (AB + 1) + il] = p;
-        dSs[(ty + 16 * a) * (AB + 1) + il] = p * (dp[a][b] - Ds[il]);
+        dSs[(ty + 16 * a) * (AB + 1) + il] = valid ? p * (dp[a][b] - Ds[il]) : 0.f;
       }
     }
     __syncthreads();
@@ -214,8 +219,8 @@ __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const 
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int j = kb * AB + ty + 16 * a;
-    if (j >= N) continue;
+    const int j = k0 + ty + 16 * a;
+    if (j >= pe) continue;
     T* row = dqkv + ((int64_t)s * N + j) * ld;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -225,12 +230,12 @@ __global__ void __launch_bounds__(256) attn_bwd_dkdv_kernel(const T* qkv, const 
   }
 }
 
-// dQ for one query block; grid (ceil(N/AB), H, n_seq).
+// dQ for one own query block; grid (ceil(np/AB), H, n_seq).
 // thread: queries ty+16a x keys tx+16b; dQ rows ty+16a x cols tx+16c.
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T* dctx,
                                                           const float* lse, const float* D,
-                                                          T* dqkv, int N, int M, int H,
+                                                          T* dqkv, int N, int p0, int np, int M, int H,
                                                           int causal, float scale) {
   FM_PDL_ENTRY();
   extern __shared__ float sm[];
@@ -243,22 +248,23 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T*
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int64_t ld = 3 * (int64_t)M;
   const T* base = qkv + (int64_t)s * N * ld;
-  load_tile<T>(Qs, base + h * DH, ld, qb * AB, N, DH);
-  load_tile<T>(dOs, dctx + (int64_t)s * N * M + h * DH, M, qb * AB, N, DH);
+  const int pe = p0 + np, q0 = p0 + qb * AB;
+  load_tile<T>(Qs, base + h * DH, ld, q0, pe, DH);
+  load_tile<T>(dOs, dctx + (int64_t)s * N * M + h * DH, M, q0, pe, DH);
   float L[4], Dv[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    int i = qb * AB + ty + 16 * a;
-    L[a] = i < N ? lse[((int64_t)s * N + i) * H + h] : 0.f;
-    Dv[a] = i < N ? D[((int64_t)s * N + i) * H + h] : 0.f;
+    int i = q0 + ty + 16 * a;
+    L[a] = i < pe ? lse[((int64_t)s * N + i) * H + h] : 0.f;
+    Dv[a] = i < pe ? D[((int64_t)s * N + i) * H + h] : 0.f;
   }
   constexpr int NC = DH / 16;
   float dq[4][NC] = {};
-  const int nkb = causal ? qb + 1 : (N + AB - 1) / AB;
+  const int nkb = causal ? (min(pe, q0 + AB) + AB - 1) / AB : (N + AB - 1) / AB;
   for (int kb = 0; kb < nkb; ++kb) {
     __syncthreads();
-    load_tile<T>(Ks, base + M + h * DH, ld, kb * AB, N, DH);
-    load_tile<T>(Vs, base + 2 * M + h * DH, ld, kb * AB, N, DH);
+    load_tile<T>(Ks, base + M + h * DH, ld, kb * AB, causal ? pe : N, DH);
+    load_tile<T>(Vs, base + 2 * M + h * DH, ld, kb * AB, causal ? pe : N, DH);
     __syncthreads();
     float sc[4][4] = {}, dp[4][4] = {};
     for (int d = 0; d < DH; ++d) {
@@ -274,13 +280,13 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T*
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const int i = qb * AB + ty + 16 * a;
+      const int i = q0 + ty + 16 * a;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int j = kb * AB + tx + 16 * b;
-        bool valid = i < N && j < N && (!causal || j <= i);
+        bool valid = i < pe && j < N && (!causal || j <= i);
         float p = valid ? expf(sc[a][b] * scale - L[a]) : 0.f;
-        dSs[(ty + 16 * a) * (AB + 1) + tx + 16 * b] = p * (dp[a][b] - Dv[a]);
+        dSs[(ty + 16 * a) * (AB + 1) + tx + 16 * b] = valid ? p * (dp[a][b] - Dv[a]) : 0.f;
       }
     }
     __syncthreads();
@@ -298,8 +304,8 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T*
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int i = qb * AB + ty + 16 * a;
-    if (i >= N) continue;
+    const int i = q0 + ty + 16 * a;
+    if (i >= pe) continue;
     T* row = dqkv + ((int64_t)s * N + i) * ld + h * DH;
 #pragma unroll
     for (int c = 0; c < NC; ++c) row[tx + 16 * c] = from_f<T>(dq[a][c] * scale);
@@ -307,37 +313,40 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const T* qkv, const T*
 }
 
 template <typename T, int DH>
-static int attn_fwd_t(const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H,
+static int attn_fwd_t(const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M, int H,
                       int causal, cudaStream_t s) {
   size_t smem = (3 * AB * (DH + 1) + AB * (AB + 1)) * sizeof(float);
   auto k = attn_fwd_kernel<T, DH>;
   static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)once;
-  dim3 grid((N + AB - 1) / AB, H, T_ / N);
-  launch_k(k, grid, 256, smem, s, (const T*)qkv, (T*)ctx, lse, N, M, H, causal, 1.0f / sqrtf((float)DH));
+  dim3 grid((np + AB - 1) / AB, H, nseq);
+  launch_k(k, grid, 256, smem, s, (const T*)qkv, (T*)ctx, lse, N, p0, np, M, H, causal, 1.0f / sqrtf((float)DH));
   return (int)cudaGetLastError();
 }
 
 template <typename T, int DH>
 static int attn_bwd_t(const void* qkv, const void* ctx, const float* lse, const void* dctx,
-                      void* dqkv, float* D, int T_, int N, int M, int H, int causal,
+                      void* dqkv, float* D, int nseq, int N, int p0, int np, int M, int H, int causal,
                       cudaStream_t s) {
   const float scale = 1.0f / sqrtf((float)DH);
-  launch_k(attn_bwd_pre_kernel<T>, (T_ * H + 255) / 256, 256, 0, s, (const T*)ctx, (const T*)dctx, D,
-                                                              T_, M, H);
-  dim3 grid((N + AB - 1) / AB, H, T_ / N);
+  // D of the own rows (contiguous: either whole sequences or one slice of one sequence);
+  // a token chunk's dK/dV reads the D rows of the later chunks, computed before it
+  const int nrow = (nseq - 1) * N + np;
+  launch_k(attn_bwd_pre_kernel<T>, (nrow * H + 255) / 256, 256, 0, s, (const T*)ctx + (int64_t)p0 * M,
+           (const T*)dctx + (int64_t)p0 * M, D + (int64_t)p0 * H, nrow, M, H);
+  dim3 grid((np + AB - 1) / AB, H, nseq);
   size_t smem1 = (4 * AB * (DH + 1) + 2 * AB * (AB + 1) + 2 * AB) * sizeof(float);
   auto k1 = attn_bwd_dkdv_kernel<T, DH>;
   static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), true);
   (void)once1;
-  launch_k(k1, grid, 256, smem1, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
-                              scale);
+  launch_k(k1, grid, 256, smem1, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, p0, np, M, H, causal,
+           scale);
   size_t smem2 = (4 * AB * (DH + 1) + AB * (AB + 1)) * sizeof(float);
   auto k2 = attn_bwd_dq_kernel<T, DH>;
   static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), true);
   (void)once2;
-  launch_k(k2, grid, 256, smem2, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, M, H, causal,
-                              scale);
+  launch_k(k2, grid, 256, smem2, s, (const T*)qkv, (const T*)dctx, lse, D, (T*)dqkv, N, p0, np, M, H, causal,
+           scale);
   return (int)cudaGetLastError();
 }
 
@@ -350,25 +359,26 @@ static int attn_bwd_t(const void* qkv, const void* ctx, const float* lse, const 
     default: return (int)cudaErrorInvalidValue;  \
   }
 
-template <int DH> static int fwd_f32(const void* a, void* b, float* c, int d, int e, int f, int g, int h, cudaStream_t s) { return attn_fwd_t<float, DH>(a, b, c, d, e, f, g, h, s); }
-template <int DH> static int fwd_bf16(const void* a, void* b, float* c, int d, int e, int f, int g, int h, cudaStream_t s) { return attn_fwd_t<bf16, DH>(a, b, c, d, e, f, g, h, s); }
-template <int DH> static int bwd_f32(const void* a, const void* b, const float* c, const void* d, void* e, float* f, int g, int h, int i, int j, int k, cudaStream_t s) { return attn_bwd_t<float, DH>(a, b, c, d, e, f, g, h, i, j, k, s); }
-template <int DH> static int bwd_bf16(const void* a, const void* b, const float* c, const void* d, void* e, float* f, int g, int h, int i, int j, int k, cudaStream_t s) { return attn_bwd_t<bf16, DH>(a, b, c, d, e, f, g, h, i, j, k, s); }
+template <int DH> static int fwd_f32(const void* a, void* b, float* c, int d, int e, int p0, int np, int f, int g, int h, cudaStream_t s) { return attn_fwd_t<float, DH>(a, b, c, d, e, p0, np, f, g, h, s); }
+template <int DH> static int fwd_bf16(const void* a, void* b, float* c, int d, int e, int p0, int np, int f, int g, int h, cudaStream_t s) { return attn_fwd_t<bf16, DH>(a, b, c, d, e, p0, np, f, g, h, s); }
+template <int DH> static int bwd_f32(const void* a, const void* b, const float* c, const void* d, void* e, float* f, int g, int h, int p0, int np, int i, int j, int k, cudaStream_t s) { return attn_bwd_t<float, DH>(a, b, c, d, e, f, g, h, p0, np, i, j, k, s); }
+template <int DH> static int bwd_bf16(const void* a, const void* b, const float* c, const void* d, void* e, float* f, int g, int h, int p0, int np, int i, int j, int k, cudaStream_t s) { return attn_bwd_t<bf16, DH>(a, b, c, d, e, f, g, h, p0, np, i, j, k, s); }
 
-int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H,
+int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M, int H,
              int causal, cudaStream_t s) {
-  if (attn_tc_supported(dtype, M, H)) return attn_fwd_tc(qkv, ctx, lse, T_, N, M, H, causal, s);
+  if (attn_tc_supported(dtype, M, H)) return attn_fwd_tc(qkv, ctx, lse, nseq, N, p0, np, M, H, causal, s);
   const int dh = M / H;
-  if (dtype == DT_F32) { FM_DH_SWITCH(dh, fwd_f32, qkv, ctx, lse, T_, N, M, H, causal, s) }
-  FM_DH_SWITCH(dh, fwd_bf16, qkv, ctx, lse, T_, N, M, H, causal, s)
+  if (dtype == DT_F32) { FM_DH_SWITCH(dh, fwd_f32, qkv, ctx, lse, nseq, N, p0, np, M, H, causal, s) }
+  FM_DH_SWITCH(dh, fwd_bf16, qkv, ctx, lse, nseq, N, p0, np, M, H, causal, s)
 }
 
 int attn_bwd(int dtype, const void* qkv, const void* ctx, const float* lse, const void* dctx,
-             void* dqkv, float* D, int T_, int N, int M, int H, int causal, cudaStream_t s) {
-  if (attn_tc_supported(dtype, M, H)) return attn_bwd_tc(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
+             void* dqkv, float* D, int nseq, int N, int p0, int np, int M, int H, int causal, cudaStream_t s) {
+  if (attn_tc_supported(dtype, M, H))
+    return attn_bwd_tc(qkv, ctx, lse, dctx, dqkv, D, nseq, N, p0, np, M, H, causal, s);
   const int dh = M / H;
-  if (dtype == DT_F32) { FM_DH_SWITCH(dh, bwd_f32, qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s) }
-  FM_DH_SWITCH(dh, bwd_bf16, qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s)
+  if (dtype == DT_F32) { FM_DH_SWITCH(dh, bwd_f32, qkv, ctx, lse, dctx, dqkv, D, nseq, N, p0, np, M, H, causal, s) }
+  FM_DH_SWITCH(dh, bwd_bf16, qkv, ctx, lse, dctx, dqkv, D, nseq, N, p0, np, M, H, causal, s)
 }
 
 }  // namespace fm

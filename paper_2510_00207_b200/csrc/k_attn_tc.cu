@@ -75,12 +75,17 @@ FM_DEV float row_dot_bf16(const bf16* o, const bf16* g) {
   return acc;
 }
 
+// Row ranges.  Sequences are N rows apart; a launch computes the "own" rows at positions
+// [p0, p0 + np) of each sequence (queries for fwd / dQ, keys for dK/dV).  Whole-sequence
+// chunks use p0 = 0, np = N; a token chunk (chunked prefill, causal only) is a slice of
+// one sequence, attending to the keys before it.
 // ============================================================== forward
-// grid (ceil(N/128), H, n_seq_in_chunk); qkv map over the chunk [T_r][3M].
+// grid (ceil(np/128), H, n_seq); qkv map over rows [0, (n_seq-1)·N + p0 + np) so rows past
+// the own range (not yet computed in a token chunk) load as zeros.
 template <int DH>
 __global__ void __launch_bounds__(AT_THREADS, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, bf16* ctx, float* lse, int N, int M,
-                       int H, int causal, float scale_log2) {
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, bf16* ctx, float* lse, int N, int p0, int np,
+                       int M, int H, int causal, float scale_log2) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -102,9 +107,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
-  const int q0 = qt * 128, row_base = sq * N;
+  const int q0 = p0 + qt * 128, row_base = sq * N;  // q0: position of the tile's first query
   int nkv = (N + 127) / 128;
-  if (causal) nkv = min(nkv, qt + 1);
+  if (causal) nkv = min(nkv, (min(p0 + np, q0 + 128) + 127) / 128);
 
   if (warp == 0 && lane == 0) {
     mbar_init(bar_q, 1);
@@ -169,7 +174,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     // ===== softmax warps: thread = query row
     const int quarter = warp & 3;
     const int rloc = quarter * 32 + lane;
-    const int qrow = q0 + rloc;
+    const int qrow = q0 + rloc;                      // position in the sequence
+    const bool own = qt * 128 + rloc < np;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
@@ -237,9 +243,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
-      if (qrow < N) store_row_bf16(dst + c * 32, v, 32);
+      if (own) store_row_bf16(dst + c * 32, v, 32);
     }
-    if (qrow < N) lse[(int64_t)(row_base + qrow) * H + h] = (m + log2f(l)) * LN2;
+    if (own) lse[(int64_t)(row_base + qrow) * H + h] = (m + log2f(l)) * LN2;
     tc_fence_before();
   }
   __syncthreads();
@@ -251,12 +257,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 // ============================================================== backward: dK, dV
-// grid (ceil(N/128) key tiles, H, n_seq).  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
+// grid (ceil(np/128) own key tiles, H, n_seq); query tiles are 128-aligned positions from
+// the key tile's diagonal (causal) to N.  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
 template <int DH>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                            const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int M,
-                            int H, int causal, float scale_log2, float scale) {
+                            const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
+                            int np, int M, int H, int causal, float scale_log2, float scale) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -280,9 +287,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
-  const int k0 = kt * 128, row_base = sq * N;
+  const int k0 = p0 + kt * 128, row_base = sq * N;
   const int nq_tiles = (N + 127) / 128;
-  const int qt0 = causal ? kt : 0;
+  const int qt0 = causal ? k0 / 128 : 0;
   const int niter = nq_tiles - qt0;
 
   if (warp == 0 && lane == 0) {
@@ -349,6 +356,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int quarter = warp & 3;
     const int kloc = quarter * 32 + lane;
     const int key = k0 + kloc;
+    const bool own = kt * 128 + kloc < np;
     const int t128 = threadIdx.x - 64;  // 0..127
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int it = 0; it < niter; ++it) {
@@ -377,10 +385,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int i = 0; i < 32; ++i) {
           const int ql = c * 32 + i;
           const int qi = qbase + ql;
-          const bool ok = qi < N && key < N && (!causal || key <= qi);
+          const bool ok = qi < N && own && (!causal || key <= qi);
           const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - sL[ql]) : 0.f;
           p[i] = pv;
-          ds[i] = pv * (__uint_as_float(rp[i]) - sD[ql]);
+          ds[i] = ok ? pv * (__uint_as_float(rp[i]) - sD[ql]) : 0.f;
         }
         st_row32_bf16(sP, kloc, c * 32, p);
         st_row32_bf16(sdS, kloc, c * 32, ds);
@@ -399,11 +407,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tmem_ld32(tdV + lane_off + c * 32, r);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = niter > 0 ? __uint_as_float(r[i]) : 0.f;
-      if (key < N) store_row_bf16(row + 2 * M + h * DH + c * 32, v, 32);
+      if (own) store_row_bf16(row + 2 * M + h * DH + c * 32, v, 32);
       tmem_ld32(tdK + lane_off + c * 32, r);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = niter > 0 ? __uint_as_float(r[i]) * scale : 0.f;
-      if (key < N) store_row_bf16(row + M + h * DH + c * 32, v, 32);
+      if (own) store_row_bf16(row + M + h * DH + c * 32, v, 32);
     }
     tc_fence_before();
   }
@@ -416,12 +424,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 // ============================================================== backward: dQ
-// grid (ceil(N/128) query tiles, H, n_seq).  TMEM: S [0,128), dP [128,256), dQ [256, 256+DH).
+// grid (ceil(np/128) own query tiles, H, n_seq).  TMEM: S [0,128), dP [128,256), dQ [256, 256+DH).
 template <int DH, int STAGES>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                          const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int M,
-                          int H, int causal, float scale_log2, float scale) {
+                          const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
+                          int np, int M, int H, int causal, float scale_log2, float scale) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -441,9 +449,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
-  const int q0 = qt * 128, row_base = sq * N;
+  const int q0 = p0 + qt * 128, row_base = sq * N;
   int nkv = (N + 127) / 128;
-  if (causal) nkv = min(nkv, qt + 1);
+  if (causal) nkv = min(nkv, (min(p0 + np, q0 + 128) + 127) / 128);
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_bar, 1);
@@ -509,10 +517,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int quarter = warp & 3;
     const int rloc = quarter * 32 + lane;
     const int qrow = q0 + rloc;
+    const bool own = qt * 128 + rloc < np;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const float L2 = qrow < N ? lse[(int64_t)(row_base + qrow) * H + h] * LOG2E : 0.f;
-    const float Dq = qrow < N ? row_dot_bf16<DH>(ctxO + (int64_t)(row_base + qrow) * M + h * DH,
-                                                 dctx + (int64_t)(row_base + qrow) * M + h * DH) : 0.f;
+    const float L2 = own ? lse[(int64_t)(row_base + qrow) * H + h] * LOG2E : 0.f;
+    const float Dq = own ? row_dot_bf16<DH>(ctxO + (int64_t)(row_base + qrow) * M + h * DH,
+                                            dctx + (int64_t)(row_base + qrow) * M + h * DH) : 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
@@ -529,9 +538,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int kj = j * 128 + c * 32 + i;
-          const bool ok = qrow < N && kj < N && (!causal || kj <= qrow);
+          const bool ok = own && kj < N && (!causal || kj <= qrow);
           const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - L2) : 0.f;
-          ds[i] = pv * (__uint_as_float(rp[i]) - Dq);
+          ds[i] = ok ? pv * (__uint_as_float(rp[i]) - Dq) : 0.f;
         }
         st_row32_bf16(sdS, rloc, c * 32, ds);
       }
@@ -549,7 +558,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tmem_ld32(tdQ + lane_off + c * 32, r);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * scale;
-      if (qrow < N) store_row_bf16(row + c * 32, v, 32);
+      if (own) store_row_bf16(row + c * 32, v, 32);
     }
     tc_fence_before();
   }
@@ -594,41 +603,41 @@ template <int DH, int ST>
 static size_t dq_smem() { return (2 + 2 * ST) * 128 * DH * 2 + 32768 + 1024 + 256; }
 
 template <int DH>
-static int attn_fwd_tc_t(const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H, int causal,
-                         cudaStream_t s) {
+static int attn_fwd_tc_t(const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M, int H,
+                         int causal, cudaStream_t s) {
   CUtensorMap tq;
-  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
+  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, (nseq - 1) * N + p0 + np, 3 * M, 64, 128)) return rc;
   auto k = attn_fwd_tc_kernel<DH>;
   const size_t smem = fwd_smem<DH>();
   static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
   (void)once;
-  dim3 grid((N + 127) / 128, H, T_ / N);
-  launch_k(k, grid, AT_THREADS, smem, s, tq, (bf16*)ctx, lse, N, M, H, causal, LOG2E / sqrtf((float)DH));
+  dim3 grid((np + 127) / 128, H, nseq);
+  launch_k(k, grid, AT_THREADS, smem, s, tq, (bf16*)ctx, lse, N, p0, np, M, H, causal, LOG2E / sqrtf((float)DH));
   return (int)cudaGetLastError();
 }
 
 template <int DH>
 static int attn_bwd_tc_t(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv,
-                         float* D, int T_, int N, int M, int H, int causal, cudaStream_t s) {
+                         float* D, int nseq, int N, int p0, int np, int M, int H, int causal, cudaStream_t s) {
   CUtensorMap tq, tdo;
-  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, T_, 3 * M, 64, 128)) return rc;
-  if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, T_, M, 64, 128)) return rc;
+  if (int rc = make_tmap_2d_bf16(&tq, qkv, 3 * M, nseq * N, 3 * M, 64, 128)) return rc;
+  if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, nseq * N, M, 64, 128)) return rc;
   (void)D;  // D = rowsum(dO ⊙ O) is computed inside the two kernels
   const float scale = 1.0f / sqrtf((float)DH), sl2 = LOG2E * scale;
-  dim3 grid((N + 127) / 128, H, T_ / N);
+  dim3 grid((np + 127) / 128, H, nseq);
   auto k1 = attn_bwd_dkdv_tc_kernel<DH>;
   const size_t sm1 = dkdv_smem<DH>();
   static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1), true);
   (void)once1;
-  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, M,
-           H, causal, sl2, scale);
+  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, p0,
+           np, M, H, causal, sl2, scale);
   constexpr int ST = DH == 128 ? 1 : 2;
   auto k2 = attn_bwd_dq_tc_kernel<DH, ST>;
   const size_t sm2 = dq_smem<DH, ST>();
   static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2), true);
   (void)once2;
-  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, M,
-           H, causal, sl2, scale);
+  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, p0,
+           np, M, H, causal, sl2, scale);
   return (int)cudaGetLastError();
 }
 
@@ -637,16 +646,16 @@ bool attn_tc_supported(int dtype, int M, int H) {
   return dtype == DT_BF16 && (dh == 64 || dh == 128) && !(attn_tc_debug_off());
 }
 
-int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int T_, int N, int M, int H, int causal,
-                cudaStream_t s) {
-  if (M / H == 64) return attn_fwd_tc_t<64>(qkv, ctx, lse, T_, N, M, H, causal, s);
-  return attn_fwd_tc_t<128>(qkv, ctx, lse, T_, N, M, H, causal, s);
+int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M, int H,
+                int causal, cudaStream_t s) {
+  if (M / H == 64) return attn_fwd_tc_t<64>(qkv, ctx, lse, nseq, N, p0, np, M, H, causal, s);
+  return attn_fwd_tc_t<128>(qkv, ctx, lse, nseq, N, p0, np, M, H, causal, s);
 }
 
 int attn_bwd_tc(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv, float* D,
-                int T_, int N, int M, int H, int causal, cudaStream_t s) {
-  if (M / H == 64) return attn_bwd_tc_t<64>(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
-  return attn_bwd_tc_t<128>(qkv, ctx, lse, dctx, dqkv, D, T_, N, M, H, causal, s);
+                int nseq, int N, int p0, int np, int M, int H, int causal, cudaStream_t s) {
+  if (M / H == 64) return attn_bwd_tc_t<64>(qkv, ctx, lse, dctx, dqkv, D, nseq, N, p0, np, M, H, causal, s);
+  return attn_bwd_tc_t<128>(qkv, ctx, lse, dctx, dqkv, D, nseq, N, p0, np, M, H, causal, s);
 }
 
 }  // namespace fm

@@ -43,21 +43,26 @@ void gemm_tc_set_debug(int flags);
 void gemm_tc_force_bn(int bn);
 
 // ---------------------------------------------------------------- attention
-// qkv [T][3M] (per sequence of N rows; head h at columns h*dh of each of Q|K|V)
-// ctx [T][M], lse [T][H] fp32.  T must be a multiple of N.
-int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int T, int N, int M, int H,
-             int causal, cudaStream_t s);
-// dctx [T][M] -> dqkv [T][3M]; Dbuf [T][H] fp32 scratch.
+// qkv [nseq·N][3M] (sequences of N rows; head h at columns h*dh of each of Q|K|V),
+// ctx [..][M], lse [..][H] fp32; all pointers at the first sequence's row 0.
+// Own rows = positions [p0, p0+np) of every sequence: whole sequences p0 = 0, np = N;
+// a token chunk (chunked prefill, causal only, nseq = 1) attends to keys [0, p0+np) and
+// reads no row at or past p0+np in the forward.  The backward's dK/dV of the own keys
+// takes every query up to N (their dctx rows must be final).
+int attn_fwd(int dtype, const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M,
+             int H, int causal, cudaStream_t s);
+// dctx [..][M] -> own rows of dqkv [..][3M]; Dbuf [..][H] fp32 scratch.
 int attn_bwd(int dtype, const void* qkv, const void* ctx, const float* lse, const void* dctx,
-             void* dqkv, float* Dbuf, int T, int N, int M, int H, int causal, cudaStream_t s);
+             void* dqkv, float* Dbuf, int nseq, int N, int p0, int np, int M, int H, int causal,
+             cudaStream_t s);
 
 // tcgen05 flash attention (bf16, d_h in {64,128}); attn_fwd/attn_bwd dispatch to these.
 bool attn_tc_supported(int dtype, int M, int H);
 int attn_tc_debug_off();
-int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int T, int N, int M, int H, int causal,
-                cudaStream_t s);
+int attn_fwd_tc(const void* qkv, void* ctx, float* lse, int nseq, int N, int p0, int np, int M, int H,
+                int causal, cudaStream_t s);
 int attn_bwd_tc(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv,
-                float* D, int T, int N, int M, int H, int causal, cudaStream_t s);
+                float* D, int nseq, int N, int p0, int np, int M, int H, int causal, cudaStream_t s);
 
 // ---------------------------------------------------------------- routing / data movement
 // K1: logits = a·Wg (fp32), top-k (ties -> lower index), gate weights.

@@ -21,6 +21,9 @@ CASES = {
     "c1_f32": PRESETS["c1"],
     "bf16_p": BlockConfig(T=512, seq_len=128, M=256, n_heads=4, E=8, top_k=2, d_ffn=512, R=2,
                           capacity_factor=1.0, causal=1, residual=1, dtype="bf16"),
+    # token chunks (reading Q1'): 4 causal slices of one 512-token sequence
+    "bf16_tok": BlockConfig(T=512, seq_len=512, M=256, n_heads=4, E=8, top_k=2, d_ffn=512, R=4,
+                            capacity_factor=1.0, causal=1, residual=1, dtype="bf16"),
 }
 
 
@@ -31,14 +34,16 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     results = {}
-    runs = [(n, c, "flowmoe", 1) for n, c in CASES.items()]  # (name, cfg, schedule, lanes)
+    runs = [(n, c, "flowmoe", 1) for n, c in CASES.items() if n != "bf16_tok"]  # (name, cfg, schedule, lanes)
     runs = [(n, c, s, l, "nccl") for n, c, s, l in runs]
     runs += [("bf16_p_" + sch, CASES["bf16_p"], sch, lanes, "nccl")
              for sch, lanes in (("flowmoe", 2), ("flowmoe_ar", 1), ("pipe_moe", 2), ("vanilla_ep", 1))]
     # peer-memory A2A (NVLink stores from our kernels) — same results as NCCL
     runs += [("c1_f32_p2p", CASES["c1_f32"], "flowmoe", 2, "p2p"),
              ("bf16_p_p2p", CASES["bf16_p"], "flowmoe", 2, "p2p"),
-             ("bf16_p_p2p_vanilla", CASES["bf16_p"], "vanilla_ep", 1, "p2p")]
+             ("bf16_p_p2p_vanilla", CASES["bf16_p"], "vanilla_ep", 1, "p2p"),
+             ("bf16_tok_nccl", CASES["bf16_tok"], "flowmoe", 1, "nccl"),
+             ("bf16_tok_p2p", CASES["bf16_tok"], "flowmoe", 4, "p2p")]
     for name, base, schedule, lanes, a2a in runs:
         cfg = base.replace(P=P)
         obj = [fm.get_unique_id() if rank == 0 else None]

@@ -59,6 +59,23 @@ def test_create_rejects_invalid_config(field, value, needle):
     assert "invalid argument" in str(ei.value) and needle in str(ei.value)
 
 
+def test_token_chunks_need_causal():
+    """R > sequences (B/R tokens a slice of one sequence) is chunked prefill: only valid
+    with the causal mask (reading Q1'); the config check runs before any CUDA call."""
+    kw = dict(GOOD, R=8)  # B/R = 32 < seq_len = 64
+    with pytest.raises(FlowMoEError) as ei:
+        FlowMoE(BlockShape(**kw, dtype="f32", causal=0))
+    assert "config.R" in str(ei.value)
+    kw = dict(GOOD, R=8, seq_len=48)  # 32 divides neither way
+    with pytest.raises(FlowMoEError) as ei:
+        FlowMoE(BlockShape(**kw, dtype="f32", causal=1))
+    assert "config.R" in str(ei.value) or "config.B" in str(ei.value)
+    try:  # passes validation; without a GPU it then fails in CUDA, not on config.R
+        FlowMoE(BlockShape(**dict(GOOD, R=8), dtype="f32", causal=1)).close()
+    except FlowMoEError as e:
+        assert "config." not in str(e)
+
+
 def test_debug_set_unknown_key():
     with pytest.raises(FlowMoEError):
         fm.debug_set(99, 1)

@@ -41,10 +41,10 @@ CASES = {
 }
 
 
-def _check_block(cfg, forced=True):
+def _check_block(cfg, forced=True, compute_streams=1):
     rep = gen_replicated(cfg)
     wk = gen_worker(cfg, 0)
-    g = run_block_gpu(cfg, rep, wk, forced=forced)
+    g = run_block_gpu(cfg, rep, wk, forced=forced, compute_streams=compute_streams)
     ys, dxs, gflat, eg, st = oracle_block(cfg, rep, [wk], forced=forced)
     tol = TOL[cfg.dtype]
     res = {"y": rel(g["y"], ys[0]), "dx": rel(g["dx"], dxs[0]),
@@ -63,12 +63,40 @@ def _check_block(cfg, forced=True):
     assert np.array_equal(g["idx"], ro.idx)
     assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
     assert np.array_equal(g["counts"], ro.counts)
+    res["_gpu"] = g
     return res
 
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_block_parity_forced_routing(name):
     _check_block(CASES[name])
+
+
+# Token chunks (reading Q1'): R exceeds the number of sequences, every chunk is a causal
+# slice of one sequence (chunked prefill).  Chunk offsets on and off the 128-row tiles.
+TOK_CASES = {
+    "tok_bf16_dh64": BlockConfig(T=512, seq_len=256, M=256, n_heads=4, E=8, top_k=2, d_ffn=512, R=4,
+                                 capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    "tok_bf16_dh128_r8": BlockConfig(T=512, seq_len=512, M=256, n_heads=2, E=4, top_k=2, d_ffn=256, R=8,
+                                     capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    "tok_bf16_ragged": BlockConfig(T=384, seq_len=192, M=128, n_heads=2, E=4, top_k=2, d_ffn=256, R=4,
+                                   capacity_factor=1.25, causal=1, residual=0, P=1, dtype="bf16"),
+    "tok_f32_dh16": BlockConfig(T=256, seq_len=128, M=64, n_heads=4, E=4, top_k=2, d_ffn=128, R=8,
+                                capacity_factor=1.0, causal=1, residual=1, P=1, dtype="f32"),
+    "tok_f32_dh32": BlockConfig(T=192, seq_len=96, M=64, n_heads=2, E=4, top_k=2, d_ffn=96, R=6,
+                                capacity_factor=0.0, causal=1, residual=0, P=1, dtype="f32"),
+}
+
+
+@pytest.mark.parametrize("name", list(TOK_CASES))
+def test_token_chunk_parity(name):
+    """One lane (the paper's serial order) and R lanes (cross-lane QKV / dctx events)
+    both match the oracle, and each other bit for bit."""
+    cfg = TOK_CASES[name]
+    one = _check_block(cfg, compute_streams=1)["_gpu"]
+    many = _check_block(cfg, compute_streams=cfg.R)["_gpu"]
+    for n in ("y", "dx", "grad_flat", "dw1", "db1", "dw2", "db2"):
+        assert np.array_equal(one[n], many[n]), n
 
 
 @pytest.mark.parametrize("name", ["c1_f32", "bf16_small", "c2_bench", "bf16_k3_dh128", "f32_k1"])
@@ -297,13 +325,14 @@ def test_block_stack_chain_parity(dtype, lanes, graph):
         assert rel(g["dw1"][l], grads[l][1]) <= tol, l
 
 
-@pytest.mark.parametrize("dtype,graph", [("bf16", False), ("bf16", True), ("float32", False)])
+@pytest.mark.parametrize("dtype,graph", [("bf16", False), ("bf16", True), ("float32", False), ("tok", True)])
 def test_stack_api_matches_per_block(dtype, graph):
     """flowmoe_stack_fwd/bwd (lanes forked once, chunks chained across blocks) gives
     bit-identical activations and grads to L block_fwd/block_bwd calls: the same kernels
     run on the same lane per chunk, only the block-boundary joins are gone."""
     from tests.gpu_util import run_stack_gpu
-    cfg = CASES["c2_bench"] if dtype == "bf16" else CASES["c1_f32"].replace(R=4, residual=1, causal=1)
+    cfg = {"bf16": CASES["c2_bench"], "tok": TOK_CASES["tok_bf16_dh128_r8"]}.get(
+        dtype, CASES["c1_f32"].replace(R=4, residual=1, causal=1))
     L = 3
     reps = [gen_replicated(cfg, block=l) for l in range(L)]
     wk = gen_worker(cfg, 0)

@@ -341,13 +341,15 @@ def test_forced_routing_gradients_finite_differences():
 
 def test_chunked_equals_unchunked_dropless():
     """Eqs.(19)-(23)/P:520: pipelining changes only the order — R=1 and
-    R in {2,4} agree (dropless, so capacity cannot differ per chunk)."""
+    R in {2,4} agree (dropless, so capacity cannot differ per chunk); so do the token
+    chunks R in {8,16} (2 or 1 tokens of a 4-token causal sequence per chunk, reading
+    Q1': chunked prefill, Table 5's R=8 at B=4)."""
     base = BlockConfig(T=16, seq_len=4, M=8, n_heads=2, E=4, top_k=2, d_ffn=16, R=1,
                        capacity_factor=0.0, causal=1, residual=1, P=2, dtype="f32")
     rep, xs, dys = _tiny_setup(base)
     ref_y, st = o.block_forward(base, rep, xs)
     ref = o.block_backward(base, rep, st, dys)
-    for R in (2, 4):
+    for R in (2, 4, 8, 16):
         cfg = base.replace(R=R)
         ys, st2 = o.block_forward(cfg, rep, xs)
         got = o.block_backward(cfg, rep, st2, dys)
@@ -360,6 +362,31 @@ def test_chunked_equals_unchunked_dropless():
         ys_ep = o.block_forward_ep(cfg, rep, xs)
         for a, b in zip(ys_ep, ref_y):
             assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+
+
+def test_chunked_prefill_attention_is_causal_attention():
+    """Reading Q1' (token chunks): chunk [p0, p0+n) of a causal sequence attends to the
+    keys [0, p0+n) it has seen so far — brute force per query row, chunk by chunk,
+    built only from the rows the chunk may read, equals the oracle's causal MHA rows."""
+    rng = np.random.default_rng(7)
+    N, M, h = 12, 8, 2
+    dh = M // h
+    x = rng.standard_normal((N, M))
+    wqkv, wo = rng.standard_normal((M, 3 * M)) / np.sqrt(M), rng.standard_normal((M, M)) / np.sqrt(M)
+    a_ref, _ = o.mha_forward(x, wqkv, wo, N, h, causal=1, residual=0)
+    for n in (1, 3, 4, 6):
+        ctx = np.zeros((N, M))
+        for p0 in range(0, N, n):
+            seen = x[:p0 + n] @ wqkv  # projections of the rows up to the chunk end only
+            for i in range(p0, p0 + n):
+                for hh in range(h):
+                    q = seen[i, hh * dh:(hh + 1) * dh]
+                    ks = seen[:i + 1, M + hh * dh:M + (hh + 1) * dh]
+                    vs = seen[:i + 1, 2 * M + hh * dh:2 * M + (hh + 1) * dh]
+                    sc = ks @ q / np.sqrt(dh)
+                    p = np.exp(sc - sc.max())
+                    ctx[i, hh * dh:(hh + 1) * dh] = (p / p.sum()) @ vs
+        assert np.max(np.abs(ctx @ wo - a_ref)) <= 1e-12 * np.max(np.abs(a_ref))
 
 
 def test_ep_forward_matches_direct_with_drops():
