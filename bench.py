@@ -63,6 +63,7 @@ def parse():
                     help="compute lanes (1 = paper's single compute stream; default R)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the per-kernel table here")
+    ap.add_argument("--trace-dir", default="/tmp", help="where the CUPTI chrome traces are written")
     ap.add_argument("--trace-iters", type=int, default=20,
                     help="CUDA-graph replays traced with CUPTI (timeline, exposed comm); 0 = off")
     return ap.parse_args()
@@ -362,7 +363,7 @@ def main():
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            tl = trace_replays(run, args.trace_iters, f"/tmp/flowmoe_trace_r{rank}.json",
+            tl = trace_replays(run, args.trace_iters, os.path.join(args.trace_dir, f"flowmoe_trace_r{rank}.json"),
                                trim=max(0, min(3, (args.trace_iters - 2) // 4)),
                                sync=(dist.barrier if world > 1 else None))
         except Exception as e:  # the timeline is diagnostics, never the measurement

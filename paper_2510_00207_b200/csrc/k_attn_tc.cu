@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int quarter = warp & 3;
     const int kloc = quarter * 32 + lane;
     const int key = k0 + kloc;
-    const bool own = kt * 128 + kloc < np;
+    const int kend = p0 + np;  // own keys: key < kend
+    const bool own = key < kend;
     const int t128 = threadIdx.x - 64;  // 0..127
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int it = 0; it < niter; ++it) {
@@ -385,10 +386,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int i = 0; i < 32; ++i) {
           const int ql = c * 32 + i;
           const int qi = qbase + ql;
-          const bool ok = qi < N && own && (!causal || key <= qi);
+          const bool ok = qi < N && key < kend && (!causal || key <= qi);
           const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - sL[ql]) : 0.f;
           p[i] = pv;
-          ds[i] = ok ? pv * (__uint_as_float(rp[i]) - sD[ql]) : 0.f;
+          ds[i] = pv * (__uint_as_float(rp[i]) - sD[ql]);  // rows past N / own range: finite, pv = 0
         }
         st_row32_bf16(sP, kloc, c * 32, p);
         st_row32_bf16(sdS, kloc, c * 32, ds);
@@ -517,7 +518,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int quarter = warp & 3;
     const int rloc = quarter * 32 + lane;
     const int qrow = q0 + rloc;
-    const bool own = qt * 128 + rloc < np;
+    const int qend = p0 + np;  // own queries: qrow < qend
+    const bool own = qrow < qend;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float L2 = own ? lse[(int64_t)(row_base + qrow) * H + h] * LOG2E : 0.f;
     const float Dq = own ? row_dot_bf16<DH>(ctxO + (int64_t)(row_base + qrow) * M + h * DH,
@@ -538,9 +540,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int kj = j * 128 + c * 32 + i;
-          const bool ok = own && kj < N && (!causal || kj <= qrow);
+          const bool ok = qrow < qend && kj < N && (!causal || kj <= qrow);
           const float pv = ok ? exp2f(__uint_as_float(rs[i]) * scale_log2 - L2) : 0.f;
-          ds[i] = ok ? pv * (__uint_as_float(rp[i]) - Dq) : 0.f;
+          ds[i] = pv * (__uint_as_float(rp[i]) - Dq);
         }
         st_row32_bf16(sdS, rloc, c * 32, ds);
       }

@@ -7,123 +7,181 @@
 //   K9 gather_gate_bwd  (B4: dI' = Σ dX + dlogits·Wgᵀ (+dO))
 //   gate_wgrad          (B4: dWg += I'ᵀ·dlogits, deterministic split-T)
 //   colsum_acc          (B2: db1, db2)
-// All HBM-bound: one warp per token row with 16-byte vector accesses.
+// All HBM-bound: 16-byte vector accesses, register tiles for the two small
+// contractions with Wg (E <= 64 columns), deterministic reductions throughout.
 // Readings: Q3 slot-major-then-token positions, Q4 top-k on fp32
 // logits with ties -> lower index, Q5 renormalised top-k weights (k>=2) or raw
 // softmax prob (k=1), Q6 no gate bias.
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "kernels.h"
 
-namespace fm {
+namespace cg = cooperative_groups;
 
-// E contiguous storage elements -> fp32 (16-byte vector loads when the row allows)
-template <typename T, int E>
-FM_DEV void load_row(const T* p, float* out) {
-  constexpr int V = 16 / sizeof(T);
-  if constexpr (E % V == 0) {
-#pragma unroll
-    for (int i = 0; i < E; i += V) load16<T>(p + i, out + i);
-  } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i) out[i] = to_f<T>(p[i]);
-  }
-}
+namespace fm {
 
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
                                 int E, int k, int C, int* hist, int* warp_tot);
 
 // ------------------------------------------------------------------ K1
-// One warp per token.  Lane l owns row elements [8l + 256i, 8l + 256i + 8) (bf16)
-// or [4l + 128i, ...) (f32) and keeps E partial dot products; xor-reduce gives
-// every lane all E logits, then top-k by repeated argmax (strictly greater ->
-// lower index wins ties).
-// With `done` != nullptr the kernel also runs K2: the CTA that finishes last (atomic
-// ticket on done[0], reset afterwards) performs the deterministic routing scan of the
-// whole chunk, saving a launch.
+// logits = A·Wg is a [T_r × M]·[M × E] product with E ≤ 64: HBM-bound on A.  A CTA
+// covers TB tokens and one slice of M; each lane keeps a 4-token × EG-expert register
+// tile (one 16-byte load of A per token feeds 4·EG·V FMAs), the 8 warps stride the
+// slice, and their partials are summed in warp order through shared memory.  The KS
+// slices of a token tile form one thread-block cluster; rank 0 sums the others'
+// partials in rank order over DSMEM (deterministic, no global scratch), then does the
+// top-k (strictly greater -> lower index wins ties) for its TB tokens.
+// With `done` != nullptr the kernel also runs K2: the rank-0 CTA that finishes last
+// (atomic ticket on done[0], reset afterwards) performs the deterministic routing scan
+// of the whole chunk, saving a launch.
+template <typename T, int E>
+struct GateTile {
+  static constexpr int NEG = E >= 4 ? 4 : E;   // expert groups across lanes
+  static constexpr int EG = E / NEG;           // experts per lane
+  static constexpr int TB = (32 / NEG) * 4;    // tokens per CTA (4 per lane)
+  static constexpr size_t smem() {
+    const size_t red = (size_t)9 * TB * E * sizeof(float);  // 8 warp partials + the sum
+    const size_t hist = (size_t)E * 256 * sizeof(int);     // fused routing scan
+    return red > hist ? red : hist;
+  }
+};
+
+// n consecutive storage elements (n·sizeof(T) in {2,4,8,16,...} bytes, aligned) -> fp32
+template <typename T, int n>
+FM_DEV void load_n(const T* p, float* out) {
+  constexpr int bytes = n * (int)sizeof(T);
+  if constexpr (bytes % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < n; i += 16 / (int)sizeof(T)) load16<T>(p + i, out + i);
+  } else if constexpr (bytes == 8) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    if constexpr (sizeof(T) == 4) {
+      out[0] = __uint_as_float(u.x); out[1] = __uint_as_float(u.y);
+    } else {
+      out[0] = __uint_as_float(u.x << 16); out[1] = __uint_as_float(u.x & 0xFFFF0000u);
+      out[2] = __uint_as_float(u.y << 16); out[3] = __uint_as_float(u.y & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < n; ++i) out[i] = to_f<T>(p[i]);
+  }
+}
+
 template <typename T, int E>
 __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
                                                         const int32_t* forced, float* logits,
-                                                        int32_t* idx, float* w, int T_, int M,
+                                                        int32_t* idx, float* w, int T_, int M, int MS,
                                                         int k, int32_t* pos, int32_t* counts,
                                                         int32_t* src, int C, unsigned int* done) {
-  FM_PDL_ENTRY();
-  extern __shared__ int hist[];  // [E][blockDim.x] for the fused scan
+  using G = GateTile<T, E>;
+  constexpr int V = 16 / sizeof(T), TB = G::TB, EG = G::EG, NEG = G::NEG;
+  extern __shared__ float gsm[];  // [8][TB][E] warp partials, [TB][E] CTA sum; later the scan's hist
   __shared__ int warp_tot[32];
   __shared__ unsigned int ticket;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp < T_) {
-  constexpr int V = 16 / sizeof(T);
-  float acc[E];
+  cg::cluster_group cl = cg::this_cluster();
+  FM_PDL_ENTRY();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tg = lane / NEG, eg = lane % NEG;
+  const int tt0 = blockIdx.x * TB;                 // first token of the tile
+  const int tl0 = tt0 + tg * 4;                    // this lane's first token
+  const int m_beg = blockIdx.y * MS, m_end = min(M, m_beg + MS);
+  float acc[4][EG];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  const T* row = a + (int64_t)warp * M;
-  for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
-    float x[8];
-    load16<T>(row + m0, x);
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      float wr[E];
-      load_row<T, E>(wg + (int64_t)(m0 + i) * E, wr);
+    for (int j = 0; j < EG; ++j) acc[i][j] = 0.f;
+  for (int m = m_beg + warp * V; m < m_end; m += 8 * V) {
+    float xa[4][V];
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = fmaf(x[i], wr[e], acc[e]);
+    for (int i = 0; i < 4; ++i) {
+      if (tl0 + i < T_) load16<T>(a + (int64_t)(tl0 + i) * M + m, xa[i]);
+      else
+#pragma unroll
+        for (int v = 0; v < V; ++v) xa[i][v] = 0.f;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float wr[EG];
+      load_n<T, EG>(wg + (int64_t)(m + v) * E + eg * EG, wr);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < EG; ++j) acc[i][j] = fmaf(xa[i][v], wr[j], acc[i][j]);
     }
   }
+  float* red = gsm + 8 * TB * E;
+  {
+    float* part = gsm + warp * TB * E;
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = warp_sum(acc[e]);
-  if (lane < E) {
-    float mine = 0.f;
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int e = 0; e < E; ++e) if (e == lane) mine = acc[e];
-    logits[(int64_t)warp * E + lane] = mine;
+      for (int j = 0; j < EG; ++j) part[(tg * 4 + i) * E + eg * EG + j] = acc[i][j];
   }
-  if (lane == 0) {
-  // top-k selection on logits
-  uint64_t taken = 0;
-  int sel[8];
-  for (int j = 0; j < k; ++j) {
-    int best = -1;
-    float bv = 0.f;
-    if (forced) {
-      best = forced[(int64_t)warp * k + j];
-    } else {
+  __syncthreads();
+  for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
+    float sum = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (!((taken >> e) & 1ull) && (best < 0 || acc[e] > bv)) { best = e; bv = acc[e]; }
-    }
-    taken |= 1ull << best;
-    sel[j] = best;
-    idx[(int64_t)warp * k + j] = best;
+    for (int ww = 0; ww < 8; ++ww) sum += gsm[ww * TB * E + q];
+    red[q] = sum;
   }
-  float lsel[8];
-  for (int j = 0; j < k; ++j) {
-    float v = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) if (e == sel[j]) v = acc[e];
-    lsel[j] = v;
-  }
-  if (k == 1) {
-    // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
-    float den = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) den += expf(acc[e] - lsel[0]);
-    w[warp] = 1.f / den;
+  // cluster (1, KS, 1): rank 0 adds the other slices' sums in rank order
+  const unsigned int nrank = cl.num_blocks(), rank = cl.block_rank();
+  if (nrank > 1) {
+    cl.sync();
+    if (rank == 0)
+      for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
+        float sum = red[q];
+        for (unsigned int r = 1; r < nrank; ++r) sum += cl.map_shared_rank(red, r)[q];
+        red[q] = sum;
+      }
+    cl.sync();  // peers keep their shared memory alive until rank 0 has read it
+    if (rank != 0) return;
   } else {
-    float mx = lsel[0];
-    for (int j = 1; j < k; ++j) mx = fmaxf(mx, lsel[j]);
-    float den = 0.f, ex[8];
-    for (int j = 0; j < k; ++j) { ex[j] = expf(lsel[j] - mx); den += ex[j]; }
-    for (int j = 0; j < k; ++j) w[(int64_t)warp * k + j] = ex[j] / den;
+    __syncthreads();
   }
-  }  // lane 0
-  }  // warp < T_
+  for (int q = threadIdx.x; q < TB * E; q += blockDim.x)
+    if (tt0 + q / E < T_) logits[(int64_t)tt0 * E + q] = red[q];
+  if (threadIdx.x < TB && tt0 + (int)threadIdx.x < T_) {
+    const int t = tt0 + threadIdx.x;
+    const float* lg = red + threadIdx.x * E;
+    // top-k selection on logits
+    uint64_t taken = 0;
+    int sel[8];
+    for (int j = 0; j < k; ++j) {
+      int best = -1;
+      float bv = 0.f;
+      if (forced) {
+        best = forced[(int64_t)t * k + j];
+      } else {
+        for (int e = 0; e < E; ++e)
+          if (!((taken >> e) & 1ull) && (best < 0 || lg[e] > bv)) { best = e; bv = lg[e]; }
+      }
+      taken |= 1ull << best;
+      sel[j] = best;
+      idx[(int64_t)t * k + j] = best;
+    }
+    if (k == 1) {
+      // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
+      const float l0 = lg[sel[0]];
+      float den = 0.f;
+      for (int e = 0; e < E; ++e) den += expf(lg[e] - l0);
+      w[t] = 1.f / den;
+    } else {
+      float mx = lg[sel[0]];
+      for (int j = 1; j < k; ++j) mx = fmaxf(mx, lg[sel[j]]);
+      float den = 0.f, ex[8];
+      for (int j = 0; j < k; ++j) { ex[j] = expf(lg[sel[j]] - mx); den += ex[j]; }
+      for (int j = 0; j < k; ++j) w[(int64_t)t * k + j] = ex[j] / den;
+    }
+  }
   if (done == nullptr) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) ticket = atomicAdd(done, 1u);
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
-  __threadfence();  // every CTA's idx is visible
-  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, warp_tot);
+  __threadfence();  // every tile's idx is visible
+  route_scan_body(idx, pos, counts, src, T_, E, k, C, reinterpret_cast<int*>(gsm), warp_tot);
   if (threadIdx.x == 0) *done = 0u;  // ready for the next use (stream-ordered)
 }
 
@@ -138,26 +196,41 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
     default: return (int)cudaErrorInvalidValue;                 \
   }
 
+// Slices of M per token tile: enough CTAs to cover ~2 waves of the 148 SMs, at most a
+// portable cluster (8), at least one 16-byte vector per warp.
+static void gate_split(int T_, int M, int TB, int V, int* KS, int* MS) {
+  const int tiles = (T_ + TB - 1) / TB, nvec = M / V;
+  int ks = (2 * 148 + tiles - 1) / tiles;
+  ks = ks < 1 ? 1 : (ks > 8 ? 8 : ks);
+  if (ks > nvec / 8) ks = nvec / 8 > 0 ? nvec / 8 : 1;
+  const int msv = (nvec + ks - 1) / ks;
+  *MS = msv * V;
+  *KS = (nvec + msv - 1) / msv;
+}
+
+template <typename T, int E>
+static void gate_topk_launch_t(const void* a, const void* wg, const int32_t* forced, float* logits, int32_t* idx,
+                               float* w, int T_, int M, int k, int32_t* pos, int32_t* counts, int32_t* src, int C,
+                               unsigned int* done, cudaStream_t s) {
+  using G = GateTile<T, E>;
+  int KS, MS;
+  gate_split(T_, M, G::TB, 16 / (int)sizeof(T), &KS, &MS);
+  auto kern = gate_topk_kernel<T, E>;
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem()), true);
+  (void)once;
+  launch_kc(kern, dim3((T_ + G::TB - 1) / G::TB, KS), 256, G::smem(), s, dim3(1, KS, 1), (const T*)a,
+            (const T*)wg, forced, logits, idx, w, T_, M, MS, k, pos, counts, src, C, done);
+}
+
 template <int E>
 static void gate_topk_launch(int dtype, const void* a, const void* wg, const int32_t* forced,
                              float* logits, int32_t* idx, float* w, int T_, int M, int k,
                              int32_t* pos, int32_t* counts, int32_t* src, int C, unsigned int* done,
                              cudaStream_t s) {
-  dim3 grid((T_ * 32 + 255) / 256);
-  const size_t smem = done ? (size_t)E * 256 * sizeof(int) : 0;
-  if (dtype == DT_F32) {
-    static bool once = (cudaFuncSetAttribute(gate_topk_kernel<float, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             E * 256 * (int)sizeof(int)), true);
-    (void)once;
-    launch_k(gate_topk_kernel<float, E>, grid, 256, smem, s, (const float*)a, (const float*)wg, forced,
-             logits, idx, w, T_, M, k, pos, counts, src, C, done);
-  } else {
-    static bool once = (cudaFuncSetAttribute(gate_topk_kernel<bf16, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             E * 256 * (int)sizeof(int)), true);
-    (void)once;
-    launch_k(gate_topk_kernel<bf16, E>, grid, 256, smem, s, (const bf16*)a, (const bf16*)wg, forced,
-             logits, idx, w, T_, M, k, pos, counts, src, C, done);
-  }
+  if (dtype == DT_F32)
+    gate_topk_launch_t<float, E>(a, wg, forced, logits, idx, w, T_, M, k, pos, counts, src, C, done, s);
+  else
+    gate_topk_launch_t<bf16, E>(a, wg, forced, logits, idx, w, T_, M, k, pos, counts, src, C, done, s);
 }
 
 int gate_topk(int dtype, const void* a, const void* wg, const int32_t* forced, float* logits,
@@ -179,61 +252,53 @@ int gate_route(int dtype, const void* a, const void* wg, const int32_t* forced, 
 
 // ------------------------------------------------------------------ K2
 // One CTA per chunk.  Slots in slot-major order s = j*T + t are split into
-// contiguous per-thread segments; pass 1 counts per expert, a block-wide
-// exclusive scan per expert gives every thread its starting position, pass 2
-// re-walks the segment assigning pos = base[e]++.  Deterministic: pos equals
-// the number of earlier slots (in slot-major order) routed to the same expert.
+// contiguous per-thread segments; pass 1 counts per expert into hist[e][thread], the
+// per-expert exclusive scans over threads run in parallel (warp w scans experts
+// w, w+nwarps, ...: each lane sums a run of consecutive threads' counts, one warp
+// shuffle scan, write-back), pass 2 re-walks the segment assigning pos = base[e]++.
+// Deterministic: pos equals the number of earlier slots (in slot-major order) routed
+// to the same expert.
 constexpr int RS_THREADS = 512;
 
-__device__ int block_excl_scan(int v, int* warp_tot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    warp_tot[lane] = t;  // inclusive over warps
-  }
-  __syncthreads();
-  int res = x - v + (wid > 0 ? warp_tot[wid - 1] : 0);
-  __syncthreads();
-  return res;
-}
-
-// Block-wide deterministic routing scan (one CTA, any block size <= 1024): hist is
-// [E][blockDim.x] ints of dynamic shared memory.
+// Block-wide deterministic routing scan (one CTA, blockDim a multiple of 32, <= 1024):
+// hist is [E][blockDim.x] ints of dynamic shared memory.
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
                                 int E, int k, int C, int* hist, int* warp_tot) {
+  (void)warp_tot;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int n = T_ * k;
   const int seg = (n + nt - 1) / nt;
   const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
   for (int e = 0; e < E; ++e) hist[e * nt + tid] = 0;
   for (int i = tid; i < E * C; i += nt) src[i] = -1;
+  __syncthreads();
   for (int s = s0; s < s1; ++s) {
-    const int j = s / T_, t = s % T_;
+    const int j = s / T_, t = s - j * T_;
     hist[idx[(int64_t)t * k + j] * nt + tid] += 1;
   }
   __syncthreads();
-  for (int e = 0; e < E; ++e) {
-    int v = hist[e * nt + tid];
-    int ex = block_excl_scan(v, warp_tot);
-    hist[e * nt + tid] = ex;
-    if (tid == nt - 1) counts[e] = ex + v;
+  const int lane = tid & 31, nw = nt >> 5, per = nt >> 5;  // per: threads summed by one lane
+  for (int e = tid >> 5; e < E; e += nw) {
+    int* h = hist + e * nt + lane * per;
+    int run = 0;
+    for (int i = 0; i < per; ++i) run += h[i];
+    int x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) counts[e] = x;
+    int ex = x - run;  // exclusive prefix of this lane's run
+    for (int i = 0; i < per; ++i) {
+      const int v = h[i];
+      h[i] = ex;
+      ex += v;
+    }
   }
   __syncthreads();
   for (int s = s0; s < s1; ++s) {
-    const int j = s / T_, t = s % T_;
+    const int j = s / T_, t = s - j * T_;
     const int e = idx[(int64_t)t * k + j];
     const int p = hist[e * nt + tid]++;
     const bool kept = p < C;
@@ -261,25 +326,32 @@ int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, 
   return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ K3
+// ------------------------------------------------------------------ K3 / K7 / K8
+// Row movement is spread one 16-byte vector per thread over (row, vector) pairs, so a
+// chunk's copy has thousands of independent loads in flight (a warp per row left most
+// SMs idle at small T_r and serialised each warp's loads at large M).
 template <typename T>
-__global__ void __launch_bounds__(256) permute_pack_kernel(const T* a, const int32_t* src,
-                                                           T* send, int rows, int C, int ldE,
+__global__ void __launch_bounds__(256) permute_pack_kernel(const T* __restrict__ a, const int32_t* __restrict__ src,
+                                                           T* __restrict__ send, int rows, int C, int ldE,
                                                            int M, int k) {
   FM_PDL_ENTRY();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const int sl = src[warp];
   constexpr int V = 16 / sizeof(T);
-  const int64_t drow = (int64_t)(warp / C) * ldE + warp % C;
-  uint4* dst = reinterpret_cast<uint4*>(send + drow * M);
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
   const int nv = M / V;
+  const int sl = src[r];
+  uint4* dst = reinterpret_cast<uint4*>(send + ((int64_t)(r / C) * ldE + r % C) * M);
   if (sl < 0) {
     for (int i = lane; i < nv; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
-  } else {
-    const uint4* srow = reinterpret_cast<const uint4*>(a + (int64_t)(sl / k) * M);
-    for (int i = lane; i < nv; i += 32) dst[i] = __ldg(srow + i);
+    return;
   }
+  const uint4* srow = reinterpret_cast<const uint4*>(a + (int64_t)(sl / k) * M);
+  int i = lane;
+  for (; i + 96 < nv; i += 128) {  // 4 independent 16-byte loads in flight per lane
+    const uint4 v0 = __ldg(srow + i), v1 = __ldg(srow + i + 32), v2 = __ldg(srow + i + 64), v3 = __ldg(srow + i + 96);
+    dst[i] = v0; dst[i + 32] = v1; dst[i + 64] = v2; dst[i + 96] = v3;
+  }
+  for (; i < nv; i += 32) dst[i] = __ldg(srow + i);
 }
 
 int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E, int C, int ldE,
@@ -294,193 +366,262 @@ int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E
   return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ K7
+// K7: out[t] = Σ_j w_tj·Y[e_tj][pos_tj] (+ resid[t]); thread = (token, 16-byte vector)
 template <typename T>
 __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, const int32_t* idx,
                                                                 const int32_t* pos, const float* w,
                                                                 const T* resid, T* out, int T_,
                                                                 int M, int k, int ldE) {
   FM_PDL_ENTRY();
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (t >= T_) return;
   constexpr int V = 16 / sizeof(T);
-  const T* rows[8];
-  float ws[8];
-  int nk = 0;
+  const int nv = M / V;
+  const unsigned int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (unsigned int)(T_ * nv)) return;
+  const int t = (int)(g / (unsigned int)nv), m = (int)(g % (unsigned int)nv) * V;
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.f;
   for (int j = 0; j < k; ++j) {
-    int p = pos[(int64_t)t * k + j];
-    if (p >= 0) {
-      rows[nk] = y + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M;
-      ws[nk] = w[(int64_t)t * k + j];
-      ++nk;
-    }
-  }
-  for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < nk; ++j) {
-      float v[8];
-      load16<T>(rows[j] + m0, v);
+    const int p = pos[(int64_t)t * k + j];
+    if (p < 0) continue;
+    const float wj = w[(int64_t)t * k + j];
+    float v[V];
+    load16<T>(y + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M + m, v);
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = fmaf(ws[j], v[i], acc[i]);
-    }
-    if (resid) {
-      float v[8];
-      load16<T>(resid + (int64_t)t * M + m0, v);
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += v[i];
-    }
-    store16<T>(out + (int64_t)t * M + m0, acc);
+    for (int i = 0; i < V; ++i) acc[i] = fmaf(wj, v[i], acc[i]);
   }
+  if (resid) {
+    float v[V];
+    load16<T>(resid + (int64_t)t * M + m, v);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] += v[i];
+  }
+  store16<T>(out + (int64_t)t * M + m, acc);
 }
 
 int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_t* pos,
                       const float* w, const void* resid, void* out, int T_, int M, int k, int ldE,
                       cudaStream_t s) {
   if (T_ <= 0) return 0;
-  dim3 grid((T_ * 32 + 255) / 256);
+  const int64_t n = (int64_t)T_ * (M / (dtype == DT_F32 ? 4 : 8));
+  if (n >= (1ll << 31)) return (int)cudaErrorInvalidValue;
+  dim3 grid((unsigned)((n + 255) / 256));
   if (dtype == DT_F32)
     launch_k(unpermute_combine_kernel<float>, grid, 256, 0, s, (const float*)y, idx, pos, w,
-                                                        (const float*)resid, (float*)out, T_, M, k, ldE);
+             (const float*)resid, (float*)out, T_, M, k, ldE);
   else
     launch_k(unpermute_combine_kernel<bf16>, grid, 256, 0, s, (const bf16*)y, idx, pos, w,
-                                                       (const bf16*)resid, (bf16*)out, T_, M, k, ldE);
+             (const bf16*)resid, (bf16*)out, T_, M, k, ldE);
   return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ K8
-// warps [0, T): token work; warps [T, T + E*C): zero the padding rows of dy.
-template <typename T>
+// K8: dY[e][pos] = w·dO[t]; dw[t][j] = <dO[t], Y[e][pos]>.  One CTA per token (threads
+// stride the 16-byte vectors of the row, all K slots in one pass, block reduction of
+// the K dots in a fixed order); CTAs past T_ zero 8 padding rows of dY each.
+template <typename T, int K>
 __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, const T* y,
                                                                const int32_t* idx,
                                                                const int32_t* pos, const float* w,
                                                                const int32_t* src, T* dy,
-                                                               float* dw, int T_, int M, int k,
+                                                               float* dw, int T_, int M,
                                                                int rows, int C, int ldE) {
+  __shared__ float red[8][K];  // [warp][slot]
   FM_PDL_ENTRY();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   constexpr int V = 16 / sizeof(T);
-  if (warp >= T_) {
-    const int r = warp - T_;
+  const int nv = M / V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= T_) {  // padding rows (src < 0) of dy get zeros
+    const int r = ((int)blockIdx.x - T_) * 8 + warp;
     if (r >= rows || src[r] >= 0) return;
     uint4* dst = reinterpret_cast<uint4*>(dy + ((int64_t)(r / C) * ldE + r % C) * M);
-    for (int i = lane; i < M / V; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < nv; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
     return;
   }
-  const int t = warp;
+  const int t = blockIdx.x;
   const T* g = dout + (int64_t)t * M;
-  for (int j = 0; j < k; ++j) {
-    const int p = pos[(int64_t)t * k + j];
-    if (p < 0) {  // dropped slot: contributes 0, so dw = 0
-      if (lane == 0) dw[(int64_t)t * k + j] = 0.f;
-      continue;
-    }
-    const int64_t row = (int64_t)idx[(int64_t)t * k + j] * ldE + p;
-    const float wj = w[(int64_t)t * k + j];
-    float dot = 0.f;
-    for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
-      float gv[8], yv[8], o[8];
-      load16<T>(g + m0, gv);
-      load16<T>(y + row * M + m0, yv);
+  int64_t row[K];
+  float wj[K], dot[K];
 #pragma unroll
-      for (int i = 0; i < V; ++i) { dot = fmaf(gv[i], yv[i], dot); o[i] = wj * gv[i]; }
-      store16<T>(dy + row * M + m0, o);
-    }
-    dot = warp_sum(dot);
-    if (lane == 0) dw[(int64_t)t * k + j] = dot;
+  for (int j = 0; j < K; ++j) {
+    const int p = pos[(int64_t)t * K + j];
+    row[j] = p < 0 ? -1 : ((int64_t)idx[(int64_t)t * K + j] * ldE + p) * M;
+    wj[j] = w[(int64_t)t * K + j];
+    dot[j] = 0.f;
   }
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    float gv[V];
+    load16<T>(g + v * V, gv);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (row[j] < 0) continue;  // dropped slot: contributes 0, so dw = 0
+      float yv[V], o[V];
+      load16<T>(y + row[j] + v * V, yv);
+#pragma unroll
+      for (int i = 0; i < V; ++i) { dot[j] = fmaf(gv[i], yv[i], dot[j]); o[i] = wj[j] * gv[i]; }
+      store16<T>(dy + row[j] + v * V, o);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const float d = warp_sum(dot[j]);
+    if (lane == 0) red[warp][j] = d;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      float d = 0.f;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) d += red[i][j];
+      dw[(int64_t)t * K + j] = row[j] < 0 ? 0.f : d;
+    }
+  }
+}
+
+template <int K>
+static void combine_bwd_launch(int dtype, const void* dout, const void* y, const int32_t* idx, const int32_t* pos,
+                               const float* w, const int32_t* src, void* dy, float* dw, int T_, int M, int rows,
+                               int C, int ldE, cudaStream_t s) {
+  dim3 grid(T_ + (rows + 7) / 8);
+  if (dtype == DT_F32)
+    launch_k(combine_bwd_pack_kernel<float, K>, grid, 256, 0, s, (const float*)dout, (const float*)y, idx, pos, w,
+             src, (float*)dy, dw, T_, M, rows, C, ldE);
+  else
+    launch_k(combine_bwd_pack_kernel<bf16, K>, grid, 256, 0, s, (const bf16*)dout, (const bf16*)y, idx, pos, w,
+             src, (bf16*)dy, dw, T_, M, rows, C, ldE);
 }
 
 int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* idx,
                      const int32_t* pos, const float* w, const int32_t* src, void* dy, float* dw,
                      int T_, int M, int k, int E, int C, int ldE, cudaStream_t s) {
   const int rows = E * C;
-  dim3 grid(((T_ + rows) * 32 + 255) / 256);
-  if (dtype == DT_F32)
-    launch_k(combine_bwd_pack_kernel<float>, grid, 256, 0, s, (const float*)dout, (const float*)y, idx,
-                                                       pos, w, src, (float*)dy, dw, T_, M, k, rows, C, ldE);
-  else
-    launch_k(combine_bwd_pack_kernel<bf16>, grid, 256, 0, s, (const bf16*)dout, (const bf16*)y, idx,
-                                                      pos, w, src, (bf16*)dy, dw, T_, M, k, rows, C, ldE);
+  switch (k) {
+    case 1: combine_bwd_launch<1>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 2: combine_bwd_launch<2>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 3: combine_bwd_launch<3>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 4: combine_bwd_launch<4>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 5: combine_bwd_launch<5>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 6: combine_bwd_launch<6>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 7: combine_bwd_launch<7>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    case 8: combine_bwd_launch<8>(dtype, dout, y, idx, pos, w, src, dy, dw, T_, M, rows, C, ldE, s); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
   return (int)cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ K9
-template <typename T, int E>
+// dA[t] = Σ_j dx[e_tj][pos_tj] + dlogits[t]·Wgᵀ (+ dO[t]).  A thread owns TPL tokens ×
+// one 16-byte column vector (V columns).  It derives the dlogits of its tokens in
+// registers (cheap: k slots), then per column reads the Wg row (E values, L2-resident)
+// once for all TPL tokens, adds the k gathered rows (+ dO) and stores.  Lanes of a warp
+// take consecutive column vectors of the same tokens (coalesced); CTAs are sized so
+// small chunks still spread over the SMs.
+template <int E>
+struct GgbTile { static constexpr int TPL = E <= 16 ? 4 : (E == 32 ? 2 : 1); };  // register-bound max
+
+template <typename T, int E, int TPL>
 __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
-    const T* dx, const int32_t* idx, const int32_t* pos, const float* w, const float* dw,
-    const float* logits, const T* wg, const T* dres, T* dA, float* dlogits, int T_, int M, int k,
-    int ldE) {
-  FM_PDL_ENTRY();
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (t >= T_) return;
+    const T* __restrict__ dx, const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
+    const float* __restrict__ w, const float* __restrict__ dw, const float* __restrict__ logits,
+    const T* __restrict__ wg, const T* __restrict__ dres, T* __restrict__ dA, float* __restrict__ dlogits, int T_,
+    int M, int k, int ldE, int CV) {
   constexpr int V = 16 / sizeof(T);
+  FM_PDL_ENTRY();
+  const int tgi = threadIdx.x / CV, cv = threadIdx.x % CV;
+  const int tb = (blockDim.x / CV) * TPL;              // tokens per CTA
+  const int t0 = blockIdx.x * tb + tgi * TPL;
+  const int m = (blockIdx.y * CV + cv) * V;
   // dlogits (reading Q5): k>=2: dl_{e_j} = w_j (dw_j - Σ w dw); k=1: dl = p ⊙ (g - <p,g>)
-  float dl[E];
+  float dl[TPL][E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) dl[e] = 0.f;
-  const float* lt = logits + (int64_t)t * E;
-  if (k == 1) {
-    const int e0 = idx[t];
-    float mx = -INFINITY;
+  for (int i = 0; i < TPL; ++i) {
+    const int t = t0 + i;
 #pragma unroll
-    for (int e = 0; e < E; ++e) mx = fmaxf(mx, lt[e]);
-    float den = 0.f;
+    for (int e = 0; e < E; ++e) dl[i][e] = 0.f;
+    if (t >= T_) continue;
+    if (k == 1) {
+      const float* lt = logits + (int64_t)t * E;
+      const int e0 = idx[t];
+      float mx = -INFINITY;
 #pragma unroll
-    for (int e = 0; e < E; ++e) { dl[e] = expf(lt[e] - mx); den += dl[e]; }
-    const float g0 = dw[t];
-    float pe0 = 0.f;
+      for (int e = 0; e < E; ++e) mx = fmaxf(mx, lt[e]);
+      float den = 0.f;
 #pragma unroll
-    for (int e = 0; e < E; ++e) { dl[e] /= den; if (e == e0) pe0 = dl[e]; }
-    // <p, g> = p_e0 * g0
+      for (int e = 0; e < E; ++e) { dl[i][e] = expf(lt[e] - mx); den += dl[i][e]; }
+      const float g0 = dw[t];
+      float pe0 = 0.f;
 #pragma unroll
-    for (int e = 0; e < E; ++e) dl[e] = dl[e] * ((e == e0 ? g0 : 0.f) - pe0 * g0);
-  } else {
-    float inner = 0.f;
-    for (int j = 0; j < k; ++j) inner += w[(int64_t)t * k + j] * dw[(int64_t)t * k + j];
+      for (int e = 0; e < E; ++e) { dl[i][e] /= den; if (e == e0) pe0 = dl[i][e]; }
+#pragma unroll
+      for (int e = 0; e < E; ++e) dl[i][e] = dl[i][e] * ((e == e0 ? g0 : 0.f) - pe0 * g0);
+    } else {
+      float inner = 0.f;
+      for (int j = 0; j < k; ++j) inner += w[(int64_t)t * k + j] * dw[(int64_t)t * k + j];
+      for (int j = 0; j < k; ++j) {
+        const int ej = idx[(int64_t)t * k + j];
+        const float v = w[(int64_t)t * k + j] * (dw[(int64_t)t * k + j] - inner);
+#pragma unroll
+        for (int e = 0; e < E; ++e) if (e == ej) dl[i][e] += v;
+      }
+    }
+    if (blockIdx.y == 0 && cv == 0)
+#pragma unroll
+      for (int e = 0; e < E; ++e) dlogits[(int64_t)t * E + e] = dl[i][e];
+  }
+  if (m >= M) return;
+  float acc[TPL][V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    float wr[E];
+    load_n<T, E>(wg + (int64_t)(m + v) * E, wr);
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) {
+      float sum = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) sum = fmaf(dl[i][e], wr[e], sum);
+      acc[i][v] = sum;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TPL; ++i) {
+    const int t = t0 + i;
+    if (t >= T_) break;
     for (int j = 0; j < k; ++j) {
-      const int ej = idx[(int64_t)t * k + j];
-      const float v = w[(int64_t)t * k + j] * (dw[(int64_t)t * k + j] - inner);
+      const int p = pos[(int64_t)t * k + j];
+      if (p < 0) continue;
+      float v8[V];
+      load16<T>(dx + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M + m, v8);
 #pragma unroll
-      for (int e = 0; e < E; ++e) if (e == ej) dl[e] += v;
-    }
-  }
-  if (lane < E) {
-    float mine = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) if (e == lane) mine = dl[e];
-    dlogits[(int64_t)t * E + lane] = mine;
-  }
-  const T* rows[8];
-  int nk = 0;
-  for (int j = 0; j < k; ++j) {
-    const int p = pos[(int64_t)t * k + j];
-    if (p >= 0) rows[nk++] = dx + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M;
-  }
-  for (int m0 = lane * V; m0 < M; m0 += 32 * V) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < nk; ++j) {
-      float v[8];
-      load16<T>(rows[j] + m0, v);
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += v[i];
-    }
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      float wr[E];
-      load_row<T, E>(wg + (int64_t)(m0 + i) * E, wr);
-      float s = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) s = fmaf(dl[e], wr[e], s);
-      acc[i] += s;
+      for (int v = 0; v < V; ++v) acc[i][v] += v8[v];
     }
     if (dres) {
-      float v[8];
-      load16<T>(dres + (int64_t)t * M + m0, v);
+      float v8[V];
+      load16<T>(dres + (int64_t)t * M + m, v8);
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += v[i];
+      for (int v = 0; v < V; ++v) acc[i][v] += v8[v];
     }
-    store16<T>(dA + (int64_t)t * M + m0, acc);
+    store16<T>(dA + (int64_t)t * M + m, acc[i]);
   }
+}
+
+template <typename T, int E>
+static void gather_gate_bwd_launch_t(const void* dx, const int32_t* idx, const int32_t* pos, const float* w,
+                                     const float* dw, const float* logits, const void* wg, const void* dres,
+                                     void* dA, float* dlogits, int T_, int M, int k, int ldE, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T), TPLX = GgbTile<E>::TPL;
+  const int nvec = M / V;
+  int cv = (nvec + 31) / 32 * 32;  // column-vector lanes per token group
+  if (cv > 256) cv = 256;
+  const int tg = 256 / cv, ctiles = (nvec + cv - 1) / cv;
+  // several tokens per thread (Wg rows reused) only when that still leaves >= 2 waves
+  const bool multi = (int64_t)((T_ + tg * TPLX - 1) / (tg * TPLX)) * ctiles >= 2 * 148;
+  const int tpl = multi ? TPLX : 1, tb = tg * tpl;
+  dim3 grid((T_ + tb - 1) / tb, ctiles);
+  if (multi)
+    launch_k(gather_gate_bwd_kernel<T, E, TPLX>, grid, cv * tg, 0, s, (const T*)dx, idx, pos, w, dw, logits,
+             (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, k, ldE, cv);
+  else
+    launch_k(gather_gate_bwd_kernel<T, E, 1>, grid, cv * tg, 0, s, (const T*)dx, idx, pos, w, dw, logits,
+             (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, k, ldE, cv);
 }
 
 template <int E>
@@ -488,15 +629,10 @@ static void gather_gate_bwd_launch(int dtype, const void* dx, const int32_t* idx
                                    const int32_t* pos, const float* w, const float* dw,
                                    const float* logits, const void* wg, const void* dres, void* dA,
                                    float* dlogits, int T_, int M, int k, int ldE, cudaStream_t s) {
-  dim3 grid((T_ * 32 + 255) / 256);
   if (dtype == DT_F32)
-    launch_k(gather_gate_bwd_kernel<float, E>, grid, 256, 0, s, 
-        (const float*)dx, idx, pos, w, dw, logits, (const float*)wg, (const float*)dres,
-        (float*)dA, dlogits, T_, M, k, ldE);
+    gather_gate_bwd_launch_t<float, E>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, k, ldE, s);
   else
-    launch_k(gather_gate_bwd_kernel<bf16, E>, grid, 256, 0, s, 
-        (const bf16*)dx, idx, pos, w, dw, logits, (const bf16*)wg, (const bf16*)dres, (bf16*)dA,
-        dlogits, T_, M, k, ldE);
+    gather_gate_bwd_launch_t<bf16, E>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, k, ldE, s);
 }
 
 int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t* pos,
@@ -510,91 +646,160 @@ int gather_gate_bwd(int dtype, const void* dx, const int32_t* idx, const int32_t
 }
 
 // ------------------------------------------------------------------ dWg
-// part[sp][m][e] = Σ_{t in split sp} A[t][m] dl[t][e]; then dwg[m][e] += Σ_sp part (in order).
-constexpr int GW_SPLIT_T = 32;
+// dWg[m][e] (+)= Σ_t A[t][m]·dl[t][e]  ([M × T]·[T × E], HBM-bound on A).
+// Part kernel: a CTA owns 4·blockDim.x columns × one token split; a thread keeps a
+// 4-column × EB-expert register tile (one 8/16-byte load of A per token), dl of the split
+// is broadcast from shared memory.  Reduce kernel: sums the splits in order
+// (deterministic).
+constexpr int GW_COLS = 4;  // columns per thread
 
 template <typename T, int E>
-__global__ void __launch_bounds__(128) gate_wgrad_part_kernel(const T* a, const float* dl,
-                                                              float* part, int T_, int M) {
+__global__ void __launch_bounds__(256) gate_wgrad_part_kernel(const T* __restrict__ a, const float* __restrict__ dl,
+                                                              float* __restrict__ part, int T_, int M, int TS) {
+  constexpr int EB = E > 16 ? 16 : E;
+  extern __shared__ float4 dls4[];  // [TS][E] floats
+  const float* dls = reinterpret_cast<const float*>(dls4);
   FM_PDL_ENTRY();
-  __shared__ float dls[GW_SPLIT_T][E];
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t0 = blockIdx.y * GW_SPLIT_T;
-  const int nt = min(GW_SPLIT_T, T_ - t0);
-  for (int i = threadIdx.x; i < nt * E; i += blockDim.x) dls[i / E][i % E] = dl[(int64_t)t0 * E + i];
+  const int t0 = blockIdx.y * TS;
+  const int nt = min(TS, T_ - t0);
+  for (int i = threadIdx.x; i < nt * E; i += blockDim.x) reinterpret_cast<float*>(dls4)[i] = dl[(int64_t)t0 * E + i];
   __syncthreads();
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) * GW_COLS;
   if (m >= M) return;
-  float acc[E];
+  float* dst = part + (int64_t)blockIdx.y * E * M + m;  // [split][E][M]
+#pragma unroll 1
+  for (int e0 = 0; e0 < E; e0 += EB) {
+    float acc[GW_COLS][EB];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  for (int t = 0; t < nt; ++t) {
-    const float x = to_f<T>(a[(int64_t)(t0 + t) * M + m]);
+    for (int c = 0; c < GW_COLS; ++c)
 #pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = fmaf(x, dls[t][e], acc[e]);
+      for (int j = 0; j < EB; ++j) acc[c][j] = 0.f;
+#pragma unroll 4
+    for (int t = 0; t < nt; ++t) {
+      float x[GW_COLS];
+      load_n<T, GW_COLS>(a + (int64_t)(t0 + t) * M + m, x);
+      float d[EB];
+      if constexpr (EB % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < EB; j += 4) {
+          const float4 q = dls4[(t * E + e0 + j) >> 2];
+          d[j] = q.x; d[j + 1] = q.y; d[j + 2] = q.z; d[j + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < EB; ++j) d[j] = dls[t * E + e0 + j];
+      }
+#pragma unroll
+      for (int j = 0; j < EB; ++j)
+#pragma unroll
+        for (int c = 0; c < GW_COLS; ++c) acc[c][j] = fmaf(x[c], d[j], acc[c][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      float4 o;
+      o.x = acc[0][j]; o.y = acc[1][j]; o.z = acc[2][j]; o.w = acc[3][j];
+      *reinterpret_cast<float4*>(dst + (int64_t)(e0 + j) * M) = o;
+    }
   }
-  float* dst = part + ((int64_t)blockIdx.y * M + m) * E;
-#pragma unroll
-  for (int e = 0; e < E; ++e) dst[e] = acc[e];
 }
 
-__global__ void gate_wgrad_reduce_kernel(const float* part, float* dwg, int nsplit, int n, int accumulate) {
+// dwg[m][e] (+)= Σ_sp part[sp][e][m] in split order; thread = (e, m) with m fastest
+__global__ void gate_wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ dwg, int nsplit, int M,
+                                         int E, int accumulate) {
   FM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= M * E) return;
+  const int e = i / M, m = i - e * M;
   float s = 0.f;
-  for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * n + i];
-  dwg[i] = accumulate ? dwg[i] + s : s;
+  for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * M * E + i];
+  float* o = dwg + (int64_t)m * E + e;
+  *o = accumulate ? *o + s : s;
+}
+
+// threads per CTA, token-split length and count: ~148 CTAs, splits of >= 16 tokens
+static void gate_wgrad_geom(int T_, int M, int E, int* threads, int* TS, int* nsplit) {
+  int th = (M / GW_COLS + 31) / 32 * 32;
+  if (th > 256) th = 256;
+  const int ctiles = (M / GW_COLS + th - 1) / th;
+  int ns = (148 + ctiles - 1) / ctiles;
+  const int max_ts = 4096 / E;  // dl tile <= 16 KB of shared memory
+  int ts = (T_ + ns - 1) / ns;
+  if (ts < 16) ts = 16;
+  if (ts > max_ts) ts = max_ts;
+  ns = (T_ + ts - 1) / ts;
+  *threads = th; *TS = ts; *nsplit = ns;
 }
 
 size_t gate_wgrad_scratch_floats(int T_, int M, int E) {
-  return (size_t)((T_ + GW_SPLIT_T - 1) / GW_SPLIT_T) * M * E;
+  int th, ts, ns;
+  gate_wgrad_geom(T_, M, E, &th, &ts, &ns);
+  return (size_t)ns * M * E;
 }
 
 template <int E>
 static void gate_wgrad_launch(int dtype, const void* a, const float* dl, float* part, int T_,
                               int M, cudaStream_t s) {
-  dim3 grid((M + 127) / 128, (T_ + GW_SPLIT_T - 1) / GW_SPLIT_T);
+  int th, ts, ns;
+  gate_wgrad_geom(T_, M, E, &th, &ts, &ns);
+  dim3 grid((M / GW_COLS + th - 1) / th, ns);
+  const size_t smem = (size_t)ts * E * sizeof(float);
   if (dtype == DT_F32)
-    launch_k(gate_wgrad_part_kernel<float, E>, grid, 128, 0, s, (const float*)a, dl, part, T_, M);
+    launch_k(gate_wgrad_part_kernel<float, E>, grid, th, smem, s, (const float*)a, dl, part, T_, M, ts);
   else
-    launch_k(gate_wgrad_part_kernel<bf16, E>, grid, 128, 0, s, (const bf16*)a, dl, part, T_, M);
+    launch_k(gate_wgrad_part_kernel<bf16, E>, grid, th, smem, s, (const bf16*)a, dl, part, T_, M, ts);
 }
 
 int gate_wgrad(int dtype, const void* a, const float* dlogits, float* dwg, float* part, int T_,
                int M, int E, int accumulate, cudaStream_t s) {
   if (T_ <= 0) return 0;
   FM_E_SWITCH(E, gate_wgrad_launch, dtype, a, dlogits, part, T_, M, s)
-  const int nsplit = (T_ + GW_SPLIT_T - 1) / GW_SPLIT_T;
-  launch_k(gate_wgrad_reduce_kernel, (M * E + 255) / 256, 256, 0, s, part, dwg, nsplit, M * E, accumulate);
+  int th, ts, ns;
+  gate_wgrad_geom(T_, M, E, &th, &ts, &ns);
+  launch_k(gate_wgrad_reduce_kernel, (M * E + 255) / 256, 256, 0, s, part, dwg, ns, M, E, accumulate);
   return (int)cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ bias grads
-// out[b][n] (+)= Σ_r x[b][r][n].  Block (32 columns x 8 row groups): thread (tx, ty)
-// sums rows ty, ty+8, ...; the 8 partials are added in a fixed order (deterministic).
+// out[b][n] (+)= Σ_r x[b][r][n].  Block = 8 column-vector lanes × 32 row groups: a thread
+// owns one 16-byte column vector and sums rows ry, ry+32, ...; the 32 partials are added
+// in a fixed order (deterministic).  Narrow column tiles keep enough CTAs at small N.
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_acc_kernel(const T* x, float* out, int rows, int N, int accumulate) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float part[32][8 * V + 1];
   FM_PDL_ENTRY();
-  __shared__ float part[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int n = blockIdx.x * 32 + tx, b = blockIdx.y;
+  const int cx = threadIdx.x & 7, ry = threadIdx.x >> 3;
+  const int n0 = (blockIdx.x * 8 + cx) * V, b = blockIdx.y;
   const T* xb = x + (int64_t)b * rows * N;
-  float s = 0.f;
-  if (n < N)
-    for (int r = ty; r < rows; r += 8) s += to_f<T>(xb[(int64_t)r * N + n]);
-  part[ty][tx] = s;
-  __syncthreads();
-  if (ty == 0 && n < N) {
-    float t = 0.f;
+  float s[V];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += part[i][tx];
-    out[(int64_t)b * N + n] = accumulate ? out[(int64_t)b * N + n] + t : t;
+  for (int v = 0; v < V; ++v) s[v] = 0.f;
+  if (n0 < N)
+#pragma unroll 4
+    for (int r = ry; r < rows; r += 32) {
+      float v8[V];
+      load16<T>(xb + (int64_t)r * N + n0, v8);
+#pragma unroll
+      for (int v = 0; v < V; ++v) s[v] += v8[v];
+    }
+#pragma unroll
+  for (int v = 0; v < V; ++v) part[ry][cx * V + v] = s[v];
+  __syncthreads();
+  if (threadIdx.x < 8 * V) {
+    const int n = blockIdx.x * 8 * V + threadIdx.x;
+    if (n < N) {
+      float t = 0.f;
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) t += part[i][threadIdx.x];
+      out[(int64_t)b * N + n] = accumulate ? out[(int64_t)b * N + n] + t : t;
+    }
   }
 }
 
 int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
                cudaStream_t s) {
-  dim3 grid((N + 31) / 32, batch);
+  const int V = dtype == DT_F32 ? 4 : 8;
+  dim3 grid((N / V + 7) / 8, batch);
   if (dtype == DT_F32) launch_k(colsum_acc_kernel<float>, grid, 256, 0, s, (const float*)x, out, rows, N, accumulate);
   else launch_k(colsum_acc_kernel<bf16>, grid, 256, 0, s, (const bf16*)x, out, rows, N, accumulate);
   return (int)cudaGetLastError();

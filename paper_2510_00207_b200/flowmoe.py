@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflowmoe.so")
+# FLOWMOE_LIB: load another build of the same ABI (A/B measurements of kernel changes)
+LIB_PATH = os.environ.get("FLOWMOE_LIB") or os.path.join(_HERE, "libflowmoe.so")
 
 FLOWMOE_F32, FLOWMOE_BF16 = 0, 1
 SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "vanilla_ep": 4}
