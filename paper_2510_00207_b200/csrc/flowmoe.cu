@@ -1013,7 +1013,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       for (int64_t q = ai + 1; q < (a0 + x->N) / Tb; ++q)
         if (x->lanes[q % nl] != sc) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dctx[q], 0));
     }
-    FM_KP(KK_ATTN_B, attn_tc_supported(dt, (int)M, (int)x->H) ? 2 : 3, attn_flops, (double)Tb * 8 * M * es, sc,
+    FM_KP(KK_ATTN_B, attn_tc_supported(dt, (int)M, (int)x->H) ? 1 : 3, attn_flops, (double)Tb * 8 * M * es, sc,
           attn_bwd(dt, at<char>(saved, L.qkv + a0 * 3 * M * es), at<char>(saved, L.ctx + a0 * M * es),
                    at<float>(saved, L.lse + a0 * x->H * 4), (char*)x->dctx + a0 * M * es,
                    (char*)x->dqkv + a0 * 3 * M * es, x->Dbuf + a0 * x->H, (int)nseq, (int)x->N, (int)p0, (int)np,

@@ -260,13 +260,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 // grid (ceil(np/128) own key tiles, H, n_seq); query tiles are 128-aligned positions from
 // the key tile's diagonal (causal) to N.  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
 template <int DH>
-__global__ void __launch_bounds__(AT_THREADS, 1)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                            const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
-                            int np, int M, int H, int causal, float scale_log2, float scale) {
+__device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const CUtensorMap& tdo, const float* lse,
+                                                   const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
+                                                   int np, int M, int H, int causal, float scale_log2, float scale,
+                                                   uint8_t* smem_raw, int kt, int h, int sq) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
-  extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint8_t* sK = smem;
   uint8_t* sV = smem + TILE;
@@ -286,7 +285,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
   const int k0 = p0 + kt * 128, row_base = sq * N;
   const int nq_tiles = (N + 127) / 128;
   const int qt0 = causal ? k0 / 128 : 0;
@@ -427,13 +425,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 // ============================================================== backward: dQ
 // grid (ceil(np/128) own query tiles, H, n_seq).  TMEM: S [0,128), dP [128,256), dQ [256, 256+DH).
 template <int DH, int STAGES>
-__global__ void __launch_bounds__(AT_THREADS, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                          const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
-                          int np, int M, int H, int causal, float scale_log2, float scale) {
+__device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CUtensorMap& tdo, const float* lse,
+                                                 const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
+                                                 int np, int M, int H, int causal, float scale_log2, float scale,
+                                                 uint8_t* smem_raw, int qt, int h, int sq) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
-  extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sdO = smem + TILE;
@@ -449,7 +446,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
   const int q0 = p0 + qt * 128, row_base = sq * N;
   int nkv = (N + 127) / 128;
   if (causal) nkv = min(nkv, (min(p0 + np, q0 + 128) + 127) / 128);
@@ -572,6 +568,23 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
 }
 
+// dK/dV and dQ of one (sequence, head) run as one launch: blockIdx.z = 2·seq + role
+// (0: dK/dV of own key tile blockIdx.x, 1: dQ of own query tile blockIdx.x).  The two
+// halves are independent (disjoint outputs, shared read-only inputs), so they co-run.
+template <int DH, int STAGES>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
+                       const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0, int np,
+                       int M, int H, int causal, float scale_log2, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  if (blockIdx.z & 1)
+    attn_bwd_dq_body<DH, STAGES>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale,
+                                 smem_raw, blockIdx.x, blockIdx.y, blockIdx.z >> 1);
+  else
+    attn_bwd_dkdv_body<DH>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale, smem_raw,
+                           blockIdx.x, blockIdx.y, blockIdx.z >> 1);
+}
+
 // D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]: one warp per token, 16-byte loads;
 // lane groups of dh/8 lanes reduce one head each (segmented shuffle reduction).
 __global__ void attn_bwd_pre_tc_kernel(const bf16* ctx, const bf16* dctx, float* D, int T_, int M,
@@ -626,20 +639,13 @@ static int attn_bwd_tc_t(const void* qkv, const void* ctx, const float* lse, con
   if (int rc = make_tmap_2d_bf16(&tdo, dctx, M, nseq * N, M, 64, 128)) return rc;
   (void)D;  // D = rowsum(dO ⊙ O) is computed inside the two kernels
   const float scale = 1.0f / sqrtf((float)DH), sl2 = LOG2E * scale;
-  dim3 grid((np + 127) / 128, H, nseq);
-  auto k1 = attn_bwd_dkdv_tc_kernel<DH>;
-  const size_t sm1 = dkdv_smem<DH>();
-  static bool once1 = (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1), true);
-  (void)once1;
-  launch_k(k1, grid, AT_THREADS, sm1, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, p0,
-           np, M, H, causal, sl2, scale);
   constexpr int ST = DH == 128 ? 1 : 2;
-  auto k2 = attn_bwd_dq_tc_kernel<DH, ST>;
-  const size_t sm2 = dq_smem<DH, ST>();
-  static bool once2 = (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2), true);
-  (void)once2;
-  launch_k(k2, grid, AT_THREADS, sm2, s, tq, tdo, lse, (const bf16*)ctx, (const bf16*)dctx, (bf16*)dqkv, N, p0,
-           np, M, H, causal, sl2, scale);
+  auto k = attn_bwd_tc_kernel<DH, ST>;
+  const size_t sm = dkdv_smem<DH>() > dq_smem<DH, ST>() ? dkdv_smem<DH>() : dq_smem<DH, ST>();
+  static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), true);
+  (void)once;
+  launch_k(k, dim3((np + 127) / 128, H, 2 * nseq), AT_THREADS, sm, s, tq, tdo, lse, (const bf16*)ctx,
+           (const bf16*)dctx, (bf16*)dqkv, N, p0, np, M, H, causal, sl2, scale);
   return (int)cudaGetLastError();
 }
 

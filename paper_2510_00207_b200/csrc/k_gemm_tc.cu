@@ -162,13 +162,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int acc = it & 1, use = it >> 1;
       const uint32_t tmem_acc = tmem_base + acc * BN;
       const int row = m0 + r0 + lane;
+    const bool row_ok = row < g.M;
+      // the per-row bf16 operand of the epilogue (Z for dGELU, the residual) is read
+      // one 32-column chunk ahead, the first chunk before the accumulator is ready,
+      // so its load latency hides under the mainloop / the previous chunk
+      const bf16* xrow = nullptr;
+      if (!f32out && row_ok) {
+        if (g.epi == EPI_DGELU)
+          xrow = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux;
+        else if (g.epi == EPI_STORE && g.resid)
+          xrow = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr;
+      }
+      uint4 pf[4];
+      auto prefetch = [&](int c) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          pf[i] = (xrow && n0 + c + 8 * i < g.N) ? *reinterpret_cast<const uint4*>(xrow + n0 + c + 8 * i)
+                                                   : make_uint4(0, 0, 0, 0);
+      };
+      prefetch(0);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-    const bool row_ok = row < g.M;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       const int nb = n0 + c0;
       if (nb >= g.N) break;  // warp-uniform
+      float xv[32];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w4[4] = {pf[i].x, pf[i].y, pf[i].z, pf[i].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xv[8 * i + 2 * q] = __uint_as_float(w4[q] << 16);
+          xv[8 * i + 2 * q + 1] = __uint_as_float(w4[q] & 0xFFFF0000u);
+        }
+      }
+      if (c0 + 32 < BN) prefetch(c0 + 32);
       uint32_t r[32];
       tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
       float v[32];
@@ -187,23 +216,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         if (g.epi == EPI_STORE && g.resid && row_ok) {
-          const bf16* R = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr + nb;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float t[8];
-            if (i < nvalid) load16<bf16>(R + i, t);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[i + q] += (i < nvalid) ? t[q] : 0.f;
-          }
+          for (int i = 0; i < 32; ++i) v[i] += xv[i];  // zeros past N
         } else if (g.epi == EPI_DGELU && row_ok) {
-          const bf16* Z = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux + nb;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float t[8];
-            if (i < nvalid) load16<bf16>(Z + i, t);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[i + q] *= (i < nvalid) ? gelu_grad_f(t[q]) : 0.f;
-          }
+          for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(xv[i]) : 0.f;
         }
       }
       // staging buffer `buf` is free once the store issued two chunks ago has read it
