@@ -6,9 +6,9 @@
 // the MHA projections (S1/S3, B5), and the batched expert GEMMs (S7, B2) whose
 // rows are the capacity-padded [E/P][P·C] buffers (uniform shapes => batched).
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
-// single-thread MMA issuer, warps 2..5 = epilogue (warp w reads TMEM lanes
-// 32*(w%4) .. +31, one output row per thread).  Persistent: grid = min(#tiles,
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer (one elected lane), warps 2..9 = epilogue (warp w reads TMEM lanes
+// 32*(w%4) .. +31, one output row per thread, alternate 32-column chunks).  Persistent: grid = min(#tiles,
 // #SMs), the smem ring runs across a CTA's tiles and the accumulator is double-
 // buffered in TMEM so tile i's epilogue overlaps tile i+1's mainloop.
 //
@@ -24,7 +24,16 @@
 
 namespace fm {
 
-constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 192;
+constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 320;  // producer, MMA, 8 epilogue warps
+
+// Phase probe (tools/probe/gemm_probe.cu builds this file with -DFM_PROBE): SM clock
+// stamps of CTA 0's phases.  Compiled out of the library.
+#ifdef FM_PROBE
+__device__ long long g_probe[32];
+#define FM_MARK(i) do { if (blockIdx.x == 0) g_probe[i] = clock64(); } while (0)
+#else
+#define FM_MARK(i) do {} while (0)
+#endif
 static int g_tc_debug = 0;  // bit0: force SIMT for bf16; bit1: swap LBO/SBO of MN-major descs
 static int g_force_bn = 0;  // 0 = wave-aware choice; 64/128/256 = forced tile width (benchmarks)
 void gemm_tc_force_bn(int bn) { g_force_bn = bn; }
@@ -59,7 +68,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // one tile per CTA: the operand ring is free when the epilogue runs, so it doubles
   // as the staging area and a single TMEM accumulator suffices (smaller footprint)
   const bool single = num_tiles <= (int)gridDim.x;
-  uint8_t* epi_smem = single ? smem : smem + RING;  // 4 epilogue warps x 2 x 4 KB staging
+  uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x 4 KB staging
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : 32768));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
@@ -69,10 +78,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = p.g;
   const uint32_t tmem_cols = single ? BN : 2 * BN;
+  if (threadIdx.x == 0) FM_MARK(0);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -82,21 +92,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) FM_MARK(1);
   FM_PDL_ENTRY();
+  if (threadIdx.x == 0) FM_MARK(2);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer: one ring across all tiles of this CTA =====
-      int gk = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
-        for (int kb = 0; kb < p.nk; ++kb, ++gk) {
-          const int s = gk % STAGES;
-          if (gk >= STAGES) mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
+    // ===== TMA producer (whole warp walks the ring, one elected lane issues) =====
+    int gk = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
+      for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+        const int s = gk % STAGES;
+        if (gk >= STAGES) mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+        const int k0 = kb * TC_BK;
+        if (elect_one()) {
           mbar_expect_tx(&full[s], STAGE_BYTES);
-          const int k0 = kb * TC_BK;
           if (!p.a_mmajor) {
             tma_load_3d(sa, &tma_a, &full[s], k0, m0, b);
           } else {
@@ -109,63 +121,85 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0, b);
           }
+          if (gk < 4) FM_MARK(24 + gk);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (one thread) =====
-      const bool swap = (p.dbg & 2) != 0;
-      const uint32_t mn_lbo = swap ? 1024u : 8192u, mn_sbo = swap ? 8192u : 1024u;
-      int gk = 0, it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        const int acc = it & 1, use = it >> 1;
-        if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained this buffer
+    // ===== MMA issuer (whole warp waits, one elected lane issues) =====
+    const bool swap = (p.dbg & 2) != 0;
+    const uint32_t mn_lbo = swap ? 1024u : 8192u, mn_sbo = swap ? 8192u : 1024u;
+    // Descriptors of stage 0 built once; a stage / UMMA_K step only adds to the 14-bit
+    // start-address field (smem < 256 KB, so no carry out of it).
+    // K-major: +32 B per UMMA_K=16 inside the 128-B swizzle row; SBO = 8 rows * 128 B.
+    // MN-major: +16 K-rows * 128 B; LBO = 64-element MN block stride (one TMA box).
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t adesc0 = p.a_mmajor ? umma_desc(s0, mn_lbo, mn_sbo) : umma_desc(s0, 16, 1024);
+    const uint64_t bdesc0 = p.b_kmajor ? umma_desc(s0 + A_BYTES, 16, 1024) : umma_desc(s0 + A_BYTES, mn_lbo, mn_sbo);
+    const uint64_t a_kstep = p.a_mmajor ? (2048 >> 4) : (32 >> 4);
+    const uint64_t b_kstep = p.b_kmajor ? (32 >> 4) : (2048 >> 4);
+    int gk = 0, it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1, use = it >> 1;
+      if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained this buffer
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+        const int s = gk % STAGES;
+        mbar_wait(&full[s], (gk / STAGES) & 1);
+        if (lane == 0 && gk == 0) FM_MARK(3);
+        if (lane == 0 && gk < 8) FM_MARK(16 + gk);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.nk; ++kb, ++gk) {
-          const int s = gk % STAGES;
-          mbar_wait(&full[s], (gk / STAGES) & 1);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+        const uint64_t soff = (uint64_t)((uint32_t)s * STAGE_BYTES >> 4);
+        if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            // K-major: +32 B per UMMA_K=16 inside the 128-B swizzle row; SBO = 8 rows * 128 B.
-            // MN-major: +16 K-rows * 128 B; LBO = 64-element MN block stride (one TMA box).
-            const uint64_t ad = p.a_mmajor ? umma_desc(sa + kk * 2048, mn_lbo, mn_sbo)
-                                           : umma_desc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = p.b_kmajor ? umma_desc(sb + kk * 32, 16, 1024)
-                                           : umma_desc(sb + kk * 2048, mn_lbo, mn_sbo);
-            tc_mma(tmem_d, ad, bd, p.idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < TC_BK / 16; ++kk)
+            tc_mma(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
+                   (kb > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&empty[s]);
+          if (gk < 4) FM_MARK(28 + gk);
         }
-        tc_commit(&tfull[acc]);
+        __syncwarp();
       }
+      if (elect_one()) {
+        tc_commit(&tfull[acc]);
+        FM_MARK(4);
+      }
+      __syncwarp();
     }
   } else {
     // ===== epilogue: TMEM -> registers -> swizzled smem tile -> TMA store / reduce-add =====
-    // Each warp owns 32 rows (its TMEM lane quarter) and walks the BN columns in
-    // 32-column chunks.  A chunk is staged as a [32 rows][32 cols] box in smem with
-    // the TMA swizzle (128 B rows for fp32, 64 B rows for bf16: conflict-free
-    // 16-byte st.shared) and written by one TMA bulk store, or a TMA bulk
-    // reduce-add (fp32 grad accumulation C += acc, done in L2).  Two staging
-    // buffers per warp (4 KB each) overlap the next chunk with the in-flight store.
-    const int quarter = warp & 3;
+    // Eight warps: warp w reads TMEM lane quarter w % 4 (32 rows, one row per thread);
+    // the two warps of a quarter take alternate 32-column chunks, halving the per-warp
+    // conversion / activation work (the epilogue is latency-bound at small tiles).  A
+    // chunk is staged as a [32 rows][32 cols] box in smem with the TMA swizzle (128 B
+    // rows for fp32, 64 B rows for bf16: conflict-free 16-byte st.shared) and written by
+    // one TMA bulk store, or a TMA bulk reduce-add (fp32 grad accumulation C += acc, done
+    // in L2).  One 4 KB staging buffer per warp.
+#ifdef FM_PROBE_OBS
+    if (threadIdx.x == 65 && blockIdx.x == 0)  // observer: when each of the first stages lands
+      for (int q = 0; q < p.nk && q < 8 && q < STAGES; ++q) {
+        mbar_wait(&full[q], 0);
+        g_probe[10 + (q < 6 ? q : 5)] = clock64();
+      }
+    __syncwarp();
+#endif
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int r0 = quarter * 32;
-    uint8_t* stage = epi_smem + quarter * 8192;
+    uint8_t* sb = epi_smem + (warp - 2) * 4096;
     const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
-    int buf = 0, it = 0;
+    bool pending = false;  // a store from sb is in flight
+    int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
       const int acc = it & 1, use = it >> 1;
       const uint32_t tmem_acc = tmem_base + acc * BN;
       const int row = m0 + r0 + lane;
-    const bool row_ok = row < g.M;
-      // the per-row bf16 operand of the epilogue (Z for dGELU, the residual) is read
-      // one 32-column chunk ahead, the first chunk before the accumulator is ready,
-      // so its load latency hides under the mainloop / the previous chunk
+      const bool row_ok = row < g.M;
+      // the per-row bf16 operand of the epilogue (Z for dGELU, the residual) and the bias
+      // are read one chunk ahead, the first chunk before the accumulator is ready, so
+      // their load latency hides under the mainloop / the previous chunk
       const bf16* xrow = nullptr;
       if (!f32out && row_ok) {
         if (g.epi == EPI_DGELU)
@@ -173,48 +207,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         else if (g.epi == EPI_STORE && g.resid)
           xrow = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr;
       }
-      uint4 pf[4];
+      const bf16* brow = (!f32out && g.bias) ? reinterpret_cast<const bf16*>(g.bias) + (int64_t)b * g.sBias : nullptr;
+      uint4 pf[4], pb[4];
       auto prefetch = [&](int c) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          pf[i] = (xrow && n0 + c + 8 * i < g.N) ? *reinterpret_cast<const uint4*>(xrow + n0 + c + 8 * i)
-                                                   : make_uint4(0, 0, 0, 0);
-      };
-      prefetch(0);
-      mbar_wait(&tfull[acc], use & 1);
-      tc_fence_after();
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      const int nb = n0 + c0;
-      if (nb >= g.N) break;  // warp-uniform
-      float xv[32];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t w4[4] = {pf[i].x, pf[i].y, pf[i].z, pf[i].w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          xv[8 * i + 2 * q] = __uint_as_float(w4[q] << 16);
-          xv[8 * i + 2 * q + 1] = __uint_as_float(w4[q] & 0xFFFF0000u);
+        for (int i = 0; i < 4; ++i) {
+          const bool in = n0 + c + 8 * i < g.N;  // N % 8 == 0: a 16-byte group is all in or all out
+          pf[i] = (xrow && in) ? *reinterpret_cast<const uint4*>(xrow + n0 + c + 8 * i) : make_uint4(0, 0, 0, 0);
+          pb[i] = (brow && in) ? *reinterpret_cast<const uint4*>(brow + n0 + c + 8 * i) : make_uint4(0, 0, 0, 0);
         }
-      }
-      if (c0 + 32 < BN) prefetch(c0 + 32);
-      uint32_t r[32];
-      tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
-      float v[32];
+      };
+      auto unpack = [](const uint4* q, float* out) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
-      const int nvalid = min(32, g.N - nb);
-      if (!f32out) {
-        if (g.bias) {
-          const bf16* bias = reinterpret_cast<const bf16*>(g.bias) + (int64_t)b * g.sBias + nb;
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t w4[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {  // 16-byte loads (N % 8 == 0, so i < nvalid covers the group)
-            float t[8];
-            if (i < nvalid) load16<bf16>(bias + i, t);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[i + q] += (i < nvalid) ? t[q] : 0.f;
+          for (int j = 0; j < 4; ++j) {
+            out[8 * i + 2 * j] = __uint_as_float(w4[j] << 16);
+            out[8 * i + 2 * j + 1] = __uint_as_float(w4[j] & 0xFFFF0000u);
           }
         }
+      };
+      prefetch(half * 32);
+      mbar_wait_sleep(&tfull[acc], use & 1);
+      if (threadIdx.x == 64) FM_MARK(5);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = half * 32; c0 < BN; c0 += 64) {
+        const int nb = n0 + c0;
+        if (nb >= g.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
+        if (threadIdx.x == 64 && c0 == 0) FM_MARK(9);
+        float xv[32], bv[32];
+        unpack(pf, xv);
+        unpack(pb, bv);
+        if (c0 + 64 < BN) prefetch(c0 + 64);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha + bv[i];  // bias 0 past N
+        const int nvalid = min(32, g.N - nb);
         if (g.epi == EPI_STORE && g.resid && row_ok) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += xv[i];  // zeros past N
@@ -222,66 +254,73 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(xv[i]) : 0.f;
         }
-      }
-      // staging buffer `buf` is free once the store issued two chunks ago has read it
-      if (lane == 0) bulk_wait_read<1>();
-      __syncwarp();
-      uint8_t* sb = stage + buf * 4096;
-      if (f32out) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          *reinterpret_cast<float4*>(sb + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+        if (threadIdx.x == 64 && c0 == 0) FM_MARK(10);
+        // the staging buffer is free once this warp's previous store has read it
+        if (pending) {
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
         }
-      } else if (g.epi == EPI_BIAS_GELU) {
-        // aux = Z (pre-activation), C = GELU(bf16(Z))
+        if (threadIdx.x == 64 && c0 == 0) FM_MARK(11);
+        if (f32out) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 zq, hq;
-          float zz[8];
+          for (int j = 0; j < 8; ++j) {
+            float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            *reinterpret_cast<float4*>(sb + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+          }
+        } else if (g.epi == EPI_BIAS_GELU) {
+          // aux = Z (pre-activation), C = GELU(bf16(Z))
 #pragma unroll
-          for (int i = 0; i < 8; ++i) zz[i] = __bfloat162float(__float2bfloat16_rn(v[8 * j + i]));
-          zq.x = pack_bf16x2(zz[0], zz[1]); zq.y = pack_bf16x2(zz[2], zz[3]);
-          zq.z = pack_bf16x2(zz[4], zz[5]); zq.w = pack_bf16x2(zz[6], zz[7]);
-          hq.x = pack_bf16x2(gelu_f(zz[0]), gelu_f(zz[1])); hq.y = pack_bf16x2(gelu_f(zz[2]), gelu_f(zz[3]));
-          hq.z = pack_bf16x2(gelu_f(zz[4]), gelu_f(zz[5])); hq.w = pack_bf16x2(gelu_f(zz[6]), gelu_f(zz[7]));
-          const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
-          *reinterpret_cast<uint4*>(sb + off) = hq;
-          *reinterpret_cast<uint4*>(sb + 2048 + off) = zq;
-        }
-      } else {
+          for (int j = 0; j < 4; ++j) {
+            uint4 zq, hq;
+            float zz[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 q;
-          q.x = pack_bf16x2(v[8 * j], v[8 * j + 1]); q.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-          q.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]); q.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
-          *reinterpret_cast<uint4*>(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = q;
-        }
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        if (g.epi == EPI_ACC_F32) {
-          tma_reduce_add_3d(&tma_c, sb, nb, m0 + r0, b);
-        } else if (g.epi == EPI_STORE_F32) {
-          tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
+            for (int i = 0; i < 8; ++i) zz[i] = __bfloat162float(__float2bfloat16_rn(v[8 * j + i]));
+            zq.x = pack_bf16x2(zz[0], zz[1]); zq.y = pack_bf16x2(zz[2], zz[3]);
+            zq.z = pack_bf16x2(zz[4], zz[5]); zq.w = pack_bf16x2(zz[6], zz[7]);
+            hq.x = pack_bf16x2(gelu_f(zz[0]), gelu_f(zz[1])); hq.y = pack_bf16x2(gelu_f(zz[2]), gelu_f(zz[3]));
+            hq.z = pack_bf16x2(gelu_f(zz[4]), gelu_f(zz[5])); hq.w = pack_bf16x2(gelu_f(zz[6]), gelu_f(zz[7]));
+            const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(sb + off) = hq;
+            *reinterpret_cast<uint4*>(sb + 2048 + off) = zq;
+          }
         } else {
-          tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
-          if (g.epi == EPI_BIAS_GELU) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 q;
+            q.x = pack_bf16x2(v[8 * j], v[8 * j + 1]); q.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+            q.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]); q.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+            *reinterpret_cast<uint4*>(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = q;
+          }
         }
-        bulk_commit();
+        if (threadIdx.x == 64 && c0 == 0) FM_MARK(12);
+        fence_async_smem();
+        __syncwarp();
+        if (threadIdx.x == 64 && c0 == 0) FM_MARK(13);
+        if (lane == 0) {
+          if (g.epi == EPI_ACC_F32) {
+            tma_reduce_add_3d(&tma_c, sb, nb, m0 + r0, b);
+          } else if (g.epi == EPI_STORE_F32) {
+            tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
+          } else {
+            tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
+            if (g.epi == EPI_BIAS_GELU) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
+          }
+          bulk_commit();
+        }
+        pending = true;
       }
-      buf ^= 1;
-    }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM reads of this tile are complete
     }
+    if (threadIdx.x == 64) FM_MARK(6);
     if (lane == 0) bulk_wait<0>();
+    if (threadIdx.x == 64) FM_MARK(7);
     __syncwarp();
     tc_fence_before();
   }
   __syncthreads();
+  if (threadIdx.x == 0) FM_MARK(8);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
