@@ -33,6 +33,12 @@ FM_DEV uint64_t kdesc(uint32_t base, int kk) {
 }
 // MN-major (contract over the 128 rows): k-step kk of 16 rows -> +2048 B; 64-col blocks 16 KB apart.
 FM_DEV uint64_t mdesc(uint32_t base, int kk) { return umma_desc(base + kk * 2048, 16384, 1024); }
+// The same as a base descriptor plus a constant added to its 14-bit address field, so
+// the issuing loop only does 64-bit adds of uniform values.
+FM_DEV uint64_t kdesc0(uint32_t base) { return umma_desc(base, 16, 1024); }
+FM_DEV uint64_t mdesc0(uint32_t base) { return umma_desc(base, 16384, 1024); }
+FM_DEV constexpr uint64_t kstep(int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); }
+FM_DEV constexpr uint64_t mstep(int kk) { return (uint64_t)((kk * 2048) >> 4); }
 
 FM_DEV uint8_t* align1k(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -128,47 +134,57 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
-    if (lane == 0) {
+    // producer: whole warp walks the K/V ring, one elected lane issues the TMA loads
+    if (elect_one()) {
       mbar_expect_tx(bar_q, TILE);
       for (int i = 0; i < NB; ++i) tma_load_2d(sQ + i * 16384, &tq, bar_q, h * DH + 64 * i, row_base + q0);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
-        uint8_t* sK = st ? sK1 : sK0;
-        uint8_t* sV = st ? sV1 : sV0;
+    }
+    __syncwarp();
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j & 1;
+      if (j >= 2) mbar_wait_sleep(&kv_empty[st], ((j >> 1) - 1) & 1);
+      uint8_t* sK = st ? sK1 : sK0;
+      uint8_t* sV = st ? sV1 : sV0;
+      if (elect_one()) {
         mbar_expect_tx(&kv_full[st], 2 * TILE);
         for (int i = 0; i < NB; ++i) {
           tma_load_2d(sK + i * 16384, &tq, &kv_full[st], M + h * DH + 64 * i, row_base + j * 128);
           tma_load_2d(sV + i * 16384, &tq, &kv_full[st], 2 * M + h * DH + 64 * i, row_base + j * 128);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
-      constexpr uint32_t id_o = idesc_bf16(128, DH, 0, 1);   // P (K-major) x V (MN-major)
-      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-      mbar_wait(bar_q, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t aK = smem_u32(st ? sK1 : sK0);
+    // MMA issuer: whole warp waits, one elected lane issues
+    constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+    constexpr uint32_t id_o = idesc_bf16(128, DH, 0, 1);   // P (K-major) x V (MN-major)
+    const uint64_t dQ = kdesc0(smem_u32(sQ)), dP = kdesc0(smem_u32(sP));
+    const uint64_t dK0 = kdesc0(smem_u32(sK0)), dK1 = kdesc0(smem_u32(sK1));
+    const uint64_t dV0 = mdesc0(smem_u32(sV0)), dV1 = mdesc0(smem_u32(sV1));
+    mbar_wait(bar_q, 0);
+    auto issue_s = [&](int j) {
+      const int st = j & 1;
+      mbar_wait(&kv_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tmem + st * 128, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tmem + st * 128, dQ + kstep(kk), (st ? dK1 : dK0) + kstep(kk), id_s, kk > 0);
         tc_commit(&s_full[st]);
-      };
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(j + 1);
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
-        const uint32_t aV = smem_u32((j & 1) ? sV1 : sV0);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkv; ++j) {
+      if (j + 1 < nkv) issue_s(j + 1);
+      mbar_wait_sleep(p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) tc_mma(tO, kdesc(aP, kk), mdesc(aV, kk), id_o, (j > 0 || kk > 0));
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tO, dP + kstep(kk), ((j & 1) ? dV1 : dV0) + mstep(kk), id_o, (j > 0 || kk > 0));
         tc_commit(o_done);
         tc_commit(&kv_empty[j & 1]);
       }
+      __syncwarp();
     }
   } else {
     // ===== softmax warps: thread = query row
@@ -308,46 +324,55 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
   const uint32_t tST = tmem, tdPT = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_expect_tx(kv_bar, 2 * TILE);
       for (int i = 0; i < NB; ++i) {
         tma_load_2d(sK + i * 16384, &tq, kv_bar, M + h * DH + 64 * i, row_base + k0);
         tma_load_2d(sV + i * 16384, &tq, kv_bar, 2 * M + h * DH + 64 * i, row_base + k0);
       }
-      for (int it = 0; it < niter; ++it) {
-        const int qr = row_base + (qt0 + it) * 128;
-        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
+    }
+    __syncwarp();
+    for (int it = 0; it < niter; ++it) {
+      const int qr = row_base + (qt0 + it) * 128;
+      if (it > 0) mbar_wait_sleep(q_empty, (it - 1) & 1);
+      if (elect_one()) {
         mbar_expect_tx(q_full, 2 * TILE);
         for (int i = 0; i < NB; ++i) {
           tma_load_2d(sQ + i * 16384, &tq, q_full, h * DH + 64 * i, qr);
           tma_load_2d(sdO + i * 16384, &tdo, q_full, h * DH + 64 * i, qr);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
-      const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
-      mbar_wait(kv_bar, 0);
-      for (int it = 0; it < niter; ++it) {
-        mbar_wait(q_full, it & 1);
-        tc_fence_after();
+    constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
+    const uint64_t dK = kdesc0(smem_u32(sK)), dV = kdesc0(smem_u32(sV)), dQk = kdesc0(smem_u32(sQ)),
+                   dOk = kdesc0(smem_u32(sdO)), dP = kdesc0(smem_u32(sP)), dS = kdesc0(smem_u32(sdS)),
+                   dOm = mdesc0(smem_u32(sdO)), dQm = mdesc0(smem_u32(sQ));
+    mbar_wait(kv_bar, 0);
+    for (int it = 0; it < niter; ++it) {
+      mbar_wait(q_full, it & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tST, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tST, dK + kstep(kk), dQk + kstep(kk), id_s, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdPT, kdesc(aV, kk), kdesc(adO, kk), id_s, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdPT, dV + kstep(kk), dOk + kstep(kk), id_s, kk > 0);
         tc_commit(s_full);
-        mbar_wait(p_full, it & 1);
-        tc_fence_after();
+      }
+      __syncwarp();
+      mbar_wait_sleep(p_full, it & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) tc_mma(tdV, kdesc(aP, kk), mdesc(adO, kk), id_g, (it > 0 || kk > 0));
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdV, dP + kstep(kk), dOm + mstep(kk), id_g, (it > 0 || kk > 0));
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) tc_mma(tdK, kdesc(adS, kk), mdesc(aQ, kk), id_g, (it > 0 || kk > 0));
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdK, dS + kstep(kk), dQm + mstep(kk), id_g, (it > 0 || kk > 0));
         tc_commit(q_empty);
         tc_commit(mm_done);
       }
+      __syncwarp();
     }
   } else {
     // ===== thread = key row
@@ -467,47 +492,56 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
   const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_expect_tx(q_bar, 2 * TILE);
       for (int i = 0; i < NB; ++i) {
         tma_load_2d(sQ + i * 16384, &tq, q_bar, h * DH + 64 * i, row_base + q0);
         tma_load_2d(sdO + i * 16384, &tdo, q_bar, h * DH + 64 * i, row_base + q0);
       }
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % STAGES;
-        if (j >= STAGES) mbar_wait(&kv_empty[st], ((j / STAGES) - 1) & 1);
-        uint8_t* sK = sKV + st * 2 * TILE;
-        uint8_t* sV = sK + TILE;
+    }
+    __syncwarp();
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j % STAGES;
+      if (j >= STAGES) mbar_wait_sleep(&kv_empty[st], ((j / STAGES) - 1) & 1);
+      uint8_t* sK = sKV + st * 2 * TILE;
+      uint8_t* sV = sK + TILE;
+      if (elect_one()) {
         mbar_expect_tx(&kv_full[st], 2 * TILE);
         for (int i = 0; i < NB; ++i) {
           tma_load_2d(sK + i * 16384, &tq, &kv_full[st], M + h * DH + 64 * i, row_base + j * 128);
           tma_load_2d(sV + i * 16384, &tq, &kv_full[st], 2 * M + h * DH + 64 * i, row_base + j * 128);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
-      const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), adS = smem_u32(sdS);
-      mbar_wait(q_bar, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % STAGES;
-        mbar_wait(&kv_full[st], (j / STAGES) & 1);
-        tc_fence_after();
-        const uint32_t aK = smem_u32(sKV + st * 2 * TILE), aV = aK + TILE;
+    constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
+    const uint64_t dQ = kdesc0(smem_u32(sQ)), dO = kdesc0(smem_u32(sdO)), dS = kdesc0(smem_u32(sdS));
+    const uint64_t dKV0 = kdesc0(smem_u32(sKV)), mKV0 = mdesc0(smem_u32(sKV));
+    mbar_wait(q_bar, 0);
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j % STAGES;
+      mbar_wait(&kv_full[st], (j / STAGES) & 1);
+      tc_fence_after();
+      const uint64_t soff = (uint64_t)((uint32_t)(st * 2 * TILE) >> 4), voff = (uint64_t)(TILE >> 4);
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tS, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tS, dQ + kstep(kk), dKV0 + soff + kstep(kk), id_s, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdP, kdesc(adO, kk), kdesc(aV, kk), id_s, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk) tc_mma(tdP, dO + kstep(kk), dKV0 + soff + voff + kstep(kk), id_s, kk > 0);
         tc_commit(s_full);
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
+      }
+      __syncwarp();
+      mbar_wait_sleep(p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) tc_mma(tdQ, kdesc(adS, kk), mdesc(aK, kk), id_g, (j > 0 || kk > 0));
+        for (int kk = 0; kk < 8; ++kk) tc_mma(tdQ, dS + kstep(kk), mKV0 + soff + mstep(kk), id_g, (j > 0 || kk > 0));
         tc_commit(&kv_empty[st]);
         tc_commit(mm_done);
       }
+      __syncwarp();
     }
   } else {
     // ===== thread = query row
