@@ -13,8 +13,9 @@
 // The same smem tile of K (or V, Q, dO) serves as a K-major operand (contracting
 // over d) and as an MN-major operand (contracting over rows), so no transposes.
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + single-thread
-// MMA issuer, warps 2..5 softmax / epilogue, one query (or key) row per thread.
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (one
+// elected lane), warps 2..9 softmax / epilogue: one query (or key) row per thread, the
+// two warps of a TMEM lane quarter splitting the tile's columns.
 #include <cuda.h>
 #include "common.cuh"
 #include "kernels.h"
@@ -22,7 +23,7 @@
 
 namespace fm {
 
-constexpr int AT_THREADS = 192;
+constexpr int AT_THREADS = 320;  // producer, MMA, 8 softmax warps (two per TMEM lane quarter)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* p_full = bars + 7;
   uint64_t* o_done = bars + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  float* xch = reinterpret_cast<float*>(bars + 16);  // [3][2 halves][128 rows]: row max (tile parity), row sum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   if (warp == 0 && lane == 0) {
     mbar_init(bar_q, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); mbar_init(&s_full[i], 1); }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
@@ -187,20 +189,25 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ===== softmax warps: thread = query row
-    const int quarter = warp & 3;
+    // ===== softmax warps: thread = query row; the two warps of a TMEM lane quarter take
+    // key columns [64·half, 64·half + 64) of each S tile and O columns [DH/2·half, ..).
+    // They share the running row max through shared memory (one 64-thread named
+    // barrier per tile); the row sums stay per half until the end.
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
     const int qrow = q0 + rloc;                      // position in the sequence
     const bool own = qt * 128 + rloc < np;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    constexpr int OC = DH / 64;                      // O chunks of 32 columns per half
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t tS = tmem + lane_off + (j & 1) * 128;
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
         uint32_t r[32];
         tmem_ld32(tS + c * 32, r);
 #pragma unroll
@@ -210,6 +217,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           if (ok) mx = fmaxf(mx, __uint_as_float(r[i]) * scale_log2);
         }
       }
+      float* xm = xch + (j & 1) * 256;  // double-buffered: the partner read the other one a tile ago
+      xm[half * 128 + rloc] = mx;
+      named_bar_sync(2 + quarter, 64);
+      mx = fmaxf(mx, xm[(half ^ 1) * 128 + rloc]);
       const float m_new = fmaxf(m, mx);
       const float corr = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
@@ -218,7 +229,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tc_fence_after();
         if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
+          for (int cc = 0; cc < OC; ++cc) {
+            const int c = half * OC + cc;
             uint32_t r[32];
             tmem_ld32(tO + lane_off + c * 32, r);
 #pragma unroll
@@ -228,8 +240,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
       }
       float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
         uint32_t r[32];
         tmem_ld32(tS + c * 32, r);
         float p[32];
@@ -250,10 +263,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     mbar_wait(o_done, (nkv - 1) & 1);
     tc_fence_after();
+    xch[512 + half * 128 + rloc] = l;
+    named_bar_sync(2 + quarter, 64);
+    l += xch[512 + (half ^ 1) * 128 + rloc];
     const float inv = l > 0.f ? 1.f / l : 0.f;
     bf16* dst = ctx + (int64_t)(row_base + qrow) * M + h * DH;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int cc = 0; cc < OC; ++cc) {
+      const int c = half * OC + cc;
       uint32_t r[32];
       tmem_ld32(tO + lane_off + c * 32, r);
       float v[32];
@@ -261,7 +278,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
       if (own) store_row_bf16(dst + c * 32, v, 32);
     }
-    if (own) lse[(int64_t)(row_base + qrow) * H + h] = (m + log2f(l)) * LN2;
+    if (own && half == 0) lse[(int64_t)(row_base + qrow) * H + h] = (m + log2f(l)) * LN2;
     tc_fence_before();
   }
   __syncthreads();
@@ -311,7 +328,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(mm_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -375,24 +392,27 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
       __syncwarp();
     }
   } else {
-    // ===== thread = key row
-    const int quarter = warp & 3;
+    // ===== thread = key row; the two warps of a TMEM lane quarter take query columns
+    // [64·half, 64·half + 64) of each tile and dV/dK columns [DH/2·half, ..)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int kloc = quarter * 32 + lane;
     const int key = k0 + kloc;
     const int kend = p0 + np;  // own keys: key < kend
     const bool own = key < kend;
-    const int t128 = threadIdx.x - 64;  // 0..127
+    const int t256 = threadIdx.x - 64;  // 0..255
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int it = 0; it < niter; ++it) {
       const int qbase = (qt0 + it) * 128;
-      named_bar_sync(1, 128);  // everyone is done reading sL/sD of the previous tile
-      {
-        const int qi = qbase + t128;
-        sL[t128] = qi < N ? lse[(int64_t)(row_base + qi) * H + h] * LOG2E : 0.f;
+      named_bar_sync(1, 256);  // everyone is done reading sL/sD of the previous tile
+      if (t256 < 128) {
+        const int qi = qbase + t256;
+        sL[t256] = qi < N ? lse[(int64_t)(row_base + qi) * H + h] * LOG2E : 0.f;
+      } else {
+        const int qi = qbase + t256 - 128;
         const int64_t ro = (int64_t)(row_base + qi) * M + h * DH;
-        sD[t128] = qi < N ? row_dot_bf16<DH>(ctxO + ro, dctx + ro) : 0.f;
+        sD[t256 - 128] = qi < N ? row_dot_bf16<DH>(ctxO + ro, dctx + ro) : 0.f;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 256);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
       if (it > 0) {
@@ -400,7 +420,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
         tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 2 * half; c < 2 * half + 2; ++c) {
         uint32_t rs[32], rp[32];
         tmem_ld32(tST + lane_off + c * 32, rs);
         tmem_ld32(tdPT + lane_off + c * 32, rp);
@@ -425,7 +445,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
     tc_fence_after();
     bf16* row = dqkv + (int64_t)(row_base + key) * 3 * M;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = half * (DH / 64); c < (half + 1) * (DH / 64); ++c) {
       uint32_t r[32];
       float v[32];
       tmem_ld32(tdV + lane_off + c * 32, r);
@@ -479,7 +499,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
     mbar_init(q_bar, 1);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(mm_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -544,8 +564,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
       __syncwarp();
     }
   } else {
-    // ===== thread = query row
-    const int quarter = warp & 3;
+    // ===== thread = query row; the two warps of a TMEM lane quarter take key columns
+    // [64·half, 64·half + 64) of each tile and dQ columns [DH/2·half, ..)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
     const int qrow = q0 + rloc;
     const int qend = p0 + np;  // own queries: qrow < qend
@@ -562,7 +583,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
         tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 2 * half; c < 2 * half + 2; ++c) {
         uint32_t rs[32], rp[32];
         tmem_ld32(tS + lane_off + c * 32, rs);
         tmem_ld32(tdP + lane_off + c * 32, rp);
@@ -584,7 +605,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
     tc_fence_after();
     bf16* row = dqkv + (int64_t)(row_base + qrow) * 3 * M + h * DH;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = half * (DH / 64); c < (half + 1) * (DH / 64); ++c) {
       uint32_t r[32];
       float v[32];
       tmem_ld32(tdQ + lane_off + c * 32, r);
@@ -645,7 +666,7 @@ __global__ void attn_bwd_pre_tc_kernel(const bf16* ctx, const bf16* dctx, float*
 
 // ------------------------------------------------------------ host
 template <int DH>
-static size_t fwd_smem() { return 5 * 128 * DH * 2 + 32768 + 1024 + 256; }
+static size_t fwd_smem() { return 5 * 128 * DH * 2 + 32768 + 1024 + 128 + 3072 + 256; }
 template <int DH>
 static size_t dkdv_smem() { return 4 * 128 * DH * 2 + 65536 + 1024 + 1024 + 256; }
 template <int DH, int ST>
