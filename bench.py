@@ -389,18 +389,29 @@ def main():
         top = max(groups.values(), key=lambda p: p["ms"])
         avg_ms = top["ms"] / top["launches"]
         tc_attn = cfg.dtype == "bf16" and (cfg.M // cfg.n_heads) in (64, 128)
-        if top["name"].startswith("gemm") or (top["name"].startswith("attn") and tc_attn):
-            bound, unit = "tensor", "TFLOP/s"   # tcgen05 kernels (GEMM, flash attention)
-            achieved = top["flops"] / top["launches"] / (avg_ms * 1e-3) / 1e12
-            peak = peaks["bf16_tflops_sustained"]
-        elif top["name"].startswith("attn"):
-            bound, unit = "alu", "TFLOP/s"   # SIMT fp32 FMA: 148 SMs x 128 lanes x 2 x clock
-            achieved = top["flops"] / top["launches"] / (avg_ms * 1e-3) / 1e12
-            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        else:
-            bound, unit = "hbm", "GB/s"
-            achieved = top["bytes"] / top["launches"] / (avg_ms * 1e-3) / 1e9
-            peak = peaks["hbm_gbs"]
+        ridge = peaks["bf16_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)  # FLOP per byte
+
+        def roof(p):
+            """Bound of one kernel group from its algorithmic arithmetic intensity: tcgen05
+            work below the ridge point (e.g. expert GEMMs streaming weights / writing fp32
+            grads at P=1) is HBM-bound, above it tensor-bound."""
+            t = p["ms"] / p["launches"] * 1e-3
+            ai = p["flops"] / p["bytes"] if p["bytes"] else float("inf")
+            tc = p["name"].startswith("gemm") or (p["name"].startswith("attn") and tc_attn)
+            if tc and ai >= ridge:
+                return "tensor", "TFLOP/s", p["flops"] / p["launches"] / t / 1e12, peaks["bf16_tflops_sustained"], ai
+            if p["name"].startswith("attn") and not tc_attn:  # SIMT fp32 FMA: 148 SMs x 128 lanes x 2 x clock
+                return ("alu", "TFLOP/s", p["flops"] / p["launches"] / t / 1e12,
+                        148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, ai)
+            return "hbm", "GB/s", p["bytes"] / p["launches"] / t / 1e9, peaks["hbm_gbs"], ai
+
+        bound, unit, achieved, peak, top_ai = roof(top)
+        per_site = []
+        for p in sorted(compute, key=lambda p: -p["ms"])[:10]:
+            b_, u_, a_, pk_, ai_ = roof(p)
+            per_site.append({"site": p["name"], "share": p["ms"] / total_ms, "bound": b_, "achieved": a_,
+                             "unit": u_, "frac": a_ / pk_, "flop_per_byte": ai_,
+                             "us_per_launch": p["ms"] / p["launches"] * 1e3})
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -421,6 +432,7 @@ def main():
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                         "flop_per_byte": top_ai, "ridge_flop_per_byte": ridge, "call_sites": per_site,
                          "peak_source": peak_src + (" sustained" if bound == "tensor" else ""),
                          "share_of_compute": top["ms"] / total_ms,
                          "per_launch_ms": avg_ms, "launches_per_step": top["launches"]},

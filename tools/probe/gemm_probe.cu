@@ -9,7 +9,8 @@
 namespace fm { int g_pdl_enabled = 1; }
 using namespace fm;
 
-static void run(const char* name, int M, int N, int K, int batch, int epi) {
+static void run(const char* name, int M, int N, int K, int batch, int epi, int dbg = 0) {
+  g_tc_debug = dbg;
   void *A, *B, *C, *Z;
   cudaMalloc(&A, (size_t)batch * M * K * 2); cudaMalloc(&B, (size_t)batch * K * N * 2);
   cudaMalloc(&C, (size_t)batch * M * N * 4); cudaMalloc(&Z, (size_t)batch * M * N * 2);
@@ -30,7 +31,7 @@ static void run(const char* name, int M, int N, int K, int batch, int epi) {
   long long h[32] = {};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int reps = 200;
+  const int reps = (int64_t)M * N * batch > (1 << 26) ? 10 : 200;
   cudaEventRecord(e0, s);
   for (int i = 0; i < reps; ++i) gemm_tc(g, s);
   cudaEventRecord(e1, s);
@@ -81,5 +82,7 @@ int main() {
   run("c2_dgelu", 64, 512, 256, 8, EPI_DGELU);
   run("c2_dw1", 256, 512, 256, 8, EPI_STORE_F32);
   run("c3_e1", 256, 2048, 1024, 8, EPI_BIAS_GELU);
+  run("c4_dw1", 4096, 16384, 256, 16, EPI_STORE_F32);
+  run("c3_dw1", 1024, 2048, 512, 16, EPI_STORE_F32);
   return 0;
 }
