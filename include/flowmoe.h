@@ -194,7 +194,8 @@ flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* log
  * swap MN-major descriptor strides (debug), key 3 = force the SIMT attention
  * kernels for bf16 (debug / A-B comparison), key 4 = programmatic dependent
  * launch on (1, default) / off (0), key 5 = force the GEMM tile width (64/128/256;
- * 0 = automatic).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
+ * 0 = automatic), key 6 = peer-memory A2A of chunk r on chunk r's compute lane (1,
+ * default) / on the A2A stream (0).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
 flowmoe_status flowmoe_debug_set(int key, int value);
 
 /* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,

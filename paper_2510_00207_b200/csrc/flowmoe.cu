@@ -28,6 +28,11 @@ using namespace fm;
 
 namespace fm {
 int g_pdl_enabled = 1;
+// Peer-memory A2A of chunk r on chunk r's compute lane (1, default) or on the A2A
+// stream of the NCCL path (0, debug key 6): with one lane per chunk the lane has
+// nothing else to run while its chunk waits for the exchange, and staying on the lane
+// saves two cross-stream event hops per exchange.
+int g_p2p_on_lane = 1;
 }
 
 namespace {
@@ -470,6 +475,7 @@ flowmoe_status flowmoe_debug_set(int key, int value) {
   else if (key == 3) flags = (flags & ~4) | (value ? 4 : 0);
   else if (key == 4) { g_pdl_enabled = value ? 1 : 0; return FLOWMOE_OK; }
   else if (key == 5) { gemm_tc_force_bn(value); return FLOWMOE_OK; }
+  else if (key == 6) { g_p2p_on_lane = value ? 1 : 0; return FLOWMOE_OK; }
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   gemm_tc_set_debug(flags);
   return FLOWMOE_OK;
@@ -781,7 +787,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)
     for (int r = 0; r < R; ++r) {
-      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_at[r], 0));
       int pi = prof_start(sa);
       if (use_p2p) {
@@ -819,7 +825,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   // ---- C_1..C_R (Eq.(4))
   if (P > 1)
     for (int r = 0; r < R; ++r) {
-      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_e[r], 0));
       int pi = prof_start(sa);
       if (use_p2p) {
@@ -899,7 +905,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
-      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_cb[r], 0));
       int pi = prof_start(sa);
       if (use_p2p) {
@@ -935,7 +941,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
-      cudaStream_t sa = x->a2a_stream[r % x->a2a_stream.size()];
+      cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_eb[r], 0));
       int pi = prof_start(sa);
       if (use_p2p) {

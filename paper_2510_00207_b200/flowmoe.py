@@ -105,6 +105,8 @@ def lib() -> ctypes.CDLL:
         L.flowmoe_debug_set(3, 1)
     if os.environ.get("FLOWMOE_NO_PDL"):  # A/B knob: plain stream-ordered launches
         L.flowmoe_debug_set(4, 0)
+    if os.environ.get("FLOWMOE_P2P_A2A_STREAM"):  # A/B knob: peer-memory A2A on the A2A stream
+        L.flowmoe_debug_set(6, 0)
     if os.environ.get("FLOWMOE_DEBUG_SWAP"):  # debug knob: swap MN-major descriptor strides
         L.flowmoe_debug_set(2, 1)
     return L
