@@ -107,6 +107,7 @@ struct flowmoe_ctx {
   bool p2p = false;
   void* p2p_arena = nullptr;            // [flags 4*R*P | piece counters 4*R*P | seen 4*R | err]
   unsigned int *flags = nullptr, *piece_cnt = nullptr, *seen = nullptr, *p2p_err = nullptr;
+  unsigned int* grid_cnt = nullptr;      // [4*R] CTA counters of the fused send+wait kernel
   std::vector<unsigned int*> peer_flags; // per rank: its flags array (mapped)
   std::vector<void*> peer_dxc;           // per rank: its dispatch-bwd receive buffer (mapped)
   std::map<const void*, std::vector<void*>> peer_saved;  // my saved ptr -> each rank's saved ptr
@@ -643,7 +644,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
     x->a2a_stream.push_back(x->s_a2a);
     if (cfg->a2a_impl == FLOWMOE_A2A_P2P) {
       const size_t nfl = (size_t)4 * x->cfg.R * x->P;
-      const size_t bytes = (2 * nfl + 4 * x->cfg.R + 1) * sizeof(unsigned int);
+      const size_t bytes = (2 * nfl + 8 * x->cfg.R + 1) * sizeof(unsigned int);
       if (!alloc(&x->p2p_arena, bytes) || cudaMemset(x->p2p_arena, 0, bytes) != cudaSuccess ||
           cudaDeviceSynchronize() != cudaSuccess)
         return cleanup_fail(fail(FLOWMOE_ERR_OOM, "p2p arena allocation failed"));
@@ -651,6 +652,7 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
       x->piece_cnt = x->flags + nfl;
       x->seen = x->piece_cnt + nfl;
       x->p2p_err = x->seen + 4 * x->cfg.R;
+      x->grid_cnt = x->p2p_err + 1;
       std::vector<void*> v;
       if (ipc_exchange(x, x->p2p_arena, &v) != FLOWMOE_OK)
         return cleanup_fail(FLOWMOE_ERR_CUDA);
@@ -794,7 +796,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.xe;
         FM_K(2, a2a_p2p(at<char>(saved, L.send), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 0, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true));
+                        x->p2p_err, 0, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true, x->grid_cnt));
       } else if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
       prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_d[r], sa));
@@ -832,7 +834,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.yc;
         FM_K(2, a2a_p2p(at<char>(saved, L.ye), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 1, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true));
+                        x->p2p_err, 1, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true, x->grid_cnt));
       } else if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
       prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_c[r], sa));
@@ -912,7 +914,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.dye;
         FM_K(2, a2a_p2p(x->dyc, dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 2, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true));
+                        x->p2p_err, 2, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true, x->grid_cnt));
       } else if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
       prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], sa));
@@ -946,7 +948,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       int pi = prof_start(sa);
       if (use_p2p) {
         FM_K(2, a2a_p2p(x->dxe, x->peer_dxc.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 3, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true));
+                        x->p2p_err, 3, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true, x->grid_cnt));
       } else if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
       prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], sa));

@@ -22,11 +22,37 @@ struct P2PArgs {
   uint8_t* dst[8];          // per-destination-rank receive buffer (mapped peer pointer or local)
   unsigned int* peer_flags[8];  // per-destination-rank arrival counters, indexed [kind][R][P]
   unsigned int* piece_cnt;  // local [kind][R][P] piece counters
+  // fused wait (send_wait kernel): the grid's last CTA waits for every source
+  const unsigned int* my_flags;  // my arrival counters [kind][R][P]
+  unsigned int* seen;            // [kind][R] completed receives
+  unsigned int* err;
+  unsigned int* grid_cnt;        // [kind][R] CTA completion counter of the send grid
   int kind, r, R, P, El, me;
   int to_experts;           // 1: owner [E][R][C] -> expert [El][R][P][C]; 0: the reverse
   int64_t blk_bytes;        // C*M*es
   int pieces;               // CTAs per (destination, local expert) block
 };
+
+// wait until every source published (kind, r) for the (seen + 1)-th time, then seen += 1
+FM_DEV void p2p_wait_sources(const unsigned int* flags, unsigned int* seen, unsigned int* err, int kind, int r,
+                             int R, int P) {
+  const unsigned int expect = seen[kind * R + r] + 1u;
+  const long long t0 = clock64();
+  for (int q = 0; q < P; ++q) {
+    const unsigned int* f = flags + ((int64_t)kind * R + r) * P + q;
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if ((int)(v - expect) >= 0) break;
+      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: report instead of hanging
+        atomicExch(err, 1u);
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  seen[kind * R + r] = expect;
+}
 
 FM_DEV int64_t owner_off(int e, int r, int R, int64_t blk) { return ((int64_t)e * R + r) * blk; }
 FM_DEV int64_t expert_off(int el, int r, int q, int R, int P, int64_t blk) {
@@ -63,6 +89,44 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_kernel(P2PArgs a) {
   }
 }
 
+// send + wait in one grid: every CTA copies its piece and publishes as in the send
+// kernel; the CTA that completes the grid then waits for every source (one launch per
+// exchange instead of two on the chunk's lane).
+__global__ void __launch_bounds__(256) a2a_p2p_send_wait_kernel(P2PArgs a) {
+  FM_PDL_ENTRY();
+  __shared__ unsigned int last;
+  const int piece = blockIdx.x, el = blockIdx.y, q = blockIdx.z;
+  int64_t soff, doff;
+  if (a.to_experts) {
+    soff = owner_off(q * a.El + el, a.r, a.R, a.blk_bytes);
+    doff = expert_off(el, a.r, a.me, a.R, a.P, a.blk_bytes);
+  } else {
+    soff = expert_off(el, a.r, q, a.R, a.P, a.blk_bytes);
+    doff = owner_off(a.me * a.El + el, a.r, a.R, a.blk_bytes);
+  }
+  const int64_t per = (a.blk_bytes / 16 + a.pieces - 1) / a.pieces;
+  const int64_t v0 = piece * per, v1 = min(a.blk_bytes / 16, v0 + per);
+  const uint4* s = reinterpret_cast<const uint4*>(a.src + soff);
+  uint4* d = reinterpret_cast<uint4*>(a.dst[q] + doff);
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) d[i] = __ldg(s + i);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* cnt = a.piece_cnt + ((int64_t)a.kind * a.R + a.r) * a.P + q;
+    const unsigned int total = (unsigned int)(a.pieces * a.El);
+    if (atomicAdd(cnt, 1u) == total - 1) {
+      __threadfence_system();
+      atomicAdd_system(a.peer_flags[q] + ((int64_t)a.kind * a.R + a.r) * a.P + a.me, 1u);
+      *cnt = 0u;
+    }
+    unsigned int* gc = a.grid_cnt + a.kind * a.R + a.r;
+    last = atomicAdd(gc, 1u) == gridDim.x * gridDim.y * gridDim.z - 1u;
+    if (last) *gc = 0u;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) p2p_wait_sources(a.my_flags, a.seen, a.err, a.kind, a.r, a.R, a.P);
+}
+
 // one CTA of P threads: wait for all sources of (kind, r)
 __global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* seen, unsigned int* err,
                                     int kind, int r, int R, int P) {
@@ -92,8 +156,23 @@ __global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* see
 int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
             unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,
             int El, int me, int to_experts, int64_t blk_bytes, cudaStream_t send_stream,
-            cudaStream_t wait_stream, bool do_send, bool do_wait) {
+            cudaStream_t wait_stream, bool do_send, bool do_wait, unsigned int* grid_cnt) {
   if (P > 8) return (int)cudaErrorInvalidValue;
+  if (do_send && do_wait && send_stream == wait_stream && grid_cnt) {  // one launch
+    P2PArgs a;
+    a.src = reinterpret_cast<const uint8_t*>(src);
+    for (int q = 0; q < 8; ++q) {
+      a.dst[q] = q < P ? reinterpret_cast<uint8_t*>(dst[q]) : nullptr;
+      a.peer_flags[q] = q < P ? peer_flags[q] : nullptr;
+    }
+    a.piece_cnt = piece_cnt;
+    a.my_flags = my_flags; a.seen = seen; a.err = err; a.grid_cnt = grid_cnt;
+    a.kind = kind; a.r = r; a.R = R; a.P = P; a.El = El; a.me = me; a.to_experts = to_experts;
+    a.blk_bytes = blk_bytes;
+    a.pieces = (int)((blk_bytes + 32767) / 32768);
+    launch_k(a2a_p2p_send_wait_kernel, dim3(a.pieces, El, P), 256, 0, send_stream, a);
+    return (int)cudaGetLastError();
+  }
   if (do_send) {
     P2PArgs a;
     a.src = reinterpret_cast<const uint8_t*>(src);

@@ -106,6 +106,6 @@ int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N,
 int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
             unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,
             int El, int me, int to_experts, int64_t blk_bytes, cudaStream_t send_stream,
-            cudaStream_t wait_stream, bool do_send, bool do_wait);
+            cudaStream_t wait_stream, bool do_send, bool do_wait, unsigned int* grid_cnt = nullptr);
 
 }  // namespace fm
