@@ -203,7 +203,8 @@ flowmoe_status flowmoe_debug_set(int key, int value);
  * A(m,k) = A[b*sA + m*lda + k] (a_mmajor=0) or A[b*sA + k*lda + m] (a_mmajor=1),
  * B(k,n) = B[b*sB + k*ldb + n] (b_kmajor=0) or B[b*sB + n*ldb + k] (b_kmajor=1).
  * epi: 0 store (+bias[n] +resid), 1 bias+GELU (aux = pre-activation),
- * 2 times GELU'(aux), 3 fp32 accumulate C += acc.  bias/resid/aux nullable;
+ * 2 times GELU'(aux), 3 fp32 accumulate C += acc, 4 fp32 store, 5 bias+GELU with
+ * aux = GELU'(pre-activation), 6 times aux.  bias/resid/aux nullable;
  * resid and aux share C's ld/stride, bias has stride N per batch. */
 flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch, const void* A,
                                  int64_t lda, int64_t sA, int a_mmajor, const void* B, int64_t ldb,

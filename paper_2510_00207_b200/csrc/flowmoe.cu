@@ -194,7 +194,8 @@ flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStre
   double bytes = ((double)g.M * g.K + (double)g.K * g.N) * es * b;
   bytes += g.epi == EPI_ACC_F32 ? 8.0 * g.M * g.N * b
                                  : (double)g.M * g.N * (g.epi == EPI_STORE_F32 ? 4 : es) * b;
-  if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) bytes += (double)g.M * g.N * es * b;
+  if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_GELU_G || g.epi == EPI_MUL_AUX)
+    bytes += (double)g.M * g.N * es * b;
   if (g.resid) bytes += (double)g.M * g.N * es * b;
   FM_KP(kind, 1, flops, bytes, s, gemm(g, dt, s));
   return FLOWMOE_OK;
@@ -275,7 +276,7 @@ SavedLayout layout_of(const flowmoe_ctx* x) {
   L.src = take(R * E * C * 4);
   L.send = take(R * E * C * M * es);
   L.xe = x->P > 1 ? take(R * E * C * M * es) : L.send;
-  L.z = take(R * E * C * F * es);  // [El][R][P*C][F] == R*E*C*F elements
+  L.z = take(R * E * C * F * es);  // GELU'(Z), [El][R][P*C][F] == R*E*C*F elements
   L.h = take(R * E * C * F * es);
   L.ye = take(R * E * C * M * es);
   L.yc = x->P > 1 ? take(R * E * C * M * es) : L.ye;
@@ -813,7 +814,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     g.C = at<char>(saved, L.h + r * PC * F * es); g.ldc = F; g.sC = R * PC * F;
     g.bias = p->b1; g.sBias = F;
     g.aux = at<char>(saved, L.z + r * PC * F * es); g.ldaux = F; g.sAux = R * PC * F;
-    g.epi = EPI_BIAS_GELU;
+    g.epi = EPI_BIAS_GELU_G;  // saves GELU'(Z) for the backward (L.z)
     FM_GEMM(KK_E1, g);
     g = GemmArgs();
     g.batch = (int)El; g.M = (int)PC; g.N = (int)M; g.K = (int)F;
@@ -930,7 +931,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     g.B = p->w2; g.ldb = M; g.sB = F * M; g.b_kmajor = 1;
     g.C = (char*)x->dz + r * PC * F * es; g.ldc = F; g.sC = R * PC * F;
     g.aux = const_cast<char*>(at<char>(saved, L.z + r * PC * F * es)); g.ldaux = F; g.sAux = R * PC * F;
-    g.epi = EPI_DGELU;
+    g.epi = EPI_MUL_AUX;  // dZ = dH ⊙ GELU'(Z), GELU'(Z) saved by the forward
     FM_GEMM(KK_DGELU, g);
     // dX_e = dZ·W1ᵀ  -> dispatch-bwd send buffer (expert side)
     g = GemmArgs();

@@ -77,6 +77,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
         if (g.resid)
           v += to_f<T>(reinterpret_cast<const T*>(g.resid)[(int64_t)b * g.sR + (int64_t)m * g.ldr + n]);
         C[(int64_t)m * g.ldc + n] = from_f<T>(v);
+      } else if (g.epi == EPI_BIAS_GELU_G) {
+        T* D = reinterpret_cast<T*>(g.aux) + (int64_t)b * g.sAux;
+        const float z = to_f<T>(from_f<T>(v));
+        D[(int64_t)m * g.ldaux + n] = from_f<T>(gelu_grad_f(z));
+        C[(int64_t)m * g.ldc + n] = from_f<T>(gelu_f(z));
+      } else if (g.epi == EPI_MUL_AUX) {
+        const T* D = reinterpret_cast<const T*>(g.aux) + (int64_t)b * g.sAux;
+        C[(int64_t)m * g.ldc + n] = from_f<T>(v * to_f<T>(D[(int64_t)m * g.ldaux + n]));
       } else if (g.epi == EPI_BIAS_GELU) {
         T* Z = reinterpret_cast<T*>(g.aux) + (int64_t)b * g.sAux;
         T zq = from_f<T>(v);

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // their load latency hides under the mainloop / the previous chunk
       const bf16* xrow = nullptr;
       if (!f32out && row_ok) {
-        if (g.epi == EPI_DGELU)
+        if (g.epi == EPI_DGELU || g.epi == EPI_MUL_AUX)
           xrow = reinterpret_cast<const bf16*>(g.aux) + (int64_t)b * g.sAux + (int64_t)row * g.ldaux;
         else if (g.epi == EPI_STORE && g.resid)
           xrow = reinterpret_cast<const bf16*>(g.resid) + (int64_t)b * g.sR + (int64_t)row * g.ldr;
@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         } else if (g.epi == EPI_DGELU && row_ok) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] *= (i < nvalid) ? gelu_grad_f(xv[i]) : 0.f;
+        } else if (g.epi == EPI_MUL_AUX && row_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= xv[i];  // zeros past N
         }
         if (threadIdx.x == 64 && c0 == 0) FM_MARK(10);
         // the staging buffer is free once this warp's previous store has read it
@@ -266,6 +269,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int j = 0; j < 8; ++j) {
             float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             *reinterpret_cast<float4*>(sb + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+          }
+        } else if (g.epi == EPI_BIAS_GELU_G) {
+          // aux = GELU'(bf16(Z)), C = GELU(bf16(Z)): one erf and one exp per element
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float hh[8], dd[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float z = __bfloat162float(__float2bfloat16_rn(v[8 * j + i]));
+              const float cdf = 0.5f * (1.0f + erff(z * 0.70710678118654752f));
+              hh[i] = z * cdf;
+              dd[i] = cdf + z * __expf(-0.5f * z * z) * 0.39894228040143268f;
+            }
+            uint4 hq, dq;
+            hq.x = pack_bf16x2(hh[0], hh[1]); hq.y = pack_bf16x2(hh[2], hh[3]);
+            hq.z = pack_bf16x2(hh[4], hh[5]); hq.w = pack_bf16x2(hh[6], hh[7]);
+            dq.x = pack_bf16x2(dd[0], dd[1]); dq.y = pack_bf16x2(dd[2], dd[3]);
+            dq.z = pack_bf16x2(dd[4], dd[5]); dq.w = pack_bf16x2(dd[6], dd[7]);
+            const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(sb + off) = hq;
+            *reinterpret_cast<uint4*>(sb + 2048 + off) = dq;
           }
         } else if (g.epi == EPI_BIAS_GELU) {
           // aux = Z (pre-activation), C = GELU(bf16(Z))
@@ -303,7 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
           } else {
             tma_store_3d(&tma_c, sb, nb, m0 + r0, b);
-            if (g.epi == EPI_BIAS_GELU) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
+            if (g.epi == EPI_BIAS_GELU || g.epi == EPI_BIAS_GELU_G) tma_store_3d(&tma_aux, sb + 2048, nb, m0 + r0, b);
           }
           bulk_commit();
         }
@@ -393,7 +417,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
                 f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   maux = mc;
-  if (g.epi == EPI_BIAS_GELU) {
+  if (g.epi == EPI_BIAS_GELU || g.epi == EPI_BIAS_GELU_G) {
     rc = make_map(&maux, g.aux, g.N, g.M, g.batch, g.ldaux, g.sAux, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }

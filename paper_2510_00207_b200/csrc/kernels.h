@@ -20,7 +20,14 @@ enum DType { DT_F32 = 0, DT_BF16 = 1 };
 //   EPI_DGELU     C = acc * GELU'(aux(m,n))                        -> storage dtype
 //   EPI_ACC_F32   Cf32(m,n) += alpha*acc                            -> fp32 (grads, accumulate)
 //   EPI_STORE_F32 Cf32(m,n)  = alpha*acc                            -> fp32 (grads, overwrite)
-enum GemmEpi { EPI_STORE = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_ACC_F32 = 3, EPI_STORE_F32 = 4 };
+//   EPI_BIAS_GELU_G  z = bf16(acc + bias[n]);  C = GELU(z), aux = GELU'(z)   -> storage dtype
+//   EPI_MUL_AUX      C = acc * aux(m,n)                              -> storage dtype
+// The expert FFN uses the last two: the forward saves GELU'(Z) instead of Z, so the
+// backward's dZ = dH ⊙ GELU'(Z) epilogue is one multiply instead of erf + exp per element.
+enum GemmEpi {
+  EPI_STORE = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_ACC_F32 = 3, EPI_STORE_F32 = 4,
+  EPI_BIAS_GELU_G = 5, EPI_MUL_AUX = 6
+};
 
 struct GemmArgs {
   int M = 0, N = 0, K = 0, batch = 1;

@@ -224,6 +224,16 @@ def test_gemm_tc_epilogues():
     fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw)
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref * o.gelu_grad(fm.to_host_f64(Z))) <= 1e-2
+    # the expert FFN pair: forward saves GELU'(z), backward multiplies by it
+    D = torch.empty_like(C)
+    fm.test_gemm("bf16", A, B, C, epi=5, bias=bias, aux=D, **kw)
+    torch.cuda.synchronize()
+    zb = fm.to_host_f64(Z)  # bf16(acc + bias) from the epi=1 call, same inputs
+    assert rel(fm.to_host_f64(C), o.gelu(zb)) <= 1e-2
+    assert rel(fm.to_host_f64(D), o.gelu_grad(zb)) <= 1e-2
+    fm.test_gemm("bf16", A, B, C, epi=6, aux=D, **kw)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref * fm.to_host_f64(D)) <= 1e-2
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])

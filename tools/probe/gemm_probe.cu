@@ -9,8 +9,9 @@
 namespace fm { int g_pdl_enabled = 1; }
 using namespace fm;
 
-static void run(const char* name, int M, int N, int K, int batch, int epi, int dbg = 0) {
+static void run(const char* name, int M, int N, int K, int batch, int epi, int dbg = 0, int bn = 0) {
   g_tc_debug = dbg;
+  gemm_tc_force_bn(bn);
   void *A, *B, *C, *Z;
   cudaMalloc(&A, (size_t)batch * M * K * 2); cudaMalloc(&B, (size_t)batch * K * N * 2);
   cudaMalloc(&C, (size_t)batch * M * N * 4); cudaMalloc(&Z, (size_t)batch * M * N * 2);
@@ -84,5 +85,14 @@ int main() {
   run("c3_e1", 256, 2048, 1024, 8, EPI_BIAS_GELU);
   run("c4_dw1", 4096, 16384, 256, 16, EPI_STORE_F32);
   run("c3_dw1", 1024, 2048, 512, 16, EPI_STORE_F32);
+  run("c3_e1_st", 256, 2048, 1024, 8, EPI_STORE);
+  run("c3_e1_bn128", 256, 2048, 1024, 8, EPI_BIAS_GELU, 0, 128);
+  run("c3_e1_bn64", 256, 2048, 1024, 8, EPI_BIAS_GELU, 0, 64);
+  run("c3_dg", 256, 2048, 1024, 8, EPI_DGELU);
+  run("c3_dg_bn128", 256, 2048, 1024, 8, EPI_DGELU, 0, 128);
+  run("c4_e1", 256, 16384, 4096, 16, EPI_BIAS_GELU);
+  run("c4_e1_bn128", 256, 16384, 4096, 16, EPI_BIAS_GELU, 0, 128);
+  run("c4_qkv", 1024, 12288, 4096, 1, EPI_STORE);
+  run("c4_qkv_bn128", 1024, 12288, 4096, 1, EPI_STORE, 0, 128);
   return 0;
 }
