@@ -290,6 +290,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 // ============================================================== backward: dK, dV
+// Q/dO tiles of the dK/dV half in flight: two for d_h = 64 (the next tile loads under the
+// current one), one for d_h = 128 (shared memory).
+template <int DH>
+constexpr int DKDV_QSTAGES = DH == 64 ? 2 : 1;
+
 // grid (ceil(np/128) own key tiles, H, n_seq); query tiles are 128-aligned positions from
 // the key tile's diagonal (causal) to N.  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
 template <int DH>
@@ -299,23 +304,23 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
                                                    uint8_t* smem_raw, int kt, int h, int sq) {
   constexpr int NB = DH / 64;
   constexpr uint32_t TILE = 128 * DH * 2;
+  constexpr int QST = DKDV_QSTAGES<DH>;  // Q/dO tiles in flight (the next one loads under this one)
   uint8_t* smem = align1k(smem_raw);
   uint8_t* sK = smem;
   uint8_t* sV = smem + TILE;
-  uint8_t* sQ = smem + 2 * TILE;
-  uint8_t* sdO = smem + 3 * TILE;
-  uint8_t* sP = smem + 4 * TILE;      // P^T  [keys][queries], 32 KB
+  uint8_t* sQ0 = smem + 2 * TILE;       // [QST] x {Q, dO}
+  uint8_t* sP = smem + (2 + 2 * QST) * TILE;  // P^T  [keys][queries], 32 KB
   uint8_t* sdS = sP + 32768;          // dS^T [keys][queries], 32 KB
   float* sL = reinterpret_cast<float*>(sdS + 32768);  // lse (log2 units) of the q tile
   float* sD = sL + 128;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 128);
   uint64_t* kv_bar = bars;
-  uint64_t* q_full = bars + 1;
-  uint64_t* q_empty = bars + 2;
-  uint64_t* s_full = bars + 3;
-  uint64_t* p_full = bars + 4;
-  uint64_t* mm_done = bars + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  uint64_t* q_full = bars + 1;         // [QST]
+  uint64_t* q_empty = bars + 1 + QST;  // [QST]
+  uint64_t* s_full = bars + 1 + 2 * QST;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* mm_done = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = p0 + kt * 128, row_base = sq * N;
@@ -325,8 +330,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_bar, 1);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < QST; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     mbar_init(s_full, 1);
     mbar_init(p_full, 256);
     mbar_init(mm_done, 1);
@@ -351,12 +355,15 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
     __syncwarp();
     for (int it = 0; it < niter; ++it) {
       const int qr = row_base + (qt0 + it) * 128;
-      if (it > 0) mbar_wait_sleep(q_empty, (it - 1) & 1);
+      const int st = it % QST;
+      if (it >= QST) mbar_wait_sleep(&q_empty[st], ((it / QST) - 1) & 1);
+      uint8_t* sQ = sQ0 + st * 2 * TILE;
+      uint8_t* sdO = sQ + TILE;
       if (elect_one()) {
-        mbar_expect_tx(q_full, 2 * TILE);
+        mbar_expect_tx(&q_full[st], 2 * TILE);
         for (int i = 0; i < NB; ++i) {
-          tma_load_2d(sQ + i * 16384, &tq, q_full, h * DH + 64 * i, qr);
-          tma_load_2d(sdO + i * 16384, &tdo, q_full, h * DH + 64 * i, qr);
+          tma_load_2d(sQ + i * 16384, &tq, &q_full[st], h * DH + 64 * i, qr);
+          tma_load_2d(sdO + i * 16384, &tdo, &q_full[st], h * DH + 64 * i, qr);
         }
       }
       __syncwarp();
@@ -364,12 +371,15 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
     constexpr uint32_t id_g = idesc_bf16(128, DH, 0, 1);
-    const uint64_t dK = kdesc0(smem_u32(sK)), dV = kdesc0(smem_u32(sV)), dQk = kdesc0(smem_u32(sQ)),
-                   dOk = kdesc0(smem_u32(sdO)), dP = kdesc0(smem_u32(sP)), dS = kdesc0(smem_u32(sdS)),
-                   dOm = mdesc0(smem_u32(sdO)), dQm = mdesc0(smem_u32(sQ));
+    const uint64_t dK = kdesc0(smem_u32(sK)), dV = kdesc0(smem_u32(sV)), dP = kdesc0(smem_u32(sP)),
+                   dS = kdesc0(smem_u32(sdS));
+    const uint64_t dQk0 = kdesc0(smem_u32(sQ0)), dQm0 = mdesc0(smem_u32(sQ0));
     mbar_wait(kv_bar, 0);
     for (int it = 0; it < niter; ++it) {
-      mbar_wait(q_full, it & 1);
+      const int st = it % QST;
+      const uint64_t qoff = (uint64_t)((uint32_t)(st * 2 * TILE) >> 4), ooff = qoff + (TILE >> 4);
+      const uint64_t dQk = dQk0 + qoff, dOk = dQk0 + ooff, dQm = dQm0 + qoff, dOm = dQm0 + ooff;
+      mbar_wait(&q_full[st], (it / QST) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -386,7 +396,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
         for (int kk = 0; kk < 8; ++kk) tc_mma(tdV, dP + kstep(kk), dOm + mstep(kk), id_g, (it > 0 || kk > 0));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) tc_mma(tdK, dS + kstep(kk), dQm + mstep(kk), id_g, (it > 0 || kk > 0));
-        tc_commit(q_empty);
+        tc_commit(&q_empty[st]);
         tc_commit(mm_done);
       }
       __syncwarp();
@@ -668,7 +678,7 @@ __global__ void attn_bwd_pre_tc_kernel(const bf16* ctx, const bf16* dctx, float*
 template <int DH>
 static size_t fwd_smem() { return 5 * 128 * DH * 2 + 32768 + 1024 + 128 + 3072 + 256; }
 template <int DH>
-static size_t dkdv_smem() { return 4 * 128 * DH * 2 + 65536 + 1024 + 1024 + 256; }
+static size_t dkdv_smem() { return (2 + 2 * DKDV_QSTAGES<DH>) * 128 * DH * 2 + 65536 + 1024 + 1024 + 256; }
 template <int DH, int ST>
 static size_t dq_smem() { return (2 + 2 * ST) * 128 * DH * 2 + 32768 + 1024 + 256; }
 
