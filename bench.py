@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
     ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--optimizer", default="", choices=["", "sgd", "adamw"],
+                    help="include the parameter update (P:1173 placement: experts behind their wgrads, "
+                         "replicated weights after their all-reduce); not part of the paper's metric")
     ap.add_argument("--per-block", action="store_true",
                     help="L block_fwd/block_bwd calls (lanes joined per block) instead of the stack API")
     ap.add_argument("--schedule", default="flowmoe",
@@ -261,11 +264,39 @@ def main():
     glist = [b["grads"] for b in blocks]
     slist = [b["saved"] for b in blocks]
 
+    opt = None
+    if args.optimizer:  # fp32 master weights + optimizer state for every parameter
+        import ctypes
+        opt = fm.Optimizer.make(args.optimizer, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+        enames, rnames = ("w1", "b1", "w2", "b2"), ("wqkv", "wo", "wg")
+        for b in blocks:
+            b["master"] = {n: b["w"][n].float().clone() for n in enames + rnames}
+            b["s1"] = {n: torch.zeros_like(b["master"][n]) for n in b["master"]}
+            b["s2"] = {n: torch.zeros_like(b["master"][n]) for n in b["master"]} if args.optimizer == "adamw" else \
+                {n: None for n in b["master"]}
+            vp4 = ctypes.c_void_p * 4
+            b["eopt"] = fm.ExpertOpt(vp4(*[b["master"][n].data_ptr() for n in enames]),
+                                     vp4(*[b["s1"][n].data_ptr() for n in enames]),
+                                     vp4(*[(b["s2"][n].data_ptr() if b["s2"][n] is not None else 0) for n in enames]),
+                                     vp4(*[b["w"][n].data_ptr() for n in enames]))
+            gf, M_, E_ = b["g"]["grad_flat"], cfg.M, cfg.E
+            b["rgrad"] = {"wqkv": gf[:3 * M_ * M_], "wo": gf[3 * M_ * M_:4 * M_ * M_], "wg": gf[4 * M_ * M_:]}
+
+    def replicated_update(stream):
+        for b in blocks:
+            for n in ("wqkv", "wo", "wg"):
+                ctx.optimizer_step(opt, 1, b["master"][n], b["s1"][n], b["s2"][n], b["rgrad"][n], b["w"][n], stream)
+
     def iteration(stream):
         if not args.per_block:  # lanes forked once per direction, chunk r chains across blocks
             ctx.stack_fwd(plist, x0, xs[1:], slist, stream)
-            for t in ctx.stack_bwd(plist, x0, xs[1:], slist, dy_top, dxs, glist, S_p, stream):
+            tickets = ctx.stack_bwd(plist, x0, xs[1:], slist, dy_top, dxs, glist, S_p, stream)
+            if opt is not None:
+                tickets += [ctx.expert_update(opt, 1, b["eopt"], b["grads"]) for b in blocks]
+            for t in tickets:
                 ctx.allreduce_wait(t, stream)
+            if opt is not None:
+                replicated_update(stream)
             return
         for l in range(L):  # Eq.(3)/(4) order, block after block
             ctx.block_fwd(blocks[l]["params"], xs[l], xs[l + 1], blocks[l]["saved"], stream)
@@ -274,9 +305,13 @@ def main():
         for l in reversed(range(L)):  # Eq.(5)/(6): blocks L..1, AR of block l under block l-1
             tickets.append(ctx.block_bwd(blocks[l]["params"], xs[l], blocks[l]["saved"], g_in, dxs[l],
                                          blocks[l]["grads"], S_p, stream))
+            if opt is not None:  # block l's experts update as soon as their grads are final
+                tickets.append(ctx.expert_update(opt, 1, blocks[l]["eopt"], blocks[l]["grads"]))
             g_in = dxs[l]
         for t in tickets:  # Alg. 1 line 22: wait for all all-reduce before the update
             ctx.allreduce_wait(t, stream)
+        if opt is not None:
+            replicated_update(stream)
 
     stream = torch.cuda.current_stream()
     # warm-up (eager) + launch count of one iteration
@@ -429,6 +464,7 @@ def main():
                        "parallelism": f"ep{world}+dp{world}", "cuda_graph": not args.no_graph,
                        "compute_streams": args.compute_streams, "schedule": args.schedule,
                        "a2a": args.a2a, "api": "per_block" if args.per_block else "stack",
+                       "optimizer": args.optimizer or "excluded (P:304-305)",
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
             "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,

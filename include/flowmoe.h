@@ -168,6 +168,44 @@ flowmoe_status flowmoe_stack_bwd(flowmoe_ctx* ctx, int L, const flowmoe_params* 
                                  const flowmoe_grads* grads, size_t chunk_bytes, flowmoe_ticket* tickets,
                                  cudaStream_t stream);
 
+/* Optimizer (reading Q17: the paper updates each block's experts as soon as their
+ * gradients are final — at E_1^l of the backward, P:1173 — and the replicated MHA/gate
+ * weights after their all-reduce, but names no optimizer).  kind FLOWMOE_OPT_SGD:
+ * d = g + wd·w, b = beta1·b + d (b = d at step 1), w -= lr·b (beta1 = momentum; beta2,
+ * eps unused).  FLOWMOE_OPT_ADAMW: m = b1·m + (1-b1)·g, v = b2·v + (1-b2)·g²,
+ * w = w·(1 - lr·wd) - lr·(m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps). */
+typedef enum { FLOWMOE_OPT_SGD = 0, FLOWMOE_OPT_ADAMW = 1 } flowmoe_opt_kind;
+typedef struct {
+  int32_t kind;  /* flowmoe_opt_kind */
+  float lr, beta1, beta2, eps, weight_decay;
+} flowmoe_optimizer;
+
+/* One step over n elements on `stream`: fp32 master weights (updated in place), state1
+ * (SGD momentum buffer / AdamW m) and state2 (AdamW v; NULL for SGD), fp32 gradient; if
+ * `weight` is non-NULL the updated value is also written there in the config dtype (the
+ * compute copy the block reads).  step >= 1 counts this tensor's updates.  Invalid
+ * arguments return FLOWMOE_ERR_INVALID before anything is enqueued. */
+flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* ctx, const flowmoe_optimizer* opt, int64_t step, float* master,
+                                      float* state1, float* state2, const float* grad, void* weight, size_t n,
+                                      cudaStream_t stream);
+
+/* Per-tensor optimizer storage of the local experts, index 0..3 = w1, b1, w2, b2 (shapes of
+ * flowmoe_params); weight[i] is the compute copy (the flowmoe_params pointer). */
+typedef struct {
+  float* master[4];
+  float* state1[4];
+  float* state2[4];
+  void* weight[4];
+} flowmoe_expert_opt;
+
+/* Expert update of the block whose flowmoe_block_bwd / flowmoe_stack_bwd was enqueued last
+ * with these grads: enqueued on the ctx's weight-gradient stream right behind that
+ * block's expert wgrads, so it overlaps the rest of the backward and the all-reduces.
+ * *done (nullable) receives a ticket: flowmoe_allreduce_wait(ctx, *done, s) makes stream s
+ * wait for the update (before the next forward reads the weights). */
+flowmoe_status flowmoe_expert_update(flowmoe_ctx* ctx, const flowmoe_optimizer* opt, int64_t step,
+                                     const flowmoe_expert_opt* st, const flowmoe_grads* grads, flowmoe_ticket* done);
+
 /* Chunked in-place sum all-reduce of buf[count] fp32 over the world on the
  * low-priority AR stream (Alg. 2 PARTITION + ARQueue).  Starts after `ready`
  * (nullable: after work already enqueued on the ctx compute stream).

@@ -3,6 +3,7 @@
 The compute lives in libflowmoe.so (C ABI: include/flowmoe.h, CUDA sm_100a);
 ``flowmoe`` is the thin ctypes binding.
 """
-from .flowmoe import (BlockShape, BlockTensors, FlowMoE, FlowMoEError, Grads, Params,  # noqa: F401
+from .flowmoe import (BlockShape, BlockTensors, ExpertOpt, FlowMoE, FlowMoEError, Grads, Optimizer,  # noqa: F401
+                      Params,
                       debug_set, get_unique_id, kernel_launches, lib, profile_begin, profile_end, test_gemm, to_device,
                       to_host_f64, torch_dtype)

@@ -1149,6 +1149,54 @@ flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* x, float* buf, size_t count
   return new_ticket(x, out);
 }
 
+static flowmoe_status check_opt(const flowmoe_optimizer* o, int64_t step) {
+  if (!o) return fail(FLOWMOE_ERR_INVALID, "optimizer is NULL");
+  if (o->kind != FLOWMOE_OPT_SGD && o->kind != FLOWMOE_OPT_ADAMW)
+    return fail(FLOWMOE_ERR_INVALID, "optimizer.kind must be FLOWMOE_OPT_SGD or FLOWMOE_OPT_ADAMW");
+  if (!(o->lr >= 0.f) || !(o->weight_decay >= 0.f) || !(o->beta1 >= 0.f && o->beta1 < 1.f))
+    return fail(FLOWMOE_ERR_INVALID, "optimizer: need lr >= 0, weight_decay >= 0, 0 <= beta1 < 1");
+  if (o->kind == FLOWMOE_OPT_ADAMW && (!(o->beta2 >= 0.f && o->beta2 < 1.f) || !(o->eps >= 0.f)))
+    return fail(FLOWMOE_ERR_INVALID, "optimizer: AdamW needs 0 <= beta2 < 1 and eps >= 0");
+  if (step < 1) return fail(FLOWMOE_ERR_INVALID, "optimizer: step must be >= 1");
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step, float* master,
+                                      float* s1, float* s2, const float* grad, void* weight, size_t n,
+                                      cudaStream_t stream) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (flowmoe_status st = check_opt(o, step)) return st;
+  if (n == 0) return FLOWMOE_OK;
+  if (!master || !s1 || !grad || (o->kind == FLOWMOE_OPT_ADAMW && !s2))
+    return fail(FLOWMOE_ERR_INVALID, "optimizer_step: NULL tensor");
+  FM_K(1, optim_step(x->dt, o->kind, o->lr, o->beta1, o->beta2, o->eps, o->weight_decay, step, master, s1, s2,
+                     grad, weight, (int64_t)n, stream));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_expert_update(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step,
+                                     const flowmoe_expert_opt* st, const flowmoe_grads* gr, flowmoe_ticket* done) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (flowmoe_status s = check_opt(o, step)) return s;
+  if (!st || !gr || !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2)
+    return fail(FLOWMOE_ERR_INVALID, "expert_update: NULL argument");
+  const float* g[4] = {gr->dw1, gr->db1, gr->dw2, gr->db2};
+  const int64_t n[4] = {x->El * x->M * x->F, x->El * x->F, x->El * x->F * x->M, x->El * x->M};
+  for (int i = 0; i < 4; ++i)
+    if (!st->master[i] || !st->state1[i] || (o->kind == FLOWMOE_OPT_ADAMW && !st->state2[i]))
+      return fail(FLOWMOE_ERR_INVALID, "expert_update: NULL optimizer tensor");
+  // behind the latest block's expert wgrads on the weight-gradient stream (in order)
+  cudaStream_t sw = x->s_wg;
+  for (int i = 0; i < 4; ++i)
+    FM_K(1, optim_step(x->dt, o->kind, o->lr, o->beta1, o->beta2, o->eps, o->weight_decay, step, st->master[i],
+                       st->state1[i], st->state2[i], g[i], st->weight[i], n[i], sw));
+  // a ticket like the all-reduce's: flowmoe_allreduce_wait(done) orders a stream after it
+  const uint64_t t = x->next_ticket++;
+  FM_CUDA(cudaEventRecord(x->ticket_ev[t % NUM_TICKET_EVENTS], sw));
+  if (done) *done = t;
+  return FLOWMOE_OK;
+}
+
 flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStream_t stream) {
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (t == 0 || t >= x->next_ticket || x->next_ticket - t > NUM_TICKET_EVENTS)

@@ -109,6 +109,11 @@ size_t gate_wgrad_scratch_floats(int T, int M, int E);
 int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N, int accumulate,
                cudaStream_t s);
 
+// Optimizer step (k_optim.cu): kind 0 SGD-momentum (s1 = momentum buffer, b1 = momentum),
+// 1 AdamW (s1 = m, s2 = v); fp32 master w; out = compute copy in `dtype` (nullable).
+int optim_step(int dtype, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step, float* w,
+               float* s1, float* s2, const float* g, void* out, int64_t n, cudaStream_t s);
+
 // A2A over NVLink peer memory (k_p2p.cu): send (copy + publish) and/or wait for (kind, r).
 int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
             unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,

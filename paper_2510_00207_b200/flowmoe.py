@@ -23,6 +23,7 @@ SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "van
 EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
     "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
+    "flowmoe_optimizer_step", "flowmoe_expert_update",
     "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
     "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
 ]
@@ -56,6 +57,26 @@ class Grads(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("grad_flat", "dw1", "db1", "dw2", "db2")]
 
 
+OPT_KINDS = {"sgd": 0, "adamw": 1}
+
+
+class Optimizer(ctypes.Structure):
+    """flowmoe_optimizer: kind ('sgd' momentum / 'adamw'), lr, beta1 (SGD momentum), beta2, eps,
+    weight_decay."""
+    _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float)]
+
+    @classmethod
+    def make(cls, kind="adamw", lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0):
+        return cls(OPT_KINDS[kind], lr, beta1, beta2, eps, weight_decay)
+
+
+class ExpertOpt(ctypes.Structure):
+    """flowmoe_expert_opt: per tensor (w1, b1, w2, b2) fp32 master, state1, state2, compute copy."""
+    _fields_ = [("master", ctypes.c_void_p * 4), ("state1", ctypes.c_void_p * 4),
+                ("state2", ctypes.c_void_p * 4), ("weight", ctypes.c_void_p * 4)]
+
+
 _lib = None
 
 
@@ -82,6 +103,9 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_stack_bwd.argtypes = [vp, i32, ctypes.POINTER(Params), vp, ctypes.POINTER(vp),
                                     ctypes.POINTER(vp), vp, ctypes.POINTER(vp), ctypes.POINTER(Grads), sz,
                                     ctypes.POINTER(u64), vp]
+    L.flowmoe_optimizer_step.argtypes = [vp, ctypes.POINTER(Optimizer), ctypes.c_int64, vp, vp, vp, vp, vp, sz, vp]
+    L.flowmoe_expert_update.argtypes = [vp, ctypes.POINTER(Optimizer), ctypes.c_int64, ctypes.POINTER(ExpertOpt),
+                                        ctypes.POINTER(Grads), ctypes.POINTER(u64)]
     L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
     L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
@@ -273,6 +297,21 @@ class FlowMoE:
     def allreduce_wait(self, ticket: int, stream=None):
         _check(lib().flowmoe_allreduce_wait(self.handle, ticket, _stream_handle(stream)),
                "flowmoe_allreduce_wait")
+
+    def optimizer_step(self, opt: "Optimizer", step: int, master, state1, state2, grad, weight=None,
+                       stream=None):
+        """One optimizer step over a tensor (fp32 master / state / grad, optional compute copy)."""
+        _check(lib().flowmoe_optimizer_step(self.handle, ctypes.byref(opt), step, _ptr(master), _ptr(state1),
+                                            _ptr(state2), _ptr(grad), _ptr(weight), master.numel(),
+                                            _stream_handle(stream)), "flowmoe_optimizer_step")
+
+    def expert_update(self, opt: "Optimizer", step: int, st: "ExpertOpt", grads: "Grads") -> int:
+        """Expert update right behind the last enqueued backward's expert wgrads (P:1173);
+        returns a ticket for allreduce_wait."""
+        t = ctypes.c_uint64(0)
+        _check(lib().flowmoe_expert_update(self.handle, ctypes.byref(opt), step, ctypes.byref(st),
+                                           ctypes.byref(grads), ctypes.byref(t)), "flowmoe_expert_update")
+        return t.value
 
 
 # ---------------------------------------------------------------- torch helpers

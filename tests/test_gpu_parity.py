@@ -2,10 +2,13 @@
 same seeded synth inputs.  Tolerances (BASELINE.json north_star): routing
 indices / counts / positions bit-exact given identical logits; fp32 values
 rel <= 1e-4; bf16 with fp32 accumulation rel <= 2e-2, rel = max|g-r|/max|r|."""
+import ctypes
+
 import numpy as np
 import pytest
 
 import oracle as o
+import paper_2510_00207_b200 as fm
 from synth import PRESETS, BlockConfig, gen_replicated, gen_worker
 from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu
 
@@ -354,3 +357,86 @@ def test_stack_api_matches_per_block(dtype, graph):
     for l in range(L):
         assert np.array_equal(g["grad_flat"][l], ref["grad_flat"][l]), l
         assert np.array_equal(g["dw1"][l], ref["dw1"][l]), l
+
+
+# --------------------------------------------------------------- optimizer (reading Q17)
+@pytest.mark.parametrize("kind", ["sgd", "adamw"])
+def test_optimizer_step_matches_oracle(kind):
+    """Three steps on a ragged-length tensor (vector + scalar tail) and on an unaligned
+    view (scalar path): fp32 master/state vs the fp64 definitions, and the bf16 compute
+    copy equals bf16(master)."""
+    import torch
+    from oracle.optim import adamw_step, sgd_momentum_step
+    dev = torch.device("cuda", 0)
+    ctx = fm.FlowMoE(fm.BlockShape(B=128, seq_len=64, M=64, n_heads=1, E=4, top_k=2, d_ffn=64, R=2,
+                                   dtype="bf16"), 0, None)
+    hp = dict(lr=3e-2, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05)
+    opt = fm.Optimizer.make(kind, **hp)
+    rng = np.random.default_rng(5)
+    for n, off in ((4099, 0), (1000, 1)):
+        w0 = rng.standard_normal(n + off)
+        buf = torch.tensor(w0, dtype=torch.float32, device=dev)
+        master = buf[off:]
+        s1 = torch.zeros(n + off, dtype=torch.float32, device=dev)[off:]
+        s2 = torch.zeros(n + off, dtype=torch.float32, device=dev)[off:]
+        wb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        w, a, b = w0[off:].astype(np.float32).astype(np.float64), np.zeros(n), np.zeros(n)
+        for step in (1, 2, 3):
+            g = rng.standard_normal(n).astype(np.float32)
+            gt = torch.tensor(g, device=dev)
+            ctx.optimizer_step(opt, step, master, s1, s2 if kind == "adamw" else None, gt, wb)
+            if kind == "adamw":
+                w, a, b = adamw_step(w, a, b, g, step=step, **hp)
+            else:
+                w, a = sgd_momentum_step(w, a, g, lr=hp["lr"], momentum=hp["beta1"],
+                                         weight_decay=hp["weight_decay"], step=step)
+        torch.cuda.synchronize()
+        got = master.cpu().numpy().astype(np.float64)
+        assert rel(got, w) <= 1e-5, (n, off)
+        assert rel(s1.cpu().numpy().astype(np.float64), a) <= 1e-5
+        assert torch.equal(wb, master.to(torch.bfloat16))
+    ctx.close()
+
+
+def test_expert_update_behind_backward():
+    """the expert update enqueued after a block's backward runs behind that block's
+    expert wgrads and updates the master and the compute copy the next forward reads."""
+    import torch
+    from oracle.optim import adamw_step
+    cfg = CASES["bf16_small"]
+    rep = gen_replicated(cfg)
+    wk = gen_worker(cfg, 0)
+    dev = torch.device("cuda", 0)
+    from tests.gpu_util import shape_of
+    ctx = fm.FlowMoE(shape_of(cfg, 1, 0, "overwrite", cfg.R, "flowmoe"), 0, None)
+    bt = fm.BlockTensors(rep, cfg.dtype, 0, 1, dev)
+    names = ("w1", "b1", "w2", "b2")
+    master = {n: bt.t[n].float().clone() for n in names}
+    m = {n: torch.zeros_like(master[n]) for n in names}
+    v = {n: torch.zeros_like(master[n]) for n in names}
+    st = fm.ExpertOpt((ctypes.c_void_p * 4)(*[master[n].data_ptr() for n in names]),
+                      (ctypes.c_void_p * 4)(*[m[n].data_ptr() for n in names]),
+                      (ctypes.c_void_p * 4)(*[v[n].data_ptr() for n in names]),
+                      (ctypes.c_void_p * 4)(*[bt.t[n].data_ptr() for n in names]))
+    hp = dict(lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    opt = fm.Optimizer.make("adamw", **hp)
+    x = fm.to_device(wk["x"], cfg.dtype, dev)
+    dy = fm.to_device(wk["dy"], cfg.dtype, dev)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    saved = torch.empty(ctx.saved_bytes, dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream()
+    w_before = {n: master[n].double().cpu().numpy() for n in names}
+    ctx.block_fwd(bt.params, x, y, saved, s)
+    t = ctx.block_bwd(bt.params, x, saved, dy, dx, bt.grads, 1 << 20, s)
+    tu = ctx.expert_update(opt, 1, st, bt.grads)
+    ctx.allreduce_wait(t, s)
+    ctx.allreduce_wait(tu, s)
+    torch.cuda.synchronize()
+    gname = {"w1": "dw1", "b1": "db1", "w2": "dw2", "b2": "db2"}
+    for n in names:
+        g = bt.g[gname[n]].double().cpu().numpy()
+        assert np.abs(g).max() > 0, n  # the grads were final when the update ran
+        want, _, _ = adamw_step(w_before[n], 0.0, 0.0, g, step=1, **hp)
+        assert rel(master[n].double().cpu().numpy(), want) <= 1e-5, n
+        assert torch.equal(bt.t[n], master[n].to(torch.bfloat16)), n
+    ctx.close()

@@ -455,3 +455,42 @@ def test_microbatch_loss_scaling_identity():
     unscaled = sum(grad(x[r * b:(r + 1) * b], y[r * b:(r + 1) * b]) for r in range(R))
     assert np.max(np.abs(scaled - full) / np.abs(full)) <= ex["max_dev"]
     assert np.allclose(unscaled, R * full)
+
+
+# --------------------------------------------------------------- optimizer (reading Q17)
+def test_adamw_first_step_is_signed_lr():
+    """Step 1: m̂ = g and v̂ = g² exactly, so the update is lr·g/(|g|+ε) ≈ lr·sign(g)
+    (plus the decoupled decay w·lr·wd) — the closed form of the first AdamW step."""
+    from oracle.optim import adamw_step
+    rng = np.random.default_rng(11)
+    w, g = rng.standard_normal(64), rng.standard_normal(64) + 3.0 * np.sign(rng.standard_normal(64))
+    z = np.zeros(64)
+    w1, m1, v1 = adamw_step(w, z, z, g, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.1, step=1)
+    assert np.allclose(m1, 0.1 * g, rtol=0, atol=1e-15) and np.allclose(v1, 0.001 * g * g, rtol=1e-14)
+    want = w * (1 - 1e-3) - 1e-2 * g / (np.abs(g) + 1e-8)
+    assert np.max(np.abs(w1 - want)) <= 1e-14
+    # lr = 0 leaves the weights alone whatever the state
+    w0, _, _ = adamw_step(w, m1, v1, g, lr=0.0, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.1, step=2)
+    assert np.array_equal(w0, w)
+
+
+def test_adamw_constant_gradient_converges_to_signed_lr_steps():
+    """A constant gradient keeps m̂ = g and v̂ = g² at every step (bias correction exact),
+    so without decay every step moves w by exactly lr·g/(|g|+ε)."""
+    from oracle.optim import adamw_step
+    g = np.array([0.5, -2.0, 1e-3])
+    w, m, v = np.zeros(3), np.zeros(3), np.zeros(3)
+    for t in range(1, 6):
+        w, m, v = adamw_step(w, m, v, g, lr=0.1, beta1=0.9, beta2=0.99, eps=0.0, weight_decay=0.0, step=t)
+    assert np.allclose(w, -5 * 0.1 * np.sign(g), rtol=1e-12, atol=1e-12)
+
+
+def test_sgd_momentum_two_steps_by_hand():
+    from oracle.optim import sgd_momentum_step
+    w, g1, g2 = np.array([1.0, -2.0]), np.array([0.5, 0.25]), np.array([-1.0, 1.0])
+    w1, b1 = sgd_momentum_step(w, np.zeros(2), g1, lr=0.1, momentum=0.9, weight_decay=0.01, step=1)
+    d1 = g1 + 0.01 * w
+    assert np.allclose(b1, d1) and np.allclose(w1, w - 0.1 * d1)
+    w2, b2 = sgd_momentum_step(w1, b1, g2, lr=0.1, momentum=0.9, weight_decay=0.01, step=2)
+    d2 = g2 + 0.01 * w1
+    assert np.allclose(b2, 0.9 * d1 + d2) and np.allclose(w2, w1 - 0.1 * (0.9 * d1 + d2))
