@@ -481,7 +481,13 @@ def main():
         }
         if tl is not None:
             ranks = tl["per_rank"] if "per_rank" in tl else [tl]
-            ok = [r for r in ranks if r and "error" not in r]
+
+            def valid(r):
+                """a usable trace holds about one iteration's kernels per replay and spans
+                about one step per replay (CUPTI occasionally drops a rank's records)"""
+                return (r and "error" not in r and r["kernels_per_iter"] >= 0.5 * launches_per_step
+                        and 0.5 * ms <= r["span_us_per_iter"] / 1e3 <= 4.0 * ms)
+            ok = [r for r in ranks if valid(r)]
             if ok and world > 1:
                 worst = max(ok, key=lambda r: r["exposed_comm_us_per_iter"])
                 line["exposed_comm"] = {
@@ -489,8 +495,10 @@ def main():
                     "frac_of_iteration": worst["exposed_comm_frac_of_iter"],
                     "exposed_ms": worst["exposed_comm_us_per_iter"] / 1e3,
                     "comm_busy_ms": worst["comm_busy_us_per_iter"] / 1e3,
+                    "ranks_valid": len(ok), "ranks": len(ranks),
                     "method": f"CUPTI trace of {args.trace_iters} graph replays (edge iterations "
-                              "trimmed); worst rank; |union(NCCL kernels) minus union(compute kernels)|"}
+                              "trimmed); worst valid rank; |union(comm kernels: NCCL, peer-memory A2A) "
+                              "minus union(compute kernels)|"}
             if ok:
                 r0 = ok[0]
                 line["timeline"] = {"span_ms": r0["span_us_per_iter"] / 1e3,
