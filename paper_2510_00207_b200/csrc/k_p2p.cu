@@ -93,7 +93,11 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_kernel(P2PArgs a) {
 // kernel; the CTA that completes the grid then waits for every source (one launch per
 // exchange instead of two on the chunk's lane).
 __global__ void __launch_bounds__(256) a2a_p2p_send_wait_kernel(P2PArgs a) {
-  FM_PDL_ENTRY();
+  // No early trigger of the dependent launch: a consumer launched while this grid waits
+  // for the peers could fill every SM (e.g. a persistent GEMM parked at its griddepcontrol
+  // wait) and starve another lane's exchange that a peer is waiting on — a cross-rank
+  // deadlock.  The completing CTA triggers it once every source has arrived.
+  griddep_wait();
   __shared__ unsigned int last;
   const int piece = blockIdx.x, el = blockIdx.y, q = blockIdx.z;
   int64_t soff, doff;
@@ -124,13 +128,17 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_wait_kernel(P2PArgs a) {
     if (last) *gc = 0u;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) p2p_wait_sources(a.my_flags, a.seen, a.err, a.kind, a.r, a.R, a.P);
+  if (last) {
+    if (threadIdx.x == 0) p2p_wait_sources(a.my_flags, a.seen, a.err, a.kind, a.r, a.R, a.P);
+    __syncthreads();
+    griddep_launch();
+  }
 }
 
 // one CTA of P threads: wait for all sources of (kind, r)
 __global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* seen, unsigned int* err,
                                     int kind, int r, int R, int P) {
-  FM_PDL_ENTRY();
+  griddep_wait();  // dependents launch only when the wait is over (see the send+wait kernel)
   __shared__ unsigned int expect;
   if (threadIdx.x == 0) expect = seen[kind * R + r] + 1u;
   __syncthreads();
