@@ -188,8 +188,11 @@ def run_reference(args, cfg, L, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": CONFIG_NAMES[args.config], "tokens_per_gpu": cfg.T, "layers": L,
-                       "R": cfg.R},
+            "config": {"workload": CONFIG_NAMES[args.config], "tokens_per_gpu": cfg.T,
+                       "seq_len": cfg.seq_len, "M": cfg.M, "n_heads": cfg.n_heads, "E": cfg.E,
+                       "top_k": cfg.top_k, "d_ffn": cfg.d_ffn, "R": cfg.R, "layers": L,
+                       "capacity_factor": cfg.capacity_factor, "parallelism": f"ep{world}+dp{world}",
+                       "runs": "rank 0 only, host cores (fp64 oracle)"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"per step: 1 block fwd+bwd over one chunk ({Tr} tokens), "
                                        f"scaled to the {L}-block iteration"},
