@@ -661,7 +661,8 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
       if (ipc_exchange(x, x->dxc, &x->peer_dxc) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
       x->p2p = true;
     }
-    for (size_t l = 1; l < x->lanes.size(); ++l) {
+    // A2A lanes (NCCL path only: the peer-memory exchanges run on the compute lanes)
+    for (size_t l = 1; l < x->lanes.size() && !x->p2p; ++l) {
       ncclConfig_t nc3 = NCCL_CONFIG_INITIALIZER;
       nc3.blocking = 1;
       ncclComm_t c2 = nullptr;
