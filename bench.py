@@ -31,7 +31,8 @@ METRIC = "MoE block iteration ms & tokens/s at 1/2/4/8 B200; exposed comm %"  # 
 LAYERS = {"c1": 1, "c2": 12, "c3": 4, "c4": 4, "dsv2s": 4}   # Table 3 L for c2; §8(d) L in {1,4} else
 # S_p defaults from BO on 2x B200 (profiles/r01/tune/): NCCL's per-call cost on NVLink puts the
 # optimum at (or near) the whole per-block tensor; 0 = whole tensor
-SP_DEFAULT = {"c1": 0, "c2": 0, "c3": 16 << 20, "c4": 0, "dsv2s": 0}
+# S_p per config from the BO / grid tuning on B200 (profiles/r01/tune_n4/; 0 = whole tensor)
+SP_DEFAULT = {"c1": 0, "c2": 0, "c3": 16 << 20, "c4": 96 << 20, "dsv2s": 0}
 CONFIG_NAMES = {
     "c1": "configs[0] single fp32 MoE block (T=256, M=64, 4 heads, E=4 top-2, F=128, R=2)",
     "c2": "configs[1] GPT2-Tiny-MoE-shaped block stack (M=256, 4 heads, E=8 top-2, F=512, R=4, L=12)",
@@ -493,11 +494,14 @@ def main():
             ok = [r for r in ranks if valid(r)]
             if ok and world > 1:
                 worst = max(ok, key=lambda r: r["exposed_comm_us_per_iter"])
+                med = sorted(ok, key=lambda r: r["exposed_comm_us_per_iter"])[len(ok) // 2]
                 line["exposed_comm"] = {
                     "frac_of_comm": worst["exposed_comm_frac_of_comm"],
                     "frac_of_iteration": worst["exposed_comm_frac_of_iter"],
                     "exposed_ms": worst["exposed_comm_us_per_iter"] / 1e3,
                     "comm_busy_ms": worst["comm_busy_us_per_iter"] / 1e3,
+                    "median_rank_frac_of_comm": med["exposed_comm_frac_of_comm"],
+                    "median_rank_exposed_ms": med["exposed_comm_us_per_iter"] / 1e3,
                     "ranks_valid": len(ok), "ranks": len(ranks),
                     "method": f"CUPTI trace of {args.trace_iters} graph replays (edge iterations "
                               "trimmed); worst valid rank; |union(comm kernels: NCCL, peer-memory A2A) "
