@@ -20,6 +20,23 @@ namespace cg = cooperative_groups;
 
 namespace fm {
 
+// Phase probe (tools/probe/gate_probe.cu builds this file with -DFM_PROBE): clock64
+// stamps of the gate kernel's phases in CTA 0 (slots 0-7) and in the scanning CTA (8-15).
+#ifdef FM_PROBE
+__device__ long long g_gprobe[16];
+#define FM_GMARK(i) do { if (threadIdx.x == 0) g_gprobe[i] = clock64(); } while (0)
+#else
+#define FM_GMARK(i) do {} while (0)
+#endif
+
+FM_DEV uint32_t rt_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cta address -> the same offset in cluster CTA `rank`'s shared memory
+FM_DEV uint32_t rt_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
                                 int E, int k, int C, int* hist, int* warp_tot);
 
@@ -39,9 +56,10 @@ struct GateTile {
   static constexpr int NEG = E >= 4 ? 4 : E;   // expert groups across lanes
   static constexpr int EG = E / NEG;           // experts per lane
   static constexpr int TB = (32 / NEG) * 4;    // tokens per CTA (4 per lane)
-  static constexpr size_t smem() {
-    const size_t red = (size_t)9 * TB * E * sizeof(float);  // 8 warp partials + the sum
-    const size_t hist = (size_t)E * 256 * sizeof(int);     // fused routing scan
+  // 8 warp partials + the CTA sum + (ks-1) peer slots (rank 0), or the fused scan's hist
+  static constexpr size_t smem(int ks = 8) {
+    const size_t red = (size_t)(8 + ks) * TB * E * sizeof(float);
+    const size_t hist = (size_t)E * (256 + 8) * sizeof(int);
     return red > hist ? red : hist;
   }
 };
@@ -78,8 +96,23 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
   extern __shared__ float gsm[];  // [8][TB][E] warp partials, [TB][E] CTA sum; later the scan's hist
   __shared__ int warp_tot[32];
   __shared__ unsigned int ticket;
+  __shared__ alignas(8) unsigned long long cbar;  // rank 0: completes when every peer's slot landed
   cg::cluster_group cl = cg::this_cluster();
+  const unsigned int nrank = cl.num_blocks(), rank = cl.block_rank();
+  float* slots = gsm + 9 * TB * E;  // rank 0: [nrank-1][TB][E] peer slice sums
+  if (nrank > 1) {
+    if (rank == 0 && threadIdx.x == 0) {
+      const uint32_t b = rt_smem(&cbar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(b) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   :: "r"(b), "r"((nrank - 1) * TB * E * 4u) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(0);
   FM_PDL_ENTRY();
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tg = lane / NEG, eg = lane % NEG;
   const int tt0 = blockIdx.x * TB;                 // first token of the tile
@@ -109,6 +142,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
         for (int j = 0; j < EG; ++j) acc[i][j] = fmaf(xa[i][v], wr[j], acc[i][j]);
     }
   }
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(2);
   float* red = gsm + 8 * TB * E;
   {
     float* part = gsm + warp * TB * E;
@@ -118,70 +152,113 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
       for (int j = 0; j < EG; ++j) part[(tg * 4 + i) * E + eg * EG + j] = acc[i][j];
   }
   __syncthreads();
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(4);
+  if (nrank > 1) {
+    // cluster (1, KS, 1): every peer pushes its slice sum into rank 0's slot with
+    // st.async (completing bytes on rank 0's mbarrier) and exits; rank 0 adds the slots
+    // in rank order (deterministic).  The cluster barrier armed at entry guarantees rank
+    // 0 is resident and its mbarrier initialised before the first remote store.
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank != 0) {
+      const uint32_t dst = rt_mapa(rt_smem(slots + (rank - 1) * TB * E), 0);
+      const uint32_t bar = rt_mapa(rt_smem(&cbar), 0);
+      for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
+        float sum = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) sum += gsm[ww * TB * E + q];
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                     :: "r"(dst + 4u * q), "r"(__float_as_uint(sum)), "r"(bar) : "memory");
+      }
+      return;
+    }
+  }
   for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
     float sum = 0.f;
 #pragma unroll
     for (int ww = 0; ww < 8; ++ww) sum += gsm[ww * TB * E + q];
     red[q] = sum;
   }
-  // cluster (1, KS, 1): rank 0 adds the other slices' sums in rank order
-  const unsigned int nrank = cl.num_blocks(), rank = cl.block_rank();
   if (nrank > 1) {
-    cl.sync();
-    if (rank == 0)
-      for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
-        float sum = red[q];
-        for (unsigned int r = 1; r < nrank; ++r) sum += cl.map_shared_rank(red, r)[q];
-        red[q] = sum;
-      }
-    cl.sync();  // peers keep their shared memory alive until rank 0 has read it
-    if (rank != 0) return;
-  } else {
-    __syncthreads();
+    if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(5);
+    asm volatile(
+        "{\n.reg .pred P;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], 0;\n"
+        "@!P bra WAIT_%=;\n}" :: "r"(rt_smem(&cbar)) : "memory");
+    for (int q = threadIdx.x; q < TB * E; q += blockDim.x) {
+      float sum = red[q];
+      for (unsigned int r = 1; r < nrank; ++r) sum += slots[(r - 1) * TB * E + q];
+      red[q] = sum;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(6);
   }
+  __syncthreads();
   for (int q = threadIdx.x; q < TB * E; q += blockDim.x)
     if (tt0 + q / E < T_) logits[(int64_t)tt0 * E + q] = red[q];
   if (threadIdx.x < TB && tt0 + (int)threadIdx.x < T_) {
     const int t = tt0 + threadIdx.x;
-    const float* lg = red + threadIdx.x * E;
-    // top-k selection on logits
+    float lg[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) lg[e] = red[threadIdx.x * E + e];
+    // top-k selection on logits, register-resident (k <= 8 unrolled, E compile-time)
     uint64_t taken = 0;
     int sel[8];
-    for (int j = 0; j < k; ++j) {
-      int best = -1;
-      float bv = 0.f;
-      if (forced) {
-        best = forced[(int64_t)t * k + j];
-      } else {
-        for (int e = 0; e < E; ++e)
-          if (!((taken >> e) & 1ull) && (best < 0 || lg[e] > bv)) { best = e; bv = lg[e]; }
+    float sv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < k) {
+        int best = -1;
+        float bv = 0.f;
+        if (forced) {
+          best = forced[(int64_t)t * k + j];
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (e == best) bv = lg[e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (!((taken >> e) & 1ull) && (best < 0 || lg[e] > bv)) { best = e; bv = lg[e]; }
+        }
+        taken |= 1ull << best;
+        sel[j] = best;
+        sv[j] = bv;
+        idx[(int64_t)t * k + j] = best;
       }
-      taken |= 1ull << best;
-      sel[j] = best;
-      idx[(int64_t)t * k + j] = best;
     }
     if (k == 1) {
       // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
-      const float l0 = lg[sel[0]];
       float den = 0.f;
-      for (int e = 0; e < E; ++e) den += expf(lg[e] - l0);
+#pragma unroll
+      for (int e = 0; e < E; ++e) den += expf(lg[e] - sv[0]);
       w[t] = 1.f / den;
     } else {
-      float mx = lg[sel[0]];
-      for (int j = 1; j < k; ++j) mx = fmaxf(mx, lg[sel[j]]);
+      float mx = sv[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (j < k) mx = fmaxf(mx, sv[j]);
       float den = 0.f, ex[8];
-      for (int j = 0; j < k; ++j) { ex[j] = expf(lg[sel[j]] - mx); den += ex[j]; }
-      for (int j = 0; j < k; ++j) w[(int64_t)t * k + j] = ex[j] / den;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) { ex[j] = expf(sv[j] - mx); den += ex[j]; }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) w[(int64_t)t * k + j] = ex[j] / den;
     }
+    (void)sel;
   }
   if (done == nullptr) return;
-  __threadfence();
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(7);
+  __syncthreads();  // the CTA's logits/idx/w stores precede thread 0's release (cumulative)
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(13);
+  if (threadIdx.x == 0)  // release: this CTA's idx; acquire: every earlier CTA's (for the scan)
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(done) : "memory");
   __syncthreads();
-  if (threadIdx.x == 0) ticket = atomicAdd(done, 1u);
-  __syncthreads();
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(3);
   if (ticket != gridDim.x - 1) return;
-  __threadfence();  // every tile's idx is visible
+  FM_GMARK(8);
+  // thread 0's acquire (the ticket) + the barrier above order every tile's idx before
+  // this CTA's reads (the grid-sync pattern)
   route_scan_body(idx, pos, counts, src, T_, E, k, C, reinterpret_cast<int*>(gsm), warp_tot);
+  FM_GMARK(12);
   if (threadIdx.x == 0) *done = 0u;  // ready for the next use (stream-ordered)
 }
 
@@ -198,11 +275,14 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
 
 // Slices of M per token tile: enough CTAs to cover ~2 waves of the 148 SMs, at most a
 // portable cluster (8), at least one 16-byte vector per warp.
+int g_gate_force_ks = 0;  // probe / A-B only: force the number of M slices (1..8)
+
 static void gate_split(int T_, int M, int TB, int V, int* KS, int* MS) {
   const int tiles = (T_ + TB - 1) / TB, nvec = M / V;
   int ks = (2 * 148 + tiles - 1) / tiles;
   ks = ks < 1 ? 1 : (ks > 8 ? 8 : ks);
   if (ks > nvec / 8) ks = nvec / 8 > 0 ? nvec / 8 : 1;
+  if (g_gate_force_ks > 0) ks = g_gate_force_ks;
   const int msv = (nvec + ks - 1) / ks;
   *MS = msv * V;
   *KS = (nvec + msv - 1) / msv;
@@ -218,7 +298,7 @@ static void gate_topk_launch_t(const void* a, const void* wg, const int32_t* for
   auto kern = gate_topk_kernel<T, E>;
   static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem()), true);
   (void)once;
-  launch_kc(kern, dim3((T_ + G::TB - 1) / G::TB, KS), 256, G::smem(), s, dim3(1, KS, 1), (const T*)a,
+  launch_kc(kern, dim3((T_ + G::TB - 1) / G::TB, KS), 256, G::smem(KS), s, dim3(1, KS, 1), (const T*)a,
             (const T*)wg, forced, logits, idx, w, T_, M, MS, k, pos, counts, src, C, done);
 }
 
@@ -260,8 +340,8 @@ int gate_route(int dtype, const void* a, const void* wg, const int32_t* forced, 
 // to the same expert.
 constexpr int RS_THREADS = 512;
 
-// Block-wide deterministic routing scan (one CTA, blockDim a multiple of 32, <= 1024):
-// hist is [E][blockDim.x] ints of dynamic shared memory.
+// Block-wide deterministic routing scan (one CTA, blockDim a power of two in [32, 1024]):
+// hist is [E][blockDim.x + blockDim.x/32] ints of dynamic shared memory (padded rows).
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
                                 int E, int k, int C, int* hist, int* warp_tot) {
   (void)warp_tot;
@@ -269,17 +349,43 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
   const int n = T_ * k;
   const int seg = (n + nt - 1) / nt;
   const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
-  for (int e = 0; e < E; ++e) hist[e * nt + tid] = 0;
+  // hist[e][th] lives at e·rs + th + th/32: one pad word per 32 threads keeps the
+  // lane-runs of the scan below (lane L reads threads L·per .. L·per+per-1) conflict-free
+  const int rs = nt + nt / 32;
+  const int my = tid + (tid >> 5);
+  // a thread's slots (slot-major: s = j·T + t) are loaded once, all in flight together,
+  // and kept in registers for both passes when they fit (seg <= SCAN_REG)
+  constexpr int SCAN_REG = 8;
+  const bool in_reg = seg <= SCAN_REG;
+  int ev[SCAN_REG];
+#pragma unroll
+  for (int i = 0; i < SCAN_REG; ++i) {
+    const int s = s0 + i;
+    ev[i] = 0;
+    if (in_reg && s < s1) {
+      const int j = s / T_, t = s - j * T_;
+      ev[i] = idx[(int64_t)t * k + j];
+    }
+  }
+  for (int e = 0; e < E; ++e) hist[e * rs + my] = 0;
   for (int i = tid; i < E * C; i += nt) src[i] = -1;
   __syncthreads();
-  for (int s = s0; s < s1; ++s) {
-    const int j = s / T_, t = s - j * T_;
-    hist[idx[(int64_t)t * k + j] * nt + tid] += 1;
+  FM_GMARK(9);
+  if (in_reg) {
+#pragma unroll
+    for (int i = 0; i < SCAN_REG; ++i)
+      if (s0 + i < s1) hist[ev[i] * rs + my] += 1;
+  } else {
+    for (int s = s0; s < s1; ++s) {
+      const int j = s / T_, t = s - j * T_;
+      hist[idx[(int64_t)t * k + j] * rs + my] += 1;
+    }
   }
   __syncthreads();
+  FM_GMARK(10);
   const int lane = tid & 31, nw = nt >> 5, per = nt >> 5;  // per: threads summed by one lane
   for (int e = tid >> 5; e < E; e += nw) {
-    int* h = hist + e * nt + lane * per;
+    int* h = hist + e * rs + lane * per + ((lane * per) >> 5);  // per <= 32: no pad inside a run
     int run = 0;
     for (int i = 0; i < per; ++i) run += h[i];
     int x = run;
@@ -297,13 +403,23 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
     }
   }
   __syncthreads();
-  for (int s = s0; s < s1; ++s) {
+  FM_GMARK(11);
+  auto place = [&](int s, int e) {
     const int j = s / T_, t = s - j * T_;
-    const int e = idx[(int64_t)t * k + j];
-    const int p = hist[e * nt + tid]++;
+    const int p = hist[e * rs + my]++;
     const bool kept = p < C;
     pos[(int64_t)t * k + j] = kept ? p : -1;
     if (kept) src[e * C + p] = t * k + j;
+  };
+  if (in_reg) {
+#pragma unroll
+    for (int i = 0; i < SCAN_REG; ++i)
+      if (s0 + i < s1) place(s0 + i, ev[i]);
+  } else {
+    for (int s = s0; s < s1; ++s) {
+      const int j = s / T_, t = s - j * T_;
+      place(s, idx[(int64_t)t * k + j]);
+    }
   }
 }
 
@@ -311,16 +427,17 @@ __global__ void __launch_bounds__(RS_THREADS) route_scan_kernel(const int32_t* i
                                                                 int32_t* counts, int32_t* src,
                                                                 int T_, int E, int k, int C) {
   FM_PDL_ENTRY();
-  extern __shared__ int hist[];  // [E][RS_THREADS]
+  extern __shared__ int hist[];  // [E][RS_THREADS + RS_THREADS/32]
   __shared__ int warp_tot[32];
   route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, warp_tot);
 }
 
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_, int E,
                int k, int C, cudaStream_t s) {
-  size_t smem = (size_t)E * RS_THREADS * sizeof(int);
+  constexpr int RS_ROW = RS_THREADS + RS_THREADS / 32;
+  size_t smem = (size_t)E * RS_ROW * sizeof(int);
   static bool once = (cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           64 * RS_THREADS * (int)sizeof(int)), true);
+                                           64 * RS_ROW * (int)sizeof(int)), true);
   (void)once;
   launch_k(route_scan_kernel, 1, RS_THREADS, smem, s, idx, pos, counts, src, T_, E, k, C);
   return (int)cudaGetLastError();
