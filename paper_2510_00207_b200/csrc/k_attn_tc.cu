@@ -114,7 +114,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   float* xch = reinterpret_cast<float*>(bars + 16);  // [3][2 halves][128 rows]: row max (tile parity), row sum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
+  // longest-first: linear block L -> query tile nt-1-L/(n_seq·H) (causal work grows with qt)
+  const int per = gridDim.y * gridDim.z;
+  const int L = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int lv = L / per, r = L - lv * per;
+  const int qt = gridDim.x - 1 - lv, h = r % gridDim.y, sq = r / gridDim.y;
   const int q0 = p0 + qt * 128, row_base = sq * N;  // q0: position of the tile's first query
   int nkv = (N + 127) / 128;
   if (causal) nkv = min(nkv, (min(p0 + np, q0 + 128) + 127) / 128);
@@ -633,21 +637,39 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tq, const CU
   }
 }
 
-// dK/dV and dQ of one (sequence, head) run as one launch: blockIdx.z = 2·seq + role
-// (0: dK/dV of own key tile blockIdx.x, 1: dQ of own query tile blockIdx.x).  The two
-// halves are independent (disjoint outputs, shared read-only inputs), so they co-run.
+// dK/dV and dQ of one (sequence, head) run as one launch of grid (own tiles, H, 2·n_seq):
+// each CTA takes one (role, sequence, head, tile) item (role 0: dK/dV of an own key
+// tile, 1: dQ of an own query tile).  The two roles are independent (disjoint outputs, shared read-only inputs), so they co-run.
 template <int DH, int STAGES>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
                        const float* lse, const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0, int np,
                        int M, int H, int causal, float scale_log2, float scale) {
   extern __shared__ uint8_t smem_raw[];
+  // Longest-first order: CTAs are dispatched in linear block order, and a causal tile's
+  // work grows with its distance from the diagonal end (dK/dV of key tile t: nt - t query
+  // tiles; dQ of query tile t: t + 1 key tiles), so linear index L takes level
+  // lv = L / (2·n_seq·H) = dK/dV tile lv and dQ tile nt-1-lv of every (sequence, head).
+  // With more CTAs than SMs the heavy tiles start in the first wave.
+  const int nt = gridDim.x, per = gridDim.y * gridDim.z;
+  const int L = blockIdx.x + nt * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int lv = L / per, r = L - lv * per, rest = r >> 1;
+  const int h = rest % gridDim.y, sq = rest / gridDim.y;
+#ifdef FM_ATTN_LINEAR  // probe A/B only: the natural (tile, head, 2·seq + role) order
   if (blockIdx.z & 1)
     attn_bwd_dq_body<DH, STAGES>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale,
                                  smem_raw, blockIdx.x, blockIdx.y, blockIdx.z >> 1);
   else
     attn_bwd_dkdv_body<DH>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale, smem_raw,
                            blockIdx.x, blockIdx.y, blockIdx.z >> 1);
+  return;
+#endif
+  if (r & 1)
+    attn_bwd_dq_body<DH, STAGES>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale,
+                                 smem_raw, nt - 1 - lv, h, sq);
+  else
+    attn_bwd_dkdv_body<DH>(tq, tdo, lse, ctxO, dctx, dqkv, N, p0, np, M, H, causal, scale_log2, scale, smem_raw,
+                           lv, h, sq);
 }
 
 // D[t][h] = sum_d dO[t][h*dh+d] * O[t][h*dh+d]: one warp per token, 16-byte loads;

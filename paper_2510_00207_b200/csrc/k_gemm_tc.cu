@@ -51,7 +51,7 @@ struct TcArgs {
 // then m, then batch).  The smem operand ring runs continuously across tiles, and the
 // accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
 // overlaps the TMA loads + MMAs of tile i+1.
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b,
@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // one tile per CTA: the operand ring is free when the epilogue runs, so it doubles
   // as the staging area and a single TMEM accumulator suffices (smaller footprint)
   const bool single = num_tiles <= (int)gridDim.x;
-  uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x 4 KB staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : 32768));
+  uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x EB x 4 KB staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : EB * 32768));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the 4 epilogue warps
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // chunk is staged as a [32 rows][32 cols] box in smem with the TMA swizzle (128 B
     // rows for fp32, 64 B rows for bf16: conflict-free 16-byte st.shared) and written by
     // one TMA bulk store, or a TMA bulk reduce-add (fp32 grad accumulation C += acc, done
-    // in L2).  One 4 KB staging buffer per warp.
+    // in L2).  EB 4 KB staging buffers per warp: with EB = 2 a chunk is staged while the
+    // previous chunk's store still reads its buffer (write-bound, small-K GEMMs).
 #ifdef FM_PROBE_OBS
     if (threadIdx.x == 65 && blockIdx.x == 0)  // observer: when each of the first stages lands
       for (int q = 0; q < p.nk && q < 8 && q < STAGES; ++q) {
@@ -187,9 +188,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #endif
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int r0 = quarter * 32;
-    uint8_t* sb = epi_smem + (warp - 2) * 4096;
+    uint8_t* sb0 = epi_smem + (warp - 2) * EB * 4096;
     const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
-    bool pending = false;  // a store from sb is in flight
+    int issued = 0;  // chunks this warp has stored (buffer issued % EB was used EB chunks ago)
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
@@ -258,9 +259,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int i = 0; i < 32; ++i) v[i] *= xv[i];  // zeros past N
         }
         if (threadIdx.x == 64 && c0 == 0) FM_MARK(10);
-        // the staging buffer is free once this warp's previous store has read it
-        if (pending) {
-          if (lane == 0) bulk_wait_read<0>();
+        // the staging buffer is free once the store that used it EB chunks ago has read it
+        uint8_t* sb = sb0 + (issued % EB) * 4096;
+        if (issued >= EB) {
+          if (lane == 0) bulk_wait_read<EB - 1>();
           __syncwarp();
         }
         if (threadIdx.x == 64 && c0 == 0) FM_MARK(11);
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           bulk_commit();
         }
-        pending = true;
+        ++issued;
       }
       tc_fence_before();
       __syncwarp();
@@ -400,7 +402,7 @@ int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EB = 1>
 static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap ma, mb;
   int rc;
@@ -431,8 +433,8 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.a_mmajor ? 1 : 0) << 15) |
             ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
             ((uint32_t)(TC_BM >> 4) << 24);
-  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 32768 + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES>;
+  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + EB * 32768 + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, STAGES, EB>;
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max), true);
   (void)attr_set;
   static int num_sms = 0;
@@ -444,7 +446,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   }
   const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM - 1) / TC_BM) * g.batch;
   const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-  const size_t smem = tiles <= grid ? smem_max - 32768 : smem_max;
+  const size_t smem = tiles <= grid ? smem_max - EB * 32768 : smem_max;
   launch_k(kern, dim3(grid), TC_THREADS, smem, s, ma, mb, mc, maux, p);
   return (int)cudaGetLastError();
 }
@@ -461,6 +463,11 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
+  // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) take a 3-stage ring
+  // and double-buffered epilogue staging (tools/probe/gemm_probe.cu: -2..-6%); the
+  // 4-stage ring stays everywhere else (3 stages cost 3-8% on longer K)
+  const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
+  if (g.N >= 256 && f32out && g.K <= 4 * TC_BK && tiles(256) >= 4 * 148) return launch_tc<256, 3, 2>(g, s);
   if (g.N >= 256 && tiles(256) >= 48) return launch_tc<256, 4>(g, s);
   if (g.N >= 128 && tiles(128) >= 48) return launch_tc<128, 6>(g, s);
   return launch_tc<64, 8>(g, s);

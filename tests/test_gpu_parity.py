@@ -203,6 +203,27 @@ def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape):
     assert rel(C32.cpu().numpy().astype(np.float64) - 1.0, ref) <= 1e-5
 
 
+@pytest.mark.parametrize("epi", [3, 4])
+def test_gemm_tc_wgrad_variant_vs_fp64(epi):
+    """The write-bound wgrad configuration (fp32 out, K <= 256, >= 4·148 tiles of 256
+    columns: 3-stage ring, double-buffered epilogue staging) on an m-major A like the
+    expert dW, ragged N and K, against the fp64 product: store (4) and accumulate (3)."""
+    import torch
+    import paper_2510_00207_b200 as fm
+    Mr, N, K = 2048, 9480, 200  # 16 x 38 = 608 tiles
+    rng = np.random.default_rng(11 + epi)
+    dev = torch.device("cuda", 0)
+    At = fm.to_device(rng.standard_normal((1, K, Mr)), "bf16", dev)  # A stored m-major [K][M]
+    Bt = fm.to_device(rng.standard_normal((1, K, N)), "bf16", dev)
+    ref = fm.to_host_f64(At)[0].T @ fm.to_host_f64(Bt)[0]
+    C = torch.full((1, Mr, N), 0.5 if epi == 3 else 7.0, dtype=torch.float32, device=dev)
+    fm.test_gemm("bf16", At, Bt, C, M=Mr, N=N, K=K, batch=1, lda=Mr, sA=Mr * K, a_mmajor=1,
+                 ldb=N, sB=K * N, ldc=N, sC=Mr * N, epi=epi)
+    torch.cuda.synchronize()
+    got = C[0].cpu().numpy().astype(np.float64) - (0.5 if epi == 3 else 0.0)
+    assert rel(got, ref) <= 1e-5
+
+
 def test_gemm_tc_epilogues():
     import torch
     import paper_2510_00207_b200 as fm

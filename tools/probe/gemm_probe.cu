@@ -9,6 +9,9 @@
 namespace fm { int g_pdl_enabled = 1; }
 using namespace fm;
 
+static int g_variant = 0;  // 1: BN=256, 3 stages, 2 staging buffers per epilogue warp
+static int call(const GemmArgs& g, cudaStream_t s) { return g_variant ? launch_tc<256, 3, 2>(g, s) : gemm_tc(g, s); }
+
 static void run(const char* name, int M, int N, int K, int batch, int epi, int dbg = 0, int bn = 0) {
   g_tc_debug = dbg;
   gemm_tc_force_bn(bn);
@@ -23,25 +26,27 @@ static void run(const char* name, int M, int N, int K, int batch, int epi, int d
   g.B = B; g.ldb = N; g.sB = (int64_t)K * N;
   g.C = C; g.ldc = N; g.sC = (int64_t)M * N;
   g.epi = epi;
-  if (epi == EPI_DGELU || epi == EPI_BIAS_GELU) { g.aux = Z; g.ldaux = N; g.sAux = (int64_t)M * N; }
-  if (epi == EPI_BIAS_GELU) { g.bias = Z; g.sBias = N; }
+  if (epi == EPI_DGELU || epi == EPI_BIAS_GELU || epi == EPI_BIAS_GELU_G || epi == EPI_MUL_AUX) {
+    g.aux = Z; g.ldaux = N; g.sAux = (int64_t)M * N;
+  }
+  if (epi == EPI_BIAS_GELU || epi == EPI_BIAS_GELU_G) { g.bias = Z; g.sBias = N; }
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  for (int i = 0; i < 20; ++i) gemm_tc(g, s);
+  for (int i = 0; i < 20; ++i) call(g, s);
   cudaStreamSynchronize(s);
   long long h[32] = {};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int reps = (int64_t)M * N * batch > (1 << 26) ? 10 : 200;
   cudaEventRecord(e0, s);
-  for (int i = 0; i < reps; ++i) gemm_tc(g, s);
+  for (int i = 0; i < reps; ++i) call(g, s);
   cudaEventRecord(e1, s);
   cudaEventSynchronize(e1);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   // single isolated launch
   cudaEventRecord(e0, s);
-  gemm_tc(g, s);
+  call(g, s);
   cudaEventRecord(e1, s);
   cudaEventSynchronize(e1);
   float ms1 = 0.f;
@@ -64,7 +69,7 @@ static void run(const char* name, int M, int N, int K, int batch, int epi, int d
   // the same shape with PDL off (plain stream order)
   g_pdl_enabled = 0;
   cudaEventRecord(e0, s);
-  for (int i = 0; i < reps; ++i) gemm_tc(g, s);
+  for (int i = 0; i < reps; ++i) call(g, s);
   cudaEventRecord(e1, s);
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
@@ -74,8 +79,51 @@ static void run(const char* name, int M, int N, int K, int batch, int epi, int d
   cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(Z);
 }
 
-int main() {
+// pure-write bandwidth baselines over n bytes: cudaMemsetAsync and a 16-byte-store kernel
+__global__ void write_v4(float4* p, size_t n4) {
+  const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+static void write_bw(size_t n) {
+  void* p;
+  cudaMalloc(&p, n);
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float ms;
+  for (int v = 0; v < 3; ++v) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0, s);
+      for (int i = 0; i < 5; ++i) {
+        if (v == 0) cudaMemsetAsync(p, 0, n, s);
+        else write_v4<<<148 * (v == 1 ? 4 : 16), 512, 0, s>>>((float4*)p, n / 16);
+      }
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    printf("write %s %.2f GB: %.1f us  %.0f GB/s\n", v == 0 ? "memset" : (v == 1 ? "v4x4" : "v4x16"), n / 1e9,
+           ms * 200.f, n / (ms / 5.f * 1e-3) / 1e9);
+  }
+  cudaFree(p);
+}
+
+int main(int argc, char** argv) {
   gemm_tc_init();
+  if (argc > 1) {  // "dw": the write baselines and the c4 expert-wgrad shapes only
+    write_bw((size_t)4096 * 16384 * 16 * 4);
+    for (g_variant = 0; g_variant < 2; ++g_variant) {
+      printf("variant %d\n", g_variant);
+      run("c4_dw1", 4096, 16384, 256, 16, EPI_STORE_F32);
+      run("c4_dw2", 16384, 4096, 256, 16, EPI_STORE_F32);
+      run("c3_dw1", 1024, 2048, 512, 16, EPI_STORE_F32);
+      run("c4_e1", 256, 16384, 4096, 16, EPI_BIAS_GELU_G);
+      run("c3_e1", 256, 2048, 1024, 16, EPI_BIAS_GELU_G);
+      run("c4_dx", 1024, 4096, 4096, 1, EPI_STORE);
+    }
+    return 0;
+  }
   run("c2_dctx", 256, 256, 256, 1, EPI_STORE);
   run("c2_qkv", 256, 768, 256, 1, EPI_STORE);
   run("c2_e1", 64, 512, 256, 8, EPI_BIAS_GELU);
