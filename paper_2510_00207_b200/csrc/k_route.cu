@@ -498,7 +498,34 @@ __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, cons
   float acc[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
-  for (int j = 0; j < k; ++j) {
+  // the first two slots' routing, rows and the residual are all requested before any is
+  // used (two dependent round trips instead of one per slot); same summation order
+  float rv[V];
+  if (resid) load16<T>(resid + (int64_t)t * M + m, rv);
+  const int k2 = k < 2 ? k : 2;
+  int p2[2], e2[2];
+  float w2[2], v2[2][V];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int64_t o = (int64_t)t * k + (j < k2 ? j : 0);
+    p2[j] = j < k2 ? pos[o] : -1;
+    e2[j] = idx[o];
+    w2[j] = w[o];
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const T* src = y + ((int64_t)e2[j] * ldE + (p2[j] < 0 ? 0 : p2[j])) * M + m;
+    if (p2[j] >= 0) load16<T>(src, v2[j]);
+    else
+#pragma unroll
+      for (int i = 0; i < V; ++i) v2[j][i] = 0.f;
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    if (p2[j] >= 0)
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = fmaf(w2[j], v2[j][i], acc[i]);
+  for (int j = 2; j < k; ++j) {
     const int p = pos[(int64_t)t * k + j];
     if (p < 0) continue;
     const float wj = w[(int64_t)t * k + j];
@@ -507,12 +534,9 @@ __global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, cons
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = fmaf(wj, v[i], acc[i]);
   }
-  if (resid) {
-    float v[V];
-    load16<T>(resid + (int64_t)t * M + m, v);
+  if (resid)
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] += v[i];
-  }
+    for (int i = 0; i < V; ++i) acc[i] += rv[i];
   store16<T>(out + (int64_t)t * M + m, acc);
 }
 
@@ -647,6 +671,25 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
   const int tb = (blockDim.x / CV) * TPL;              // tokens per CTA
   const int t0 = blockIdx.x * tb + tgi * TPL;
   const int m = (blockIdx.y * CV + cv) * V;
+  // TPL == 1 (small, latency-bound chunks): the gathered rows of the first two slots and
+  // dO do not depend on the dlogits, so their loads are issued first and land under the
+  // dlogits / Wg work (same summation order as the late loads below)
+  constexpr bool PF = TPL == 1 && E <= 32;  // E = 64: the register budget goes to dl and Wg
+  float px[2][V], pr[V];
+  bool pok[2] = {false, false};
+  if constexpr (PF) {
+    const int t = t0;
+    if (t < T_ && m < M) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (j < k) {
+          const int p = pos[(int64_t)t * k + j];
+          pok[j] = p >= 0;
+          if (pok[j]) load16<T>(dx + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M + m, px[j]);
+        }
+      if (dres) load16<T>(dres + (int64_t)t * M + m, pr);
+    }
+  }
   // dlogits (reading Q5): k>=2: dl_{e_j} = w_j (dw_j - Σ w dw); k=1: dl = p ⊙ (g - <p,g>)
   float dl[TPL][E];
 #pragma unroll
@@ -702,7 +745,16 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
   for (int i = 0; i < TPL; ++i) {
     const int t = t0 + i;
     if (t >= T_) break;
-    for (int j = 0; j < k; ++j) {
+    int j0 = 0;
+    if constexpr (PF) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (pok[j])
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[i][v] += px[j][v];
+      j0 = 2;
+    }
+    for (int j = j0; j < k; ++j) {
       const int p = pos[(int64_t)t * k + j];
       if (p < 0) continue;
       float v8[V];
@@ -712,7 +764,12 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
     }
     if (dres) {
       float v8[V];
-      load16<T>(dres + (int64_t)t * M + m, v8);
+      if (PF) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) v8[v] = pr[v];
+      } else {
+        load16<T>(dres + (int64_t)t * M + m, v8);
+      }
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[i][v] += v8[v];
     }

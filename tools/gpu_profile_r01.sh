@@ -23,6 +23,7 @@ done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 600 -c 6 -o $O/full_c2_gemm $B > $O/full_c2_gemm.log 2>&1; echo "full c2 gemm rc=$?" >> $S
 B3="python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline --trace-iters 0"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"attn_bwd_tc|attn_fwd_tc" -s 40 -c 4 -o $O/full_c3_attn $B3 > $O/full_c3_attn.log 2>&1; echo "full c3 attn rc=$?" >> $S
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gate_topk -s 40 -c 4 -o $O/full_c3_gate $B3 > $O/full_c3_gate.log 2>&1; echo "full c3 gate rc=$?" >> $S
 B4="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline --trace-iters 0 --layers 1"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 30 -c 10 -o $O/full_c4_gemm $B4 > $O/full_c4_gemm.log 2>&1; echo "full c4 gemm rc=$?" >> $S
 cat $S; ls -la $O

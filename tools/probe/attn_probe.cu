@@ -36,8 +36,22 @@ static void run(const char* name, int nseq, int N, int M, int H) {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms[pass], e0, e1);
   }
-  printf("%-4s nseq=%d N=%d M=%d H=%d: fwd %.2f us  bwd %.2f us  (%s)\n", name, nseq, N, M, H, ms[0] * 10.f,
-         ms[1] * 10.f, cudaGetErrorString(cudaGetLastError()));
+  // isolated launches (synchronised on both sides: no overlap with a neighbour launch)
+  float iso[2] = {0.f, 0.f};
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i < 20; ++i) {
+      cudaStreamSynchronize(s);
+      cudaEventRecord(e0, s);
+      if (pass == 0) attn_fwd_tc(qkv, ctx, lse, nseq, N, 0, N, M, H, 1, s);
+      else attn_bwd_tc(qkv, ctx, lse, dctx, dqkv, D, nseq, N, 0, N, M, H, 1, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float t;
+      cudaEventElapsedTime(&t, e0, e1);
+      iso[pass] += t * 1000.f / 20;
+    }
+  printf("%-4s nseq=%d N=%d M=%d H=%d: back-to-back fwd %.2f us  bwd %.2f us | isolated fwd %.2f us  bwd %.2f us (%s)\n",
+         name, nseq, N, M, H, ms[0] * 10.f, ms[1] * 10.f, iso[0], iso[1], cudaGetErrorString(cudaGetLastError()));
   cudaFree(qkv); cudaFree(ctx); cudaFree(dctx); cudaFree(dqkv); cudaFree(lse); cudaFree(D);
 }
 
