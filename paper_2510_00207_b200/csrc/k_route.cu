@@ -556,40 +556,46 @@ int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_
   return (int)cudaGetLastError();
 }
 
-// K8: dY[e][pos] = w·dO[t]; dw[t][j] = <dO[t], Y[e][pos]>.  One CTA per token (threads
-// stride the 16-byte vectors of the row, all K slots in one pass, block reduction of
-// the K dots in a fixed order); CTAs past T_ zero 8 padding rows of dY each.
+// K8: dY[e][pos] = w·dO[t]; dw[t][j] = <dO[t], Y[e][pos]>.  tpt threads per token (the
+// power of two >= 32 that covers the row's 16-byte vectors in one pass, at most 256: a
+// warp per token for narrow rows, a CTA per token for wide ones), all K slots in one
+// pass, reduction of the K dots over the token's warps in a fixed order; CTAs past the
+// token CTAs zero 8 padding rows of dY each.
 template <typename T, int K>
 __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, const T* y,
                                                                const int32_t* idx,
                                                                const int32_t* pos, const float* w,
                                                                const int32_t* src, T* dy,
                                                                float* dw, int T_, int M,
-                                                               int rows, int C, int ldE) {
+                                                               int rows, int C, int ldE, int tpt) {
   __shared__ float red[8][K];  // [warp][slot]
   FM_PDL_ENTRY();
   constexpr int V = 16 / sizeof(T);
   const int nv = M / V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if ((int)blockIdx.x >= T_) {  // padding rows (src < 0) of dy get zeros
-    const int r = ((int)blockIdx.x - T_) * 8 + warp;
+  const int tpc = (int)blockDim.x / tpt, ntb = (T_ + tpc - 1) / tpc;  // tokens per CTA, token CTAs
+  if ((int)blockIdx.x >= ntb) {  // padding rows (src < 0) of dy get zeros
+    const int r = ((int)blockIdx.x - ntb) * 8 + warp;
     if (r >= rows || src[r] >= 0) return;
     uint4* dst = reinterpret_cast<uint4*>(dy + ((int64_t)(r / C) * ldE + r % C) * M);
     for (int i = lane; i < nv; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
     return;
   }
-  const int t = blockIdx.x;
+  // tpt threads (a power of two >= 32) per token: a warp per token for narrow rows
+  const int grp = (int)threadIdx.x / tpt, gt = (int)threadIdx.x % tpt;
+  const int t = (int)blockIdx.x * tpc + grp;
+  const bool tok = t < T_;
   const T* g = dout + (int64_t)t * M;
   int64_t row[K];
   float wj[K], dot[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const int p = pos[(int64_t)t * K + j];
+    const int p = tok ? pos[(int64_t)t * K + j] : -1;
     row[j] = p < 0 ? -1 : ((int64_t)idx[(int64_t)t * K + j] * ldE + p) * M;
-    wj[j] = w[(int64_t)t * K + j];
+    wj[j] = tok ? w[(int64_t)t * K + j] : 0.f;
     dot[j] = 0.f;
   }
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+  for (int v = gt; tok && v < nv; v += tpt) {
     float gv[V];
     load16<T>(g + v * V, gv);
 #pragma unroll
@@ -608,11 +614,12 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
     if (lane == 0) red[warp][j] = d;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (gt == 0 && tok) {  // the token's warps in order (fixed: deterministic)
+    const int w0 = grp * (tpt >> 5), nw = tpt >> 5;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       float d = 0.f;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) d += red[i][j];
+      for (int i = w0; i < w0 + nw; ++i) d += red[i][j];
       dw[(int64_t)t * K + j] = row[j] < 0 ? 0.f : d;
     }
   }
@@ -622,13 +629,17 @@ template <int K>
 static void combine_bwd_launch(int dtype, const void* dout, const void* y, const int32_t* idx, const int32_t* pos,
                                const float* w, const int32_t* src, void* dy, float* dw, int T_, int M, int rows,
                                int C, int ldE, cudaStream_t s) {
-  dim3 grid(T_ + (rows + 7) / 8);
+  const int nv = M / (dtype == DT_F32 ? 4 : 8);
+  int tpt = 32;  // threads per token: enough 16-byte lanes for one pass over the row, <= 256
+  while (tpt < nv && tpt < 256) tpt *= 2;
+  const int tpc = 256 / tpt;
+  dim3 grid((T_ + tpc - 1) / tpc + (rows + 7) / 8);
   if (dtype == DT_F32)
     launch_k(combine_bwd_pack_kernel<float, K>, grid, 256, 0, s, (const float*)dout, (const float*)y, idx, pos, w,
-             src, (float*)dy, dw, T_, M, rows, C, ldE);
+             src, (float*)dy, dw, T_, M, rows, C, ldE, tpt);
   else
     launch_k(combine_bwd_pack_kernel<bf16, K>, grid, 256, 0, s, (const bf16*)dout, (const bf16*)y, idx, pos, w,
-             src, (bf16*)dy, dw, T_, M, rows, C, ldE);
+             src, (bf16*)dy, dw, T_, M, rows, C, ldE, tpt);
 }
 
 int combine_bwd_pack(int dtype, const void* dout, const void* y, const int32_t* idx,
