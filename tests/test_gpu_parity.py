@@ -41,6 +41,17 @@ CASES = {
     "bf16_ragged_seq_causal": BlockConfig(T=400, seq_len=200, M=128, n_heads=2, E=4, top_k=2,
                                           d_ffn=256, R=2, capacity_factor=1.0, causal=1, residual=1,
                                           P=1, dtype="bf16"),
+    # gate kernel variants: wide E with k up to 8 and an 8-CTA cluster split over M
+    # (peer slices pushed with st.async), E = 64, E = 2 with k = 1, and a chunk whose
+    # routing scan exceeds the per-thread register segment (T_r·k = 4096 slots)
+    "gate_e32_k8": BlockConfig(T=512, seq_len=128, M=512, n_heads=4, E=32, top_k=8, d_ffn=128, R=2,
+                               capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    "gate_e64_k4": BlockConfig(T=512, seq_len=128, M=256, n_heads=4, E=64, top_k=4, d_ffn=64, R=2,
+                               capacity_factor=1.5, causal=0, residual=1, P=1, dtype="bf16"),
+    "gate_e2_k1": BlockConfig(T=256, seq_len=64, M=256, n_heads=4, E=2, top_k=1, d_ffn=128, R=2,
+                              capacity_factor=1.0, causal=1, residual=0, P=1, dtype="bf16"),
+    "scan_wide_chunk": BlockConfig(T=4096, seq_len=256, M=128, n_heads=2, E=8, top_k=2, d_ffn=128, R=2,
+                                   capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
 }
 
 
@@ -102,7 +113,8 @@ def test_token_chunk_parity(name):
         assert np.array_equal(one[n], many[n]), n
 
 
-@pytest.mark.parametrize("name", ["c1_f32", "bf16_small", "c2_bench", "bf16_k3_dh128", "f32_k1"])
+@pytest.mark.parametrize("name", ["c1_f32", "bf16_small", "c2_bench", "bf16_k3_dh128", "f32_k1",
+                                  "gate_e32_k8", "gate_e64_k4", "gate_e2_k1", "scan_wide_chunk"])
 def test_routing_bitexact_given_gpu_logits(name):
     """Natural routing: the oracle routes from the GPU's own fp32 logits; indices,
     positions and per-chunk counts must match bit for bit, weights to fp32 rounding."""
