@@ -189,6 +189,28 @@ flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* ctx, const flowmoe_optimizer*
                                       float* state1, float* state2, const float* grad, void* weight, size_t n,
                                       cudaStream_t stream);
 
+/* ---- Model edges around the block stack ----
+ * Token embedding, forward: x[t][:] = table[ids[t]][:] for t < T; table [V][M] and x
+ * [T][M] in the config dtype, ids [T] int32 on the device; an id outside [0, V) gives a
+ * zero row (ids are not validated on the host).  Backward: dtable[v][:] += Σ_{t: ids[t]=v}
+ * dx[t][:] into an fp32 [V][M] gradient (ACCUMULATED, like flowmoe_grads), deterministic
+ * (tokens added in t order, one writer per element).  M is the config's model dim; M·size
+ * of the dtype must be a multiple of 16 bytes.  Errors: FLOWMOE_ERR_INVALID (NULL pointer,
+ * T < 0, V < 1) before anything is enqueued. */
+flowmoe_status flowmoe_embed_fwd(flowmoe_ctx* ctx, const void* table, int64_t V, const int32_t* ids, int64_t T,
+                                 void* x, cudaStream_t stream);
+flowmoe_status flowmoe_embed_bwd(flowmoe_ctx* ctx, const int32_t* ids, int64_t T, const void* dx, int64_t V,
+                                 float* dtable, cudaStream_t stream);
+
+/* Softmax cross-entropy over fp32 logits [T][V] with int32 labels [T] (label < 0 or >= V:
+ * row ignored).  losses [T] fp32 (caller scratch) receives lse_t - l_t[y_t]; loss [1] fp32
+ * (nullable) = scale · Σ_t losses[t]; dlogits [T][V] in the config dtype (nullable) =
+ * scale · (softmax(l_t) - onehot(y_t)).  The chunked loss of Eqs.(19)-(23) is the sum of
+ * per-chunk calls with scale = 1/T_total (reading Q18).  Deterministic (fixed-order
+ * reductions).  Errors: FLOWMOE_ERR_INVALID (NULL logits/labels/losses, T < 0, V < 1). */
+flowmoe_status flowmoe_xent(flowmoe_ctx* ctx, const float* logits, const int32_t* labels, int64_t T, int64_t V,
+                            float scale, float* losses, float* loss, void* dlogits, cudaStream_t stream);
+
 /* Per-tensor optimizer storage of the local experts, index 0..3 = w1, b1, w2, b2 (shapes of
  * flowmoe_params); weight[i] is the compute copy (the flowmoe_params pointer). */
 typedef struct {

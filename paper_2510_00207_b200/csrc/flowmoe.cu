@@ -1175,6 +1175,35 @@ flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* x, const flowmoe_optimizer* o
   return FLOWMOE_OK;
 }
 
+flowmoe_status flowmoe_embed_fwd(flowmoe_ctx* x, const void* table, int64_t V, const int32_t* ids, int64_t T,
+                                 void* out, cudaStream_t stream) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "embed_fwd: need T >= 0 and V >= 1");
+  if (T == 0) return FLOWMOE_OK;
+  if (!table || !ids || !out) return fail(FLOWMOE_ERR_INVALID, "embed_fwd: NULL pointer");
+  FM_K(1, embed_fwd(x->dt, table, ids, out, T, V, (int)x->M, stream));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_embed_bwd(flowmoe_ctx* x, const int32_t* ids, int64_t T, const void* dx, int64_t V,
+                                 float* dtable, cudaStream_t stream) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "embed_bwd: need T >= 0 and V >= 1");
+  if (T == 0) return FLOWMOE_OK;
+  if (!ids || !dx || !dtable) return fail(FLOWMOE_ERR_INVALID, "embed_bwd: NULL pointer");
+  FM_K(1, embed_bwd(x->dt, ids, dx, dtable, T, V, (int)x->M, stream));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_xent(flowmoe_ctx* x, const float* logits, const int32_t* labels, int64_t T, int64_t V,
+                            float scale, float* losses, float* loss, void* dlogits, cudaStream_t stream) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "xent: need T >= 0 and V >= 1");
+  if (T > 0 && (!logits || !labels || !losses)) return fail(FLOWMOE_ERR_INVALID, "xent: NULL logits/labels/losses");
+  FM_K(T > 0 ? 1 + (loss ? 1 : 0) : 0, xent(x->dt, logits, labels, T, V, scale, losses, loss, dlogits, stream));
+  return FLOWMOE_OK;
+}
+
 flowmoe_status flowmoe_expert_update(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step,
                                      const flowmoe_expert_opt* st, const flowmoe_grads* gr, flowmoe_ticket* done) {
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");

@@ -114,6 +114,14 @@ int colsum_acc(int dtype, const void* x, float* out, int batch, int rows, int N,
 int optim_step(int dtype, int kind, float lr, float b1, float b2, float eps, float wd, int64_t step, float* w,
                float* s1, float* s2, const float* g, void* out, int64_t n, cudaStream_t s);
 
+// Model edges (k_model.cu): token embedding and softmax cross-entropy.
+int embed_fwd(int dtype, const void* table, const int32_t* ids, void* x, int64_t T_, int64_t V, int M,
+              cudaStream_t s);
+int embed_bwd(int dtype, const int32_t* ids, const void* dx, float* dtable, int64_t T_, int64_t V, int M,
+              cudaStream_t s);
+int xent(int dtype, const float* logits, const int32_t* labels, int64_t T_, int64_t V, float scale, float* losses,
+         float* loss, void* dlogits, cudaStream_t s);
+
 // A2A over NVLink peer memory (k_p2p.cu): send (copy + publish) and/or wait for (kind, r).
 int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,
             unsigned int* my_flags, unsigned int* seen, unsigned int* err, int kind, int r, int R, int P,

@@ -23,7 +23,7 @@ SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "van
 EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
     "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
-    "flowmoe_optimizer_step", "flowmoe_expert_update",
+    "flowmoe_optimizer_step", "flowmoe_expert_update", "flowmoe_embed_fwd", "flowmoe_embed_bwd", "flowmoe_xent",
     "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
     "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
 ]
@@ -88,7 +88,7 @@ def lib() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise FlowMoEError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = ctypes.CDLL(LIB_PATH)
-    vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+    vp, sz, i32, u64, i64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64
     L.flowmoe_get_unique_id.argtypes = [ctypes.c_char_p]
     L.flowmoe_create.argtypes = [ctypes.POINTER(Config), ctypes.c_char_p, i32, ctypes.POINTER(vp)]
     L.flowmoe_saved_bytes.argtypes = [vp]
@@ -106,13 +106,15 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_optimizer_step.argtypes = [vp, ctypes.POINTER(Optimizer), ctypes.c_int64, vp, vp, vp, vp, vp, sz, vp]
     L.flowmoe_expert_update.argtypes = [vp, ctypes.POINTER(Optimizer), ctypes.c_int64, ctypes.POINTER(ExpertOpt),
                                         ctypes.POINTER(Grads), ctypes.POINTER(u64)]
+    L.flowmoe_embed_fwd.argtypes = [vp, vp, i64, vp, i64, vp, vp]
+    L.flowmoe_embed_bwd.argtypes = [vp, vp, i64, vp, i64, vp, vp]
+    L.flowmoe_xent.argtypes = [vp, vp, vp, i64, i64, ctypes.c_float, vp, vp, vp, vp]
     L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
     L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
     L.flowmoe_saved_routing_offsets.argtypes = [vp] + [ctypes.POINTER(sz)] * 5
     L.flowmoe_debug_set.argtypes = [i32, i32]
     L.flowmoe_kernel_launches.restype = u64
-    i64 = ctypes.c_int64
     L.flowmoe_test_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
                                     vp, i64, i64, i32, vp, vp, vp, vp]
     L.flowmoe_profile_end.argtypes = [ctypes.POINTER(ProfEntry), i32]
@@ -304,6 +306,23 @@ class FlowMoE:
         _check(lib().flowmoe_optimizer_step(self.handle, ctypes.byref(opt), step, _ptr(master), _ptr(state1),
                                             _ptr(state2), _ptr(grad), _ptr(weight), master.numel(),
                                             _stream_handle(stream)), "flowmoe_optimizer_step")
+
+    def embed_fwd(self, table, ids, x, stream=None):
+        """x[t] = table[ids[t]] (table [V][M], ids [T] int32, x [T][M], config dtype)."""
+        _check(lib().flowmoe_embed_fwd(self.handle, _ptr(table), table.shape[0], _ptr(ids), ids.numel(), _ptr(x),
+                                       _stream_handle(stream)), "flowmoe_embed_fwd")
+
+    def embed_bwd(self, ids, dx, dtable, stream=None):
+        """dtable[v] += sum of dx[t] over ids[t] == v (dtable fp32 [V][M], deterministic)."""
+        _check(lib().flowmoe_embed_bwd(self.handle, _ptr(ids), ids.numel(), _ptr(dx), dtable.shape[0], _ptr(dtable),
+                                       _stream_handle(stream)), "flowmoe_embed_bwd")
+
+    def xent(self, logits, labels, scale: float, losses, loss=None, dlogits=None, stream=None):
+        """Softmax cross-entropy of fp32 logits [T][V]: per-row losses, loss = scale·sum,
+        dlogits = scale·(softmax - onehot) in the config dtype (rows with label < 0 ignored)."""
+        T, V = logits.shape
+        _check(lib().flowmoe_xent(self.handle, _ptr(logits), _ptr(labels), T, V, scale, _ptr(losses), _ptr(loss),
+                                  _ptr(dlogits), _stream_handle(stream)), "flowmoe_xent")
 
     def expert_update(self, opt: "Optimizer", step: int, st: "ExpertOpt", grads: "Grads") -> int:
         """Expert update right behind the last enqueued backward's expert wgrads (P:1173);

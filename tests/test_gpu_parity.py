@@ -473,3 +473,49 @@ def test_expert_update_behind_backward():
         assert rel(master[n].double().cpu().numpy(), want) <= 1e-5, n
         assert torch.equal(bt.t[n], master[n].to(torch.bfloat16)), n
     ctx.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_embedding_and_xent_vs_oracle(dtype):
+    """Model edges through the C ABI: embedding gather (exact), its deterministic
+    scatter-add (several id tiles, repeated and out-of-range ids, accumulate mode) and
+    the softmax cross-entropy (ignored rows, ragged V) against oracle/model.py."""
+    import torch
+    from oracle.model import embed_backward, embed_forward, xent
+    from tests.gpu_util import shape_of
+    cfg = CASES["c1_f32"] if dtype == "f32" else CASES["bf16_small"]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    ctx = fm.FlowMoE(shape_of(cfg, 1, 0), 0, None)
+    rng = np.random.default_rng(21)
+    V, T, M = 1000, 3000, cfg.M
+    table = fm.to_device(rng.standard_normal((V, M)), dtype, dev)
+    ids_h = rng.integers(0, V, T).astype(np.int32)
+    ids_h[rng.integers(0, T, 40)] = 17          # a hot row
+    ids_h[[5, 2999]] = [-1, V + 3]              # out of range: zero rows, no gradient
+    ids = torch.from_numpy(ids_h).to(dev)
+    x = torch.empty((T, M), dtype=fm.torch_dtype(dtype), device=dev)
+    ctx.embed_fwd(table, ids, x)
+    dx = fm.to_device(rng.standard_normal((T, M)), dtype, dev)
+    dtab = torch.full((V, M), 0.5, dtype=torch.float32, device=dev)
+    ctx.embed_bwd(ids, dx, dtab)
+    Vx, T2 = 5000, 300
+    lg_h = rng.standard_normal((T2, Vx)) * 3
+    lab_h = rng.integers(0, Vx, T2).astype(np.int32)
+    lab_h[[0, 7, 299]] = -1
+    lg = torch.from_numpy(lg_h.astype(np.float32)).to(dev)
+    lab = torch.from_numpy(lab_h).to(dev)
+    losses = torch.empty(T2, dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    dl = torch.empty((T2, Vx), dtype=fm.torch_dtype(dtype), device=dev)
+    ctx.xent(lg, lab, 1.0 / T2, losses, loss, dl)
+    torch.cuda.synchronize()
+    ctx.close()
+    tab_h = fm.to_host_f64(table)
+    assert np.array_equal(fm.to_host_f64(x), embed_forward(tab_h, ids_h))
+    ref = embed_backward(ids_h, fm.to_host_f64(dx), V)
+    assert rel(dtab.cpu().numpy().astype(np.float64) - 0.5, ref) <= 1e-5
+    rl, rloss, rdl = xent(lg.cpu().numpy().astype(np.float64), lab_h, 1.0 / T2)
+    assert rel(losses.cpu().numpy().astype(np.float64), rl) <= 1e-5
+    assert abs(float(loss.item()) - rloss) <= 1e-5 * abs(rloss)
+    assert rel(fm.to_host_f64(dl), rdl) <= (1e-5 if dtype == "f32" else 1e-2)

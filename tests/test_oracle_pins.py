@@ -494,3 +494,71 @@ def test_sgd_momentum_two_steps_by_hand():
     w2, b2 = sgd_momentum_step(w1, b1, g2, lr=0.1, momentum=0.9, weight_decay=0.01, step=2)
     d2 = g2 + 0.01 * w1
     assert np.allclose(b2, 0.9 * d1 + d2) and np.allclose(w2, w1 - 0.1 * (0.9 * d1 + d2))
+
+
+# --------------------------------------------------------------- model edges (reading Q18)
+def test_xent_uniform_logits_is_log_vocab():
+    """Equal logits: every labelled token costs log V exactly, and the gradient row is
+    scale·(1/V − onehot)."""
+    from oracle.model import xent
+    T, V = 5, 7
+    labels = np.array([0, 3, -1, 6, 2])
+    losses, loss, dl = xent(np.full((T, V), 0.37), labels, 0.25)
+    assert np.allclose(losses[[0, 1, 3, 4]], np.log(V)) and losses[2] == 0.0
+    assert np.isclose(loss, 0.25 * 4 * np.log(V))
+    want = np.full(V, 0.25 / V)
+    want[3] -= 0.25
+    assert np.allclose(dl[1], want) and np.all(dl[2] == 0.0)
+
+
+def test_xent_gradient_by_finite_differences_and_shift_invariance():
+    from oracle.model import xent
+    rng = np.random.default_rng(5)
+    T, V, s = 3, 6, 0.5
+    lg = rng.standard_normal((T, V)) * 2
+    labels = np.array([4, 0, 5])
+    _, loss, dl = xent(lg, labels, s)
+    h = 1e-6
+    for t, v in [(0, 4), (1, 2), (2, 5), (2, 0)]:
+        p = lg.copy(); p[t, v] += h
+        m = lg.copy(); m[t, v] -= h
+        fd = (xent(p, labels, s)[1] - xent(m, labels, s)[1]) / (2 * h)
+        assert abs(fd - dl[t, v]) < 1e-8
+    # softmax is shift invariant per row; gradient rows sum to zero
+    assert np.isclose(xent(lg + np.array([[3.0], [-7.0], [0.5]]), labels, s)[1], loss)
+    assert np.allclose(dl.sum(axis=1), 0.0)
+
+
+def test_xent_chunked_losses_add_to_the_full_loss():
+    """Eqs.(19)-(23): R chunks with scale 1/B each sum to the full mean loss, and their
+    gradient rows are the full gradient's rows."""
+    from oracle.model import xent
+    rng = np.random.default_rng(9)
+    B, V, R = 12, 5, 4
+    lg = rng.standard_normal((B, V))
+    labels = rng.integers(0, V, B)
+    _, full, dfull = xent(lg, labels, 1.0 / B)
+    parts = [xent(lg[r * (B // R):(r + 1) * (B // R)],
+                  labels[r * (B // R):(r + 1) * (B // R)], 1.0 / B) for r in range(R)]
+    assert np.isclose(sum(p[1] for p in parts), full)
+    assert np.allclose(np.concatenate([p[2] for p in parts]), dfull)
+    # and the full loss is the plain mean of -log softmax at the label
+    p = np.exp(lg) / np.exp(lg).sum(axis=1, keepdims=True)
+    assert np.isclose(full, -np.mean(np.log(p[np.arange(B), labels])))
+
+
+def test_embedding_gather_and_scatter_brute_force():
+    from oracle.model import embed_backward, embed_forward
+    rng = np.random.default_rng(2)
+    V, M = 6, 4
+    table = rng.standard_normal((V, M))
+    ids = np.array([2, 5, 2, 0, 9, 2])  # a repeated id and an out-of-range one
+    x = embed_forward(table, ids)
+    assert np.array_equal(x[0], table[2]) and np.array_equal(x[1], table[5]) and np.all(x[4] == 0)
+    dx = rng.standard_normal((len(ids), M))
+    d = embed_backward(ids, dx, V)
+    assert np.allclose(d[2], dx[0] + dx[2] + dx[5]) and np.allclose(d[0], dx[3])
+    assert np.all(d[[1, 3, 4]] == 0)
+    # adjoint identity <embed(table), dx> = <table, embed_backward(dx)> over in-range ids
+    keep = ids < V
+    assert np.isclose(np.sum(embed_forward(table, ids)[keep] * dx[keep]), np.sum(table * d))
