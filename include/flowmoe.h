@@ -211,6 +211,17 @@ flowmoe_status flowmoe_embed_bwd(flowmoe_ctx* ctx, const int32_t* ids, int64_t T
 flowmoe_status flowmoe_xent(flowmoe_ctx* ctx, const float* logits, const int32_t* labels, int64_t T, int64_t V,
                             float scale, float* losses, float* loss, void* dlogits, cudaStream_t stream);
 
+/* LM head (the projection between the last block and flowmoe_xent), tcgen05 GEMMs:
+ * forward logits[T][V] (fp32) = h[T][M] · W[V][M]ᵀ; backward dh[T][M] = dlogits[T][V] · W
+ * (config dtype, overwritten; nullable) and dW[V][M] += dlogitsᵀ · h (fp32, ACCUMULATED;
+ * nullable).  h, W and dlogits in the config dtype, row-major, M = the config's model dim;
+ * V must be a positive multiple of 8 (16-byte TMA strides).  Errors: FLOWMOE_ERR_INVALID
+ * before anything is enqueued. */
+flowmoe_status flowmoe_lm_head_fwd(flowmoe_ctx* ctx, const void* h, const void* w, int64_t T, int64_t V,
+                                   float* logits, cudaStream_t stream);
+flowmoe_status flowmoe_lm_head_bwd(flowmoe_ctx* ctx, const void* h, const void* w, const void* dlogits, int64_t T,
+                                   int64_t V, void* dh, float* dw, cudaStream_t stream);
+
 /* Per-tensor optimizer storage of the local experts, index 0..3 = w1, b1, w2, b2 (shapes of
  * flowmoe_params); weight[i] is the compute copy (the flowmoe_params pointer). */
 typedef struct {

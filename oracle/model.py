@@ -53,3 +53,13 @@ def xent(logits: np.ndarray, labels: np.ndarray, scale: float):
         p[y] -= 1.0
         dl[t] = scale * p
     return losses, scale * losses.sum(), dl
+
+
+def lm_head_forward(h: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """logits[t][v] = Σ_m h[t][m]·W[v][m] (the projection feeding the loss)."""
+    return h @ w.T
+
+
+def lm_head_backward(h: np.ndarray, w: np.ndarray, dlogits: np.ndarray):
+    """dh = dlogits·W, dW = dlogitsᵀ·h (the two adjoints of the projection)."""
+    return dlogits @ w, dlogits.T @ h

@@ -1204,6 +1204,51 @@ flowmoe_status flowmoe_xent(flowmoe_ctx* x, const float* logits, const int32_t* 
   return FLOWMOE_OK;
 }
 
+static flowmoe_status check_lm(const flowmoe_ctx* x, int64_t T, int64_t V) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (T < 0 || V < 8 || V % 8 != 0 || T > INT32_MAX || V > INT32_MAX)
+    return fail(FLOWMOE_ERR_INVALID, "lm_head: need 0 <= T < 2^31 and V a positive multiple of 8 (< 2^31)");
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_lm_head_fwd(flowmoe_ctx* x, const void* h, const void* w, int64_t T, int64_t V, float* logits,
+                                   cudaStream_t stream) {
+  if (flowmoe_status st = check_lm(x, T, V)) return st;
+  if (T == 0) return FLOWMOE_OK;
+  if (!h || !w || !logits) return fail(FLOWMOE_ERR_INVALID, "lm_head_fwd: NULL pointer");
+  GemmArgs g;  // logits[T][V] = h[T][M] · W[V][M]ᵀ (W is K-major for this product)
+  g.M = (int)T; g.N = (int)V; g.K = (int)x->M;
+  g.A = h; g.lda = x->M;
+  g.B = w; g.ldb = x->M; g.b_kmajor = 1;
+  g.C = logits; g.ldc = V; g.epi = EPI_STORE_F32;
+  FM_K(1, gemm(g, x->dt, stream));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_lm_head_bwd(flowmoe_ctx* x, const void* h, const void* w, const void* dlogits, int64_t T,
+                                   int64_t V, void* dh, float* dw, cudaStream_t stream) {
+  if (flowmoe_status st = check_lm(x, T, V)) return st;
+  if (T == 0) return FLOWMOE_OK;
+  if (!dlogits || (dh && !w) || (dw && !h)) return fail(FLOWMOE_ERR_INVALID, "lm_head_bwd: NULL pointer");
+  if (dh) {
+    GemmArgs g;  // dh[T][M] = dlogits[T][V] · W[V][M]
+    g.M = (int)T; g.N = (int)x->M; g.K = (int)V;
+    g.A = dlogits; g.lda = V;
+    g.B = w; g.ldb = x->M;
+    g.C = dh; g.ldc = x->M; g.epi = EPI_STORE;
+    FM_K(1, gemm(g, x->dt, stream));
+  }
+  if (dw) {
+    GemmArgs g;  // dW[V][M] += dlogitsᵀ · h  (dlogits is M-major for this product)
+    g.M = (int)V; g.N = (int)x->M; g.K = (int)T;
+    g.A = dlogits; g.lda = V; g.a_mmajor = 1;
+    g.B = h; g.ldb = x->M;
+    g.C = dw; g.ldc = x->M; g.epi = EPI_ACC_F32;
+    FM_K(1, gemm(g, x->dt, stream));
+  }
+  return FLOWMOE_OK;
+}
+
 flowmoe_status flowmoe_expert_update(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step,
                                      const flowmoe_expert_opt* st, const flowmoe_grads* gr, flowmoe_ticket* done) {
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");

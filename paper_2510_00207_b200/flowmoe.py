@@ -24,6 +24,7 @@ EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
     "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
     "flowmoe_optimizer_step", "flowmoe_expert_update", "flowmoe_embed_fwd", "flowmoe_embed_bwd", "flowmoe_xent",
+    "flowmoe_lm_head_fwd", "flowmoe_lm_head_bwd",
     "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
     "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
 ]
@@ -109,6 +110,8 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_embed_fwd.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.flowmoe_embed_bwd.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.flowmoe_xent.argtypes = [vp, vp, vp, i64, i64, ctypes.c_float, vp, vp, vp, vp]
+    L.flowmoe_lm_head_fwd.argtypes = [vp, vp, vp, i64, i64, vp, vp]
+    L.flowmoe_lm_head_bwd.argtypes = [vp, vp, vp, vp, i64, i64, vp, vp, vp]
     L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
     L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
@@ -323,6 +326,17 @@ class FlowMoE:
         T, V = logits.shape
         _check(lib().flowmoe_xent(self.handle, _ptr(logits), _ptr(labels), T, V, scale, _ptr(losses), _ptr(loss),
                                   _ptr(dlogits), _stream_handle(stream)), "flowmoe_xent")
+
+    def lm_head_fwd(self, h, w, logits, stream=None):
+        """logits [T][V] fp32 = h [T][M] · w [V][M]ᵀ."""
+        _check(lib().flowmoe_lm_head_fwd(self.handle, _ptr(h), _ptr(w), h.shape[0], w.shape[0], _ptr(logits),
+                                         _stream_handle(stream)), "flowmoe_lm_head_fwd")
+
+    def lm_head_bwd(self, h, w, dlogits, dh=None, dw=None, stream=None):
+        """dh = dlogits · w (overwritten), dw += dlogitsᵀ · h (fp32)."""
+        _check(lib().flowmoe_lm_head_bwd(self.handle, _ptr(h), _ptr(w), _ptr(dlogits), dlogits.shape[0],
+                                         dlogits.shape[1], _ptr(dh), _ptr(dw), _stream_handle(stream)),
+               "flowmoe_lm_head_bwd")
 
     def expert_update(self, opt: "Optimizer", step: int, st: "ExpertOpt", grads: "Grads") -> int:
         """Expert update right behind the last enqueued backward's expert wgrads (P:1173);

@@ -519,3 +519,40 @@ def test_embedding_and_xent_vs_oracle(dtype):
     assert rel(losses.cpu().numpy().astype(np.float64), rl) <= 1e-5
     assert abs(float(loss.item()) - rloss) <= 1e-5 * abs(rloss)
     assert rel(fm.to_host_f64(dl), rdl) <= (1e-5 if dtype == "f32" else 1e-2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_lm_head_and_loss_chain_vs_oracle(dtype):
+    """h -> logits (LM head) -> cross-entropy -> dlogits -> dh, dW through the C ABI,
+    against oracle/model.py on the same device-rounded inputs (ragged T, V = 5000)."""
+    import torch
+    from oracle.model import lm_head_backward, lm_head_forward, xent
+    from tests.gpu_util import shape_of
+    cfg = CASES["c1_f32"] if dtype == "f32" else CASES["bf16_small"]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    ctx = fm.FlowMoE(shape_of(cfg, 1, 0), 0, None)
+    rng = np.random.default_rng(33)
+    T, V, M = 300, 5000, cfg.M
+    h = fm.to_device(rng.standard_normal((T, M)), dtype, dev)
+    w = fm.to_device(rng.standard_normal((V, M)) / np.sqrt(M), dtype, dev)
+    lab = torch.from_numpy(rng.integers(0, V, T).astype(np.int32)).to(dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    logits = torch.empty((T, V), **f32)
+    ctx.lm_head_fwd(h, w, logits)
+    losses, loss = torch.empty(T, **f32), torch.empty(1, **f32)
+    dl = torch.empty((T, V), dtype=fm.torch_dtype(dtype), device=dev)
+    ctx.xent(logits, lab, 1.0 / T, losses, loss, dl)
+    dh = torch.empty((T, M), dtype=fm.torch_dtype(dtype), device=dev)
+    dw = torch.full((V, M), 0.25, **f32)
+    ctx.lm_head_bwd(h, w, dl, dh, dw)
+    torch.cuda.synchronize()
+    ctx.close()
+    tol = TOL[dtype]
+    hh, wh, dlh = fm.to_host_f64(h), fm.to_host_f64(w), fm.to_host_f64(dl)
+    assert rel(logits.cpu().numpy().astype(np.float64), lm_head_forward(hh, wh)) <= (1e-5 if dtype == "f32" else 1e-3)
+    _, rloss, _ = xent(logits.cpu().numpy().astype(np.float64), lab.cpu().numpy(), 1.0 / T)
+    assert abs(float(loss.item()) - rloss) <= 1e-5 * abs(rloss)
+    rdh, rdw = lm_head_backward(hh, wh, dlh)
+    assert rel(fm.to_host_f64(dh), rdh) <= tol
+    assert rel(dw.cpu().numpy().astype(np.float64) - 0.25, rdw) <= (1e-4 if dtype == "f32" else 1e-3)

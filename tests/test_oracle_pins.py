@@ -562,3 +562,17 @@ def test_embedding_gather_and_scatter_brute_force():
     # adjoint identity <embed(table), dx> = <table, embed_backward(dx)> over in-range ids
     keep = ids < V
     assert np.isclose(np.sum(embed_forward(table, ids)[keep] * dx[keep]), np.sum(table * d))
+
+
+def test_lm_head_brute_force_and_adjoints():
+    from oracle.model import lm_head_backward, lm_head_forward
+    rng = np.random.default_rng(4)
+    T, M, V = 3, 4, 5
+    h, w, g = rng.standard_normal((T, M)), rng.standard_normal((V, M)), rng.standard_normal((T, V))
+    lg = lm_head_forward(h, w)
+    for t in range(T):
+        for v in range(V):
+            assert np.isclose(lg[t, v], sum(h[t, m] * w[v, m] for m in range(M)))
+    dh, dw = lm_head_backward(h, w, g)
+    # <lm_head(h), g> = <h, dh> = <w, dw> (both adjoints)
+    assert np.isclose(np.sum(lg * g), np.sum(h * dh)) and np.isclose(np.sum(lg * g), np.sum(w * dw))
