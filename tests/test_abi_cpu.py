@@ -87,3 +87,21 @@ def test_sass_has_tcgen05_and_tma():
     if not out:
         pytest.skip("cuobjdump unavailable")
     assert "UTCHMMA" in out and "UTMALDG" in out and "LDTM" in out
+
+
+def test_model_edge_calls_validate_before_any_cuda_call():
+    """The model-edge and optimizer entry points reject a NULL ctx / bad sizes with
+    FLOWMOE_ERR_INVALID and a message, touching nothing (no GPU needed)."""
+    L = fm.lib()
+    bad = [
+        ("flowmoe_embed_fwd", (None, None, 10, None, 4, None, None)),
+        ("flowmoe_embed_bwd", (None, None, 4, None, 10, None, None)),
+        ("flowmoe_xent", (None, None, None, 4, 10, ctypes.c_float(1.0), None, None, None, None)),
+        ("flowmoe_lm_head_fwd", (None, None, None, 4, 16, None, None)),
+        ("flowmoe_lm_head_bwd", (None, None, None, None, 4, 16, None, None, None)),
+        ("flowmoe_optimizer_step", (None, None, 1, None, None, None, None, None, 0, None)),
+    ]
+    for name, args in bad:
+        rc = getattr(L, name)(*args)
+        assert rc == 1, name  # FLOWMOE_ERR_INVALID
+        assert b"ctx is NULL" in L.flowmoe_last_error(), name
