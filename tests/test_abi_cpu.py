@@ -105,3 +105,28 @@ def test_model_edge_calls_validate_before_any_cuda_call():
         rc = getattr(L, name)(*args)
         assert rc == 1, name  # FLOWMOE_ERR_INVALID
         assert b"ctx is NULL" in L.flowmoe_last_error(), name
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the extension absent the binding raises on first use."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import paper_2510_00207_b200 as fm\n"
+            "from paper_2510_00207_b200.flowmoe import FlowMoEError\n"
+            "try:\n    fm.lib()\nexcept FlowMoEError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, FLOWMOE_LIB=str(tmp_path / "absent.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert "RAISED" in out.stdout and "missing" in out.stdout, out.stdout + out.stderr
+
+
+def test_product_package_never_touches_the_oracle():
+    """The oracle is test infrastructure: nothing under the package imports or runs it."""
+    pkg = os.path.dirname(os.path.abspath(fm.__file__))
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), f
+                assert not re.search(r"(import_module|spec_from_file_location|CDLL|subprocess)\(.*oracle", src), f
