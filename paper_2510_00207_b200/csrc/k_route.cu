@@ -23,7 +23,7 @@ namespace fm {
 // Phase probe (tools/probe/gate_probe.cu builds this file with -DFM_PROBE): clock64
 // stamps of the gate kernel's phases in CTA 0 (slots 0-7) and in the scanning CTA (8-15).
 #ifdef FM_PROBE
-__device__ long long g_gprobe[16];
+__device__ long long g_gprobe[24];
 #define FM_GMARK(i) do { if (threadIdx.x == 0) g_gprobe[i] = clock64(); } while (0)
 #else
 #define FM_GMARK(i) do {} while (0)
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < EG; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
   for (int m = m_beg + warp * V; m < m_end; m += 8 * V) {
     float xa[4][V];
 #pragma unroll
@@ -192,8 +193,10 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
     if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(6);
   }
   __syncthreads();
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(16);
   for (int q = threadIdx.x; q < TB * E; q += blockDim.x)
     if (tt0 + q / E < T_) logits[(int64_t)tt0 * E + q] = red[q];
+  if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(17);
   if (threadIdx.x < TB && tt0 + (int)threadIdx.x < T_) {
     const int t = tt0 + threadIdx.x;
     float lg[E];
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
         idx[(int64_t)t * k + j] = best;
       }
     }
+    if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(18);
     if (k == 1) {
       // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
       float den = 0.f;

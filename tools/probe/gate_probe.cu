@@ -39,8 +39,9 @@ static void run(const char* name, int T, int M, int E, int k, int C) {
   cudaEventElapsedTime(&ms, e0, e1);
   gate_route(DT_BF16, a, wg, nullptr, logits, idx, w, pos, counts, src, done, T, M, E, k, C, s);
   cudaStreamSynchronize(s);
-  long long g[16];
+  long long g[24];
   cudaMemcpyFromSymbol(g, g_gprobe, sizeof(g));
+  printf("  topk phase: sync %lld logits %lld select %lld\n", g[16] - g[0], g[17] - g[0], g[18] - g[0]);
   printf("%-6s T=%d M=%d E=%d: back-to-back %.2f us | cta0: pdl %lld gemv %lld part %lld cs1 %lld cs2 %lld topk %lld fence %lld ticket %lld | scan cta: init %lld pass1 %lld scan %lld pass2 %lld (%s)\n",
          name, T, M, E, ms * 1000.f / 200, g[1] - g[0], g[2] - g[0], g[4] - g[0], g[5] - g[0], g[6] - g[0], g[7] - g[0], g[13] - g[0], g[3] - g[0], g[9] - g[8],
          g[10] - g[9], g[11] - g[10], g[12] - g[11], cudaGetErrorString(cudaGetLastError()));
@@ -54,6 +55,9 @@ int main() {
   run("c2ks2", 256, 256, 8, 2, 64);
   g_gate_force_ks = 0;
   run("c3", 1024, 1024, 16, 2, 128);
+  g_gate_force_ks = 2;
+  run("c3ks2", 1024, 1024, 16, 2, 128);
+  g_gate_force_ks = 0;
   run("c4", 1024, 4096, 16, 2, 128);
   return 0;
 }
