@@ -327,10 +327,10 @@ def main():
     torch.cuda.synchronize()
 
     # per-kernel live timing (eager iteration, CUDA events on each kernel's own stream)
-    fm.profile_begin()
+    ctx.profile_begin()
     for _ in range(2):
         iteration(stream)
-    prof = fm.profile_end()
+    prof = ctx.profile_end()
     for p in prof:
         p["launches"] //= 2
         p["ms"] /= 2

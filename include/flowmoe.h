@@ -143,7 +143,9 @@ flowmoe_status flowmoe_block_fwd(flowmoe_ctx* ctx, const flowmoe_params* params,
                                  void* y, void* saved, cudaStream_t stream);
 
 /* Backward of one block given dy [B][M]: dx [B][M] (nullable: skipped), grads
- * accumulated (+=).  Compute order Eq.(5) (E_R..E_1, AT_R..AT_1), A2A order
+ * accumulated (+=).  `x` is the block's forward input [B][M] (the same pointer passed to
+ * block_fwd; read by the deferred dWqkv = xᵀ·dQKV GEMM) — an extension of SURVEY §8(b)'s
+ * signature, which would otherwise have to copy x into `saved` (B·M more bytes per block).  Compute order Eq.(5) (E_R..E_1, AT_R..AT_1), A2A order
  * Eq.(6).  The AR of grad_flat is auto-submitted in chunks of `chunk_bytes`
  * (S_p; positive multiple of 16; >= bytes => one chunk; last chunk is the
  * remainder) at priority 1 as soon as the grads are final
@@ -247,58 +249,34 @@ flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* ctx, float* buf, size_t cou
                                         size_t chunk_bytes, int priority, cudaEvent_t ready,
                                         flowmoe_ticket* out);
 
-/* Make `stream` wait for every chunk of the ticket's all-reduce; polls NCCL async errors. */
+/* Make `stream` wait for every chunk of the ticket's all-reduce; polls NCCL async errors.
+ * FLOWMOE_ERR_STATE for an unknown / expired ticket. */
 flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* ctx, flowmoe_ticket ticket, cudaStream_t stream);
+
+/* Peer-memory A2A (a2a_impl = FLOWMOE_A2A_P2P, world_size > 1): map a `saved` stash into
+ * every peer (CUDA IPC).  Collective: every rank registers its stashes in the same order,
+ * outside CUDA-graph capture, before the first flowmoe_block_fwd / stack_fwd that uses them;
+ * the exchange is all-or-nothing (either every rank maps every peer or every rank gets
+ * FLOWMOE_ERR_CUDA and the stash uses the NCCL path on all ranks).  A registered stash must
+ * stay allocated until flowmoe_unregister_saved (or destroy): the peers keep writing into it.
+ * Registering the same pointer again is a no-op; world_size == 1 or NCCL A2A: no-op.
+ * A stash never registered is registered on first use (same rules; during capture it uses
+ * NCCL).  unregister: local; synchronises the device, then closes this rank's mappings of
+ * the peers' stashes (call it on every rank before freeing the stash anywhere). */
+flowmoe_status flowmoe_register_saved(flowmoe_ctx* ctx, const void* saved);
+flowmoe_status flowmoe_unregister_saved(flowmoe_ctx* ctx, const void* saved);
+
+/* Health of the asynchronous exchange machinery, for callers that replay CUDA graphs (where
+ * no host-side check runs): FLOWMOE_ERR_STATE / FLOWMOE_ERR_CUDA if a peer-memory A2A wait
+ * timed out (~10-20 s without a peer's arrival; the waiting kernel then traps, faulting the
+ * context, so consumers never read stale buffers), FLOWMOE_ERR_NCCL on an asynchronous NCCL
+ * error.  Host-synchronous (reads one word from the device). */
+flowmoe_status flowmoe_check_health(flowmoe_ctx* ctx);
 
 /* Test hook: force the top-k indices ([B][k] int32 device array, distinct
  * experts per row) instead of selecting them; gate weights are still computed
  * from the logits at those indices.  NULL restores normal routing. */
 flowmoe_status flowmoe_set_forced_routing(flowmoe_ctx* ctx, const int32_t* idx);
-
-/* Byte offsets inside `saved` of the fp32 gate logits [B][E], indices [B][k]
- * int32, gate weights [B][k] fp32, positions [B][k] int32 (-1 = dropped) and
- * per-chunk counts [R][E] int32 (test inspection of routing). */
-flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* logits, size_t* idx,
-                                             size_t* w, size_t* pos, size_t* counts);
-
-/* Test/benchmark knobs: key 1 = force the SIMT GEMM for bf16 (debug), key 2 =
- * swap MN-major descriptor strides (debug), key 3 = force the SIMT attention
- * kernels for bf16 (debug / A-B comparison), key 4 = programmatic dependent
- * launch on (1, default) / off (0), key 5 = force the GEMM tile width (64/128/256;
- * 0 = automatic), key 6 = peer-memory A2A of chunk r on chunk r's compute lane (1,
- * default) / on the A2A stream (0).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
-flowmoe_status flowmoe_debug_set(int key, int value);
-
-/* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,
- * fp32 SIMT for F32).  C(m,n) = epi(sum_k A(m,k) B(k,n)) per batch b, with
- * A(m,k) = A[b*sA + m*lda + k] (a_mmajor=0) or A[b*sA + k*lda + m] (a_mmajor=1),
- * B(k,n) = B[b*sB + k*ldb + n] (b_kmajor=0) or B[b*sB + n*ldb + k] (b_kmajor=1).
- * epi: 0 store (+bias[n] +resid), 1 bias+GELU (aux = pre-activation),
- * 2 times GELU'(aux), 3 fp32 accumulate C += acc, 4 fp32 store, 5 bias+GELU with
- * aux = GELU'(pre-activation), 6 times aux.  bias/resid/aux nullable;
- * resid and aux share C's ld/stride, bias has stride N per batch. */
-flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch, const void* A,
-                                 int64_t lda, int64_t sA, int a_mmajor, const void* B, int64_t ldb,
-                                 int64_t sB, int b_kmajor, void* C, int64_t ldc, int64_t sC, int epi,
-                                 const void* bias, const void* resid, void* aux, cudaStream_t stream);
-
-/* Per-kernel device timing (bench.py's live roofline).  Between begin and end,
- * every kernel / NCCL call the library enqueues outside CUDA-graph capture is
- * bracketed by timing events on its own stream.  end synchronises the device
- * and writes one entry per kernel kind that ran: launches, summed device ms,
- * summed algorithmic FLOPs and HBM (or bus) bytes.  While profiling, the
- * compute lanes are collapsed onto one stream so every duration is the
- * kernel's own.  Returns the number of entries written, or -1 on error. */
-typedef struct {
-  const char* name;   /* static string owned by the library */
-  int64_t launches;
-  double ms, flops, bytes;
-} flowmoe_prof_entry;
-flowmoe_status flowmoe_profile_begin(void);
-int flowmoe_profile_end(flowmoe_prof_entry* out, int max_entries);
-
-/* Number of kernels this library has launched in the calling process (bench accounting). */
-uint64_t flowmoe_kernel_launches(void);
 
 const char* flowmoe_status_string(flowmoe_status s);
 const char* flowmoe_last_error(void); /* thread-local message of the last failing call */

@@ -1,0 +1,84 @@
+/* flowmoe_test.h — test, inspection and benchmark hooks of libflowmoe.so.
+ *
+ * NOT part of the product ABI (include/flowmoe.h): these calls exist so the parity tests
+ * (tests/) and bench.py can look inside the block (routing decisions in the `saved` stash),
+ * drive single kernels, time kernels, and simulate several ranks on one GPU.  Same
+ * conventions as flowmoe.h (return codes, thread-local message, nothing throws).  Knobs and
+ * profiles are per ctx: they are installed into the kernel modules at the start of each
+ * enqueueing call of that ctx (not thread-safe across ctxs driven from several threads).
+ */
+#ifndef FLOWMOE_TEST_H
+#define FLOWMOE_TEST_H
+
+#include "flowmoe.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Byte offsets inside `saved` of the fp32 gate logits [B][E], indices [B][k]
+ * int32, gate weights [B][k] fp32, positions [B][k] int32 (-1 = dropped) and
+ * per-chunk counts [R][E] int32 (test inspection of routing). */
+flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* logits, size_t* idx,
+                                             size_t* w, size_t* pos, size_t* counts);
+
+/* Per-ctx test/benchmark knobs: key 1 = force the SIMT GEMM for bf16 (debug), key 2 =
+ * swap MN-major descriptor strides (debug), key 3 = force the SIMT attention
+ * kernels for bf16 (debug / A-B comparison), key 4 = programmatic dependent
+ * launch on (1, default) / off (0), key 5 = force the GEMM tile width (64/128/256;
+ * 0 = automatic), key 6 = peer-memory A2A of chunk r on chunk r's compute lane (1,
+ * default) / on the A2A stream (0).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
+flowmoe_status flowmoe_debug_set(flowmoe_ctx* ctx, int key, int value);
+
+/* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,
+ * fp32 SIMT for F32), with ctx's knobs and profile (ctx nullable: library defaults).
+ * C(m,n) = epi(sum_k A(m,k) B(k,n)) per batch b, with
+ * A(m,k) = A[b*sA + m*lda + k] (a_mmajor=0) or A[b*sA + k*lda + m] (a_mmajor=1),
+ * B(k,n) = B[b*sB + k*ldb + n] (b_kmajor=0) or B[b*sB + n*ldb + k] (b_kmajor=1).
+ * epi: 0 store (+bias[n] +resid), 1 bias+GELU (aux = pre-activation),
+ * 2 times GELU'(aux), 3 fp32 accumulate C += acc, 4 fp32 store, 5 bias+GELU with
+ * aux = GELU'(pre-activation), 6 times aux.  bias/resid/aux nullable;
+ * resid and aux share C's ld/stride, bias has stride N per batch. */
+flowmoe_status flowmoe_test_gemm(flowmoe_ctx* ctx, int dtype, int M, int N, int K, int batch, const void* A,
+                                 int64_t lda, int64_t sA, int a_mmajor, const void* B, int64_t ldb,
+                                 int64_t sB, int b_kmajor, void* C, int64_t ldc, int64_t sC, int epi,
+                                 const void* bias, const void* resid, void* aux, cudaStream_t stream);
+
+/* Per-kernel device timing of one ctx.  Between begin and end, every kernel / NCCL
+ * call the library enqueues for that ctx outside CUDA-graph capture is
+ * bracketed by timing events on its own stream.  end synchronises the device
+ * and writes one entry per kernel kind that ran: launches, summed device ms,
+ * summed algorithmic FLOPs and HBM (or bus) bytes.  While profiling, the
+ * compute lanes are collapsed onto one stream so every duration is the
+ * kernel's own.  Returns the number of entries written, or -1 on error. */
+typedef struct {
+  const char* name;   /* static string owned by the library */
+  int64_t launches;
+  double ms, flops, bytes;
+} flowmoe_prof_entry;
+flowmoe_status flowmoe_profile_begin(flowmoe_ctx* ctx);
+int flowmoe_profile_end(flowmoe_ctx* ctx, flowmoe_prof_entry* out, int max_entries);
+
+/* Number of kernels this library has launched in the calling process (bench accounting). */
+uint64_t flowmoe_kernel_launches(void);
+
+/* In-process simulated world for one-GPU tests of the exchange rows (S6/S8/B1/B3 peer-
+ * memory A2A kernels and arrival counters, B6 S_p chunking of the all-reduce): P ctxs
+ * (2 <= P <= 8; out[P]) of world_size P, ranks 0..P-1, on ONE device, peers' buffers mapped
+ * as plain device pointers (a2a_impl forced to P2P; no NCCL).  The all-reduce of a
+ * submission runs once every rank made its matching submission: the P ranks' buffers are
+ * summed chunk by chunk (the same S_p partition as the NCCL path) in rank order on a group
+ * stream and the sum is written back to every rank; flowmoe_allreduce_wait on a ticket whose
+ * peers have not submitted yet returns FLOWMOE_ERR_STATE.  Each rank must register its
+ * `saved` stashes (flowmoe_register_saved) before the first forward.  Enqueue each phase
+ * for all ranks before waiting (the ranks' kernels wait for each other on the device), and
+ * give the process >= 4 + P·(R + 3) hardware queues (CUDA_DEVICE_MAX_CONNECTIONS=32) so the
+ * ranks' streams never share one.  Schedules FLOWMOE and FLOWMOE_AR only (the centralized-AR
+ * policies flush inside allreduce_wait, before the other ranks could submit).  Destroy every
+ * member with flowmoe_destroy; each drains the device first. */
+flowmoe_status flowmoe_create_local_group(const flowmoe_config* cfg, int P, int device, flowmoe_ctx** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWMOE_TEST_H */

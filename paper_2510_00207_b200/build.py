@@ -36,7 +36,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     nccl = nccl_dir()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        [os.path.join(ROOT, "include", "flowmoe.h")]
+        [os.path.join(ROOT, "include", "flowmoe.h"), os.path.join(ROOT, "include", "flowmoe_test.h")]
     hdr_mtime = max(os.path.getmtime(h) for h in hdrs)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

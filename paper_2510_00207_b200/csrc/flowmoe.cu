@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 #include <atomic>
@@ -22,6 +23,7 @@
 #include <cuda.h>
 
 #include "../../include/flowmoe.h"
+#include "../../include/flowmoe_test.h"
 #include "kernels.h"
 
 using namespace fm;
@@ -51,9 +53,61 @@ struct SavedLayout {
   size_t qkv, ctx, lse, a, logits, idx, w, pos, counts, src, send, xe, z, h, ye, yc, dye, total;
 };
 
+// ---- per-kernel profiling (eager mode only; bench.py's live roofline) ----
+enum KKind {
+  KK_QKV, KK_ATTN_F, KK_OPROJ, KK_GATE, KK_ROUTE, KK_PACK, KK_E1, KK_E2, KK_COMBINE,
+  KK_CBPACK, KK_DGELU, KK_DW2, KK_DB2, KK_DW1, KK_DB1, KK_DXE, KK_GATHER, KK_DCTX, KK_ATTN_B,
+  KK_DX, KK_DWG, KK_DWO, KK_DWQKV, KK_A2A_D, KK_A2A_C, KK_A2A_CB, KK_A2A_DB, KK_AR, KK_TEST, KK_COUNT
+};
+const char* KK_NAMES[KK_COUNT] = {
+  "gemm_qkv", "attn_fwd", "gemm_oproj", "gate_topk", "route_scan", "permute_pack",
+  "gemm_expert1_gelu", "gemm_expert2", "unpermute_combine", "combine_bwd_pack", "gemm_expert_dgelu",
+  "gemm_expert_dw2", "colsum_db2", "gemm_expert_dw1", "colsum_db1", "gemm_expert_dx",
+  "gather_gate_bwd", "gemm_dctx", "attn_bwd", "gemm_dx", "gate_wgrad", "gemm_dwo", "gemm_dwqkv",
+  "a2a_dispatch", "a2a_combine", "a2a_combine_bwd", "a2a_dispatch_bwd", "allreduce_chunk", "test_gemm"};
+struct ProfRec { int kind; int ev; double flops, bytes; };
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<ProfRec> recs;
+};
+// the profile of the ctx whose call is being enqueued (apply_ctx); null = off
+thread_local Prof* g_prof = nullptr;
+
+int prof_start(cudaStream_t s) {
+  if (!g_prof || !g_prof->on) return -1;
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+  Prof& pr = *g_prof;
+  while (pr.pool.size() < pr.used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    pr.pool.push_back(e);
+  }
+  int i = (int)pr.used;
+  pr.used += 2;
+  cudaEventRecord(pr.pool[i], s);
+  return i;
+}
+void prof_stop(int i, int kind, double flops, double bytes, cudaStream_t s) {
+  if (i < 0 || !g_prof) return;
+  cudaEventRecord(g_prof->pool[i + 1], s);
+  g_prof->recs.push_back({kind, i, flops, bytes});
+}
+#define FM_KP(kind, nk, fl, by, strm, call)            \
+  do {                                                  \
+    int pi_ = prof_start(strm);                         \
+    FM_K(nk, call);                                     \
+    prof_stop(pi_, kind, (double)(fl), (double)(by), strm); \
+  } while (0)
+
+
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
+
+struct LocalGroup;
 
 struct flowmoe_ctx {
   flowmoe_config cfg;
@@ -111,11 +165,42 @@ struct flowmoe_ctx {
   std::vector<unsigned int*> peer_flags; // per rank: its flags array (mapped)
   std::vector<void*> peer_dxc;           // per rank: its dispatch-bwd receive buffer (mapped)
   std::map<const void*, std::vector<void*>> peer_saved;  // my saved ptr -> each rank's saved ptr
+  std::map<const void*, std::vector<void*>> saved_opened;  // my saved ptr -> peer mappings opened for it
   std::vector<void*> ipc_opened;         // peer mappings to close at destroy
+  void* xchg = nullptr;                  // device scratch of the registration collectives
   // scheduling policy (flowmoe_schedule): AT split into R subtasks? AR chunked per block?
   bool at_split = true, ar_pipelined = true;
   struct PendingAR { float* buf; size_t count; uint64_t ticket; };
   std::vector<PendingAR> pending_ar;  // centralized-AR policies: flushed at allreduce_wait
+  // per-ctx test/benchmark knobs (flowmoe_test.h) and per-kernel profile, applied to the
+  // kernel modules by apply_ctx() at the start of every enqueueing call
+  int dbg_flags = 0, pdl = 1, force_bn = 0, p2p_on_lane = 1;
+  Prof prof;
+  // saved stashes registered for peer-memory A2A, in registration order (collective)
+  std::vector<const void*> saved_order;
+  // in-process simulated world (flowmoe_create_local_group): P ctxs on one device
+  LocalGroup* group = nullptr;
+};
+
+// In-process simulated world (flowmoe_create_local_group, include/flowmoe_test.h): P ctxs
+// of world_size P on ONE device, so the exchange rows (S6, S8, B1, B3: the peer-memory A2A
+// kernels and their arrival counters; B6: the S_p chunk loop of the all-reduce) run on a
+// one-GPU box.  Peers' buffers are plain device pointers.  The all-reduce of a submission
+// is enqueued once every rank has made its matching submission: it sums the P ranks'
+// buffers chunk by chunk (same S_p partition as the NCCL path) in rank order on the
+// group's stream and writes the sum back to every rank.
+struct LocalGroup {
+  int P = 0;
+  std::vector<flowmoe_ctx*> m;                   // members by rank (null once destroyed)
+  std::vector<std::vector<const void*>> saved;   // registered stashes per rank, in order
+  cudaStream_t s = nullptr;
+  struct Sub { float* buf; size_t count, chunk_bytes; cudaEvent_t ready; };
+  std::vector<std::vector<Sub>> subs;            // per rank, AR submissions in order
+  std::vector<std::map<uint64_t, size_t>> ticket_sub;  // per rank: ticket -> its last submission
+  std::vector<std::map<uint64_t, size_t>> ticket_done;  // per rank: enqueued tickets
+  size_t done = 0;                               // submissions enqueued (same index on every rank)
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -141,51 +226,16 @@ namespace {
                                         cudaGetErrorString((cudaError_t)e_));              \
   } while (0)
 
-// ---- per-kernel profiling (eager mode only; bench.py's live roofline) ----
-enum KKind {
-  KK_QKV, KK_ATTN_F, KK_OPROJ, KK_GATE, KK_ROUTE, KK_PACK, KK_E1, KK_E2, KK_COMBINE,
-  KK_CBPACK, KK_DGELU, KK_DW2, KK_DB2, KK_DW1, KK_DB1, KK_DXE, KK_GATHER, KK_DCTX, KK_ATTN_B,
-  KK_DX, KK_DWG, KK_DWO, KK_DWQKV, KK_A2A_D, KK_A2A_C, KK_A2A_CB, KK_A2A_DB, KK_AR, KK_TEST, KK_COUNT
-};
-const char* KK_NAMES[KK_COUNT] = {
-  "gemm_qkv", "attn_fwd", "gemm_oproj", "gate_topk", "route_scan", "permute_pack",
-  "gemm_expert1_gelu", "gemm_expert2", "unpermute_combine", "combine_bwd_pack", "gemm_expert_dgelu",
-  "gemm_expert_dw2", "colsum_db2", "gemm_expert_dw1", "colsum_db1", "gemm_expert_dx",
-  "gather_gate_bwd", "gemm_dctx", "attn_bwd", "gemm_dx", "gate_wgrad", "gemm_dwo", "gemm_dwqkv",
-  "a2a_dispatch", "a2a_combine", "a2a_combine_bwd", "a2a_dispatch_bwd", "allreduce_chunk", "test_gemm"};
-struct ProfRec { int kind; int ev; double flops, bytes; };
-struct Prof {
-  bool on = false;
-  std::vector<cudaEvent_t> pool;
-  size_t used = 0;
-  std::vector<ProfRec> recs;
-} g_prof;
-
-int prof_start(cudaStream_t s) {
-  if (!g_prof.on) return -1;
-  cudaStreamCaptureStatus cs;
-  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
-  while (g_prof.pool.size() < g_prof.used + 2) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return -1;
-    g_prof.pool.push_back(e);
-  }
-  int i = (int)g_prof.used;
-  g_prof.used += 2;
-  cudaEventRecord(g_prof.pool[i], s);
-  return i;
+// Install the ctx's knobs and profile into the (process-global) kernel modules for the
+// call being enqueued; every enqueueing entry point calls this first.
+void apply_ctx(flowmoe_ctx* x) {
+  if (!x) return;
+  gemm_tc_set_debug(x->dbg_flags);
+  gemm_tc_force_bn(x->force_bn);
+  g_pdl_enabled = x->pdl;
+  g_p2p_on_lane = x->p2p_on_lane;
+  g_prof = &x->prof;
 }
-void prof_stop(int i, int kind, double flops, double bytes, cudaStream_t s) {
-  if (i < 0) return;
-  cudaEventRecord(g_prof.pool[i + 1], s);
-  g_prof.recs.push_back({kind, i, flops, bytes});
-}
-#define FM_KP(kind, nk, fl, by, strm, call)            \
-  do {                                                  \
-    int pi_ = prof_start(strm);                         \
-    FM_K(nk, call);                                     \
-    prof_stop(pi_, kind, (double)(fl), (double)(by), strm); \
-  } while (0)
 
 // GEMM with its algorithmic work: 2·M·N·K flops; bytes = A + B + C (+C read for fp32 accumulate)
 flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStream_t s) {
@@ -358,67 +408,113 @@ flowmoe_status join_lanes(flowmoe_ctx* x, cudaStream_t dst) {
   return FLOWMOE_OK;
 }
 
+// broadcast: every other compute lane waits for the work enqueued so far on `src`
+flowmoe_status lanes_follow(flowmoe_ctx* x, cudaStream_t src) {
+  FM_CUDA(cudaEventRecord(x->ev_in, src));
+  for (cudaStream_t l : x->lanes)
+    if (l != src) FM_CUDA(cudaStreamWaitEvent(l, x->ev_in, 0));
+  return FLOWMOE_OK;
+}
+
 // ---- CUDA-IPC exchange over the A2A communicator (outside graph capture only)
 typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 struct IpcRec {
   cudaIpcMemHandle_t h;
   uint64_t offset;
+  int32_t ok;  // 0: this rank could not export the allocation (every rank then fails)
 };
 
 // every rank publishes (handle of the allocation containing `ptr`, offset of ptr in it);
-// returns each rank's view pointer (own = ptr)
-flowmoe_status ipc_exchange(flowmoe_ctx* x, void* ptr, std::vector<void*>* out) {
+// returns each rank's view pointer (own = ptr).  Collective over the A2A communicator and
+// all-or-nothing: a rank that cannot export or open a handle still takes part in both
+// agreement rounds, so either every rank maps every peer or every rank reports failure
+// (and all of them fall back to NCCL together) — no rank is left waiting in a collective.
+flowmoe_status ipc_exchange(flowmoe_ctx* x, void* ptr, std::vector<void*>* out, std::vector<void*>* opened_out) {
   static PFN_getAddressRange get_range = nullptr;
   if (!get_range) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-      return fail(FLOWMOE_ERR_CUDA, "cuMemGetAddressRange unavailable");
-    get_range = reinterpret_cast<PFN_getAddressRange>(fn);
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+      get_range = reinterpret_cast<PFN_getAddressRange>(fn);
   }
   // quiesce: earlier NCCL work of this communicator (any stream) must be done on every
   // rank before the exchange collective (eager path, once per registered buffer)
   FM_CUDA(cudaDeviceSynchronize());
+  IpcRec mine;
+  memset(&mine, 0, sizeof(mine));
   CUdeviceptr base = 0;
   size_t size = 0;
-  if (get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
-    return fail(FLOWMOE_ERR_CUDA, "cuMemGetAddressRange failed");
-  IpcRec mine;
-  FM_CUDA(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)));
-  mine.offset = (uint64_t)((CUdeviceptr)ptr - base);
+  if (get_range && get_range(&base, &size, (CUdeviceptr)ptr) == CUDA_SUCCESS &&
+      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    mine.offset = (uint64_t)((CUdeviceptr)ptr - base);
+    mine.ok = 1;
+  }
+  cudaGetLastError();  // a failed export is reported through the agreement, not here
   const int P = (int)x->P;
-  IpcRec* d = nullptr;
-  FM_CUDA(cudaMalloc(&d, sizeof(IpcRec) * (P + 1)));
+  IpcRec* d = reinterpret_cast<IpcRec*>(x->xchg);
   FM_CUDA(cudaMemcpy(d + P, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice));
   FM_NCCL(ncclAllGather(d + P, d, sizeof(IpcRec), ncclUint8, x->comm_a2a, x->s_comp));
   FM_CUDA(cudaStreamSynchronize(x->s_comp));
   std::vector<IpcRec> all(P);
   FM_CUDA(cudaMemcpy(all.data(), d, sizeof(IpcRec) * P, cudaMemcpyDeviceToHost));
-  cudaFree(d);
+  bool ok = true;
+  for (const IpcRec& r : all) ok = ok && r.ok;
+  std::vector<void*> opened;
   out->assign(P, nullptr);
-  for (int q = 0; q < P; ++q) {
+  for (int q = 0; q < P && ok; ++q) {
     if (q == x->cfg.rank) { (*out)[q] = ptr; continue; }
     void* pb = nullptr;
-    FM_CUDA(cudaIpcOpenMemHandle(&pb, all[q].h, cudaIpcMemLazyEnablePeerAccess));
-    x->ipc_opened.push_back(pb);
+    if (cudaIpcOpenMemHandle(&pb, all[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      break;
+    }
+    opened.push_back(pb);
     (*out)[q] = reinterpret_cast<char*>(pb) + all[q].offset;
   }
+  // second round: did every rank open every peer?
+  int32_t* flag = reinterpret_cast<int32_t*>(d + P + 1);
+  const int32_t mine_ok = ok ? 1 : 0;
+  FM_CUDA(cudaMemcpy(flag, &mine_ok, sizeof(int32_t), cudaMemcpyHostToDevice));
+  FM_NCCL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, x->comm_a2a, x->s_comp));
+  FM_CUDA(cudaStreamSynchronize(x->s_comp));
+  int32_t all_ok = 0;
+  FM_CUDA(cudaMemcpy(&all_ok, flag, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (!all_ok) {
+    for (void* pb : opened) cudaIpcCloseMemHandle(pb);
+    out->clear();
+    return fail(FLOWMOE_ERR_CUDA, "peer-memory registration failed on some rank (CUDA IPC export/open)");
+  }
+  for (void* pb : opened) opened_out->push_back(pb);
   return FLOWMOE_OK;
 }
 
-// P2P usable for this `saved` buffer?  Registers it (collectively) on first sight; a buffer
-// first seen during graph capture uses NCCL (every rank sees the same sequence of calls).
-bool p2p_ready(flowmoe_ctx* x, const void* saved, cudaStream_t stream) {
-  if (!x->p2p) return false;
-  if (x->peer_saved.count(saved)) return true;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(stream, &cs);
-  if (cs != cudaStreamCaptureStatusNone) return false;
-  std::vector<void*> v;
-  if (ipc_exchange(x, const_cast<void*>(saved), &v) != FLOWMOE_OK) return false;
-  x->peer_saved[saved] = v;
-  return true;
+flowmoe_status register_saved(flowmoe_ctx* x, const void* saved);
+
+// Peer-memory A2A for this `saved` stash?  *use = true when every rank's stash is mapped.
+// A stash that was not registered (flowmoe_register_saved) is registered here on first
+// sight, collectively, outside graph capture; during capture it uses NCCL (every rank sees
+// the same sequence of calls, so every rank decides the same).  The in-process simulated
+// world has no NCCL: there every stash must be registered on all ranks first.
+flowmoe_status resolve_p2p(flowmoe_ctx* x, const void* saved, cudaStream_t stream, bool* use) {
+  *use = false;
+  if (x->P == 1 || !x->p2p) return FLOWMOE_OK;
+  if (x->peer_saved.count(saved)) { *use = true; return FLOWMOE_OK; }
+  if (!x->group) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return FLOWMOE_OK;
+    if (register_saved(x, saved) != FLOWMOE_OK) return FLOWMOE_OK;  // all ranks failed: NCCL
+    *use = x->peer_saved.count(saved) > 0;
+    return FLOWMOE_OK;
+  }
+  if (flowmoe_status st = register_saved(x, saved)) return st;
+  *use = x->peer_saved.count(saved) > 0;
+  if (!*use)
+    return fail(FLOWMOE_ERR_STATE, "local group: saved stash not registered on every rank "
+                                   "(call flowmoe_register_saved on each rank before the first block_fwd)");
+  return FLOWMOE_OK;
 }
 
 template <typename P_>
@@ -428,23 +524,86 @@ const P_* at(const void* base, size_t off) {
   return reinterpret_cast<const P_*>(reinterpret_cast<const char*>(base) + off);
 }
 
-flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_bytes,
-                         cudaEvent_t ready) {
-  if (ready) FM_CUDA(cudaStreamWaitEvent(x->s_ar, ready, 0));
-  if (x->P == 1 || count == 0) return FLOWMOE_OK;
+// The S_p partition of Alg. 2 PARTITION: chunks of chunk_bytes/4 floats, the
+// last one the remainder.  Shared by the NCCL path and the simulated world.
+template <typename F_>
+flowmoe_status for_each_ar_chunk(size_t count, size_t chunk_bytes, F_&& f) {
   const size_t chunk = chunk_bytes / 4;
   for (size_t off = 0; off < count; off += chunk) {
     const size_t n = (count - off < chunk) ? count - off : chunk;
-    int pi = prof_start(x->s_ar);
-    FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
-    prof_stop(pi, KK_AR, 0, 4.0 * n * 2.0 * (x->P - 1) / x->P, x->s_ar);
+    if (flowmoe_status st = f(off, n)) return st;
   }
   return FLOWMOE_OK;
 }
 
+// simulated world: enqueue every submission index that all ranks have reached
+flowmoe_status group_flush(LocalGroup* g) {
+  while (true) {
+    for (int q = 0; q < g->P; ++q)
+      if (g->subs[q].size() <= g->done) return FLOWMOE_OK;
+    const size_t n = g->done;
+    const LocalGroup::Sub& s0 = g->subs[0][n];
+    float* bufs[8] = {};
+    for (int q = 0; q < g->P; ++q) {
+      const LocalGroup::Sub& sq = g->subs[q][n];
+      if (sq.count != s0.count || sq.chunk_bytes != s0.chunk_bytes)
+        return fail(FLOWMOE_ERR_STATE, "local group: all-reduce submissions differ across ranks");
+      FM_CUDA(cudaStreamWaitEvent(g->s, sq.ready, 0));
+      bufs[q] = sq.buf;
+    }
+    flowmoe_ctx* x0 = g->m[0];
+    if (flowmoe_status st = for_each_ar_chunk(s0.count, s0.chunk_bytes, [&](size_t off, size_t cnt) {
+          int pi = prof_start(g->s);
+          FM_K(1, local_allreduce(bufs, g->P, (int64_t)off, (int64_t)cnt, g->s));
+          prof_stop(pi, KK_AR, 0, 4.0 * cnt * 2.0 * (g->P - 1) / g->P, g->s);
+          return FLOWMOE_OK;
+        }))
+      return st;
+    (void)x0;
+    for (int q = 0; q < g->P; ++q)
+      for (auto& kv : g->ticket_sub[q])
+        if (kv.second == n) {
+          FM_CUDA(cudaEventRecord(g->m[q]->ticket_ev[kv.first % NUM_TICKET_EVENTS], g->s));
+          g->ticket_done[q][kv.first] = n;
+        }
+    g->done = n + 1;
+  }
+}
+
+flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_bytes,
+                         cudaEvent_t ready) {
+  if (ready) FM_CUDA(cudaStreamWaitEvent(x->s_ar, ready, 0));
+  if (x->P == 1 || count == 0) return FLOWMOE_OK;
+  if (LocalGroup* g = x->group) {
+    // snapshot the readiness (the caller's event may be re-recorded by the next block)
+    if (g->ev_used == g->ev_pool.size()) {
+      cudaEvent_t e;
+      FM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      g->ev_pool.push_back(e);
+    }
+    cudaEvent_t e = g->ev_pool[g->ev_used++];
+    FM_CUDA(cudaEventRecord(e, x->s_ar));
+    g->subs[x->cfg.rank].push_back({buf, count, chunk_bytes, e});
+    return group_flush(g);
+  }
+  return for_each_ar_chunk(count, chunk_bytes, [&](size_t off, size_t n) {
+    int pi = prof_start(x->s_ar);
+    FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
+    prof_stop(pi, KK_AR, 0, 4.0 * n * 2.0 * (x->P - 1) / x->P, x->s_ar);
+    return FLOWMOE_OK;
+  });
+}
+
 flowmoe_status new_ticket(flowmoe_ctx* x, flowmoe_ticket* out) {
   const uint64_t t = x->next_ticket++;
-  FM_CUDA(cudaEventRecord(x->ticket_ev[t % NUM_TICKET_EVENTS], x->s_ar));
+  LocalGroup* g = x->group;
+  const int rk = x->cfg.rank;
+  if (g && !g->subs[rk].empty() && g->subs[rk].size() > g->done) {
+    g->ticket_sub[rk][t] = g->subs[rk].size() - 1;  // recorded when that submission is enqueued
+  } else {
+    // simulated world: this rank's all-reduces so far are on the group's stream
+    FM_CUDA(cudaEventRecord(x->ticket_ev[t % NUM_TICKET_EVENTS], g ? g->s : x->s_ar));
+  }
   if (out) *out = t;
   return FLOWMOE_OK;
 }
@@ -470,37 +629,42 @@ const char* flowmoe_last_error(void) { return g_err.c_str(); }
 
 uint64_t flowmoe_kernel_launches(void) { return g_launches.load(); }
 
-flowmoe_status flowmoe_debug_set(int key, int value) {
-  static int flags = 0;
-  if (key == 1) flags = (flags & ~1) | (value ? 1 : 0);
-  else if (key == 2) flags = (flags & ~2) | (value ? 2 : 0);
-  else if (key == 3) flags = (flags & ~4) | (value ? 4 : 0);
-  else if (key == 4) { g_pdl_enabled = value ? 1 : 0; return FLOWMOE_OK; }
-  else if (key == 5) { gemm_tc_force_bn(value); return FLOWMOE_OK; }
-  else if (key == 6) { g_p2p_on_lane = value ? 1 : 0; return FLOWMOE_OK; }
+flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (key == 1) x->dbg_flags = (x->dbg_flags & ~1) | (value ? 1 : 0);
+  else if (key == 2) x->dbg_flags = (x->dbg_flags & ~2) | (value ? 2 : 0);
+  else if (key == 3) x->dbg_flags = (x->dbg_flags & ~4) | (value ? 4 : 0);
+  else if (key == 4) x->pdl = value ? 1 : 0;
+  else if (key == 5) x->force_bn = value;
+  else if (key == 6) x->p2p_on_lane = value ? 1 : 0;
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
-  gemm_tc_set_debug(flags);
   return FLOWMOE_OK;
 }
 
-flowmoe_status flowmoe_profile_begin(void) {
-  g_prof.recs.clear();
-  g_prof.used = 0;
-  g_prof.on = true;
+flowmoe_status flowmoe_profile_begin(flowmoe_ctx* x) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  x->prof.recs.clear();
+  x->prof.used = 0;
+  x->prof.on = true;
   return FLOWMOE_OK;
 }
 
-int flowmoe_profile_end(flowmoe_prof_entry* out, int max_entries) {
-  g_prof.on = false;
+int flowmoe_profile_end(flowmoe_ctx* x, flowmoe_prof_entry* out, int max_entries) {
+  if (!x) {
+    fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+    return -1;
+  }
+  Prof& pr = x->prof;
+  pr.on = false;
   if (cudaDeviceSynchronize() != cudaSuccess) {
     fail(FLOWMOE_ERR_CUDA, "flowmoe_profile_end: device synchronize failed");
     return -1;
   }
   std::vector<flowmoe_prof_entry> agg(KK_COUNT);
   for (int i = 0; i < KK_COUNT; ++i) agg[i] = {KK_NAMES[i], 0, 0.0, 0.0, 0.0};
-  for (const ProfRec& r : g_prof.recs) {
+  for (const ProfRec& r : pr.recs) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, g_prof.pool[r.ev], g_prof.pool[r.ev + 1]);
+    cudaEventElapsedTime(&ms, pr.pool[r.ev], pr.pool[r.ev + 1]);
     agg[r.kind].launches += 1;
     agg[r.kind].ms += ms;
     agg[r.kind].flops += r.flops;
@@ -509,8 +673,8 @@ int flowmoe_profile_end(flowmoe_prof_entry* out, int max_entries) {
   int n = 0;
   for (int i = 0; i < KK_COUNT; ++i)
     if (agg[i].launches > 0 && n < max_entries && out) out[n++] = agg[i];
-  g_prof.recs.clear();
-  g_prof.used = 0;
+  pr.recs.clear();
+  pr.used = 0;
   return n;
 }
 
@@ -523,14 +687,25 @@ flowmoe_status flowmoe_get_unique_id(uint8_t id[128]) {
   return FLOWMOE_OK;
 }
 
-flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], int device,
-                              flowmoe_ctx** out) {
+}  // extern "C"
+
+namespace {
+int ar_max_ctas() {
+  const char* e = getenv("FLOWMOE_AR_MAX_CTAS");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : 16;
+}
+
+// `g` non-null: a member of the in-process simulated world (no NCCL; peers wired later)
+flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int device, LocalGroup* g,
+                           flowmoe_ctx** out) {
   if (!out) return fail(FLOWMOE_ERR_INVALID, "out is NULL");
   *out = nullptr;
   if (flowmoe_status s = validate(cfg)) return s;
-  if (cfg->world_size > 1 && !id) return fail(FLOWMOE_ERR_INVALID, "id is NULL with world_size > 1");
+  if (cfg->world_size > 1 && !id && !g) return fail(FLOWMOE_ERR_INVALID, "id is NULL with world_size > 1");
   auto* x = new flowmoe_ctx();
   x->cfg = *cfg;
+  x->group = g;
   // VANILLA_EP treats the block as one chunk (R = 1); PIPE_MOE and FLOWMOE_AR keep the
   // MHA+gate task AT unsplit; only FLOWMOE_AR and FLOWMOE pipeline the AR (Table 6)
   if (cfg->schedule == FLOWMOE_SCHED_VANILLA_EP) x->cfg.R = 1;
@@ -630,52 +805,177 @@ flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], 
   if (x->P == 1) x->dxc = x->dxe;
   if (x->dt == DT_BF16 && gemm_tc_init() != 0)
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable"));
-  if (x->P > 1) {
+  if (x->P > 1 && !g) {
+    if (!alloc(&x->xchg, (x->P + 2) * sizeof(IpcRec)))
+      return cleanup_fail(fail(FLOWMOE_ERR_OOM, "workspace allocation failed"));
     ncclUniqueId u;
     memcpy(&u, id, 128);
     ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
     nc.blocking = 1;
     if (ncclCommInitRankConfig(&x->comm_a2a, (int)x->P, u, cfg->rank, &nc) != ncclSuccess)
       return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommInitRankConfig failed"));
+    // the AR communicator runs in the gaps of the compute: cap its CTAs so a long AR chunk
+    // never takes more than a few SMs from the compute lanes
     ncclConfig_t nc2 = NCCL_CONFIG_INITIALIZER;
     nc2.blocking = 1;
+    nc2.maxCTAs = ar_max_ctas();
     if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &x->comm_ar, &nc2) != ncclSuccess)
       return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit failed"));
     x->a2a_comm.push_back(x->comm_a2a);
-    x->a2a_stream.push_back(x->s_a2a);
-    if (cfg->a2a_impl == FLOWMOE_A2A_P2P) {
-      const size_t nfl = (size_t)4 * x->cfg.R * x->P;
-      const size_t bytes = (2 * nfl + 8 * x->cfg.R + 1) * sizeof(unsigned int);
-      if (!alloc(&x->p2p_arena, bytes) || cudaMemset(x->p2p_arena, 0, bytes) != cudaSuccess ||
-          cudaDeviceSynchronize() != cudaSuccess)
-        return cleanup_fail(fail(FLOWMOE_ERR_OOM, "p2p arena allocation failed"));
-      x->flags = reinterpret_cast<unsigned int*>(x->p2p_arena);
-      x->piece_cnt = x->flags + nfl;
-      x->seen = x->piece_cnt + nfl;
-      x->p2p_err = x->seen + 4 * x->cfg.R;
-      x->grid_cnt = x->p2p_err + 1;
+  }
+  if (x->P > 1) x->a2a_stream.push_back(x->s_a2a);
+  if (x->P > 1 && (g || cfg->a2a_impl == FLOWMOE_A2A_P2P)) {
+    const size_t nfl = (size_t)4 * x->cfg.R * x->P;
+    const size_t bytes = (2 * nfl + 8 * x->cfg.R + 1) * sizeof(unsigned int);
+    if (!alloc(&x->p2p_arena, bytes) || cudaMemset(x->p2p_arena, 0, bytes) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return cleanup_fail(fail(FLOWMOE_ERR_OOM, "p2p arena allocation failed"));
+    x->flags = reinterpret_cast<unsigned int*>(x->p2p_arena);
+    x->piece_cnt = x->flags + nfl;
+    x->seen = x->piece_cnt + nfl;
+    x->p2p_err = x->seen + 4 * x->cfg.R;
+    x->grid_cnt = x->p2p_err + 1;
+    if (!g) {
       std::vector<void*> v;
-      if (ipc_exchange(x, x->p2p_arena, &v) != FLOWMOE_OK)
+      if (ipc_exchange(x, x->p2p_arena, &v, &x->ipc_opened) != FLOWMOE_OK)
         return cleanup_fail(FLOWMOE_ERR_CUDA);
       for (void* q : v) x->peer_flags.push_back(reinterpret_cast<unsigned int*>(q));
-      if (ipc_exchange(x, x->dxc, &x->peer_dxc) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
+      if (ipc_exchange(x, x->dxc, &x->peer_dxc, &x->ipc_opened) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
       x->p2p = true;
     }
-    // A2A lanes (NCCL path only: the peer-memory exchanges run on the compute lanes)
-    for (size_t l = 1; l < x->lanes.size() && !x->p2p; ++l) {
-      ncclConfig_t nc3 = NCCL_CONFIG_INITIALIZER;
-      nc3.blocking = 1;
-      ncclComm_t c2 = nullptr;
-      cudaStream_t s2 = nullptr;
-      if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &c2, &nc3) != ncclSuccess)
-        return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit (A2A lane) failed"));
-      x->a2a_comm.push_back(c2);
-      if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))
-        return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
-      x->a2a_stream.push_back(s2);
-    }
+  }
+  // A2A lanes (NCCL path only: the peer-memory exchanges run on the compute lanes)
+  for (size_t l = 1; l < x->lanes.size() && x->P > 1 && !x->p2p && !g; ++l) {
+    ncclConfig_t nc3 = NCCL_CONFIG_INITIALIZER;
+    nc3.blocking = 1;
+    ncclComm_t c2 = nullptr;
+    cudaStream_t s2 = nullptr;
+    if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &c2, &nc3) != ncclSuccess)
+      return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit (A2A lane) failed"));
+    x->a2a_comm.push_back(c2);
+    if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))
+      return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "stream creation failed"));
+    x->a2a_stream.push_back(s2);
   }
   *out = x;
+  return FLOWMOE_OK;
+}
+
+// collective registration of one saved stash (NCCL world: CUDA-IPC exchange with
+// agreement; simulated world: record it, peers resolved once every rank registered)
+flowmoe_status register_saved(flowmoe_ctx* x, const void* saved) {
+  if (x->P == 1 || !x->p2p || x->peer_saved.count(saved)) return FLOWMOE_OK;
+  if (LocalGroup* g = x->group) {
+    auto& mine = g->saved[x->cfg.rank];
+    size_t n = 0;
+    while (n < mine.size() && mine[n] != saved) ++n;
+    if (n == mine.size()) mine.push_back(saved);
+    for (int q = 0; q < g->P; ++q)
+      if (g->saved[q].size() <= n) return FLOWMOE_OK;  // resolved when the last rank registers
+    for (int q = 0; q < g->P; ++q) {  // every rank's n-th stash is now known
+      std::vector<void*> v(g->P);
+      for (int q2 = 0; q2 < g->P; ++q2) v[q2] = const_cast<void*>(g->saved[q2][n]);
+      g->m[q]->peer_saved[g->saved[q][n]] = v;
+    }
+    return FLOWMOE_OK;
+  }
+  std::vector<void*> v, opened;
+  if (flowmoe_status st = ipc_exchange(x, const_cast<void*>(saved), &v, &opened)) return st;
+  x->peer_saved[saved] = v;
+  x->saved_opened[saved] = opened;
+  x->saved_order.push_back(saved);
+  return FLOWMOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+flowmoe_status flowmoe_create(const flowmoe_config* cfg, const uint8_t id[128], int device,
+                              flowmoe_ctx** out) {
+  return create_impl(cfg, id, device, nullptr, out);
+}
+
+flowmoe_status flowmoe_register_saved(flowmoe_ctx* x, const void* saved) {
+  if (!x || !saved) return fail(FLOWMOE_ERR_INVALID, "register_saved: NULL argument");
+  return register_saved(x, saved);
+}
+
+flowmoe_status flowmoe_unregister_saved(flowmoe_ctx* x, const void* saved) {
+  if (!x || !saved) return fail(FLOWMOE_ERR_INVALID, "unregister_saved: NULL argument");
+  if (x->group) return fail(FLOWMOE_ERR_UNSUPPORTED, "unregister_saved: not supported in a local group");
+  auto it = x->saved_opened.find(saved);
+  if (it != x->saved_opened.end()) {
+    FM_CUDA(cudaDeviceSynchronize());  // no enqueued exchange may still target the mapping
+    for (void* pb : it->second) cudaIpcCloseMemHandle(pb);
+    x->saved_opened.erase(it);
+  }
+  x->peer_saved.erase(saved);
+  for (size_t i = 0; i < x->saved_order.size(); ++i)
+    if (x->saved_order[i] == saved) { x->saved_order.erase(x->saved_order.begin() + i); break; }
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_check_health(flowmoe_ctx* x) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  if (x->p2p_err) {
+    unsigned int e = 0;
+    if (cudaMemcpy(&e, x->p2p_err, sizeof(e), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(FLOWMOE_ERR_CUDA, std::string("device fault (a peer-memory A2A wait that timed out traps): ") +
+                                        cudaGetErrorString(cudaGetLastError()));
+    if (e) return fail(FLOWMOE_ERR_STATE, "peer-memory A2A timed out waiting for a peer");
+  }
+  ncclResult_t a = ncclSuccess;
+  for (ncclComm_t c : x->a2a_comm) {
+    ncclResult_t e = ncclSuccess;
+    if (c) ncclCommGetAsyncError(c, &e);
+    if (e != ncclSuccess) a = e;
+  }
+  if (x->comm_ar) {
+    ncclResult_t e = ncclSuccess;
+    ncclCommGetAsyncError(x->comm_ar, &e);
+    if (e != ncclSuccess) a = e;
+  }
+  if (a != ncclSuccess) return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a));
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_create_local_group(const flowmoe_config* cfg, int P, int device, flowmoe_ctx** out) {
+  if (!cfg || !out) return fail(FLOWMOE_ERR_INVALID, "create_local_group: NULL argument");
+  if (P < 2 || P > 8) return fail(FLOWMOE_ERR_INVALID, "create_local_group: P must be in [2, 8]");
+  if (cfg->schedule != FLOWMOE_SCHED_FLOWMOE && cfg->schedule != FLOWMOE_SCHED_FLOWMOE_AR)
+    return fail(FLOWMOE_ERR_UNSUPPORTED, "create_local_group: only the per-block (pipelined) AR schedules");
+  for (int q = 0; q < P; ++q) out[q] = nullptr;
+  auto* g = new LocalGroup();
+  g->P = P;
+  g->m.assign(P, nullptr);
+  g->saved.resize(P);
+  g->subs.resize(P);
+  g->ticket_sub.resize(P);
+  g->ticket_done.resize(P);
+  for (int q = 0; q < P; ++q) {
+    flowmoe_config c = *cfg;
+    c.world_size = P;
+    c.rank = q;
+    c.a2a_impl = FLOWMOE_A2A_P2P;
+    flowmoe_status st = create_impl(&c, nullptr, device, g, &out[q]);
+    if (st) {
+      const std::string msg = g_err;
+      for (int q2 = 0; q2 < q; ++q2) flowmoe_destroy(out[q2]);
+      return fail(st, msg);
+    }
+    g->m[q] = out[q];
+  }
+  for (int q = 0; q < P; ++q) {
+    flowmoe_ctx* x = out[q];
+    for (int q2 = 0; q2 < P; ++q2) {
+      x->peer_flags.push_back(out[q2]->flags);
+      x->peer_dxc.push_back(out[q2]->dxc);
+    }
+    x->p2p = true;
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  FM_CUDA(cudaStreamCreateWithPriority(&g->s, cudaStreamNonBlocking, lo));
   return FLOWMOE_OK;
 }
 
@@ -721,10 +1021,15 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   const SavedLayout& L = x->L;
   // the per-kernel profile (flowmoe_profile_begin) collapses the lanes so that each
   // kernel's event-timed duration is its own, not shared with co-running chunks
-  const int nl = g_prof.on ? 1 : (int)x->lanes.size();
-  const bool use_p2p = P > 1 && p2p_ready(x, saved, stream);
+  const int nl = x->prof.on ? 1 : (int)x->lanes.size();
+  bool use_p2p = false;
+  if (flowmoe_status st = resolve_p2p(x, saved, stream, &use_p2p)) return st;
   if (fork)
     if (flowmoe_status st = fork_lanes(x, stream)) return st;
+  // Unsplit AT (PIPE_MOE, FLOWMOE_AR) reads all T rows of x on lane 0; inside a stack
+  // (no fork) the previous block wrote chunk r of x on lane r, so join the lanes first.
+  if (!fork && !x->at_split && nl > 1)
+    if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer.
   // Policies that keep AT unsplit (PIPE_MOE, FLOWMOE_AR) run MHA + gate once over all
   // tokens, then route/pack per chunk (capacity is per chunk in every policy).
@@ -877,7 +1182,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   const SavedLayout& L = x->L;
   // the per-kernel profile (flowmoe_profile_begin) collapses the lanes so that each
   // kernel's event-timed duration is its own, not shared with co-running chunks
-  const int nl = g_prof.on ? 1 : (int)x->lanes.size();
+  const int nl = x->prof.on ? 1 : (int)x->lanes.size();
   // grad_mode: every weight grad of a block is produced by exactly one kernel (the
   // expert wgrads over all chunks, the deferred K=T MHA/gate wgrads), so "overwrite"
   // is a plain store and "accumulate" a TMA reduce-add / read-modify-write.
@@ -885,10 +1190,16 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   const int gepi = gacc ? EPI_ACC_F32 : EPI_STORE_F32;
   if (fork)
     if (flowmoe_status st = fork_lanes(x, stream)) return st;
+  // Unsplit AT^bwd (PIPE_MOE, FLOWMOE_AR) wrote all T rows of the previous block's dx and
+  // read x->dw on lane 0; inside a stack (no fork) chunk r's combine_bwd_pack on lane r
+  // reads those dx rows and rewrites dw, so every lane first waits for lane 0.
+  if (!fork && !x->at_split && nl > 1)
+    if (flowmoe_status st = lanes_follow(x, x->lanes[0])) return st;
   const int wset = x->ev_wg_done[1] ? (int)(x->bwd_calls++ & 1) : 0;
   x->dyc = x->ws_dyc[wset]; x->dye = x->ws_dye[wset]; x->dz = x->ws_dz[wset];
   if (P > 1) x->dye = const_cast<char*>(at<char>(saved, L.dye));  // per-block landing buffer
-  const bool use_p2p = P > 1 && p2p_ready(x, saved, stream);
+  bool use_p2p = false;
+  if (flowmoe_status st = resolve_p2p(x, saved, stream, &use_p2p)) return st;
   x->dA = x->ws_dA[wset]; x->dqkv = x->ws_dqkv[wset]; x->dl = x->ws_dl[wset];
   // the wgrads that last read this workspace set must be done; an event recorded in
   // another capture (or outside the current one) is already ordered by the graph /
@@ -1100,6 +1411,7 @@ extern "C" {
 
 flowmoe_status flowmoe_block_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* xin,
                                  void* y, void* saved, cudaStream_t stream) {
+  apply_ctx(x);
   return enqueue_fwd(x, p, xin, y, saved, stream, true, true);
 }
 
@@ -1107,11 +1419,13 @@ flowmoe_status flowmoe_block_bwd(flowmoe_ctx* x, const flowmoe_params* p, const 
                                  const void* saved, const void* dy, void* dx,
                                  const flowmoe_grads* gr, size_t chunk_bytes, flowmoe_ticket* ar,
                                  cudaStream_t stream) {
+  apply_ctx(x);
   return enqueue_bwd(x, p, xin, saved, dy, dx, gr, chunk_bytes, ar, stream, true, true);
 }
 
 flowmoe_status flowmoe_stack_fwd(flowmoe_ctx* x, int L, const flowmoe_params* params, const void* x0,
                                  void* const* ys, void* const* saved, cudaStream_t stream) {
+  apply_ctx(x);
   if (!x || L < 1 || !params || !x0 || !ys || !saved) return fail(FLOWMOE_ERR_INVALID, "stack_fwd: bad argument");
   for (int l = 0; l < L; ++l)
     if (flowmoe_status s = enqueue_fwd(x, &params[l], l ? ys[l - 1] : x0, ys[l], saved[l], stream, l == 0,
@@ -1124,6 +1438,7 @@ flowmoe_status flowmoe_stack_bwd(flowmoe_ctx* x, int L, const flowmoe_params* pa
                                  void* const* ys, void* const* saved, const void* dy, void* const* dxs,
                                  const flowmoe_grads* grads, size_t chunk_bytes, flowmoe_ticket* tickets,
                                  cudaStream_t stream) {
+  apply_ctx(x);
   if (!x || L < 1 || !params || !x0 || !ys || !saved || !dy || !dxs || !grads)
     return fail(FLOWMOE_ERR_INVALID, "stack_bwd: bad argument");
   for (int l = L - 1; l >= 0; --l)
@@ -1137,6 +1452,7 @@ flowmoe_status flowmoe_stack_bwd(flowmoe_ctx* x, int L, const flowmoe_params* pa
 flowmoe_status flowmoe_allreduce_submit(flowmoe_ctx* x, float* buf, size_t count,
                                         size_t chunk_bytes, int priority, cudaEvent_t ready,
                                         flowmoe_ticket* out) {
+  apply_ctx(x);
   if (!x || (!buf && count)) return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: NULL argument");
   if (priority < 1) return fail(FLOWMOE_ERR_INVALID, "allreduce_submit: priority must be >= 1 (0 is A2A)");
   if (chunk_bytes == 0 || chunk_bytes % 16)
@@ -1165,6 +1481,7 @@ static flowmoe_status check_opt(const flowmoe_optimizer* o, int64_t step) {
 flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step, float* master,
                                       float* s1, float* s2, const float* grad, void* weight, size_t n,
                                       cudaStream_t stream) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (flowmoe_status st = check_opt(o, step)) return st;
   if (n == 0) return FLOWMOE_OK;
@@ -1177,6 +1494,7 @@ flowmoe_status flowmoe_optimizer_step(flowmoe_ctx* x, const flowmoe_optimizer* o
 
 flowmoe_status flowmoe_embed_fwd(flowmoe_ctx* x, const void* table, int64_t V, const int32_t* ids, int64_t T,
                                  void* out, cudaStream_t stream) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "embed_fwd: need T >= 0 and V >= 1");
   if (T == 0) return FLOWMOE_OK;
@@ -1187,6 +1505,7 @@ flowmoe_status flowmoe_embed_fwd(flowmoe_ctx* x, const void* table, int64_t V, c
 
 flowmoe_status flowmoe_embed_bwd(flowmoe_ctx* x, const int32_t* ids, int64_t T, const void* dx, int64_t V,
                                  float* dtable, cudaStream_t stream) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "embed_bwd: need T >= 0 and V >= 1");
   if (T == 0) return FLOWMOE_OK;
@@ -1197,6 +1516,7 @@ flowmoe_status flowmoe_embed_bwd(flowmoe_ctx* x, const int32_t* ids, int64_t T, 
 
 flowmoe_status flowmoe_xent(flowmoe_ctx* x, const float* logits, const int32_t* labels, int64_t T, int64_t V,
                             float scale, float* losses, float* loss, void* dlogits, cudaStream_t stream) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (T < 0 || V < 1) return fail(FLOWMOE_ERR_INVALID, "xent: need T >= 0 and V >= 1");
   if (T > 0 && (!logits || !labels || !losses)) return fail(FLOWMOE_ERR_INVALID, "xent: NULL logits/labels/losses");
@@ -1213,6 +1533,7 @@ static flowmoe_status check_lm(const flowmoe_ctx* x, int64_t T, int64_t V) {
 
 flowmoe_status flowmoe_lm_head_fwd(flowmoe_ctx* x, const void* h, const void* w, int64_t T, int64_t V, float* logits,
                                    cudaStream_t stream) {
+  apply_ctx(x);
   if (flowmoe_status st = check_lm(x, T, V)) return st;
   if (T == 0) return FLOWMOE_OK;
   if (!h || !w || !logits) return fail(FLOWMOE_ERR_INVALID, "lm_head_fwd: NULL pointer");
@@ -1227,6 +1548,7 @@ flowmoe_status flowmoe_lm_head_fwd(flowmoe_ctx* x, const void* h, const void* w,
 
 flowmoe_status flowmoe_lm_head_bwd(flowmoe_ctx* x, const void* h, const void* w, const void* dlogits, int64_t T,
                                    int64_t V, void* dh, float* dw, cudaStream_t stream) {
+  apply_ctx(x);
   if (flowmoe_status st = check_lm(x, T, V)) return st;
   if (T == 0) return FLOWMOE_OK;
   if (!dlogits || (dh && !w) || (dw && !h)) return fail(FLOWMOE_ERR_INVALID, "lm_head_bwd: NULL pointer");
@@ -1251,6 +1573,7 @@ flowmoe_status flowmoe_lm_head_bwd(flowmoe_ctx* x, const void* h, const void* w,
 
 flowmoe_status flowmoe_expert_update(flowmoe_ctx* x, const flowmoe_optimizer* o, int64_t step,
                                      const flowmoe_expert_opt* st, const flowmoe_grads* gr, flowmoe_ticket* done) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (flowmoe_status s = check_opt(o, step)) return s;
   if (!st || !gr || !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2)
@@ -1273,24 +1596,26 @@ flowmoe_status flowmoe_expert_update(flowmoe_ctx* x, const flowmoe_optimizer* o,
 }
 
 flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStream_t stream) {
+  apply_ctx(x);
   if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
   if (t == 0 || t >= x->next_ticket || x->next_ticket - t > NUM_TICKET_EVENTS)
     return fail(FLOWMOE_ERR_STATE, "allreduce_wait: unknown or expired ticket");
-  if (x->P > 1) {
+  if (x->P > 1 && !x->group) {
     ncclResult_t a = ncclSuccess, b = ncclSuccess;
     for (ncclComm_t c : x->a2a_comm) {
       ncclResult_t e = ncclSuccess;
       ncclCommGetAsyncError(c, &e);
       if (e != ncclSuccess) a = e;
     }
-    ncclCommGetAsyncError(x->comm_ar, &b);
-    if (x->p2p) {
-      unsigned int e = 0;
-      cudaMemcpy(&e, x->p2p_err, sizeof(e), cudaMemcpyDeviceToHost);
-      if (e) return fail(FLOWMOE_ERR_STATE, "peer-memory A2A timed out waiting for a peer");
-    }
+    if (x->comm_ar) ncclCommGetAsyncError(x->comm_ar, &b);
     if (a != ncclSuccess || b != ncclSuccess)
       return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
+  }
+  if (LocalGroup* g = x->group) {
+    const int rk = x->cfg.rank;
+    if (g->ticket_sub[rk].count(t) && !g->ticket_done[rk].count(t))
+      return fail(FLOWMOE_ERR_STATE, "allreduce_wait: the other ranks of the local group have not submitted "
+                                     "their matching all-reduce yet");
   }
   if (!x->pending_ar.empty()) {
     // centralized AR: every pending block AR, whole tensors, after the last backward
@@ -1307,6 +1632,19 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
 
 void flowmoe_destroy(flowmoe_ctx* x) {
   if (!x) return;
+  LocalGroup* g = x->group;
+  if (g) {  // peers may still be exchanging with this member: drain the device first
+    cudaDeviceSynchronize();
+    g->m[x->cfg.rank] = nullptr;
+    bool last = true;
+    for (flowmoe_ctx* m : g->m) last = last && !m;
+    if (last) {
+      if (g->s) cudaStreamDestroy(g->s);
+      for (auto e : g->ev_pool) cudaEventDestroy(e);
+      delete g;
+    }
+    x->group = nullptr;
+  }
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamSynchronize(x->lanes[l]);
   if (x->s_wg && x->s_wg != x->s_comp) cudaStreamSynchronize(x->s_wg);
   if (x->s_comp) cudaStreamSynchronize(x->s_comp);
@@ -1327,6 +1665,8 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   if (x->s_wg && x->s_wg != x->s_comp) cudaStreamDestroy(x->s_wg);
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b, x->ev_bwd_done}) if (e) cudaEventDestroy(e);
   for (void* p : x->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (auto e : x->prof.pool) cudaEventDestroy(e);
+  if (g_prof == &x->prof) g_prof = nullptr;
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);
   if (x->s_a2a) cudaStreamDestroy(x->s_a2a);
@@ -1336,7 +1676,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
 
 }  // extern "C"
 
-extern "C" flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int batch,
+extern "C" flowmoe_status flowmoe_test_gemm(flowmoe_ctx* x, int dtype, int M, int N, int K, int batch,
                                             const void* A, int64_t lda, int64_t sA, int a_mmajor,
                                             const void* B, int64_t ldb, int64_t sB, int b_kmajor,
                                             void* C, int64_t ldc, int64_t sC, int epi,
@@ -1351,6 +1691,14 @@ extern "C" flowmoe_status flowmoe_test_gemm(int dtype, int M, int N, int K, int 
   g.resid = resid; g.ldr = ldc; g.sR = sC;
   g.aux = aux; g.ldaux = ldc; g.sAux = sC;
   if (dtype != DT_F32 && dtype != DT_BF16) return fail(FLOWMOE_ERR_INVALID, "dtype");
+  if (x) {
+    apply_ctx(x);
+  } else {  // library defaults, no profile
+    gemm_tc_set_debug(0);
+    gemm_tc_force_bn(0);
+    g_pdl_enabled = 1;
+    g_prof = nullptr;
+  }
   FM_KP(KK_TEST, 1, 2.0 * M * N * (double)K * batch, 0, stream, gemm(g, dtype, stream));
   return FLOWMOE_OK;
 }

@@ -33,6 +33,15 @@ struct P2PArgs {
   int pieces;               // CTAs per (destination, local expert) block
 };
 
+// A timed-out wait must not let its consumers read stale buffers (the arrival counters
+// would then stay out of step with `seen` for good): flag it, then trap, which faults the
+// context so the next stream synchronisation / flowmoe_check_health reports it.
+FM_DEV void timeout_trap(unsigned int* err) {
+  atomicExch(err, 1u);
+  __threadfence_system();
+  __trap();
+}
+
 // wait until every source published (kind, r) for the (seen + 1)-th time, then seen += 1
 FM_DEV void p2p_wait_sources(const unsigned int* flags, unsigned int* seen, unsigned int* err, int kind, int r,
                              int R, int P) {
@@ -44,8 +53,8 @@ FM_DEV void p2p_wait_sources(const unsigned int* flags, unsigned int* seen, unsi
     while (true) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if ((int)(v - expect) >= 0) break;
-      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: report instead of hanging
-        atomicExch(err, 1u);
+      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: a peer is gone
+        timeout_trap(err);
         break;
       }
       __nanosleep(32);
@@ -150,8 +159,8 @@ __global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* see
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if ((int)(v - expect) >= 0) break;
-      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: report instead of hanging
-        atomicExch(err, 1u);
+      if (clock64() - t0 > (1ll << 35)) {  // ~10-20 s: a peer is gone
+        timeout_trap(err);
         break;
       }
       __nanosleep(64);
@@ -159,6 +168,48 @@ __global__ void a2a_p2p_wait_kernel(const unsigned int* flags, unsigned int* see
   }
   __syncthreads();
   if (threadIdx.x == 0) seen[kind * R + r] = expect;
+}
+
+// Simulated world (flowmoe_create_local_group): sum of the P ranks' fp32 buffers over
+// [off, off+n), in rank order, written back to every rank (one thread per element or
+// 4-float vector: each reads all P values before writing, so in place is safe).
+struct LocalArArgs {
+  float* b[8];
+  int P;
+  int64_t off, n;
+};
+
+__global__ void __launch_bounds__(256) local_allreduce_kernel(LocalArArgs a) {
+  FM_PDL_ENTRY();
+  const int64_t nv = a.n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < a.P; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(a.b[q] + a.off)[i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    for (int q = 0; q < a.P; ++q) reinterpret_cast<float4*>(a.b[q] + a.off)[i] = acc;
+  }
+  for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    float acc = 0.f;
+    for (int q = 0; q < a.P; ++q) acc += a.b[q][a.off + i];
+    for (int q = 0; q < a.P; ++q) a.b[q][a.off + i] = acc;
+  }
+}
+
+int local_allreduce(float* const* bufs, int P, int64_t off, int64_t n, cudaStream_t s) {
+  if (P > 8 || n < 0) return (int)cudaErrorInvalidValue;
+  LocalArArgs a;
+  for (int q = 0; q < 8; ++q) a.b[q] = q < P ? bufs[q] : nullptr;
+  for (int q = 0; q < P; ++q)  // the vector path needs 16-byte aligned chunk starts
+    if ((reinterpret_cast<uintptr_t>(bufs[q] + off) & 15) != 0) return (int)cudaErrorMisalignedAddress;
+  a.P = P; a.off = off; a.n = n;
+  const int64_t nv = (n + 3) / 4;
+  int grid = (int)((nv + 255) / 256);
+  grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
+  launch_k(local_allreduce_kernel, grid, 256, 0, s, a);
+  return (int)cudaGetLastError();
 }
 
 int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* piece_cnt,

@@ -128,4 +128,8 @@ int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, 
             int El, int me, int to_experts, int64_t blk_bytes, cudaStream_t send_stream,
             cudaStream_t wait_stream, bool do_send, bool do_wait, unsigned int* grid_cnt = nullptr);
 
+// Simulated world all-reduce (flowmoe_create_local_group): bufs[q][off, off+n) of the P
+// ranks summed in rank order and written back to all of them; 16-byte aligned chunk starts.
+int local_allreduce(float* const* bufs, int P, int64_t off, int64_t n, cudaStream_t s);
+
 }  // namespace fm

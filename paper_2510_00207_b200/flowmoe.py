@@ -20,13 +20,18 @@ LIB_PATH = os.environ.get("FLOWMOE_LIB") or os.path.join(_HERE, "libflowmoe.so")
 FLOWMOE_F32, FLOWMOE_BF16 = 0, 1
 SCHEDULES = {"flowmoe": 0, "flowmoe_ar": 1, "flowmoe_at": 2, "pipe_moe": 3, "vanilla_ep": 4}
 
+# include/flowmoe.h (product ABI) and include/flowmoe_test.h (test / benchmark hooks)
 EXPORTED = [
     "flowmoe_get_unique_id", "flowmoe_create", "flowmoe_saved_bytes", "flowmoe_grad_flat_count",
-    "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit", "flowmoe_allreduce_wait",
+    "flowmoe_block_fwd", "flowmoe_block_bwd", "flowmoe_stack_fwd", "flowmoe_stack_bwd", "flowmoe_allreduce_submit",
+    "flowmoe_allreduce_wait", "flowmoe_register_saved", "flowmoe_unregister_saved", "flowmoe_check_health",
     "flowmoe_optimizer_step", "flowmoe_expert_update", "flowmoe_embed_fwd", "flowmoe_embed_bwd", "flowmoe_xent",
-    "flowmoe_lm_head_fwd", "flowmoe_lm_head_bwd",
-    "flowmoe_set_forced_routing", "flowmoe_saved_routing_offsets", "flowmoe_debug_set",
-    "flowmoe_kernel_launches", "flowmoe_test_gemm", "flowmoe_profile_begin", "flowmoe_profile_end", "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
+    "flowmoe_lm_head_fwd", "flowmoe_lm_head_bwd", "flowmoe_set_forced_routing",
+    "flowmoe_status_string", "flowmoe_last_error", "flowmoe_destroy",
+]
+EXPORTED_TEST = [
+    "flowmoe_saved_routing_offsets", "flowmoe_debug_set", "flowmoe_test_gemm", "flowmoe_profile_begin",
+    "flowmoe_profile_end", "flowmoe_kernel_launches", "flowmoe_create_local_group",
 ]
 
 
@@ -114,13 +119,18 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_lm_head_bwd.argtypes = [vp, vp, vp, vp, i64, i64, vp, vp, vp]
     L.flowmoe_allreduce_submit.argtypes = [vp, vp, sz, sz, i32, vp, ctypes.POINTER(u64)]
     L.flowmoe_allreduce_wait.argtypes = [vp, u64, vp]
+    L.flowmoe_register_saved.argtypes = [vp, vp]
+    L.flowmoe_unregister_saved.argtypes = [vp, vp]
+    L.flowmoe_check_health.argtypes = [vp]
+    L.flowmoe_create_local_group.argtypes = [ctypes.POINTER(Config), i32, i32, ctypes.POINTER(vp)]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
     L.flowmoe_saved_routing_offsets.argtypes = [vp] + [ctypes.POINTER(sz)] * 5
-    L.flowmoe_debug_set.argtypes = [i32, i32]
+    L.flowmoe_debug_set.argtypes = [vp, i32, i32]
     L.flowmoe_kernel_launches.restype = u64
-    L.flowmoe_test_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
+    L.flowmoe_test_gemm.argtypes = [vp, i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
                                     vp, i64, i64, i32, vp, vp, vp, vp]
-    L.flowmoe_profile_end.argtypes = [ctypes.POINTER(ProfEntry), i32]
+    L.flowmoe_profile_begin.argtypes = [vp]
+    L.flowmoe_profile_end.argtypes = [vp, ctypes.POINTER(ProfEntry), i32]
     L.flowmoe_profile_end.restype = i32
     L.flowmoe_status_string.argtypes = [i32]
     L.flowmoe_status_string.restype = ctypes.c_char_p
@@ -128,17 +138,21 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_destroy.argtypes = [vp]
     L.flowmoe_destroy.restype = None
     _lib = L
-    if os.environ.get("FLOWMOE_DEBUG_SIMT"):  # debug knob: route bf16 GEMMs to the SIMT kernel
-        L.flowmoe_debug_set(1, 1)
-    if os.environ.get("FLOWMOE_DEBUG_SIMT_ATTN"):  # debug knob: SIMT attention for bf16
-        L.flowmoe_debug_set(3, 1)
-    if os.environ.get("FLOWMOE_NO_PDL"):  # A/B knob: plain stream-ordered launches
-        L.flowmoe_debug_set(4, 0)
-    if os.environ.get("FLOWMOE_P2P_A2A_STREAM"):  # A/B knob: peer-memory A2A on the A2A stream
-        L.flowmoe_debug_set(6, 0)
-    if os.environ.get("FLOWMOE_DEBUG_SWAP"):  # debug knob: swap MN-major descriptor strides
-        L.flowmoe_debug_set(2, 1)
     return L
+
+
+# environment knobs applied to every ctx at creation (flowmoe_test.h flowmoe_debug_set)
+_ENV_KNOBS = (("FLOWMOE_DEBUG_SIMT", 1, 1),        # debug: route bf16 GEMMs to the SIMT kernel
+              ("FLOWMOE_DEBUG_SWAP", 2, 1),        # debug: swap MN-major descriptor strides
+              ("FLOWMOE_DEBUG_SIMT_ATTN", 3, 1),   # debug: SIMT attention for bf16
+              ("FLOWMOE_NO_PDL", 4, 0),            # A/B: plain stream-ordered launches
+              ("FLOWMOE_P2P_A2A_STREAM", 6, 0))    # A/B: peer-memory A2A on the A2A stream
+
+
+def _apply_env_knobs(handle):
+    for env, key, val in _ENV_KNOBS:
+        if os.environ.get(env):
+            _check(lib().flowmoe_debug_set(handle, key, val), "flowmoe_debug_set")
 
 
 def _check(rc: int, what: str):
@@ -154,32 +168,14 @@ def get_unique_id() -> bytes:
     return buf.raw
 
 
-def debug_set(key: int, value: int):
-    _check(lib().flowmoe_debug_set(key, value), "flowmoe_debug_set")
-
-
-def profile_begin():
-    _check(lib().flowmoe_profile_begin(), "flowmoe_profile_begin")
-
-
-def profile_end() -> list[dict]:
-    """Per-kernel-kind device time and algorithmic work since profile_begin()."""
-    buf = (ProfEntry * 64)()
-    n = lib().flowmoe_profile_end(buf, 64)
-    if n < 0:
-        raise FlowMoEError(f"flowmoe_profile_end: {lib().flowmoe_last_error().decode()}")
-    return [dict(name=buf[i].name.decode(), launches=buf[i].launches, ms=buf[i].ms,
-                 flops=buf[i].flops, bytes=buf[i].bytes) for i in range(n)]
-
-
 def kernel_launches() -> int:
     return int(lib().flowmoe_kernel_launches())
 
 
 def test_gemm(dtype: str, A, B, C, *, M, N, K, batch=1, lda, sA=0, a_mmajor=0, ldb, sB=0,
-              b_kmajor=0, ldc, sC=0, epi=0, bias=None, resid=None, aux=None, stream=None):
-    """One GEMM through the library's GEMM kernels (include/flowmoe.h flowmoe_test_gemm)."""
-    _check(lib().flowmoe_test_gemm(FLOWMOE_BF16 if dtype == "bf16" else FLOWMOE_F32, M, N, K, batch,
+              b_kmajor=0, ldc, sC=0, epi=0, bias=None, resid=None, aux=None, stream=None, ctx=None):
+    """One GEMM through the library's GEMM kernels (include/flowmoe_test.h flowmoe_test_gemm)."""
+    _check(lib().flowmoe_test_gemm(ctx.handle if ctx is not None else None, FLOWMOE_BF16 if dtype == "bf16" else FLOWMOE_F32, M, N, K, batch,
                                    _ptr(A), lda, sA, a_mmajor, _ptr(B), ldb, sB, b_kmajor, _ptr(C),
                                    ldc, sC, epi, _ptr(bias), _ptr(resid), _ptr(aux),
                                    _stream_handle(stream)), "flowmoe_test_gemm")
@@ -226,16 +222,55 @@ class BlockShape:
 class FlowMoE:
     """One FlowMoE context (one rank): flowmoe_create ... flowmoe_destroy."""
 
-    def __init__(self, shape: BlockShape, device: int = 0, unique_id: bytes | None = None):
+    def __init__(self, shape: BlockShape, device: int = 0, unique_id: bytes | None = None, _handle=None):
         L = lib()
         self.shape = shape
         self._cfg = shape.to_c()
-        h = ctypes.c_void_p()
-        _check(L.flowmoe_create(ctypes.byref(self._cfg), unique_id, device, ctypes.byref(h)),
-               "flowmoe_create")
+        if _handle is None:
+            h = ctypes.c_void_p()
+            _check(L.flowmoe_create(ctypes.byref(self._cfg), unique_id, device, ctypes.byref(h)),
+                   "flowmoe_create")
+        else:
+            h = _handle
         self.handle = h
+        _apply_env_knobs(h)
         self.saved_bytes = int(L.flowmoe_saved_bytes(h))
         self.grad_flat_count = int(L.flowmoe_grad_flat_count(h))
+
+    @classmethod
+    def local_group(cls, shape: BlockShape, P: int, device: int = 0) -> list:
+        """P ctxs of world_size P on one device (flowmoe_test.h flowmoe_create_local_group):
+        the simulated world of the one-GPU exchange tests."""
+        import dataclasses
+        cfg = dataclasses.replace(shape, world_size=P, rank=0, a2a_impl="p2p").to_c()
+        hs = (ctypes.c_void_p * P)()
+        _check(lib().flowmoe_create_local_group(ctypes.byref(cfg), P, device, hs), "flowmoe_create_local_group")
+        return [cls(dataclasses.replace(shape, world_size=P, rank=q, a2a_impl="p2p"), device,
+                    _handle=ctypes.c_void_p(hs[q])) for q in range(P)]
+
+    def register_saved(self, saved):
+        _check(lib().flowmoe_register_saved(self.handle, _ptr(saved)), "flowmoe_register_saved")
+
+    def unregister_saved(self, saved):
+        _check(lib().flowmoe_unregister_saved(self.handle, _ptr(saved)), "flowmoe_unregister_saved")
+
+    def check_health(self):
+        _check(lib().flowmoe_check_health(self.handle), "flowmoe_check_health")
+
+    def debug_set(self, key: int, value: int):
+        _check(lib().flowmoe_debug_set(self.handle, key, value), "flowmoe_debug_set")
+
+    def profile_begin(self):
+        _check(lib().flowmoe_profile_begin(self.handle), "flowmoe_profile_begin")
+
+    def profile_end(self) -> list[dict]:
+        """Per-kernel-kind device time and algorithmic work since profile_begin()."""
+        buf = (ProfEntry * 64)()
+        n = lib().flowmoe_profile_end(self.handle, buf, 64)
+        if n < 0:
+            raise FlowMoEError(f"flowmoe_profile_end: {lib().flowmoe_last_error().decode()}")
+        return [dict(name=buf[i].name.decode(), launches=buf[i].launches, ms=buf[i].ms,
+                     flops=buf[i].flops, bytes=buf[i].bytes) for i in range(n)]
 
     def close(self):
         if getattr(self, "handle", None):

@@ -1,6 +1,10 @@
 import os
 import sys
 
+# The simulated-world tests (tests/test_gpu_group.py) run P ranks' streams in one process:
+# give every stream its own hardware queue, set before any CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -153,10 +153,132 @@ def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: in
         gr.replay()
     torch.cuda.synchronize()
     out = {"y": fm.to_host_f64(xs[L]), "dx": fm.to_host_f64(dxs[0]),
+           "xs": [fm.to_host_f64(t) for t in xs], "dxs": [fm.to_host_f64(t) for t in dxs],
            "grad_flat": [bt.g["grad_flat"].cpu().numpy().astype(np.float64) for bt in bts],
            "dw1": [bt.g["dw1"].cpu().numpy().astype(np.float64) for bt in bts]}
     if graph:
         del gr
         torch.cuda.synchronize()
     ctx.close()
+    return out
+
+
+def chain_per_block_errors(cfg, reps, forced, dy_top, g, rank=0, P=1):
+    """Per-block parity of an L-block chain: the oracle runs block l on the GPU's own input
+    to that block (x_l, and for the backward the GPU's dx_{l+1}), so every block is held to
+    the single-block tolerance (no compounding of bf16 rounding through the chain).  With
+    P > 1 every worker's GPU inputs are needed: `g` is then the list of per-rank results."""
+    import oracle as o
+    gs = g if isinstance(g, list) else [g]
+    L = len(reps)
+    res = {}
+    for l in range(L):
+        xin = [gg["xs"][l] for gg in gs]
+        ys, st = o.block_forward(cfg, reps[l], xin, [f[l] for f in forced] if forced else None)
+        dyin = [(gg["dxs"][l + 1] if l + 1 < L else dy_top[q]) for q, gg in enumerate(gs)]
+        dxl, gflat, eg = o.block_backward(cfg, reps[l], st, dyin)
+        me = gs[rank] if len(gs) > 1 else gs[0]
+        El = cfg.E // P
+        res[f"y{l}"] = rel(me["xs"][l + 1], ys[rank])
+        res[f"dx{l}"] = rel(me["dxs"][l], dxl[rank])
+        res[f"grad_flat{l}"] = rel(me["grad_flat"][l], gflat)
+        res[f"dw1_{l}"] = rel(me["dw1"][l], np.stack([eg[e][0] for e in range(rank * El, (rank + 1) * El)]))
+    return res
+
+
+def run_group_gpu(cfg: BlockConfig, rep: dict, wks: list, *, forced: bool = True, chunk_bytes: int = 4096 + 16,
+                  compute_streams: int = 1, schedule: str = "flowmoe", repeat: int = 2, device: int = 0,
+                  stack_reps: list | None = None, graph: bool = False) -> list:
+    """P = len(wks) ranks of one block (or, with stack_reps, an L-block stack through the
+    stack API) in the in-process simulated world on ONE GPU (flowmoe_create_local_group):
+    the real peer-memory A2A kernels exchange between the ranks' buffers and the all-reduce
+    runs the S_p chunk loop.  Each phase is enqueued for every rank before anything waits.
+    repeat > 1 re-runs the iteration (arrival counters advance).  Returns per-rank results."""
+    import torch
+    P = len(wks)
+    dev = torch.device("cuda", device)
+    torch.cuda.set_device(dev)
+    shape = shape_of(cfg, P, 0, "overwrite", compute_streams, schedule, "p2p")
+    ctxs = fm.FlowMoE.local_group(shape, P, device)
+    reps = stack_reps if stack_reps is not None else [rep]
+    L = len(reps)
+    bts = [[fm.BlockTensors(r, cfg.dtype, q, P, dev) for r in reps] for q in range(P)]
+    xs = [[fm.to_device(wks[q]["x"], cfg.dtype, dev)] + [None] * L for q in range(P)]
+    for q in range(P):
+        for l in range(L):
+            xs[q][l + 1] = torch.empty_like(xs[q][0])
+    dxs = [[torch.empty_like(xs[q][0]) for _ in range(L)] for q in range(P)]
+    dys = [fm.to_device(wks[q]["dy"], cfg.dtype, dev) for q in range(P)]
+    saved = [[torch.empty(ctxs[q].saved_bytes, dtype=torch.uint8, device=dev) for _ in range(L)] for q in range(P)]
+    for l in range(L):  # collective registration, same order on every rank
+        for q in range(P):
+            ctxs[q].register_saved(saved[q][l])
+    fidx = None
+    if forced:  # the same forced indices for every block of a stack
+        fidx = [torch.from_numpy(np.ascontiguousarray(wks[q]["forced_idx"], dtype=np.int32)).to(dev)
+                for q in range(P)]
+        for q in range(P):
+            ctxs[q].set_forced_routing(fidx[q])
+
+    def iteration(s):
+        tickets = [[] for _ in range(P)]
+        if stack_reps is not None:
+            for q in range(P):
+                ctxs[q].stack_fwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], s)
+            for q in range(P):
+                tickets[q] = ctxs[q].stack_bwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], dys[q],
+                                               dxs[q], [b.grads for b in bts[q]], chunk_bytes, s)
+        else:
+            for q in range(P):
+                ctxs[q].block_fwd(bts[q][0].params, xs[q][0], xs[q][1], saved[q][0], s)
+            for q in range(P):
+                tickets[q] = [ctxs[q].block_bwd(bts[q][0].params, xs[q][0], saved[q][0], dys[q], dxs[q][0],
+                                                bts[q][0].grads, chunk_bytes, s)]
+        for q in range(P):
+            for t in tickets[q]:
+                ctxs[q].allreduce_wait(t, s)
+
+    s = torch.cuda.current_stream()
+    for _ in range(repeat):
+        iteration(s)
+    gr = None
+    if graph:  # the P ranks' whole iteration captured into one graph and replayed twice
+        for q in range(P):
+            for bt in bts[q]:
+                for v in bt.g.values():
+                    v.fill_(7.0)
+        gr = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(s)
+        with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
+            iteration(torch.cuda.current_stream())
+        gr.replay()
+        gr.replay()
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_health()
+    out = []
+    T, E, k, R = cfg.T, cfg.E, cfg.top_k, cfg.R
+    for q in range(P):
+        off = ctxs[q].routing_offsets()
+
+        def view(o, n, dt, q=q):
+            return saved[q][0][o:o + n * 4].view(dt).cpu().numpy().copy()
+
+        out.append({
+            "y": fm.to_host_f64(xs[q][L]), "dx": fm.to_host_f64(dxs[q][0]),
+            "xs": [fm.to_host_f64(t) for t in xs[q]], "dxs": [fm.to_host_f64(t) for t in dxs[q]],
+            "grad_flat_l": [bt.g["grad_flat"].cpu().numpy().astype(np.float64) for bt in bts[q]],
+            "dw1_l": [bt.g["dw1"].cpu().numpy().astype(np.float64) for bt in bts[q]],
+            "grad_flat": bts[q][0].g["grad_flat"].cpu().numpy().astype(np.float64),
+            **{n: bts[q][0].g[n].cpu().numpy().astype(np.float64) for n in ("dw1", "db1", "dw2", "db2")},
+            "idx": view(off["idx"], T * k, torch.int32).reshape(T, k),
+            "pos": view(off["pos"], T * k, torch.int32).reshape(T, k),
+            "counts": view(off["counts"], R * E, torch.int32).reshape(R, E),
+        })
+    if gr is not None:
+        del gr
+        torch.cuda.synchronize()
+    for c in ctxs:
+        c.close()
     return out

@@ -15,7 +15,8 @@ import torch.distributed as dist  # noqa: E402
 import oracle as o  # noqa: E402
 import paper_2510_00207_b200 as fm  # noqa: E402
 from synth import PRESETS, BlockConfig, gen_replicated, gen_worker  # noqa: E402
-from tests.gpu_util import expert_grads, oracle_block, rel, run_block_gpu, run_stack_gpu  # noqa: E402
+from tests.gpu_util import (chain_per_block_errors, expert_grads, oracle_block, rel,  # noqa: E402
+                            run_block_gpu, run_stack_gpu)
 
 CASES = {
     "c1_f32": PRESETS["c1"],
@@ -77,7 +78,6 @@ def main():
         reps = [gen_replicated(cfg, block=l) for l in range(L)]
         wks = [gen_worker(cfg, p) for p in range(P)]
         forced = [[gen_worker(cfg, p, block=l)["forced_idx"] for p in range(P)] for l in range(L)]
-        r = {}
         runs_api = {}
         for api, fr in (("per_block", True), ("per_block_free", False), ("stack", False)):
             obj = [fm.get_unique_id() if rank == 0 else None]
@@ -88,25 +88,16 @@ def main():
                                           api="stack" if api == "stack" else "per_block", P=P, rank=rank,
                                           uid=obj[0], a2a_impl=a2a, chunk_bytes=4096 + 16,
                                           graph=(api == "stack"))
-        xs, sts = [[w["x"] for w in wks]], []
-        for l in range(L):
-            ys, st = o.block_forward(cfg, reps[l], xs[-1], forced[l])
-            xs.append(ys)
-            sts.append(st)
-        dys, ref_g = [w["dy"] for w in wks], [None] * L
-        for l in reversed(range(L)):
-            dxl, gflat, eg = o.block_backward(cfg, reps[l], sts[l], dys)
-            ref_g[l] = (gflat, expert_grads(eg, rank * (cfg.E // P), (rank + 1) * (cfg.E // P))["dw1"])
-            dys = dxl
-        g = runs_api["per_block"]
-        r["y"] = rel(g["y"], xs[-1][rank])
-        r["dx"] = rel(g["dx"], dys[rank])
-        r["grad_flat"] = max(rel(g["grad_flat"][l], ref_g[l][0]) for l in range(L))
-        r["dw1"] = max(rel(g["dw1"][l], ref_g[l][1]) for l in range(L))
+        # per-block parity: the oracle's P workers run block l on every rank's GPU input
+        # to that block (single-block tolerance, no compounding through the chain)
+        mine = {n: runs_api["per_block"][n] for n in ("xs", "dxs", "grad_flat", "dw1")}
+        allg = [None] * P
+        dist.all_gather_object(allg, mine)
+        r = chain_per_block_errors(cfg, reps, [[forced[l][p] for l in range(L)] for p in range(P)],
+                                   [w["dy"] for w in wks], allg, rank=rank, P=P)
         a, b = runs_api["stack"], runs_api["per_block_free"]
         r["stack_bitwise"] = bool(all(np.array_equal(a[n], b[n]) for n in ("y", "dx")) and all(
             np.array_equal(a[n][l], b[n][l]) for n in ("grad_flat", "dw1") for l in range(L)))
-        r["depth"] = L
         results[name] = r
     out = [None] * P
     dist.all_gather_object(out, results)

@@ -31,10 +31,9 @@ def test_multi_gpu_parity(P):
     per_rank = json.loads(line[0][len("MP_RESULTS "):])
     for rank, res in enumerate(per_rank):
         for case, r in res.items():
-            if case.startswith("stack_"):  # 3-block chain: bf16 rounding compounds with depth
+            if case.startswith("stack_"):  # 3-block chain, checked block by block
                 assert r.pop("stack_bitwise"), (rank, case)
-                depth = r.pop("depth")
-                tol = 1e-4 if "f32" in case else 2e-2 * depth
+                tol = 1e-4 if "f32" in case else 2e-2
             else:
                 assert r.pop("routing_exact"), (rank, case)
                 tol = TOL.get(case, TOL["bf16_p"])

@@ -132,6 +132,40 @@ def test_routing_bitexact_given_gpu_logits(name):
     assert rel(g["logits"], st.route[0].logits) <= TOL[cfg.dtype]
 
 
+@pytest.mark.parametrize("name", ["bf16_small", "gate_e32_k8", "c1_f32", "gate_e64_k4"])
+def test_routing_crafted_ties(name):
+    """Reading Q4 on the GPU with ties forced: duplicated gate columns give bit-equal
+    logits, so top-k must pick the lower expert index; and an all-equal gate (every
+    column the same) must route every token to experts 0..k-1 with weights 1/k."""
+    cfg = CASES[name]
+    wk = gen_worker(cfg, 0)
+    rep = gen_replicated(cfg)
+    E = cfg.E
+    wg = rep["wg"].copy()
+    pairs = [(0, E - 1), (1, E // 2 + 1), (2, 3)] if E >= 8 else [(0, E - 1), (1, E - 2)]
+    for lo, hi in pairs:
+        wg[:, hi] = wg[:, lo]
+    g = run_block_gpu(cfg, dict(rep, wg=wg), wk, forced=False)
+    for lo, hi in pairs:
+        assert np.array_equal(g["logits"][:, lo], g["logits"][:, hi]), "duplicated columns must tie exactly"
+    ro = o.route_worker(cfg, None, None, logits=g["logits"].astype(np.float64))
+    assert np.array_equal(g["idx"], ro.idx)
+    assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
+    assert np.array_equal(g["counts"], ro.counts)
+    decided = sum(int(np.sum(np.any(g["idx"] == lo, axis=1) & ~np.any(g["idx"] == hi, axis=1)))
+                  for lo, hi in pairs)
+    assert decided > 0, "some token must sit on a tie at the k-th place"
+    for lo, hi in pairs:  # the higher index never wins a tie against the lower one
+        assert not np.any(np.any(g["idx"] == hi, axis=1) & ~np.any(g["idx"] == lo, axis=1))
+    g = run_block_gpu(cfg, dict(rep, wg=np.repeat(rep["wg"][:, :1], E, axis=1)), wk, forced=False)
+    assert np.array_equal(g["idx"], np.tile(np.arange(cfg.top_k, dtype=np.int32), (cfg.T, 1)))
+    want_w = 1.0 / cfg.top_k if cfg.top_k > 1 else 1.0 / E
+    assert np.max(np.abs(g["w"] - want_w)) < 1e-6
+    ro = o.route_worker(cfg, None, None, logits=g["logits"].astype(np.float64))
+    assert np.array_equal(g["pos"], np.where(ro.kept, ro.pos, -1))
+    assert np.array_equal(g["counts"], ro.counts)
+
+
 def test_skewed_routing_with_drops_bf16():
     """Zipf-skewed expert popularity (input recipe 'skew'): uneven loads and drops."""
     cfg = CASES["bf16_small"]
@@ -331,12 +365,21 @@ def test_vanilla_ep_is_the_unchunked_block():
     assert np.array_equal(g["counts"], st.route[0].counts)
 
 
+def check_chain_per_block(cfg, reps, forced, dy_top, g):
+    from tests.gpu_util import chain_per_block_errors
+    res = chain_per_block_errors(cfg, reps, forced, dy_top, g)
+    bad = {k: v for k, v in res.items() if not v <= TOL[cfg.dtype]}
+    assert not bad, (bad, res)
+    return res
+
+
 @pytest.mark.parametrize("dtype,lanes,graph", [("f32", 1, False), ("bf16", 4, False), ("bf16", 4, True),
                                                ("f32", 2, True)])
 def test_block_stack_chain_parity(dtype, lanes, graph):
-    """3 chained blocks (different weights, forced routing): forward y_3 and backward dx_0
-    plus every block's grads vs the oracle chain; exercises cross-block reuse of the
-    ctx workspaces, compute lanes, the overlapped weight-grad stream, CUDA-graph replay."""
+    """3 chained blocks (different weights, forced routing): every block's forward output,
+    backward dx and grads vs the oracle run on that block's GPU inputs (per-block
+    tolerance); f32 also end to end.  Exercises cross-block reuse of the ctx workspaces,
+    compute lanes, the overlapped weight-grad stream, CUDA-graph replay."""
     from tests.gpu_util import run_stack_gpu
     base = CASES["c2_bench"] if dtype == "bf16" else CASES["c1_f32"].replace(R=4, residual=1, causal=1)
     cfg = base
@@ -345,30 +388,51 @@ def test_block_stack_chain_parity(dtype, lanes, graph):
     wk = gen_worker(cfg, 0)
     wk["forced"] = [gen_worker(cfg, 0, block=l)["forced_idx"] for l in range(L)]
     g = run_stack_gpu(cfg, reps, wk, compute_streams=lanes, graph=graph)
-    xs, sts = [wk["x"]], []
-    for l in range(L):
-        ys, st = o.block_forward(cfg, reps[l], [xs[-1]], [wk["forced"][l]])
-        xs.append(ys[0])
-        sts.append(st)
-    dy, grads = wk["dy"], [None] * L
-    for l in reversed(range(L)):
-        dxs, gflat, eg = o.block_backward(cfg, reps[l], sts[l], [dy])
-        grads[l] = (gflat, np.stack([eg[e][0] for e in range(cfg.E)]))
-        dy = dxs[0]
-    # bf16 rounding of every activation compounds through the chain: the tolerance
-    # scales with depth; the f32 cases and the bitwise lanes==1 check prove the logic
-    tol = TOL[dtype] * (L if dtype == "bf16" else 1)
-    if dtype == "bf16":
+    check_chain_per_block(cfg, reps, [wk["forced"]], [wk["dy"]], g)
+    if dtype == "bf16":  # lanes and graph replay change nothing, bit for bit
         ref = run_stack_gpu(cfg, reps, wk, compute_streams=1, graph=False)
         for n in ("y", "dx"):
             assert np.array_equal(g[n], ref[n]), n
         for l in range(L):
             assert np.array_equal(g["grad_flat"][l], ref["grad_flat"][l]) and np.array_equal(g["dw1"][l], ref["dw1"][l])
-    assert rel(g["y"], xs[-1]) <= tol
-    assert rel(g["dx"], dy) <= tol
+        return
+    # fp32: the whole chain end to end at the fp32 tolerance as well
+    xs, sts = [wk["x"]], []
     for l in range(L):
-        assert rel(g["grad_flat"][l], grads[l][0]) <= tol, l
-        assert rel(g["dw1"][l], grads[l][1]) <= tol, l
+        ys, st = o.block_forward(cfg, reps[l], [xs[-1]], [wk["forced"][l]])
+        xs.append(ys[0])
+        sts.append(st)
+    dy = wk["dy"]
+    for l in reversed(range(L)):
+        dxs, gflat, eg = o.block_backward(cfg, reps[l], sts[l], [dy])
+        assert rel(g["grad_flat"][l], gflat) <= TOL[dtype], l
+        dy = dxs[0]
+    assert rel(g["y"], xs[-1]) <= TOL[dtype]
+    assert rel(g["dx"], dy) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("schedule", ["flowmoe_ar", "pipe_moe", "flowmoe_at"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_stack_api_unsplit_schedules(schedule, graph):
+    """The stack API with R compute lanes under the policies that keep AT unsplit
+    (FLOWMOE_AR, PIPE_MOE: all T rows of a block's input on lane 0, written chunk-wise on
+    the lanes by the previous block) and FLOWMOE_AT: bit-identical to per-block calls of
+    the default schedule on one lane (P = 1: the policies change only the schedule).
+    Repeated three times to give a missing cross-lane dependency a chance to show."""
+    from tests.gpu_util import run_stack_gpu
+    cfg = CASES["c2_bench"]
+    L = 3
+    reps = [gen_replicated(cfg, block=l) for l in range(L)]
+    wk = gen_worker(cfg, 0)
+    wk["forced"] = None
+    ref = run_stack_gpu(cfg, reps, wk, compute_streams=1, api="per_block")
+    for _ in range(3):
+        g = run_stack_gpu(cfg, reps, wk, compute_streams=cfg.R, graph=graph, api="stack", schedule=schedule)
+        for n in ("y", "dx"):
+            assert np.array_equal(g[n], ref[n]), n
+        for l in range(L):
+            assert np.array_equal(g["grad_flat"][l], ref["grad_flat"][l]), l
+            assert np.array_equal(g["dw1"][l], ref["dw1"][l]), l
 
 
 @pytest.mark.parametrize("dtype,graph", [("bf16", False), ("bf16", True), ("float32", False), ("tok", True)])

@@ -216,6 +216,22 @@ def test_gelu_closed_form_and_identity_expert():
     hh = 1e-6
     fd = (o.gelu(z + hh) - o.gelu(z - hh)) / (2 * hh)
     assert np.allclose(fd, o.gelu_grad(z), atol=1e-8)
+    # value pins (the odd-part identities above also hold for tanh-GELU and for erf
+    # without the 1/√2): GELU(z) = z·Φ(z) with Φ the standard normal CDF (reading Q8),
+    # Φ(1) = 0.8413447460685429 and φ(1) = e^{-1/2}/√(2π) = 0.24197072451914337
+    # (normal-distribution tables, Abramowitz & Stegun 26.2), so GELU(1) = Φ(1),
+    # GELU(-1) = -(1 - Φ(1)), GELU'(1) = Φ(1) + φ(1), GELU'(-1) = 1 - Φ(1) - φ(1).
+    phi1, dens1 = 0.8413447460685429, 0.24197072451914337
+    g = o.gelu(np.array([1.0, -1.0, 2.0]))
+    assert abs(g[0] - phi1) < 1e-15
+    assert abs(g[1] + (1.0 - phi1)) < 1e-15
+    assert abs(g[2] - 2.0 * 0.9772498680518208) < 1e-14  # Φ(2) = 0.9772498680518208
+    gg = o.gelu_grad(np.array([1.0, -1.0]))
+    assert abs(gg[0] - (phi1 + dens1)) < 1e-15
+    assert abs(gg[1] - (1.0 - phi1 - dens1)) < 1e-15
+    # and against an independent library CDF over the whole range
+    from scipy.special import ndtr
+    assert np.allclose(o.gelu(z), z * ndtr(z), rtol=1e-14, atol=1e-15)
     # identity expert: W1 = [I, −I], W2 = [I; −I], b = 0  ->  FFN(x) = x
     M = 6
     w1 = np.concatenate([np.eye(M), -np.eye(M)], axis=1)
