@@ -62,6 +62,12 @@ int flowmoe_profile_end(flowmoe_ctx* ctx, flowmoe_prof_entry* out, int max_entri
 /* Number of kernels this library has launched in the calling process (bench accounting). */
 uint64_t flowmoe_kernel_launches(void);
 
+/* The peer-memory A2A arrival counters of this rank: out[(kind·R + r)·P + src] = how many
+ * times source rank `src` has delivered exchange `kind` (0 D_r, 1 C_r, 2 C_r^bwd, 3 D_r^bwd)
+ * of chunk r into this rank (monotonic).  n >= 4·R·world_size.  Synchronises the device.
+ * FLOWMOE_ERR_STATE without a peer-memory A2A. */
+flowmoe_status flowmoe_test_arrivals(const flowmoe_ctx* ctx, unsigned int* out, size_t n);
+
 /* In-process simulated world for one-GPU tests of the exchange rows (S6/S8/B1/B3 peer-
  * memory A2A kernels and arrival counters, B6 S_p chunking of the all-reduce): P ctxs
  * (2 <= P <= 8; out[P]) of world_size P, ranks 0..P-1, on ONE device, peers' buffers mapped
@@ -70,10 +76,12 @@ uint64_t flowmoe_kernel_launches(void);
  * summed chunk by chunk (the same S_p partition as the NCCL path) in rank order on a group
  * stream and the sum is written back to every rank; flowmoe_allreduce_wait on a ticket whose
  * peers have not submitted yet returns FLOWMOE_ERR_STATE.  Each rank must register its
- * `saved` stashes (flowmoe_register_saved) before the first forward.  Enqueue each phase
- * for all ranks before waiting (the ranks' kernels wait for each other on the device), and
- * give the process >= 4 + P·(R + 3) hardware queues (CUDA_DEVICE_MAX_CONNECTIONS=32) so the
- * ranks' streams never share one.  Schedules FLOWMOE and FLOWMOE_AR only (the centralized-AR
+ * `saved` stashes (flowmoe_register_saved) before the first forward.  Drive every rank from
+ * its own host thread: no kernel waits for another launch on the device (nothing guarantees
+ * that separate launches on one GPU run at the same time); instead each exchange records an
+ * event after this rank's send kernel, the member threads meet at a host barrier (120 s
+ * timeout: FLOWMOE_ERR_STATE), and every rank's stream waits for its peers' send events.
+ * Not capturable into a CUDA graph.  Call allreduce_wait after every rank's backward.  Schedules FLOWMOE and FLOWMOE_AR only (the centralized-AR
  * policies flush inside allreduce_wait, before the other ranks could submit).  Destroy every
  * member with flowmoe_destroy; each drains the device first. */
 flowmoe_status flowmoe_create_local_group(const flowmoe_config* cfg, int P, int device, flowmoe_ctx** out);

@@ -17,6 +17,9 @@
 #include <stdio.h>
 #include <string.h>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <map>
 #include <vector>
@@ -180,6 +183,7 @@ struct flowmoe_ctx {
   std::vector<const void*> saved_order;
   // in-process simulated world (flowmoe_create_local_group): P ctxs on one device
   LocalGroup* group = nullptr;
+  std::vector<cudaEvent_t> ev_sent;  // simulated world: [4 kinds][R] end of this rank's send
 };
 
 // In-process simulated world (flowmoe_create_local_group, include/flowmoe_test.h): P ctxs
@@ -201,6 +205,11 @@ struct LocalGroup {
   size_t done = 0;                               // submissions enqueued (same index on every rank)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  // member threads: barrier of the exchanges, lock of the shared state above
+  std::mutex mu;
+  std::condition_variable cv;
+  int bar_count = 0;
+  uint64_t bar_gen = 0;
 };
 
 namespace {
@@ -510,7 +519,10 @@ flowmoe_status resolve_p2p(flowmoe_ctx* x, const void* saved, cudaStream_t strea
     return FLOWMOE_OK;
   }
   if (flowmoe_status st = register_saved(x, saved)) return st;
-  *use = x->peer_saved.count(saved) > 0;
+  {
+    std::lock_guard<std::mutex> lk(x->group->mu);
+    *use = x->peer_saved.count(saved) > 0;
+  }
   if (!*use)
     return fail(FLOWMOE_ERR_STATE, "local group: saved stash not registered on every rank "
                                    "(call flowmoe_register_saved on each rank before the first block_fwd)");
@@ -575,6 +587,7 @@ flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_
   if (ready) FM_CUDA(cudaStreamWaitEvent(x->s_ar, ready, 0));
   if (x->P == 1 || count == 0) return FLOWMOE_OK;
   if (LocalGroup* g = x->group) {
+    std::lock_guard<std::mutex> lk(g->mu);
     // snapshot the readiness (the caller's event may be re-recorded by the next block)
     if (g->ev_used == g->ev_pool.size()) {
       cudaEvent_t e;
@@ -598,6 +611,8 @@ flowmoe_status new_ticket(flowmoe_ctx* x, flowmoe_ticket* out) {
   const uint64_t t = x->next_ticket++;
   LocalGroup* g = x->group;
   const int rk = x->cfg.rank;
+  std::unique_lock<std::mutex> lk;
+  if (g) lk = std::unique_lock<std::mutex>(g->mu);
   if (g && !g->subs[rk].empty() && g->subs[rk].size() > g->done) {
     g->ticket_sub[rk][t] = g->subs[rk].size() - 1;  // recorded when that submission is enqueued
   } else {
@@ -769,6 +784,11 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
     for (auto& e : *v)
       if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
   }
+  if (g) {
+    x->ev_sent.resize(4 * x->cfg.R);
+    for (auto& e : x->ev_sent)
+      if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
+  }
   x->ticket_ev.resize(NUM_TICKET_EVENTS);
   for (auto& e : x->ticket_ev)
     if (!mk(&e)) return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "event creation failed"));
@@ -866,6 +886,7 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
 flowmoe_status register_saved(flowmoe_ctx* x, const void* saved) {
   if (x->P == 1 || !x->p2p || x->peer_saved.count(saved)) return FLOWMOE_OK;
   if (LocalGroup* g = x->group) {
+    std::lock_guard<std::mutex> lk(g->mu);
     auto& mine = g->saved[x->cfg.rank];
     size_t n = 0;
     while (n < mine.size() && mine[n] != saved) ++n;
@@ -912,6 +933,16 @@ flowmoe_status flowmoe_unregister_saved(flowmoe_ctx* x, const void* saved) {
   x->peer_saved.erase(saved);
   for (size_t i = 0; i < x->saved_order.size(); ++i)
     if (x->saved_order[i] == saved) { x->saved_order.erase(x->saved_order.begin() + i); break; }
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_test_arrivals(const flowmoe_ctx* x, unsigned int* out, size_t n) {
+  if (!x || !out) return fail(FLOWMOE_ERR_INVALID, "test_arrivals: NULL argument");
+  const size_t nfl = (size_t)4 * x->cfg.R * x->P;
+  if (!x->flags) return fail(FLOWMOE_ERR_STATE, "test_arrivals: no peer-memory A2A in this ctx");
+  if (n < nfl) return fail(FLOWMOE_ERR_INVALID, "test_arrivals: need 4*R*world_size entries");
+  FM_CUDA(cudaDeviceSynchronize());
+  FM_CUDA(cudaMemcpy(out, x->flags, nfl * sizeof(unsigned int), cudaMemcpyDeviceToHost));
   return FLOWMOE_OK;
 }
 
@@ -1003,6 +1034,48 @@ flowmoe_status flowmoe_set_forced_routing(flowmoe_ctx* x, const int32_t* idx) {
 }
 
 }  // extern "C"
+
+namespace {
+// Simulated world: host-side rendezvous of the P member threads (each rank is driven by its
+// own host thread, e.g. a Python thread: ctypes releases the GIL).  false on timeout.
+bool group_barrier(LocalGroup* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  const uint64_t gen = g->bar_gen;
+  if (++g->bar_count == g->P) {
+    g->bar_count = 0;
+    ++g->bar_gen;
+    g->cv.notify_all();
+    return true;
+  }
+  return g->cv.wait_for(lk, std::chrono::seconds(120), [&] { return g->bar_gen != gen; });
+}
+
+// One peer-memory exchange (kind 0 D_r, 1 C_r, 2 C_r^bwd, 3 D_r^bwd) of chunk r on stream sa:
+// this rank's CTAs store its C×M blocks into every destination's receive buffer and bump
+// the destinations' arrival counters.  Across GPUs the completing CTA then waits (acquire)
+// for every source's arrival.  In the simulated world no kernel ever waits for another
+// launch (nothing guarantees that separate launches on one GPU run at the same time): the
+// send kernel records an event, the member threads meet at a host barrier, and the stream
+// waits for every peer's send event instead; a second barrier keeps any member from
+// re-recording its event before every peer has enqueued its wait.
+flowmoe_status p2p_exchange(flowmoe_ctx* x, int kind, int r, const void* src, void* const* dst, int to_experts,
+                            cudaStream_t sa) {
+  const int R = x->cfg.R;
+  const int64_t blk = x->C * x->M * (int64_t)x->es;
+  LocalGroup* g = x->group;
+  FM_K(1, a2a_p2p(src, dst, x->peer_flags.data(), x->piece_cnt, x->flags, x->seen, x->p2p_err, kind, r, R,
+                  (int)x->P, (int)x->El, x->cfg.rank, to_experts, blk, sa, sa, true, g == nullptr,
+                  g ? nullptr : x->grid_cnt));
+  if (!g) return FLOWMOE_OK;
+  cudaEvent_t ev = x->ev_sent[kind * R + r];
+  FM_CUDA(cudaEventRecord(ev, sa));
+  if (!group_barrier(g)) return fail(FLOWMOE_ERR_STATE, "local group: a peer did not reach the exchange (120 s)");
+  for (int q = 0; q < g->P; ++q)
+    if (q != x->cfg.rank) FM_CUDA(cudaStreamWaitEvent(sa, g->m[q]->ev_sent[kind * R + r], 0));
+  if (!group_barrier(g)) return fail(FLOWMOE_ERR_STATE, "local group: a peer did not reach the exchange (120 s)");
+  return FLOWMOE_OK;
+}
+}  // namespace
 
 namespace {
 // One block's forward.  fork: lanes first wait for `stream`; join: `stream` then waits for
@@ -1102,8 +1175,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       if (use_p2p) {
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.xe;
-        FM_K(2, a2a_p2p(at<char>(saved, L.send), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 0, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true, x->grid_cnt));
+        if (flowmoe_status st_ = p2p_exchange(x, 0, r, at<char>(saved, L.send), dst.data(), 1, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
       prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_d[r], sa));
@@ -1140,8 +1212,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       if (use_p2p) {
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.yc;
-        FM_K(2, a2a_p2p(at<char>(saved, L.ye), dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 1, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true, x->grid_cnt));
+        if (flowmoe_status st_ = p2p_exchange(x, 1, r, at<char>(saved, L.ye), dst.data(), 0, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
       prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_c[r], sa));
@@ -1226,8 +1297,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       if (use_p2p) {
         std::vector<void*> dst(P);
         for (int q = 0; q < P; ++q) dst[q] = (char*)x->peer_saved[saved][q] + L.dye;
-        FM_K(2, a2a_p2p(x->dyc, dst.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 2, r, R, (int)P, (int)El, x->cfg.rank, 1, C * M * es, sa, sa, true, true, x->grid_cnt));
+        if (flowmoe_status st_ = p2p_exchange(x, 2, r, x->dyc, dst.data(), 1, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
       prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], sa));
@@ -1260,8 +1330,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_eb[r], 0));
       int pi = prof_start(sa);
       if (use_p2p) {
-        FM_K(2, a2a_p2p(x->dxe, x->peer_dxc.data(), x->peer_flags.data(), x->piece_cnt, x->flags, x->seen,
-                        x->p2p_err, 3, r, R, (int)P, (int)El, x->cfg.rank, 0, C * M * es, sa, sa, true, true, x->grid_cnt));
+        if (flowmoe_status st_ = p2p_exchange(x, 3, r, x->dxe, x->peer_dxc.data(), 0, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
       prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, sa);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], sa));
@@ -1612,6 +1681,7 @@ flowmoe_status flowmoe_allreduce_wait(flowmoe_ctx* x, flowmoe_ticket t, cudaStre
       return fail(FLOWMOE_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
   }
   if (LocalGroup* g = x->group) {
+    std::lock_guard<std::mutex> lk(g->mu);
     const int rk = x->cfg.rank;
     if (g->ticket_sub[rk].count(t) && !g->ticket_done[rk].count(t))
       return fail(FLOWMOE_ERR_STATE, "allreduce_wait: the other ranks of the local group have not submitted "
@@ -1659,6 +1729,7 @@ void flowmoe_destroy(flowmoe_ctx* x) {
                   &x->ev_qkv, &x->ev_dctx, &x->ev_atb})
     for (auto e : *v) if (e) cudaEventDestroy(e);
   for (auto e : x->ticket_ev) if (e) cudaEventDestroy(e);
+  for (auto e : x->ev_sent) if (e) cudaEventDestroy(e);
   for (auto e : x->ev_lane) if (e) cudaEventDestroy(e);
   for (auto e : x->ev_wg_done) if (e) cudaEventDestroy(e);
   for (size_t l = 1; l < x->lanes.size(); ++l) cudaStreamDestroy(x->lanes[l]);

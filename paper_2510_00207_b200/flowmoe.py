@@ -31,7 +31,7 @@ EXPORTED = [
 ]
 EXPORTED_TEST = [
     "flowmoe_saved_routing_offsets", "flowmoe_debug_set", "flowmoe_test_gemm", "flowmoe_profile_begin",
-    "flowmoe_profile_end", "flowmoe_kernel_launches", "flowmoe_create_local_group",
+    "flowmoe_profile_end", "flowmoe_kernel_launches", "flowmoe_create_local_group", "flowmoe_test_arrivals",
 ]
 
 
@@ -122,6 +122,7 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_register_saved.argtypes = [vp, vp]
     L.flowmoe_unregister_saved.argtypes = [vp, vp]
     L.flowmoe_check_health.argtypes = [vp]
+    L.flowmoe_test_arrivals.argtypes = [vp, ctypes.POINTER(ctypes.c_uint), sz]
     L.flowmoe_create_local_group.argtypes = [ctypes.POINTER(Config), i32, i32, ctypes.POINTER(vp)]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
     L.flowmoe_saved_routing_offsets.argtypes = [vp] + [ctypes.POINTER(sz)] * 5
@@ -253,6 +254,13 @@ class FlowMoE:
 
     def unregister_saved(self, saved):
         _check(lib().flowmoe_unregister_saved(self.handle, _ptr(saved)), "flowmoe_unregister_saved")
+
+    def arrivals(self) -> np.ndarray:
+        """Peer-memory A2A arrival counters [4 kinds][R][world_size] (flowmoe_test_arrivals)."""
+        n = 4 * self.shape.R * self.shape.world_size
+        buf = (ctypes.c_uint * n)()
+        _check(lib().flowmoe_test_arrivals(self.handle, buf, n), "flowmoe_test_arrivals")
+        return np.array(buf[:], dtype=np.int64).reshape(4, self.shape.R, self.shape.world_size)
 
     def check_health(self):
         _check(lib().flowmoe_check_health(self.handle), "flowmoe_check_health")

@@ -188,12 +188,16 @@ def chain_per_block_errors(cfg, reps, forced, dy_top, g, rank=0, P=1):
 
 def run_group_gpu(cfg: BlockConfig, rep: dict, wks: list, *, forced: bool = True, chunk_bytes: int = 4096 + 16,
                   compute_streams: int = 1, schedule: str = "flowmoe", repeat: int = 2, device: int = 0,
-                  stack_reps: list | None = None, graph: bool = False) -> list:
+                  stack_reps: list | None = None) -> list:
     """P = len(wks) ranks of one block (or, with stack_reps, an L-block stack through the
     stack API) in the in-process simulated world on ONE GPU (flowmoe_create_local_group):
-    the real peer-memory A2A kernels exchange between the ranks' buffers and the all-reduce
-    runs the S_p chunk loop.  Each phase is enqueued for every rank before anything waits.
-    repeat > 1 re-runs the iteration (arrival counters advance).  Returns per-rank results."""
+    the real peer-memory A2A send kernels move the blocks between the ranks' buffers and the
+    all-reduce runs the S_p chunk loop.  Every rank is driven by its own host thread (the
+    exchanges meet at host barriers; no kernel waits for another launch), the all-reduce
+    waits run once every rank's backward is enqueued.  repeat > 1 re-runs the iteration.
+    Returns per-rank results, incl. the A2A arrival counters."""
+    import threading
+
     import torch
     P = len(wks)
     dev = torch.device("cuda", device)
@@ -219,41 +223,39 @@ def run_group_gpu(cfg: BlockConfig, rep: dict, wks: list, *, forced: bool = True
                 for q in range(P)]
         for q in range(P):
             ctxs[q].set_forced_routing(fidx[q])
+    s = torch.cuda.current_stream()
+    torch.cuda.synchronize()
 
-    def iteration(s):
-        tickets = [[] for _ in range(P)]
+    def rank_fwd_bwd(q, tickets):
+        torch.cuda.set_device(dev)
         if stack_reps is not None:
-            for q in range(P):
-                ctxs[q].stack_fwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], s)
-            for q in range(P):
-                tickets[q] = ctxs[q].stack_bwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], dys[q],
-                                               dxs[q], [b.grads for b in bts[q]], chunk_bytes, s)
+            ctxs[q].stack_fwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], s)
+            tickets[q] = ctxs[q].stack_bwd([b.params for b in bts[q]], xs[q][0], xs[q][1:], saved[q], dys[q],
+                                           dxs[q], [b.grads for b in bts[q]], chunk_bytes, s)
         else:
-            for q in range(P):
-                ctxs[q].block_fwd(bts[q][0].params, xs[q][0], xs[q][1], saved[q][0], s)
-            for q in range(P):
-                tickets[q] = [ctxs[q].block_bwd(bts[q][0].params, xs[q][0], saved[q][0], dys[q], dxs[q][0],
-                                                bts[q][0].grads, chunk_bytes, s)]
+            ctxs[q].block_fwd(bts[q][0].params, xs[q][0], xs[q][1], saved[q][0], s)
+            tickets[q] = [ctxs[q].block_bwd(bts[q][0].params, xs[q][0], saved[q][0], dys[q], dxs[q][0],
+                                            bts[q][0].grads, chunk_bytes, s)]
+
+    for _ in range(repeat):
+        tickets, errs = [None] * P, [None] * P
+
+        def body(q):
+            try:
+                rank_fwd_bwd(q, tickets)
+            except BaseException as e:  # re-raised below
+                errs[q] = e
+        th = [threading.Thread(target=body, args=(q,)) for q in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
         for q in range(P):
             for t in tickets[q]:
                 ctxs[q].allreduce_wait(t, s)
-
-    s = torch.cuda.current_stream()
-    for _ in range(repeat):
-        iteration(s)
-    gr = None
-    if graph:  # the P ranks' whole iteration captured into one graph and replayed twice
-        for q in range(P):
-            for bt in bts[q]:
-                for v in bt.g.values():
-                    v.fill_(7.0)
-        gr = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(s)
-        with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
-            iteration(torch.cuda.current_stream())
-        gr.replay()
-        gr.replay()
     torch.cuda.synchronize()
     for c in ctxs:
         c.check_health()
@@ -275,10 +277,8 @@ def run_group_gpu(cfg: BlockConfig, rep: dict, wks: list, *, forced: bool = True
             "idx": view(off["idx"], T * k, torch.int32).reshape(T, k),
             "pos": view(off["pos"], T * k, torch.int32).reshape(T, k),
             "counts": view(off["counts"], R * E, torch.int32).reshape(R, E),
+            "arrivals": ctxs[q].arrivals(),
         })
-    if gr is not None:
-        del gr
-        torch.cuda.synchronize()
     for c in ctxs:
         c.close()
     return out
