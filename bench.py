@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="flowmoe", choices=["flowmoe", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(LAYERS))
+    ap.add_argument("--config", default="dsv2s", choices=sorted(LAYERS),
+                    help="workload (default: configs[4] DeepSeek-V2-S-shaped, the largest single-GPU config)")
     ap.add_argument("--layers", type=int, default=0, help="blocks in the stack (default per config)")
     ap.add_argument("--R", type=int, default=0, help="override pipelining degree")
     ap.add_argument("--chunk-bytes", type=int, default=0, help="S_p (default per config)")

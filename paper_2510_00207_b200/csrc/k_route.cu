@@ -358,8 +358,9 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
   const int rs = nt + nt / 32;
   const int my = tid + (tid >> 5);
   // a thread's slots (slot-major: s = j·T + t) are loaded once, all in flight together,
-  // and kept in registers for both passes when they fit (seg <= SCAN_REG)
-  constexpr int SCAN_REG = 8;
+  // and kept in registers for both passes when they fit (seg <= SCAN_REG): a dependent
+  // L2 round trip per slot (the loop below) cost ~20 µs at T_r·k = 4096 slots
+  constexpr int SCAN_REG = 32;
   const bool in_reg = seg <= SCAN_REG;
   int ev[SCAN_REG];
 #pragma unroll
@@ -487,61 +488,80 @@ int permute_pack(int dtype, const void* a, const int32_t* src, void* send, int E
   return (int)cudaGetLastError();
 }
 
-// K7: out[t] = Σ_j w_tj·Y[e_tj][pos_tj] (+ resid[t]); thread = (token, 16-byte vector)
-template <typename T>
-__global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* y, const int32_t* idx,
-                                                                const int32_t* pos, const float* w,
-                                                                const T* resid, T* out, int T_,
-                                                                int M, int k, int ldE) {
+// K7: out[t] = Σ_j w_tj·Y[e_tj][pos_tj] (+ resid[t]); thread = (token, 16-byte vector).
+// K compile-time: the routing of all K slots, then all K rows and the residual are
+// requested before any is used (one dependent round trip for the routing, one for the
+// rows), summed in slot order.
+template <typename T, int K>
+__global__ void __launch_bounds__(256) unpermute_combine_kernel(const T* __restrict__ y, const int32_t* __restrict__ idx,
+                                                                const int32_t* __restrict__ pos,
+                                                                const float* __restrict__ w,
+                                                                const T* __restrict__ resid, T* __restrict__ out,
+                                                                int T_, int M, int ldE) {
   FM_PDL_ENTRY();
   constexpr int V = 16 / sizeof(T);
   const int nv = M / V;
   const unsigned int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (unsigned int)(T_ * nv)) return;
   const int t = (int)(g / (unsigned int)nv), m = (int)(g % (unsigned int)nv) * V;
+  int pj[K], ej[K];
+  float wj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    pj[j] = pos[(int64_t)t * K + j];
+    ej[j] = idx[(int64_t)t * K + j];
+    wj[j] = w[(int64_t)t * K + j];
+  }
+  uint4 raw[K], rr = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    raw[j] = make_uint4(0, 0, 0, 0);
+    if (pj[j] >= 0) raw[j] = *reinterpret_cast<const uint4*>(y + ((int64_t)ej[j] * ldE + pj[j]) * M + m);
+  }
+  if (resid) rr = *reinterpret_cast<const uint4*>(resid + (int64_t)t * M + m);
   float acc[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
-  // the first two slots' routing, rows and the residual are all requested before any is
-  // used (two dependent round trips instead of one per slot); same summation order
-  float rv[V];
-  if (resid) load16<T>(resid + (int64_t)t * M + m, rv);
-  const int k2 = k < 2 ? k : 2;
-  int p2[2], e2[2];
-  float w2[2], v2[2][V];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int64_t o = (int64_t)t * k + (j < k2 ? j : 0);
-    p2[j] = j < k2 ? pos[o] : -1;
-    e2[j] = idx[o];
-    w2[j] = w[o];
-  }
+  for (int j = 0; j < K; ++j)
+    if (pj[j] >= 0) {
+      float v[V];
+      load16<T>(reinterpret_cast<const T*>(&raw[j]), v);
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const T* src = y + ((int64_t)e2[j] * ldE + (p2[j] < 0 ? 0 : p2[j])) * M + m;
-    if (p2[j] >= 0) load16<T>(src, v2[j]);
-    else
-#pragma unroll
-      for (int i = 0; i < V; ++i) v2[j][i] = 0.f;
-  }
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-    if (p2[j] >= 0)
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = fmaf(w2[j], v2[j][i], acc[i]);
-  for (int j = 2; j < k; ++j) {
-    const int p = pos[(int64_t)t * k + j];
-    if (p < 0) continue;
-    const float wj = w[(int64_t)t * k + j];
-    float v[V];
-    load16<T>(y + ((int64_t)idx[(int64_t)t * k + j] * ldE + p) * M + m, v);
-#pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = fmaf(wj, v[i], acc[i]);
-  }
-  if (resid)
+      for (int i = 0; i < V; ++i) acc[i] = fmaf(wj[j], v[i], acc[i]);
+    }
+  if (resid) {
+    float rv[V];
+    load16<T>(reinterpret_cast<const T*>(&rr), rv);
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] += rv[i];
+  }
   store16<T>(out + (int64_t)t * M + m, acc);
+}
+
+template <typename T, int K>
+static void unpermute_combine_launch(const void* y, const int32_t* idx, const int32_t* pos, const float* w,
+                                     const void* resid, void* out, int T_, int M, int ldE, cudaStream_t s) {
+  const int64_t n = (int64_t)T_ * (M / (16 / (int)sizeof(T)));
+  launch_k(unpermute_combine_kernel<T, K>, (unsigned)((n + 255) / 256), 256, 0, s, (const T*)y, idx, pos, w,
+           (const T*)resid, (T*)out, T_, M, ldE);
+}
+
+template <typename T>
+static int unpermute_combine_t(const void* y, const int32_t* idx, const int32_t* pos, const float* w,
+                               const void* resid, void* out, int T_, int M, int k, int ldE, cudaStream_t s) {
+  switch (k) {
+    case 1: unpermute_combine_launch<T, 1>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 2: unpermute_combine_launch<T, 2>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 3: unpermute_combine_launch<T, 3>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 4: unpermute_combine_launch<T, 4>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 5: unpermute_combine_launch<T, 5>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 6: unpermute_combine_launch<T, 6>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 7: unpermute_combine_launch<T, 7>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    case 8: unpermute_combine_launch<T, 8>(y, idx, pos, w, resid, out, T_, M, ldE, s); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
+  return 0;
 }
 
 int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_t* pos,
@@ -550,13 +570,9 @@ int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_
   if (T_ <= 0) return 0;
   const int64_t n = (int64_t)T_ * (M / (dtype == DT_F32 ? 4 : 8));
   if (n >= (1ll << 31)) return (int)cudaErrorInvalidValue;
-  dim3 grid((unsigned)((n + 255) / 256));
-  if (dtype == DT_F32)
-    launch_k(unpermute_combine_kernel<float>, grid, 256, 0, s, (const float*)y, idx, pos, w,
-             (const float*)resid, (float*)out, T_, M, k, ldE);
-  else
-    launch_k(unpermute_combine_kernel<bf16>, grid, 256, 0, s, (const bf16*)y, idx, pos, w,
-             (const bf16*)resid, (bf16*)out, T_, M, k, ldE);
+  const int rc = dtype == DT_F32 ? unpermute_combine_t<float>(y, idx, pos, w, resid, out, T_, M, k, ldE, s)
+                                 : unpermute_combine_t<bf16>(y, idx, pos, w, resid, out, T_, M, k, ldE, s);
+  if (rc) return rc;
   return (int)cudaGetLastError();
 }
 
@@ -566,11 +582,12 @@ int unpermute_combine(int dtype, const void* y, const int32_t* idx, const int32_
 // pass, reduction of the K dots over the token's warps in a fixed order; CTAs past the
 // token CTAs zero 8 padding rows of dY each.
 template <typename T, int K>
-__global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, const T* y,
-                                                               const int32_t* idx,
-                                                               const int32_t* pos, const float* w,
-                                                               const int32_t* src, T* dy,
-                                                               float* dw, int T_, int M,
+__global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* __restrict__ dout, const T* __restrict__ y,
+                                                               const int32_t* __restrict__ idx,
+                                                               const int32_t* __restrict__ pos,
+                                                               const float* __restrict__ w,
+                                                               const int32_t* __restrict__ src, T* __restrict__ dy,
+                                                               float* __restrict__ dw, int T_, int M,
                                                                int rows, int C, int ldE, int tpt) {
   __shared__ float red[8][K];  // [warp][slot]
   FM_PDL_ENTRY();
@@ -600,13 +617,19 @@ __global__ void __launch_bounds__(256) combine_bwd_pack_kernel(const T* dout, co
     dot[j] = 0.f;
   }
   for (int v = gt; tok && v < nv; v += tpt) {
+    // dO and all K rows of Y requested together (K + 1 loads in flight), then used
+    const uint4 graw = *reinterpret_cast<const uint4*>(g + v * V);
+    uint4 yraw[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      yraw[j] = row[j] < 0 ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(y + row[j] + v * V);
     float gv[V];
-    load16<T>(g + v * V, gv);
+    load16<T>(reinterpret_cast<const T*>(&graw), gv);
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (row[j] < 0) continue;  // dropped slot: contributes 0, so dw = 0
       float yv[V], o[V];
-      load16<T>(y + row[j] + v * V, yv);
+      load16<T>(reinterpret_cast<const T*>(&yraw[j]), yv);
 #pragma unroll
       for (int i = 0; i < V; ++i) { dot[j] = fmaf(gv[i], yv[i], dot[j]); o[i] = wj[j] * gv[i]; }
       store16<T>(dy + row[j] + v * V, o);
@@ -792,12 +815,140 @@ __global__ void __launch_bounds__(256) gather_gate_bwd_kernel(
   }
 }
 
+// Wide rows (M/V >= 64 column vectors): one thread per (token, 16-byte column vector), all
+// K gathered rows requested at once (K compile-time) so every thread has K + 1 loads in
+// flight — the per-slot loop above left a thread one dependent load at a time, 11% of HBM
+// at k = 8 (dsv2s).  The token's dlogits are recomputed by each of its threads from
+// warp-uniform loads of its k slots; the Wg rows come from L1/L2.  Same summation order
+// as the kernel above: dlogits·Wgᵀ, then the slots in order, then dO.
+template <typename T, int E, int K>
+__global__ void __launch_bounds__(256) gather_gate_bwd_wide_kernel(
+    const T* __restrict__ dx, const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
+    const float* __restrict__ w, const float* __restrict__ dw, const float* __restrict__ logits,
+    const T* __restrict__ wg, const T* __restrict__ dres, T* __restrict__ dA, float* __restrict__ dlogits, int T_,
+    int M, int ldE) {
+  constexpr int V = 16 / sizeof(T);
+  FM_PDL_ENTRY();
+  const int nv = M / V;
+  const unsigned int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (unsigned int)T_ * (unsigned int)nv) return;
+  const int t = (int)(g / (unsigned int)nv), cvec = (int)(g % (unsigned int)nv), m = cvec * V;
+  int ej[K], pj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    ej[j] = idx[(int64_t)t * K + j];
+    pj[j] = pos[(int64_t)t * K + j];
+  }
+  uint4 raw[K], rres = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    raw[j] = make_uint4(0, 0, 0, 0);
+    if (pj[j] >= 0) raw[j] = *reinterpret_cast<const uint4*>(dx + ((int64_t)ej[j] * ldE + pj[j]) * M + m);
+  }
+  if (dres) rres = *reinterpret_cast<const uint4*>(dres + (int64_t)t * M + m);
+  // dlogits (reading Q5): k>=2: dl_{e_j} = w_j (dw_j - Σ w dw); k=1: dl = p ⊙ (g - <p,g>)
+  float dl[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) dl[e] = 0.f;
+  if constexpr (K == 1) {
+    const float* lt = logits + (int64_t)t * E;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < E; ++e) mx = fmaxf(mx, lt[e]);
+    float den = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { dl[e] = expf(lt[e] - mx); den += dl[e]; }
+    const float g0 = dw[t];
+    float pe0 = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { dl[e] /= den; if (e == ej[0]) pe0 = dl[e]; }
+#pragma unroll
+    for (int e = 0; e < E; ++e) dl[e] = dl[e] * ((e == ej[0] ? g0 : 0.f) - pe0 * g0);
+  } else {
+    float wj[K], dwj[K], inner = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      wj[j] = w[(int64_t)t * K + j];
+      dwj[j] = dw[(int64_t)t * K + j];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) inner += wj[j] * dwj[j];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const float v = wj[j] * (dwj[j] - inner);
+      // predicated adds (an `if` here becomes a dynamically indexed dl[] in local memory)
+#pragma unroll
+      for (int e = 0; e < E; ++e) dl[e] += (e == ej[j]) ? v : 0.f;
+    }
+  }
+  if (cvec == 0)
+#pragma unroll
+    for (int e = 0; e < E; ++e) dlogits[(int64_t)t * E + e] = dl[e];
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    float wr[E];
+    load_n<T, E>(wg + (int64_t)(m + v) * E, wr);
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) sum = fmaf(dl[e], wr[e], sum);
+    acc[v] = sum;
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (pj[j] >= 0) {
+      float v8[V];
+      load16<T>(reinterpret_cast<const T*>(&raw[j]), v8);
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] += v8[v];
+    }
+  if (dres) {
+    float v8[V];
+    load16<T>(reinterpret_cast<const T*>(&rres), v8);
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] += v8[v];
+  }
+  store16<T>(dA + (int64_t)t * M + m, acc);
+}
+
+template <typename T, int E, int K>
+static void gather_gate_bwd_wide_launch(const void* dx, const int32_t* idx, const int32_t* pos, const float* w,
+                                        const float* dw, const float* logits, const void* wg, const void* dres,
+                                        void* dA, float* dlogits, int T_, int M, int ldE, cudaStream_t s) {
+  const int64_t n = (int64_t)T_ * (M / (16 / (int)sizeof(T)));
+  launch_k(gather_gate_bwd_wide_kernel<T, E, K>, (unsigned)((n + 255) / 256), 256, 0, s, (const T*)dx, idx, pos, w,
+           dw, logits, (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, ldE);
+}
+
+template <typename T, int E>
+struct GgbWide {
+  template <int K>
+  static void run(const void* dx, const int32_t* idx, const int32_t* pos, const float* w, const float* dw,
+                  const float* logits, const void* wg, const void* dres, void* dA, float* dlogits, int T_, int M,
+                  int ldE, cudaStream_t s) {
+    gather_gate_bwd_wide_launch<T, E, K>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s);
+  }
+};
+
 template <typename T, int E>
 static void gather_gate_bwd_launch_t(const void* dx, const int32_t* idx, const int32_t* pos, const float* w,
                                      const float* dw, const float* logits, const void* wg, const void* dres,
                                      void* dA, float* dlogits, int T_, int M, int k, int ldE, cudaStream_t s) {
   constexpr int V = 16 / sizeof(T), TPLX = GgbTile<E>::TPL;
   const int nvec = M / V;
+  if (nvec >= 64 && E <= 32) {  // wide rows: one thread per (token, column vector), K loads in flight
+    switch (k) {
+      case 1: GgbWide<T, E>::template run<1>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 2: GgbWide<T, E>::template run<2>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 3: GgbWide<T, E>::template run<3>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 4: GgbWide<T, E>::template run<4>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 5: GgbWide<T, E>::template run<5>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 6: GgbWide<T, E>::template run<6>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 7: GgbWide<T, E>::template run<7>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      case 8: GgbWide<T, E>::template run<8>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s); return;
+      default: break;
+    }
+  }
   int cv = (nvec + 31) / 32 * 32;  // column-vector lanes per token group
   if (cv > 256) cv = 256;
   const int tg = 256 / cv, ctiles = (nvec + cv - 1) / cv;

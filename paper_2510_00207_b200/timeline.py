@@ -61,11 +61,35 @@ def short_name(name: str) -> str:
     return (m.group(1) if m else n)[:80]
 
 
-def analyze(trace_path: str, n_iters: int, trim: int = 0) -> dict:
+# CUDA kernel name -> the kernel group the library's per-call-site profile uses
+# (flowmoe_profile_* names: gemm_* -> "gemm", attn_fwd, attn_bwd, gate_topk, ...)
+_GROUPS = (("gemm_tc_kernel", "gemm"), ("gemm_simt", "gemm"), ("attn_fwd", "attn_fwd"),
+           ("attn_bwd", "attn_bwd"), ("gate_topk", "gate_topk"), ("gate_route", "gate_topk"),
+           ("route_scan", "route_scan"), ("unpermute_combine", "unpermute_combine"),
+           ("permute_pack", "permute_pack"), ("combine_bwd_pack", "combine_bwd_pack"),
+           ("gather_gate_bwd", "gather_gate_bwd"), ("gate_wgrad", "gate_wgrad"), ("colsum", "colsum"),
+           ("a2a_p2p", "a2a"), ("local_allreduce", "allreduce"))
+
+
+def kernel_group(name: str) -> str:
+    if is_comm(name) and "a2a_p2p" not in name:
+        return "nccl"
+    for needle, g in _GROUPS:
+        if needle in name:
+            return g
+    return "other"
+
+
+def analyze(trace_path: str, n_iters: int, trim: int = 0, a2a_bytes: float = 0.0, link_gbs: float = 770.0) -> dict:
     """Interval statistics of the traced kernels.  With trim > 0 the first and last
     `trim` iterations' worth of time are cut off (kernel intervals clipped to the
     middle window), so rank skew at the edges of the trace (NCCL kernels spinning
-    on a late peer) does not count as exposed communication."""
+    on a late peer) does not count as exposed communication.
+
+    A peer-memory exchange kernel copies first and then waits for the peers' arrivals; the
+    wait is time spent on a slower peer (its compute or its copy), not on this rank's
+    transfer.  With a2a_bytes (bytes one exchange moves over NVLink) the "transfer-only"
+    exposure also counts each exchange kernel only over its first a2a_bytes / link_gbs."""
     ev = json.load(open(trace_path))
     ev = ev["traceEvents"] if isinstance(ev, dict) else ev
     kern = [e for e in ev if e.get("cat") == "kernel" and "dur" in e]
@@ -94,8 +118,25 @@ def analyze(trace_path: str, n_iters: int, trim: int = 0) -> dict:
         k = short_name(e["name"])
         per[k][0] += 1
         per[k][1] += e["dur"]
+    by_group = collections.defaultdict(list)
+    for e in kern:
+        by_group[kernel_group(e["name"])].append((e["ts"], e["ts"] + e["dur"]))
+    groups = {g: {"launches_per_iter": len(iv) / n_iters,
+                  "sum_us_per_iter": sum(b - a for a, b in iv) / n_iters,
+                  "busy_us_per_iter": _length(_union(iv)) / n_iters}
+              for g, iv in by_group.items()}
     comm_us = _length(uc)
     exposed_us = _subtract(uc, up)
+    xfer = []
+    for e in kern:
+        if not is_comm(e["name"]):
+            continue
+        d = e["dur"]
+        if "a2a_p2p" in e["name"] and a2a_bytes > 0:
+            d = min(d, a2a_bytes / (link_gbs * 1e3))  # bytes / (GB/s) in us
+        xfer.append((e["ts"], e["ts"] + d))
+    ux = _union(xfer)
+    xfer_us, exposed_xfer_us = _length(ux), _subtract(ux, up)
     span_us = t1 - t0
     return {
         "iterations": n_iters,
@@ -106,13 +147,17 @@ def analyze(trace_path: str, n_iters: int, trim: int = 0) -> dict:
         "exposed_comm_frac_of_comm": (exposed_us / comm_us) if comm_us > 0 else None,
         "exposed_comm_frac_of_iter": exposed_us / span_us if span_us > 0 else None,
         "idle_us_per_iter": (span_us - _length(busy)) / n_iters,
+        "transfer_comm_us_per_iter": xfer_us / n_iters,
+        "exposed_transfer_us_per_iter": exposed_xfer_us / n_iters,
+        "exposed_transfer_frac_of_transfer": (exposed_xfer_us / xfer_us) if xfer_us > 0 else None,
         "kernels_per_iter": len(kern) / n_iters,
+        "groups": groups,
         "top_kernels": sorted(([k, c // n_iters, d / n_iters] for k, (c, d) in per.items()),
                               key=lambda x: -x[2])[:25],
     }
 
 
-def trace_replays(run, n_iters: int, path: str, trim: int = 0, sync=None):
+def trace_replays(run, n_iters: int, path: str, trim: int = 0, sync=None, a2a_bytes: float = 0.0):
     """Run `run()` n_iters times under torch.profiler (CUDA activities) and write a chrome trace.
     `sync()` (e.g. a process-group barrier) runs once the profiler is live, so ranks whose
     CUPTI start-up took different times still enter the traced replays together."""
@@ -127,4 +172,4 @@ def trace_replays(run, n_iters: int, path: str, trim: int = 0, sync=None):
             run()
         torch.cuda.synchronize()
     prof.export_chrome_trace(path)
-    return analyze(path, n_iters, trim)
+    return analyze(path, n_iters, trim, a2a_bytes=a2a_bytes)

@@ -52,6 +52,12 @@ CASES = {
                               capacity_factor=1.0, causal=1, residual=0, P=1, dtype="bf16"),
     "scan_wide_chunk": BlockConfig(T=4096, seq_len=256, M=128, n_heads=2, E=8, top_k=2, d_ffn=128, R=2,
                                    capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    # T_r·k = 9216 slots > 32 per thread of the fused scan: its streaming (non-register) path
+    "scan_beyond_reg": BlockConfig(T=4608, seq_len=256, M=128, n_heads=2, E=8, top_k=4, d_ffn=128, R=2,
+                                   capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
+    # k = 8 of 16 with wide rows (the dsv2s routing shape at a small M): wide gather kernels
+    "bf16_k8_wide": BlockConfig(T=512, seq_len=256, M=512, n_heads=4, E=16, top_k=8, d_ffn=256, R=2,
+                                capacity_factor=1.0, causal=1, residual=1, P=1, dtype="bf16"),
 }
 
 
@@ -114,7 +120,8 @@ def test_token_chunk_parity(name):
 
 
 @pytest.mark.parametrize("name", ["c1_f32", "bf16_small", "c2_bench", "bf16_k3_dh128", "f32_k1",
-                                  "gate_e32_k8", "gate_e64_k4", "gate_e2_k1", "scan_wide_chunk"])
+                                  "gate_e32_k8", "gate_e64_k4", "gate_e2_k1", "scan_wide_chunk",
+                                  "scan_beyond_reg", "bf16_k8_wide"])
 def test_routing_bitexact_given_gpu_logits(name):
     """Natural routing: the oracle routes from the GPU's own fp32 logits; indices,
     positions and per-chunk counts must match bit for bit, weights to fp32 rounding."""
@@ -142,7 +149,7 @@ def test_routing_crafted_ties(name):
     rep = gen_replicated(cfg)
     E = cfg.E
     wg = rep["wg"].copy()
-    pairs = [(0, E - 1), (1, E // 2 + 1), (2, 3)] if E >= 8 else [(0, E - 1), (1, E - 2)]
+    pairs = [(0, E - 1), (1, E // 2 + 1), (2, 3)] if E >= 8 else [(0, E - 1)]
     for lo, hi in pairs:
         wg[:, hi] = wg[:, lo]
     g = run_block_gpu(cfg, dict(rep, wg=wg), wk, forced=False)
@@ -155,8 +162,11 @@ def test_routing_crafted_ties(name):
     decided = sum(int(np.sum(np.any(g["idx"] == lo, axis=1) & ~np.any(g["idx"] == hi, axis=1)))
                   for lo, hi in pairs)
     assert decided > 0, "some token must sit on a tie at the k-th place"
-    for lo, hi in pairs:  # the higher index never wins a tie against the lower one
+    for lo, hi in pairs:  # the higher index never wins a tie against the lower one ...
         assert not np.any(np.any(g["idx"] == hi, axis=1) & ~np.any(g["idx"] == lo, axis=1))
+        both = np.any(g["idx"] == lo, axis=1) & np.any(g["idx"] == hi, axis=1)
+        slot = lambda e: np.argmax(g["idx"][both] == e, axis=1)  # noqa: E731
+        assert np.all(slot(lo) < slot(hi))  # ... and takes the earlier slot when both are picked
     g = run_block_gpu(cfg, dict(rep, wg=np.repeat(rep["wg"][:, :1], E, axis=1)), wk, forced=False)
     assert np.array_equal(g["idx"], np.tile(np.arange(cfg.top_k, dtype=np.int32), (cfg.T, 1)))
     want_w = 1.0 / cfg.top_k if cfg.top_k > 1 else 1.0 / E
