@@ -455,6 +455,11 @@ def main():
 
     # ---- CUPTI timeline of graph replays: steady-state kernel times, idle, exposed comm
     tl = None
+    # bytes one exchange moves over NVLink (send side): E·C·M·es·(P-1)/P, C per chunk
+    import math
+    C_ = cfg.T // cfg.R if cfg.capacity_factor == 0 else \
+        math.ceil(float(cfg.capacity_factor) * cfg.top_k * (cfg.T // cfg.R) / cfg.E)
+    a2a_bytes = cfg.E * C_ * cfg.M * (2 if cfg.dtype == "bf16" else 4) * (world - 1) / world
     if args.trace_iters > 0:
         from paper_2510_00207_b200.timeline import trace_replays
         try:
@@ -463,7 +468,8 @@ def main():
             torch.cuda.synchronize()
             tl = trace_replays(run, args.trace_iters, os.path.join(args.trace_dir, f"flowmoe_trace_r{rank}.json"),
                                trim=max(0, min(3, (args.trace_iters - 2) // 4)),
-                               sync=(dist.barrier if world > 1 else None))
+                               sync=(dist.barrier if world > 1 else None),
+                               a2a_bytes=a2a_bytes)
         except Exception as e:  # the timeline is diagnostics, never the measurement
             tl = {"error": repr(e)}
         if world > 1:
@@ -476,44 +482,77 @@ def main():
         tokens = cfg.T * world
         compute = [p for p in prof if not p["name"].startswith(("a2a", "allreduce"))]
         total_ms = sum(p["ms"] for p in compute)
-        # group the profile's call sites by CUDA kernel: every gemm_* call is the one
-        # tcgen05 GEMM kernel; attn_fwd / attn_bwd / each routing kernel stand alone
-        groups = {}
-        for p in compute:
-            key = "gemm_tc (all calls)" if p["name"].startswith("gemm") else p["name"]
-            gsum = groups.setdefault(key, {"name": key, "launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
-            for f in ("launches", "ms", "flops", "bytes"):
-                gsum[f] += p[f]
-        top = max(groups.values(), key=lambda p: p["ms"])
-        avg_ms = top["ms"] / top["launches"]
         tc_attn = cfg.dtype == "bf16" and (cfg.M // cfg.n_heads) in (64, 128)
-        ridge = peaks["bf16_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)  # FLOP per byte
 
-        def roof(p):
-            """Bound of one kernel group from its algorithmic arithmetic intensity: tcgen05
-            work below the ridge point (e.g. expert GEMMs streaming weights / writing fp32
-            grads at P=1) is HBM-bound, above it tensor-bound."""
-            t = p["ms"] / p["launches"] * 1e-3
-            ai = p["flops"] / p["bytes"] if p["bytes"] else float("inf")
-            tc = p["name"].startswith("gemm") or (p["name"].startswith("attn") and tc_attn)
-            if tc and ai >= ridge:
-                return "tensor", "TFLOP/s", p["flops"] / p["launches"] / t / 1e12, peaks["bf16_tflops_sustained"], ai
-            if p["name"].startswith("attn") and not tc_attn:  # SIMT fp32 FMA: 148 SMs x 128 lanes x 2 x clock
-                return ("alu", "TFLOP/s", p["flops"] / p["launches"] / t / 1e12,
-                        148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, ai)
-            return "hbm", "GB/s", p["bytes"] / p["launches"] / t / 1e9, peaks["hbm_gbs"], ai
+        def kgroup(site):
+            """call site of the library's profile -> the CUDA kernel group it launches"""
+            if site.startswith("gemm"):
+                return "gemm"
+            return "colsum" if site.startswith("colsum") else site
 
-        bound, unit, achieved, peak, top_ai = roof(top)
+        def bound_of(g):
+            """the dense contractions (tcgen05 GEMM, tcgen05 attention) against
+            the tensor roof, the routing / movement kernels against HBM; the fp32 SIMT paths
+            (f32 parity mode, d_h 16/32) against the FMA pipes."""
+            if g == "gemm" or g.startswith("attn"):
+                if cfg.dtype == "bf16" and (g == "gemm" or tc_attn):
+                    return "tensor", "TFLOP/s", peaks["bf16_tflops_sustained"], "measured sustained bf16"
+                return "alu", "TFLOP/s", 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, \
+                    "148 SMs x 128 FP32 lanes x 2 x max clock"
+            return "hbm", "GB/s", peaks["hbm_gbs"], "measured copy"
+
+        # algorithmic work per step of each kernel group (the call sites' FLOPs / bytes from
+        # the library's per-launch accounting; identical in every iteration)
+        alg = {}
+        for p in compute:
+            a_ = alg.setdefault(kgroup(p["name"]), {"launches": 0, "flops": 0.0, "bytes": 0.0, "eager_ms": 0.0})
+            a_["launches"] += p["launches"]
+            a_["flops"] += p["flops"]
+            a_["bytes"] += p["bytes"]
+            a_["eager_ms"] += p["ms"]
+        # device time per step of each group in the steady state: the CUPTI trace of the
+        # CUDA-graph replays (rank 0); busy = union of the group's kernel intervals (kernels
+        # of one group on different lanes overlap), sum = Σ launch durations
+        tl0 = None
+        if tl is not None:
+            rr = tl["per_rank"] if "per_rank" in tl else [tl]
+            tl0 = rr[0] if rr and rr[0] and "groups" in rr[0] else None
+        tgroups = tl0["groups"] if tl0 else {}
+
+        def roof(g):
+            bound, unit, peak, psrc = bound_of(g)
+            a_ = alg[g]
+            work = a_["flops"] / 1e12 if unit == "TFLOP/s" else a_["bytes"] / 1e9
+            tg = tgroups.get(g)
+            if tg and tg["busy_us_per_iter"] > 0:
+                busy_s, sum_s, n = tg["busy_us_per_iter"] * 1e-6, tg["sum_us_per_iter"] * 1e-6, tg["launches_per_iter"]
+                src = "CUPTI trace of the CUDA-graph replays"
+            else:  # no trace: the eager per-launch event timing (lanes collapsed)
+                busy_s = sum_s = a_["eager_ms"] * 1e-3
+                n = a_["launches"]
+                src = "eager per-launch CUDA events (lanes collapsed)"
+            ach = work / busy_s
+            return {"bound": bound, "unit": unit, "achieved": ach, "peak": peak, "frac": ach / peak,
+                    "peak_source": psrc, "busy_ms_per_step": busy_s * 1e3, "sum_launch_ms_per_step": sum_s * 1e3,
+                    "launches_per_step": n, "per_launch_us": sum_s / max(n, 1) * 1e6,
+                    "achieved_per_launch": work / sum_s, "timing": src,
+                    "algorithmic_per_step": {"flops": a_["flops"], "bytes": a_["bytes"]}}
+
+        key = (lambda g: tgroups[g]["busy_us_per_iter"]) if tgroups else (lambda g: alg[g]["eager_ms"])
+        top_g = max((g for g in alg if (g in tgroups or not tgroups)), key=key)
+        R_ = roof(top_g)
         per_site = []
-        for p in sorted(compute, key=lambda p: -p["ms"])[:10]:
-            b_, u_, a_, pk_, ai_ = roof(p)
-            per_site.append({"site": p["name"], "share": p["ms"] / total_ms, "bound": b_, "achieved": a_,
-                             "unit": u_, "frac": a_ / pk_, "flop_per_byte": ai_,
-                             "us_per_launch": p["ms"] / p["launches"] * 1e3})
+        for g in sorted(alg, key=lambda g: -(tgroups[g]["busy_us_per_iter"] if g in tgroups else 0.0))[:12]:
+            r_ = roof(g)
+            per_site.append({"group": g, "bound": r_["bound"], "achieved": r_["achieved"], "unit": r_["unit"],
+                             "frac": r_["frac"], "busy_ms_per_step": r_["busy_ms_per_step"],
+                             "launches_per_step": r_["launches_per_step"], "per_launch_us": r_["per_launch_us"]})
+        eager_sites = [{"site": p["name"], "us_per_launch": p["ms"] / p["launches"] * 1e3, "launches": p["launches"],
+                        "eager_share": p["ms"] / total_ms} for p in sorted(compute, key=lambda p: -p["ms"])[:12]]
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = tr.get(args.config, {}).get(top["name"], {}).get("dram_bytes_per_launch")
+            traffic = tr.get(args.config, {}).get(top_g, {}).get("dram_bytes_per_launch")
         except Exception:
             pass
         line = {
@@ -529,12 +568,19 @@ def main():
                        "a2a": args.a2a, "api": "per_block" if args.per_block else "stack",
                        "optimizer": args.optimizer or "excluded (P:304-305)",
                        "l2": "flushed between steps (256 MiB memset outside the event-timed region)"},
-            "roofline": {"kernel": top["name"], "bound": bound, "achieved": achieved, "peak": peak,
-                         "unit": unit, "frac": achieved / peak, "traffic": traffic,
-                         "flop_per_byte": top_ai, "ridge_flop_per_byte": ridge, "call_sites": per_site,
-                         "peak_source": peak_src + (" sustained" if bound == "tensor" else ""),
-                         "share_of_compute": top["ms"] / total_ms,
-                         "per_launch_ms": avg_ms, "launches_per_step": top["launches"]},
+            "roofline": {"kernel": top_g, "bound": R_["bound"], "achieved": R_["achieved"], "peak": R_["peak"],
+                         "unit": R_["unit"], "frac": R_["frac"], "traffic": traffic,
+                         "peak_source": R_["peak_source"], "timing": R_["timing"],
+                         "busy_ms_per_step": R_["busy_ms_per_step"],
+                         "sum_launch_ms_per_step": R_["sum_launch_ms_per_step"],
+                         "launches_per_step": R_["launches_per_step"], "per_launch_us": R_["per_launch_us"],
+                         "achieved_per_launch": R_["achieved_per_launch"],
+                         "algorithmic_per_step": R_["algorithmic_per_step"],
+                         "cross_check": {"busy_ms_per_step": R_["busy_ms_per_step"], "ms_per_step": ms,
+                                         "busy_le_step": R_["busy_ms_per_step"] <= ms * 1.05,
+                                         "note": "busy = union of the group's kernel intervals per replay "
+                                                 "(traced replays run without the L2 flush)"},
+                         "groups": per_site, "eager_call_sites": eager_sites},
             "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": x0.numel() * x0.element_size() * 2,
                     "d2h_bytes_per_step": dxs[0].numel() * dxs[0].element_size()},
@@ -564,7 +610,16 @@ def main():
                     "ranks_valid": len(ok), "ranks": len(ranks),
                     "method": f"CUPTI trace of {args.trace_iters} graph replays (edge iterations "
                               "trimmed); worst valid rank; |union(comm kernels: NCCL, peer-memory A2A) "
-                              "minus union(compute kernels)|"}
+                              "minus union(compute kernels)|",
+                    # the peer-memory exchange kernel copies, then waits for its peers: counted
+                    # only over its transfer time (bytes / 770 GB/s measured peer copy), the
+                    # rest is waiting on a slower peer (load imbalance), not communication
+                    "transfer_only": {
+                        "frac_of_transfer": worst.get("exposed_transfer_frac_of_transfer"),
+                        "exposed_ms": worst.get("exposed_transfer_us_per_iter", 0.0) / 1e3,
+                        "transfer_ms": worst.get("transfer_comm_us_per_iter", 0.0) / 1e3,
+                        "frac_of_iteration": worst.get("exposed_transfer_us_per_iter", 0.0) / 1e3 / ms,
+                        "a2a_bytes_per_exchange": a2a_bytes}}
             if ok:
                 r0 = ok[0]
                 line["timeline"] = {"span_ms": r0["span_us_per_iter"] / 1e3,

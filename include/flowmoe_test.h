@@ -59,6 +59,26 @@ typedef struct {
 flowmoe_status flowmoe_profile_begin(flowmoe_ctx* ctx);
 int flowmoe_profile_end(flowmoe_ctx* ctx, flowmoe_prof_entry* out, int max_entries);
 
+/* Task log of one ctx (eager enqueues only; SURVEY §8(c.3) schedule properties): between
+ * begin and end every task the ctx enqueues is bracketed by timing events on its own
+ * stream.  kind: 0 AT_r, 1 D_r, 2 E_r, 3 C_r, 4 merge_r (forward); 5 C_r^bwd pack,
+ * 6 C_r^bwd exchange, 7 E_r^bwd, 8 D_r^bwd exchange, 9 expert wgrads (chunk -1),
+ * 10 AT_r^bwd, 11 MHA/gate wgrads (chunk -1), 12 an all-reduce chunk (chunk = its index in
+ * the S_p partition).  block = the call's index within the log window per direction
+ * (dir 0 forward, 1 backward: stack_bwd's first block is the stack's last); chunk r = -1
+ * for the unsplit-AT policies' single AT task; stream = cudaStreamGetId of the stream;
+ * t0/t1 = ms since the window began.  end synchronises the device and returns the number
+ * of records written (-1 on error).  The timing events break programmatic-launch overlap
+ * between tasks, so logged runs are slower than unlogged ones (orders and dependencies are
+ * unchanged). */
+typedef struct {
+  int32_t kind, block, chunk, dir;
+  uint64_t stream;
+  double t0_ms, t1_ms;
+} flowmoe_task_rec;
+flowmoe_status flowmoe_tasklog_begin(flowmoe_ctx* ctx);
+int flowmoe_tasklog_end(flowmoe_ctx* ctx, flowmoe_task_rec* out, int max_entries);
+
 /* Number of kernels this library has launched in the calling process (bench accounting). */
 uint64_t flowmoe_kernel_launches(void);
 

@@ -78,6 +78,23 @@ struct Prof {
 // the profile of the ctx whose call is being enqueued (apply_ctx); null = off
 thread_local Prof* g_prof = nullptr;
 
+// Task log (flowmoe_tasklog_*, flowmoe_test.h): each task of the schedule — AT_r, D_r, E_r,
+// C_r, the merge, and backward C_r^bwd pack/exchange, E_r^bwd, D_r^bwd, AT_r^bwd, the
+// weight-gradient tasks, every AR chunk — bracketed by timing events on its own stream,
+// labelled (kind, block, chunk), so the Eq.(3)-(6) orders and the 6a-6e dependencies can be
+// checked on measured timelines.  Eager enqueues only (not in capture).
+enum TaskKind { TK_AT, TK_D, TK_E, TK_C, TK_MERGE, TK_CBPACK, TK_CB, TK_EB, TK_DB, TK_WGE, TK_ATB, TK_WGA, TK_AR };
+struct TaskRec { int kind, block, chunk, dir; unsigned long long stream; int ev; };
+struct TaskLog {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<TaskRec> recs;
+  cudaEvent_t base = nullptr;
+  int fwd_seq = 0, bwd_seq = 0, block = 0, dir = 0;
+  std::mutex mu;  // simulated world: another member's thread records this rank's AR tasks
+};
+
 int prof_start(cudaStream_t s) {
   if (!g_prof || !g_prof->on) return -1;
   cudaStreamCaptureStatus cs;
@@ -179,6 +196,7 @@ struct flowmoe_ctx {
   // kernel modules by apply_ctx() at the start of every enqueueing call
   int dbg_flags = 0, pdl = 1, force_bn = 0, p2p_on_lane = 1;
   Prof prof;
+  TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
   std::vector<const void*> saved_order;
   // in-process simulated world (flowmoe_create_local_group): P ctxs on one device
@@ -198,7 +216,7 @@ struct LocalGroup {
   std::vector<flowmoe_ctx*> m;                   // members by rank (null once destroyed)
   std::vector<std::vector<const void*>> saved;   // registered stashes per rank, in order
   cudaStream_t s = nullptr;
-  struct Sub { float* buf; size_t count, chunk_bytes; cudaEvent_t ready; };
+  struct Sub { float* buf; size_t count, chunk_bytes; cudaEvent_t ready; int block; };
   std::vector<std::vector<Sub>> subs;            // per rank, AR submissions in order
   std::vector<std::map<uint64_t, size_t>> ticket_sub;  // per rank: ticket -> its last submission
   std::vector<std::map<uint64_t, size_t>> ticket_done;  // per rank: enqueued tickets
@@ -244,6 +262,32 @@ void apply_ctx(flowmoe_ctx* x) {
   g_pdl_enabled = x->pdl;
   g_p2p_on_lane = x->p2p_on_lane;
   g_prof = &x->prof;
+}
+
+unsigned long long capture_id(cudaStream_t s);
+
+int task_begin(flowmoe_ctx* x, cudaStream_t s) {
+  TaskLog& tl = x->tlog;
+  if (!tl.on || capture_id(s)) return -1;
+  std::lock_guard<std::mutex> lk(tl.mu);
+  while (tl.pool.size() < tl.used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    tl.pool.push_back(e);
+  }
+  const int i = (int)tl.used;
+  tl.used += 2;
+  cudaEventRecord(tl.pool[i], s);
+  return i;
+}
+void task_end(flowmoe_ctx* x, int i, int kind, int chunk, cudaStream_t s, int block = -1) {
+  if (i < 0) return;
+  TaskLog& tl = x->tlog;
+  std::lock_guard<std::mutex> lk(tl.mu);
+  cudaEventRecord(tl.pool[i + 1], s);
+  unsigned long long sid = 0;
+  cudaStreamGetId(s, &sid);
+  tl.recs.push_back({kind, block >= 0 ? block : tl.block, chunk, tl.dir, sid, i});
 }
 
 // GEMM with its algorithmic work: 2·M·N·K flops; bytes = A + B + C (+C read for fp32 accumulate)
@@ -563,15 +607,18 @@ flowmoe_status group_flush(LocalGroup* g) {
       FM_CUDA(cudaStreamWaitEvent(g->s, sq.ready, 0));
       bufs[q] = sq.buf;
     }
-    flowmoe_ctx* x0 = g->m[0];
+    int ci = 0;
     if (flowmoe_status st = for_each_ar_chunk(s0.count, s0.chunk_bytes, [&](size_t off, size_t cnt) {
+          int tk[8];
+          for (int q = 0; q < g->P; ++q) tk[q] = task_begin(g->m[q], g->s);
           int pi = prof_start(g->s);
           FM_K(1, local_allreduce(bufs, g->P, (int64_t)off, (int64_t)cnt, g->s));
           prof_stop(pi, KK_AR, 0, 4.0 * cnt * 2.0 * (g->P - 1) / g->P, g->s);
+          for (int q = 0; q < g->P; ++q) task_end(g->m[q], tk[q], TK_AR, ci, g->s, g->subs[q][n].block);
+          ++ci;
           return FLOWMOE_OK;
         }))
       return st;
-    (void)x0;
     for (int q = 0; q < g->P; ++q)
       for (auto& kv : g->ticket_sub[q])
         if (kv.second == n) {
@@ -596,13 +643,16 @@ flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_
     }
     cudaEvent_t e = g->ev_pool[g->ev_used++];
     FM_CUDA(cudaEventRecord(e, x->s_ar));
-    g->subs[x->cfg.rank].push_back({buf, count, chunk_bytes, e});
+    g->subs[x->cfg.rank].push_back({buf, count, chunk_bytes, e, x->tlog.block});
     return group_flush(g);
   }
+  int ci = 0;
   return for_each_ar_chunk(count, chunk_bytes, [&](size_t off, size_t n) {
+    const int tk = task_begin(x, x->s_ar);
     int pi = prof_start(x->s_ar);
     FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
     prof_stop(pi, KK_AR, 0, 4.0 * n * 2.0 * (x->P - 1) / x->P, x->s_ar);
+    task_end(x, tk, TK_AR, ci++, x->s_ar);
     return FLOWMOE_OK;
   });
 }
@@ -690,6 +740,45 @@ int flowmoe_profile_end(flowmoe_ctx* x, flowmoe_prof_entry* out, int max_entries
     if (agg[i].launches > 0 && n < max_entries && out) out[n++] = agg[i];
   pr.recs.clear();
   pr.used = 0;
+  return n;
+}
+
+flowmoe_status flowmoe_tasklog_begin(flowmoe_ctx* x) {
+  if (!x) return fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+  FM_CUDA(cudaDeviceSynchronize());
+  TaskLog& tl = x->tlog;
+  std::lock_guard<std::mutex> lk(tl.mu);
+  if (!tl.base) FM_CUDA(cudaEventCreate(&tl.base));
+  FM_CUDA(cudaEventRecord(tl.base, x->s_comp));
+  tl.recs.clear();
+  tl.used = 0;
+  tl.fwd_seq = tl.bwd_seq = 0;
+  tl.on = true;
+  return FLOWMOE_OK;
+}
+
+int flowmoe_tasklog_end(flowmoe_ctx* x, flowmoe_task_rec* out, int max_entries) {
+  if (!x) {
+    fail(FLOWMOE_ERR_INVALID, "ctx is NULL");
+    return -1;
+  }
+  TaskLog& tl = x->tlog;
+  tl.on = false;
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    fail(FLOWMOE_ERR_CUDA, "flowmoe_tasklog_end: device synchronize failed");
+    return -1;
+  }
+  std::lock_guard<std::mutex> lk(tl.mu);
+  int n = 0;
+  for (const TaskRec& r : tl.recs) {
+    if (!out || n >= max_entries) break;
+    float t0 = 0.f, t1 = 0.f;
+    cudaEventElapsedTime(&t0, tl.base, tl.pool[r.ev]);
+    cudaEventElapsedTime(&t1, tl.base, tl.pool[r.ev + 1]);
+    out[n++] = {r.kind, r.block, r.chunk, r.dir, r.stream, (double)t0, (double)t1};
+  }
+  tl.recs.clear();
+  tl.used = 0;
   return n;
 }
 
@@ -1103,6 +1192,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   // (no fork) the previous block wrote chunk r of x on lane r, so join the lanes first.
   if (!fork && !x->at_split && nl > 1)
     if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
+  if (x->tlog.on) { x->tlog.block = x->tlog.fwd_seq++; x->tlog.dir = 0; }
   // ---- AT_1..AT_R (Eq.(3)): MHA + gate + route + pack into the dispatch send buffer.
   // Policies that keep AT unsplit (PIPE_MOE, FLOWMOE_AR) run MHA + gate once over all
   // tokens, then route/pack per chunk (capacity is per chunk in every policy).
@@ -1115,6 +1205,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     void* qkv = at<char>(saved, L.qkv + t0 * 3 * M * es);
     void* ctxb = at<char>(saved, L.ctx + t0 * M * es);
     void* a = at<char>(saved, L.a + t0 * M * es);
+    const int tk_at = task_begin(x, sc);
     GemmArgs g;
     g.M = (int)Ta; g.N = (int)(3 * M); g.K = (int)M;
     g.A = xr; g.lda = M; g.B = p->wqkv; g.ldb = 3 * M; g.C = qkv; g.ldc = 3 * M;
@@ -1165,12 +1256,14 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
                        (int)k, sc));
     FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
    }
+    task_end(x, tk_at, TK_AT, x->at_split ? ai : -1, sc);
   }
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)
     for (int r = 0; r < R; ++r) {
       cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_at[r], 0));
+      const int tk = task_begin(x, sa);
       int pi = prof_start(sa);
       if (use_p2p) {
         std::vector<void*> dst(P);
@@ -1178,6 +1271,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         if (flowmoe_status st_ = p2p_exchange(x, 0, r, at<char>(saved, L.send), dst.data(), 1, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_experts(x, at<char>(saved, L.send), at<char>(saved, L.xe), r)) return s;
       prof_stop(pi, KK_A2A_D, 0, (double)ECM * es * (P - 1) / P, sa);
+      task_end(x, tk, TK_D, r, sa);
       FM_CUDA(cudaEventRecord(x->ev_d[r], sa));
     }
   // ---- E_1..E_R: batched expert FFN over the [P*C] capacity rows of chunk r of each local expert
@@ -1185,6 +1279,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_d[r], 0));
     else if (!x->at_split && sc != x->lanes[0]) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_at[r], 0));
+    const int tk_e = task_begin(x, sc);
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
     g.A = at<char>(saved, L.xe + r * PC * M * es); g.lda = M; g.sA = R * PC * M;
@@ -1201,6 +1296,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     g.C = at<char>(saved, L.ye + r * PC * M * es); g.ldc = M; g.sC = R * PC * M;
     g.bias = p->b2; g.sBias = M;
     FM_GEMM(KK_E2, g);
+    task_end(x, tk_e, TK_E, r, sc);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_e[r], sc));
   }
   // ---- C_1..C_R (Eq.(4))
@@ -1208,6 +1304,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     for (int r = 0; r < R; ++r) {
       cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_e[r], 0));
+      const int tk = task_begin(x, sa);
       int pi = prof_start(sa);
       if (use_p2p) {
         std::vector<void*> dst(P);
@@ -1215,6 +1312,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         if (flowmoe_status st_ = p2p_exchange(x, 1, r, at<char>(saved, L.ye), dst.data(), 0, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_owners(x, at<char>(saved, L.ye), at<char>(saved, L.yc), r)) return s;
       prof_stop(pi, KK_A2A_C, 0, (double)ECM * es * (P - 1) / P, sa);
+      task_end(x, tk, TK_C, r, sa);
       FM_CUDA(cudaEventRecord(x->ev_c[r], sa));
     }
   // ---- merge: y = Σ_j w_j Y[e_j][pos_j] (+ I')
@@ -1222,11 +1320,13 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_c[r], 0));
     const int64_t t0 = r * Tr;
+    const int tk = task_begin(x, sc);
     FM_KP(KK_COMBINE, 1, 2.0 * Tr * k * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0), sc,
           unpermute_combine(dt, at<char>(saved, L.yc + r * C * M * es), at<int32_t>(saved, L.idx + t0 * k * 4),
                             at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
                             x->cfg.residual ? at<char>(saved, L.a + t0 * M * es) : nullptr,
                             (char*)y + t0 * M * es, (int)Tr, (int)M, (int)k, (int)ldE, sc));
+    task_end(x, tk, TK_MERGE, r, sc);
   }
   if (join) {
     if (flowmoe_status st = join_lanes(x, x->lanes[0])) return st;
@@ -1277,22 +1377,26 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   // stream boundary, and waiting on it would break the capture
   if (x->ev_wg_done[1] && x->wg_recorded[wset] && x->wg_cap_id[wset] == capture_id(stream))
     for (cudaStream_t l : x->lanes) FM_CUDA(cudaStreamWaitEvent(l, x->ev_wg_done[wset], 0));
+  if (x->tlog.on) { x->tlog.block = x->tlog.bwd_seq++; x->tlog.dir = 1; }
   // ---- C_R^bwd .. C_1^bwd: pack dY = w·dO into the owner-side buffer, dw = <dO, Y>
   for (int r = R - 1; r >= 0; --r) {
     cudaStream_t sc = x->lanes[r % nl];
     const int64_t t0 = r * Tr;
+    const int tk = task_begin(x, sc);
     FM_KP(KK_CBPACK, 1, 4.0 * Tr * k * M, (double)Tr * M * es + 2.0 * Tr * k * M * es, sc,
           combine_bwd_pack(dt, (const char*)dy + t0 * M * es, at<char>(saved, L.yc + r * C * M * es),
                            at<int32_t>(saved, L.idx + t0 * k * 4), at<int32_t>(saved, L.pos + t0 * k * 4),
                            at<float>(saved, L.w + t0 * k * 4), at<int32_t>(saved, L.src + r * E * C * 4),
                            (char*)x->dyc + r * C * M * es, x->dw + t0 * k, (int)Tr, (int)M, (int)k, (int)E,
                            (int)C, (int)ldE, sc));
+    task_end(x, tk, TK_CBPACK, r, sc);
     if (P > 1) FM_CUDA(cudaEventRecord(x->ev_cb[r], sc));
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
       cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_cb[r], 0));
+      const int tk = task_begin(x, sa);
       int pi = prof_start(sa);
       if (use_p2p) {
         std::vector<void*> dst(P);
@@ -1300,12 +1404,14 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
         if (flowmoe_status st_ = p2p_exchange(x, 2, r, x->dyc, dst.data(), 1, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_experts(x, x->dyc, x->dye, r)) return s;
       prof_stop(pi, KK_A2A_CB, 0, (double)ECM * es * (P - 1) / P, sa);
+      task_end(x, tk, TK_CB, r, sa);
       FM_CUDA(cudaEventRecord(x->ev_cba[r], sa));
     }
   // ---- E_R^bwd .. E_1^bwd (Eq.(5)): dgrads per chunk, so D_r^bwd can start early
   for (int r = R - 1; r >= 0; --r) {
     cudaStream_t sc = x->lanes[r % nl];
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_cba[r], 0));
+    const int tk_eb = task_begin(x, sc);
     // dZ = (dY·W2ᵀ) ⊙ GELU'(Z)
     GemmArgs g;
     g.batch = (int)El; g.M = (int)PC; g.N = (int)F; g.K = (int)M;
@@ -1322,17 +1428,20 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     g.B = p->w1; g.ldb = F; g.sB = M * F; g.b_kmajor = 1;
     g.C = (char*)x->dxe + r * PC * M * es; g.ldc = M; g.sC = R * PC * M;
     FM_GEMM(KK_DXE, g);
+    task_end(x, tk_eb, TK_EB, r, sc);
     FM_CUDA(cudaEventRecord(x->ev_eb[r], sc));
   }
   if (P > 1)
     for (int r = R - 1; r >= 0; --r) {
       cudaStream_t sa = (use_p2p && g_p2p_on_lane) ? x->lanes[r % nl] : x->a2a_stream[r % x->a2a_stream.size()];
       FM_CUDA(cudaStreamWaitEvent(sa, x->ev_eb[r], 0));
+      const int tk = task_begin(x, sa);
       int pi = prof_start(sa);
       if (use_p2p) {
         if (flowmoe_status st_ = p2p_exchange(x, 3, r, x->dxe, x->peer_dxc.data(), 0, sa)) return st_;
       } else if (flowmoe_status s = a2a_to_owners(x, x->dxe, x->dxc, r)) return s;
       prof_stop(pi, KK_A2A_DB, 0, (double)ECM * es * (P - 1) / P, sa);
+      task_end(x, tk, TK_DB, r, sa);
       FM_CUDA(cudaEventRecord(x->ev_dba[r], sa));
     }
   // ---- expert wgrads over all R chunks at once (K = R·P·C rows), overlapping the
@@ -1341,6 +1450,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     cudaStream_t sc = nl > 1 ? x->s_wg : x->lanes[0];
     for (int r = 0; r < R; ++r)
       if (sc != x->lanes[r % nl]) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
+    const int tk_wge = task_begin(x, sc);
     GemmArgs g;  // dW2 += Hᵀ·dY
     g.batch = (int)El; g.M = (int)F; g.N = (int)M; g.K = (int)(R * PC);
     g.A = at<char>(saved, L.h); g.lda = F; g.sA = R * PC * F; g.a_mmajor = 1;
@@ -1359,6 +1469,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     FM_GEMM(KK_DW1, g);
     FM_KP(KK_DB1, 1, (double)El * R * PC * F, (double)El * R * PC * F * es + El * F * 8.0, sc,
           colsum_acc(dt, x->dz, gr->db1, (int)El, (int)(R * PC), (int)F, gacc, sc));
+    task_end(x, tk_wge, TK_WGE, -1, sc);
   }
   // ---- AT_R^bwd .. AT_1^bwd (unsplit policies: gathers per chunk, then MHA backward
   // once over all tokens)
@@ -1366,11 +1477,13 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   const int64_t Tb = x->at_split ? Tr : x->T;
   for (int ai = n_atb - 1; ai >= 0; --ai) {
     cudaStream_t sc = x->lanes[ai % nl];
+    int tk_atb = -1;
    for (int r = x->at_split ? ai : R - 1; r >= (x->at_split ? ai : 0); --r) {
     if (P > 1) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_dba[r], 0));
     else if (sc != x->lanes[r % nl] || !x->at_split) FM_CUDA(cudaStreamWaitEvent(sc, x->ev_eb[r], 0));
     const int64_t t0 = r * Tr;
     void* dA = (char*)x->dA + t0 * M * es;
+    if (tk_atb < 0) tk_atb = task_begin(x, sc);
     FM_KP(KK_GATHER, 1, 2.0 * Tr * E * M, (double)Tr * k * M * es + Tr * M * es * (x->cfg.residual ? 2.0 : 1.0) + M * E * es, sc,
           gather_gate_bwd(dt, (char*)x->dxc + r * C * M * es, at<int32_t>(saved, L.idx + t0 * k * 4),
                           at<int32_t>(saved, L.pos + t0 * k * 4), at<float>(saved, L.w + t0 * k * 4),
@@ -1421,11 +1534,13 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
       if (x->cfg.residual) { g.resid = dA; g.ldr = M; }
       FM_GEMM(KK_DX, g);
     }
+    task_end(x, tk_atb, TK_ATB, x->at_split ? ai : -1, sc);
   }
   // ---- deferred MHA/gate wgrads over all T tokens (one K=T GEMM each), in the order
   // Wg, Wo (AR of [dWo|dWg] released), then Wqkv (AR of dWqkv released).
   cudaStream_t sc = nl > 1 ? x->s_wg : x->lanes[0];
   if (flowmoe_status st = join_lanes(x, sc)) return st;
+  const int tk_wga = task_begin(x, sc);
   float* gf = gr->grad_flat;
   FM_KP(KK_DWG, 2, 2.0 * x->T * M * E, (double)x->T * M * es + x->T * E * 4.0 + M * E * 8.0, sc,
         gate_wgrad(dt, at<char>(saved, L.a), x->dl, gf + 4 * M * M, x->wg_part, (int)x->T, (int)M, (int)E, gacc, sc));
@@ -1442,6 +1557,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   g.B = x->dqkv; g.ldb = 3 * M;
   g.C = gf; g.ldc = 3 * M; g.epi = gepi;
   FM_GEMM(KK_DWQKV, g);
+  task_end(x, tk_wga, TK_WGA, -1, sc);
   FM_CUDA(cudaEventRecord(x->ev_grads_b, sc));
   // ---- AR of the replicated grads, low priority, chunked by S_p (Alg. 2); centralized
   // policies defer every block's AR until the backward pass is over (allreduce_wait).
@@ -1737,6 +1853,8 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   for (auto e : {x->ev_in, x->ev_done, x->ev_grads_a, x->ev_grads_b, x->ev_bwd_done}) if (e) cudaEventDestroy(e);
   for (void* p : x->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto e : x->prof.pool) cudaEventDestroy(e);
+  for (auto e : x->tlog.pool) cudaEventDestroy(e);
+  if (x->tlog.base) cudaEventDestroy(x->tlog.base);
   if (g_prof == &x->prof) g_prof = nullptr;
   for (void* p : x->allocs) cudaFree(p);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);

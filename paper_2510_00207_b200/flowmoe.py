@@ -32,7 +32,9 @@ EXPORTED = [
 EXPORTED_TEST = [
     "flowmoe_saved_routing_offsets", "flowmoe_debug_set", "flowmoe_test_gemm", "flowmoe_profile_begin",
     "flowmoe_profile_end", "flowmoe_kernel_launches", "flowmoe_create_local_group", "flowmoe_test_arrivals",
+    "flowmoe_tasklog_begin", "flowmoe_tasklog_end",
 ]
+TASK_KINDS = ("AT", "D", "E", "C", "MERGE", "CBPACK", "CB", "EB", "DB", "WGE", "ATB", "WGA", "AR")
 
 
 class FlowMoEError(RuntimeError):
@@ -53,6 +55,12 @@ class Config(ctypes.Structure):
 class ProfEntry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("launches", ctypes.c_int64), ("ms", ctypes.c_double),
                 ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class TaskRec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("block", ctypes.c_int32), ("chunk", ctypes.c_int32),
+                ("dir", ctypes.c_int32), ("stream", ctypes.c_uint64), ("t0_ms", ctypes.c_double),
+                ("t1_ms", ctypes.c_double)]
 
 
 class Params(ctypes.Structure):
@@ -131,6 +139,9 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_test_gemm.argtypes = [vp, i32, i32, i32, i32, i32, vp, i64, i64, i32, vp, i64, i64, i32,
                                     vp, i64, i64, i32, vp, vp, vp, vp]
     L.flowmoe_profile_begin.argtypes = [vp]
+    L.flowmoe_tasklog_begin.argtypes = [vp]
+    L.flowmoe_tasklog_end.argtypes = [vp, ctypes.POINTER(TaskRec), i32]
+    L.flowmoe_tasklog_end.restype = i32
     L.flowmoe_profile_end.argtypes = [vp, ctypes.POINTER(ProfEntry), i32]
     L.flowmoe_profile_end.restype = i32
     L.flowmoe_status_string.argtypes = [i32]
@@ -267,6 +278,18 @@ class FlowMoE:
 
     def debug_set(self, key: int, value: int):
         _check(lib().flowmoe_debug_set(self.handle, key, value), "flowmoe_debug_set")
+
+    def tasklog_begin(self):
+        _check(lib().flowmoe_tasklog_begin(self.handle), "flowmoe_tasklog_begin")
+
+    def tasklog_end(self, max_entries: int = 65536) -> list[dict]:
+        """Measured task intervals since tasklog_begin (flowmoe_test.h flowmoe_tasklog_end)."""
+        buf = (TaskRec * max_entries)()
+        n = lib().flowmoe_tasklog_end(self.handle, buf, max_entries)
+        if n < 0:
+            raise FlowMoEError(f"flowmoe_tasklog_end: {lib().flowmoe_last_error().decode()}")
+        return [dict(kind=TASK_KINDS[buf[i].kind], block=buf[i].block, chunk=buf[i].chunk, dir=buf[i].dir,
+                     stream=buf[i].stream, t0=buf[i].t0_ms, t1=buf[i].t1_ms) for i in range(n)]
 
     def profile_begin(self):
         _check(lib().flowmoe_profile_begin(self.handle), "flowmoe_profile_begin")
