@@ -99,7 +99,7 @@ def expert_grads(eg: dict, lo: int, hi: int):
 def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: int = 1,
                   schedule: str = "flowmoe", graph: bool = False, device: int = 0,
                   api: str = "per_block", P: int = 1, rank: int = 0, uid: bytes | None = None,
-                  a2a_impl: str = "nccl", chunk_bytes: int = 1 << 20) -> dict:
+                  a2a_impl: str = "nccl", chunk_bytes: int = 1 << 20, tasklog: bool = False) -> dict:
     """L = len(reps) blocks chained through the C ABI on one rank (forced routing per
     block from wk['forced'][l], or the gate's own routing when wk['forced'] is None):
     forward x -> y_L, backward from wk['dy'] to dx_0.  api='stack' drives the same
@@ -140,6 +140,12 @@ def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: in
 
     s = torch.cuda.current_stream()
     iteration(s)
+    log = None
+    if tasklog:  # a second eager iteration with the task log on (schedule properties)
+        torch.cuda.synchronize()
+        ctx.tasklog_begin()
+        iteration(s)
+        log = ctx.tasklog_end()
     if graph:  # capture the same iteration and replay it twice (overwrite grads -> same values)
         for bt in bts:
             for v in bt.g.values():
@@ -155,7 +161,7 @@ def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: in
     out = {"y": fm.to_host_f64(xs[L]), "dx": fm.to_host_f64(dxs[0]),
            "xs": [fm.to_host_f64(t) for t in xs], "dxs": [fm.to_host_f64(t) for t in dxs],
            "grad_flat": [bt.g["grad_flat"].cpu().numpy().astype(np.float64) for bt in bts],
-           "dw1": [bt.g["dw1"].cpu().numpy().astype(np.float64) for bt in bts]}
+           "dw1": [bt.g["dw1"].cpu().numpy().astype(np.float64) for bt in bts], "log": log}
     if graph:
         del gr
         torch.cuda.synchronize()

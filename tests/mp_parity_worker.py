@@ -99,6 +99,24 @@ def main():
         r["stack_bitwise"] = bool(all(np.array_equal(a[n], b[n]) for n in ("y", "dx")) and all(
             np.array_equal(a[n][l], b[n][l]) for n in ("grad_flat", "dw1") for l in range(L)))
         results[name] = r
+    # schedule properties on the measured timeline of a real P-rank stack iteration
+    # (SURVEY §8(c.3)): orders, 6a-6e, FIFO per stream, AR order and the priority rule
+    from paper_2510_00207_b200.schedule import check_schedule, violations
+    cfg = BlockConfig(T=1024, seq_len=256, M=512, n_heads=4, E=8, top_k=2, d_ffn=1024, R=4,
+                      capacity_factor=1.0, causal=1, residual=1, dtype="bf16", P=P)
+    for a2a in ("p2p", "nccl"):
+        L = 3
+        reps = [gen_replicated(cfg, block=l) for l in range(L)]
+        obj = [fm.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        wk = dict(gen_worker(cfg, rank), forced=None)
+        g = run_stack_gpu(cfg, reps, wk, compute_streams=cfg.R, device=dev.index, api="stack", P=P, rank=rank,
+                          uid=obj[0], a2a_impl=a2a, chunk_bytes=256 << 10, tasklog=True)
+        res = check_schedule(g["log"], L, cfg.R, P)
+        v = violations(res)
+        results[f"sched_{a2a}"] = {"violations": {k: len(x) for k, x in v.items()},
+                                   "examples": {k: [list(map(str, e)) for e in x[:3]] for k, x in v.items()},
+                                   "checked": res["checked"], "priority": res["priority_stats"]}
     out = [None] * P
     dist.all_gather_object(out, results)
     if rank == 0:

@@ -31,6 +31,11 @@ def test_multi_gpu_parity(P):
     per_rank = json.loads(line[0][len("MP_RESULTS "):])
     for rank, res in enumerate(per_rank):
         for case, r in res.items():
+            if case.startswith("sched_"):  # measured schedule properties: no violation at all
+                assert r["violations"] == {}, (rank, case, r)
+                for prop in ("eq3", "eq4", "eq5", "eq6", "6a", "6c", "6e", "priority"):
+                    assert r["checked"].get(prop, 0) > 0, (rank, case, prop, r["checked"])
+                continue
             if case.startswith("stack_"):  # 3-block chain, checked block by block
                 assert r.pop("stack_bitwise"), (rank, case)
                 tol = 1e-4 if "f32" in case else 2e-2
