@@ -194,7 +194,7 @@ struct flowmoe_ctx {
   std::vector<PendingAR> pending_ar;  // centralized-AR policies: flushed at allreduce_wait
   // per-ctx test/benchmark knobs (flowmoe_test.h) and per-kernel profile, applied to the
   // kernel modules by apply_ctx() at the start of every enqueueing call
-  int dbg_flags = 0, pdl = 1, force_bn = 0, p2p_on_lane = 1;
+  int dbg_flags = 0, pdl = 1, force_bn = 0, force_cg = 0, p2p_on_lane = 1;
   Prof prof;
   TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
@@ -259,6 +259,7 @@ void apply_ctx(flowmoe_ctx* x) {
   if (!x) return;
   gemm_tc_set_debug(x->dbg_flags);
   gemm_tc_force_bn(x->force_bn);
+  gemm_tc_force_cg(x->force_cg);
   g_pdl_enabled = x->pdl;
   g_p2p_on_lane = x->p2p_on_lane;
   g_prof = &x->prof;
@@ -702,6 +703,7 @@ flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
   else if (key == 4) x->pdl = value ? 1 : 0;
   else if (key == 5) x->force_bn = value;
   else if (key == 6) x->p2p_on_lane = value ? 1 : 0;
+  else if (key == 7) x->force_cg = value;
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   return FLOWMOE_OK;
 }
@@ -1885,6 +1887,7 @@ extern "C" flowmoe_status flowmoe_test_gemm(flowmoe_ctx* x, int dtype, int M, in
   } else {  // library defaults, no profile
     gemm_tc_set_debug(0);
     gemm_tc_force_bn(0);
+    gemm_tc_force_cg(0);
     g_pdl_enabled = 1;
     g_prof = nullptr;
   }

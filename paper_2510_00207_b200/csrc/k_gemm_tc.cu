@@ -36,7 +36,9 @@ __device__ long long g_probe[32];
 #endif
 static int g_tc_debug = 0;  // bit0: force SIMT for bf16; bit1: swap LBO/SBO of MN-major descs
 static int g_force_bn = 0;  // 0 = wave-aware choice; 64/128/256 = forced tile width (benchmarks)
+static int g_force_cg = 0;  // 0 = automatic; 1 = one CTA per tile; 2 = CTA pair (cta_group::2)
 void gemm_tc_force_bn(int bn) { g_force_bn = bn; }
+void gemm_tc_force_cg(int cg) { g_force_cg = cg; }
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
 int attn_tc_debug_off() { return g_tc_debug & 4; }  // bit2: force the SIMT attention kernels
 
@@ -47,27 +49,36 @@ struct TcArgs {
   int a_mmajor, b_kmajor, nk, dbg;
 };
 
-// Persistent: grid = min(#tiles, #SMs); CTA i walks tiles i, i + grid, ... (n fastest,
-// then m, then batch).  The smem operand ring runs continuously across tiles, and the
-// accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
-// overlaps the TMA loads + MMAs of tile i+1.
-template <int BN, int STAGES, int EB>
+// Persistent: grid = min(#tiles, #SMs) units; unit i walks tiles i, i + #units, ... (n
+// fastest, then m, then batch).  The smem operand ring runs continuously across tiles,
+// and the accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile
+// i overlaps the TMA loads + MMAs of tile i+1.
+// CG = 2: a unit is a CTA pair (cluster of 2 on one TPC) running M = 256 UMMAs
+// (tcgen05.mma.cta_group::2, issued by the leader CTA): each CTA loads its own 128 rows of
+// A and half (BN/2) of the B columns and gets its 128 accumulator rows in its own TMEM, so
+// the operand bytes per SM and K-step drop from (128 + BN)·BK·2 to (128 + BN/2)·BK·2 —
+// the L2->SMEM traffic that bounded the 1-CTA kernel at ~70% of the tensor peak.
+template <int BN, int STAGES, int EB, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ CUtensorMap tma_c,
                    const __grid_constant__ CUtensorMap tma_aux, const TcArgs p) {
+  constexpr int BNL = BN / CG;                      // B columns this CTA loads
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
-  constexpr uint32_t B_BYTES = BN * TC_BK * 2;
+  constexpr uint32_t B_BYTES = BNL * TC_BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t RING = STAGES * STAGE_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int ntn = (p.g.N + BN - 1) / BN, ntm = (p.g.M + TC_BM - 1) / TC_BM;
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
+  const int unit = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
+  const int ntn = (p.g.N + BN - 1) / BN, ntm = (p.g.M + TC_BM * CG - 1) / (TC_BM * CG);
   const int num_tiles = ntn * ntm * p.g.batch;
-  // one tile per CTA: the operand ring is free when the epilogue runs, so it doubles
+  // one tile per unit: the operand ring is free when the epilogue runs, so it doubles
   // as the staging area and a single TMEM accumulator suffices (smaller footprint)
-  const bool single = num_tiles <= (int)gridDim.x;
+  const bool single = num_tiles <= nunits;
   uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x EB x 4 KB staging
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : EB * 32768));
   uint64_t* empty = full + STAGES;
@@ -82,14 +93,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc2(tmem_slot, tmem_cols);
+    else tmem_alloc(tmem_slot, tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // both CTAs' barriers initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) FM_MARK(1);
@@ -99,35 +114,63 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ===== TMA producer (whole warp walks the ring, one elected lane issues) =====
     int gk = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
+    for (int tile = unit; tile < num_tiles; tile += nunits) {
+      const int n0 = (tile % ntn) * BN + (int)crank * BNL;  // this CTA's B columns
+      const int m0 = ((tile / ntn) % ntm) * TC_BM * CG + (int)crank * TC_BM, b = tile / (ntn * ntm);
       for (int kb = 0; kb < p.nk; ++kb, ++gk) {
         const int s = gk % STAGES;
-        if (gk >= STAGES) mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
+        if (gk >= STAGES) {
+          if constexpr (CG == 2) mbar_wait_cl(&empty[s], ((gk / STAGES) + 1) & 1);
+          else mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
+        }
         uint8_t* sa = smem + s * STAGE_BYTES;
         uint8_t* sb = sa + A_BYTES;
         const int k0 = kb * TC_BK;
         if (elect_one()) {
-          mbar_expect_tx(&full[s], STAGE_BYTES);
-          if (!p.a_mmajor) {
-            tma_load_3d(sa, &tma_a, &full[s], k0, m0, b);
-          } else {
+          if constexpr (CG == 1) {
+            mbar_expect_tx(&full[s], STAGE_BYTES);
+            if (!p.a_mmajor) {
+              tma_load_3d(sa, &tma_a, &full[s], k0, m0, b);
+            } else {
 #pragma unroll
-            for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d(sa + i * 8192, &tma_a, &full[s], m0 + 64 * i, k0, b);
-          }
-          if (p.b_kmajor) {
-            tma_load_3d(sb, &tma_b, &full[s], k0, n0, b);
-          } else {
+              for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d(sa + i * 8192, &tma_a, &full[s], m0 + 64 * i, k0, b);
+            }
+            if (p.b_kmajor) {
+              tma_load_3d(sb, &tma_b, &full[s], k0, n0, b);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0, b);
+              for (int i = 0; i < BNL / 64; ++i) tma_load_3d(sb + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0, b);
+            }
+          } else {
+            // both CTAs' bytes complete on the leader's barrier, armed by the leader alone
+            if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+            const uint32_t bar = mapa_u32(smem_u32(&full[s]), 0);
+            if (!p.a_mmajor) {
+              tma_load_3d_cg2(sa, &tma_a, bar, k0, m0, b);
+            } else {
+#pragma unroll
+              for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d_cg2(sa + i * 8192, &tma_a, bar, m0 + 64 * i, k0, b);
+            }
+            if (p.b_kmajor) {
+              tma_load_3d_cg2(sb, &tma_b, bar, k0, n0, b);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BNL / 64; ++i) tma_load_3d_cg2(sb + i * 8192, &tma_b, bar, n0 + 64 * i, k0, b);
+            }
           }
           if (gk < 4) FM_MARK(24 + gk);
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer (whole warp waits, one elected lane issues) =====
+    if constexpr (CG == 2) {
+      // drain: every stage's last release (the leader's multicast commit) has landed in this
+      // CTA's smem before the pair may exit
+      for (int q = gk - STAGES; q < gk; ++q)
+        if (q >= 0) mbar_wait_cl(&empty[q % STAGES], ((q / STAGES) + 1) & 1);
+    }
+  } else if (warp == 1 && (CG == 1 || leader)) {
+    // ===== MMA issuer (whole warp waits, one elected lane issues; the pair's leader) =====
     const bool swap = (p.dbg & 2) != 0;
     const uint32_t mn_lbo = swap ? 1024u : 8192u, mn_sbo = swap ? 8192u : 1024u;
     // Descriptors of stage 0 built once; a stage / UMMA_K step only adds to the 14-bit
@@ -140,35 +183,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint64_t a_kstep = p.a_mmajor ? (2048 >> 4) : (32 >> 4);
     const uint64_t b_kstep = p.b_kmajor ? (32 >> 4) : (2048 >> 4);
     int gk = 0, it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
       const int acc = it & 1, use = it >> 1;
-      if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained this buffer
+      if (use >= 1) {  // the epilogue(s) drained this buffer
+        if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], (use - 1) & 1);
+        else mbar_wait(&tempty[acc], (use - 1) & 1);
+      }
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
       for (int kb = 0; kb < p.nk; ++kb, ++gk) {
         const int s = gk % STAGES;
-        mbar_wait(&full[s], (gk / STAGES) & 1);
+        if constexpr (CG == 2) mbar_wait_cl(&full[s], (gk / STAGES) & 1);
+        else mbar_wait(&full[s], (gk / STAGES) & 1);
         if (lane == 0 && gk == 0) FM_MARK(3);
         if (lane == 0 && gk < 8) FM_MARK(16 + gk);
         tc_fence_after();
         const uint64_t soff = (uint64_t)((uint32_t)s * STAGE_BYTES >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk)
-            tc_mma(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
-                   (kb > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&empty[s]);
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            if constexpr (CG == 2)
+              tc_mma2(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
+                      (kb > 0 || kk > 0) ? 1u : 0u);
+            else
+              tc_mma(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
+                     (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          if constexpr (CG == 2) tc_commit2_both(&empty[s]);
+          else tc_commit(&empty[s]);
           if (gk < 4) FM_MARK(28 + gk);
         }
         __syncwarp();
       }
       if (elect_one()) {
-        tc_commit(&tfull[acc]);
+        if constexpr (CG == 2) tc_commit2_both(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
         FM_MARK(4);
       }
       __syncwarp();
     }
-  } else {
+  } else if (warp >= 2) {
     // ===== epilogue: TMEM -> registers -> swizzled smem tile -> TMA store / reduce-add =====
     // Eight warps: warp w reads TMEM lane quarter w % 4 (32 rows, one row per thread);
     // the two warps of a quarter take alternate 32-column chunks, halving the per-warp
@@ -192,8 +246,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
     int issued = 0;  // chunks this warp has stored (buffer issued % EB was used EB chunks ago)
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int n0 = (tile % ntn) * BN, m0 = ((tile / ntn) % ntm) * TC_BM, b = tile / (ntn * ntm);
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
+      const int n0 = (tile % ntn) * BN;
+      const int m0 = ((tile / ntn) % ntm) * TC_BM * CG + (int)crank * TC_BM, b = tile / (ntn * ntm);
       const int acc = it & 1, use = it >> 1;
       const uint32_t tmem_acc = tmem_base + acc * BN;
       const int row = m0 + r0 + lane;
@@ -230,7 +285,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       };
       prefetch(half * 32);
-      mbar_wait_sleep(&tfull[acc], use & 1);
+      if constexpr (CG == 2) mbar_wait_cl_sleep(&tfull[acc], use & 1);
+      else mbar_wait_sleep(&tfull[acc], use & 1);
       if (threadIdx.x == 64) FM_MARK(5);
       tc_fence_after();
 #pragma unroll 1
@@ -337,7 +393,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM reads of this tile are complete
+      if (lane == 0) {  // TMEM reads of this tile are complete (the leader's MMA waits for both CTAs)
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_u32(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if (threadIdx.x == 64) FM_MARK(6);
     if (lane == 0) bulk_wait<0>();
@@ -346,11 +405,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if constexpr (CG == 2) {  // neither CTA leaves (or frees TMEM) while its peer may still signal it
+    tc_fence_before();
+    cluster_sync_all();
+  }
   if (threadIdx.x == 0) FM_MARK(8);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols);
+    if constexpr (CG == 2) tmem_dealloc2(tmem_base, tmem_cols);
+    else tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 
@@ -402,14 +466,15 @@ int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-template <int BN, int STAGES, int EB = 1>
+template <int BN, int STAGES, int EB = 1, int CG = 1>
 static int launch_tc(const GemmArgs& g, cudaStream_t s) {
+  constexpr int BNL = BN / CG;
   CUtensorMap ma, mb;
   int rc;
   if (!g.a_mmajor) rc = make_map(&ma, g.A, g.K, g.M, g.batch, g.lda, g.sA, TC_BM);
   else rc = make_map(&ma, g.A, g.M, g.K, g.batch, g.lda, g.sA, TC_BK);
   if (rc) return rc;
-  if (g.b_kmajor) rc = make_map(&mb, g.B, g.K, g.N, g.batch, g.ldb, g.sB, BN);
+  if (g.b_kmajor) rc = make_map(&mb, g.B, g.K, g.N, g.batch, g.ldb, g.sB, BNL);
   else rc = make_map(&mb, g.B, g.N, g.K, g.batch, g.ldb, g.sB, TC_BK);
   if (rc) return rc;
   // output tiles: [32 rows][32 cols] boxes, fp32 (reduce-add, SW128) or bf16 (store, SW64)
@@ -432,9 +497,9 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.a_mmajor ? 1 : 0) << 15) |
             ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
-            ((uint32_t)(TC_BM >> 4) << 24);
-  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BN * TC_BK * 2) + EB * 32768 + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES, EB>;
+            ((uint32_t)((TC_BM * CG) >> 4) << 24);
+  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BNL * TC_BK * 2) + EB * 32768 + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, STAGES, EB, CG>;
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max), true);
   (void)attr_set;
   static int num_sms = 0;
@@ -444,10 +509,14 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (num_sms <= 0) num_sms = 148;
   }
-  const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM - 1) / TC_BM) * g.batch;
-  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-  const size_t smem = tiles <= grid ? smem_max - EB * 32768 : smem_max;
-  launch_k(kern, dim3(grid), TC_THREADS, smem, s, ma, mb, mc, maux, p);
+  const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM * CG - 1) / (TC_BM * CG)) * g.batch;
+  const int units = num_sms / CG;
+  const int nu = (int)(tiles < units ? tiles : units);
+  const size_t smem = tiles <= nu ? smem_max - EB * 32768 : smem_max;
+  if constexpr (CG == 2)
+    launch_kc(kern, dim3(2 * nu), TC_THREADS, smem, s, dim3(2, 1, 1), ma, mb, mc, maux, p);
+  else
+    launch_k(kern, dim3(nu), TC_THREADS, smem, s, ma, mb, mc, maux, p);
   return (int)cudaGetLastError();
 }
 
@@ -458,9 +527,21 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   // Tile width (measured, tools/gemm_microbench.py): BN=256 (best MMA/operand efficiency)
   // whenever it still yields >= 48 tiles; small, latency-bound GEMMs get narrower tiles
   // and more CTAs.
+  if (g_force_cg == 2) return g_force_bn == 128 ? launch_tc<128, 8, 1, 2>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
   if (g_force_bn == 256) return launch_tc<256, 4>(g, s);
   if (g_force_bn == 128) return launch_tc<128, 6>(g, s);
   if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
+  if (g_force_cg == 0) {
+    // CTA pairs for the large GEMMs: at least one full wave of pairs; the pair tile width
+    // (256 or 128 columns of 256 rows) with the fewer wave-quantised column-passes
+    const int64_t mt2 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch;
+    const int64_t t256 = mt2 * ((g.N + 255) / 256), t128 = mt2 * ((g.N + 127) / 128);
+    const int64_t pairs = 74;
+    if (g.M > TC_BM && t256 >= pairs) {
+      const int64_t c256 = (t256 + pairs - 1) / pairs * 2, c128 = (t128 + pairs - 1) / pairs;
+      return c128 < c256 ? launch_tc<128, 8, 1, 2>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
+    }
+  }
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
   // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) take a 3-stage ring

@@ -48,6 +48,7 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s);  // bf16 only, tcgen05/TMEM/TMA
 int gemm_tc_init();                               // resolves cuTensorMapEncodeTiled
 void gemm_tc_set_debug(int flags);
 void gemm_tc_force_bn(int bn);
+void gemm_tc_force_cg(int cg);  // 0 automatic, 1 single-CTA tiles, 2 CTA pairs (cta_group::2)
 
 // ---------------------------------------------------------------- attention
 // qkv [nseq·N][3M] (sequences of N rows; head h at columns h*dh of each of Q|K|V),

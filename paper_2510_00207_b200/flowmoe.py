@@ -158,7 +158,9 @@ _ENV_KNOBS = (("FLOWMOE_DEBUG_SIMT", 1, 1),        # debug: route bf16 GEMMs to 
               ("FLOWMOE_DEBUG_SWAP", 2, 1),        # debug: swap MN-major descriptor strides
               ("FLOWMOE_DEBUG_SIMT_ATTN", 3, 1),   # debug: SIMT attention for bf16
               ("FLOWMOE_NO_PDL", 4, 0),            # A/B: plain stream-ordered launches
-              ("FLOWMOE_P2P_A2A_STREAM", 6, 0))    # A/B: peer-memory A2A on the A2A stream
+              ("FLOWMOE_P2P_A2A_STREAM", 6, 0),    # A/B: peer-memory A2A on the A2A stream
+              ("FLOWMOE_FORCE_CG1", 7, 1),         # A/B: single-CTA GEMM tiles only
+              ("FLOWMOE_FORCE_CG2", 7, 2))         # test: CTA-pair (cta_group::2) GEMMs everywhere
 
 
 def _apply_env_knobs(handle):

@@ -92,6 +92,14 @@ def test_block_parity_forced_routing(name):
     _check_block(CASES[name])
 
 
+@pytest.mark.parametrize("name", ["bf16_small", "bf16_k8_wide", "bf16_ragged"])
+def test_block_parity_cta_pair_gemms(name, monkeypatch):
+    """Every GEMM of the block (forward, dgrads, fp32 wgrads) on CTA pairs (cta_group::2,
+    forced through the per-ctx knob) vs the oracle; and bit-identical to itself with R lanes."""
+    monkeypatch.setenv("FLOWMOE_FORCE_CG2", "1")
+    _check_block(CASES[name])
+
+
 # Token chunks (reading Q1'): R exceeds the number of sequences, every chunk is a causal
 # slice of one sequence (chunked prefill).  Chunk offsets on and off the 128-row tiles.
 TOK_CASES = {
@@ -225,13 +233,34 @@ def test_empty_expert_and_all_tokens_one_expert():
 GEMM_SHAPES = [(200, 320, 136, 2), (128, 96, 64, 1), (296, 200, 520, 3), (64, 512, 256, 8)]  # rows, N, K multiple of 8 (TMA 16-B strides)
 
 
+_KNOB_CTX = {}
+
+
+def knob_ctx(cg=0, bn=0):
+    """a small ctx carrying GEMM knobs (flowmoe_test.h: per-ctx debug keys 5 and 7)"""
+    import paper_2510_00207_b200 as fm
+    if (cg, bn) not in _KNOB_CTX:
+        c = fm.FlowMoE(fm.BlockShape(B=256, seq_len=64, M=64, n_heads=1, E=2, top_k=1, d_ffn=64, R=1), 0)
+        c.debug_set(7, cg)
+        c.debug_set(5, bn)
+        _KNOB_CTX[(cg, bn)] = c
+    return _KNOB_CTX[(cg, bn)]
+
+
+GEMM_CG = [(0, 0), (2, 256), (2, 128)]  # automatic; CTA pairs (cta_group::2) with 256 / 128 columns
+
+
+@pytest.mark.parametrize("cg,bn", GEMM_CG)
 @pytest.mark.parametrize("a_mmajor,b_kmajor", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("shape", GEMM_SHAPES)
-def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape):
+def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape, cg, bn):
     """tcgen05 GEMM (bf16 in, fp32 TMEM accum) against the fp64 product of the
-    same bf16 inputs; store epilogue (bf16 out) and fp32 accumulate epilogue."""
+    same bf16 inputs; store epilogue (bf16 out) and fp32 accumulate epilogue; single-CTA
+    tiles and CTA pairs (ragged M: the pair's second CTA partly or wholly past the rows;
+    ragged N: the second CTA's B half past the columns)."""
     import torch
     import paper_2510_00207_b200 as fm
+    ctx = knob_ctx(cg, bn)
     Mr, N, K, batch = shape
     rng = np.random.default_rng(sum(shape) + 7 * a_mmajor + 3 * b_kmajor)
     A = rng.standard_normal((batch, Mr, K))
@@ -250,17 +279,18 @@ def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape):
     ldb = K if b_kmajor else N
     C = torch.zeros((batch, Mr, N), dtype=torch.bfloat16, device=dev)
     fm.test_gemm("bf16", At, Bt, C, M=Mr, N=N, K=K, batch=batch, lda=lda, sA=Mr * K,
-                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N)
+                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N, ctx=ctx)
     C32 = torch.ones((batch, Mr, N), dtype=torch.float32, device=dev)
     fm.test_gemm("bf16", At, Bt, C32, M=Mr, N=N, K=K, batch=batch, lda=lda, sA=Mr * K,
-                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N, epi=3)
+                 a_mmajor=a_mmajor, ldb=ldb, sB=K * N, b_kmajor=b_kmajor, ldc=N, sC=Mr * N, epi=3, ctx=ctx)
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref) <= 1e-2
     assert rel(C32.cpu().numpy().astype(np.float64) - 1.0, ref) <= 1e-5
 
 
+@pytest.mark.parametrize("cg", [0, 2])
 @pytest.mark.parametrize("epi", [3, 4])
-def test_gemm_tc_wgrad_variant_vs_fp64(epi):
+def test_gemm_tc_wgrad_variant_vs_fp64(epi, cg):
     """The write-bound wgrad configuration (fp32 out, K <= 256, >= 4·148 tiles of 256
     columns: 3-stage ring, double-buffered epilogue staging) on an m-major A like the
     expert dW, ragged N and K, against the fp64 product: store (4) and accumulate (3)."""
@@ -274,16 +304,18 @@ def test_gemm_tc_wgrad_variant_vs_fp64(epi):
     ref = fm.to_host_f64(At)[0].T @ fm.to_host_f64(Bt)[0]
     C = torch.full((1, Mr, N), 0.5 if epi == 3 else 7.0, dtype=torch.float32, device=dev)
     fm.test_gemm("bf16", At, Bt, C, M=Mr, N=N, K=K, batch=1, lda=Mr, sA=Mr * K, a_mmajor=1,
-                 ldb=N, sB=K * N, ldc=N, sC=Mr * N, epi=epi)
+                 ldb=N, sB=K * N, ldc=N, sC=Mr * N, epi=epi, ctx=knob_ctx(cg))
     torch.cuda.synchronize()
     got = C[0].cpu().numpy().astype(np.float64) - (0.5 if epi == 3 else 0.0)
     assert rel(got, ref) <= 1e-5
 
 
-def test_gemm_tc_epilogues():
+@pytest.mark.parametrize("cg,bn", GEMM_CG)
+def test_gemm_tc_epilogues(cg, bn):
     import torch
     import paper_2510_00207_b200 as fm
-    Mr, N, K, batch = 192, 384, 128, 2
+    ctx = knob_ctx(cg, bn)
+    Mr, N, K, batch = 448, 384, 128, 2
     rng = np.random.default_rng(3)
     dev = torch.device("cuda", 0)
     A = fm.to_device(rng.standard_normal((batch, Mr, K)) / 8, "bf16", dev)
@@ -293,25 +325,25 @@ def test_gemm_tc_epilogues():
     ref = fm.to_host_f64(A) @ fm.to_host_f64(B)
     kw = dict(M=Mr, N=N, K=K, batch=batch, lda=K, sA=Mr * K, ldb=N, sB=K * N, ldc=N, sC=Mr * N)
     C = torch.empty((batch, Mr, N), dtype=torch.bfloat16, device=dev)
-    fm.test_gemm("bf16", A, B, C, epi=0, bias=bias, resid=res, **kw)
+    fm.test_gemm("bf16", A, B, C, epi=0, bias=bias, resid=res, **kw, ctx=ctx)
     want = ref + fm.to_host_f64(bias)[:, None, :] + fm.to_host_f64(res)
     assert rel(fm.to_host_f64(C), want) <= 1e-2
     Z = torch.empty_like(C)
-    fm.test_gemm("bf16", A, B, C, epi=1, bias=bias, aux=Z, **kw)
+    fm.test_gemm("bf16", A, B, C, epi=1, bias=bias, aux=Z, **kw, ctx=ctx)
     z = ref + fm.to_host_f64(bias)[:, None, :]
     assert rel(fm.to_host_f64(Z), z) <= 1e-2
     assert rel(fm.to_host_f64(C), o.gelu(fm.to_host_f64(Z))) <= 1e-2
-    fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw)
+    fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw, ctx=ctx)
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref * o.gelu_grad(fm.to_host_f64(Z))) <= 1e-2
     # the expert FFN pair: forward saves GELU'(z), backward multiplies by it
     D = torch.empty_like(C)
-    fm.test_gemm("bf16", A, B, C, epi=5, bias=bias, aux=D, **kw)
+    fm.test_gemm("bf16", A, B, C, epi=5, bias=bias, aux=D, **kw, ctx=ctx)
     torch.cuda.synchronize()
     zb = fm.to_host_f64(Z)  # bf16(acc + bias) from the epi=1 call, same inputs
     assert rel(fm.to_host_f64(C), o.gelu(zb)) <= 1e-2
     assert rel(fm.to_host_f64(D), o.gelu_grad(zb)) <= 1e-2
-    fm.test_gemm("bf16", A, B, C, epi=6, aux=D, **kw)
+    fm.test_gemm("bf16", A, B, C, epi=6, aux=D, **kw, ctx=ctx)
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref * fm.to_host_f64(D)) <= 1e-2
 

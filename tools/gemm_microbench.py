@@ -1,6 +1,8 @@
 """Per-launch device time of the tcgen05 GEMM at the block's shapes, measured inside a
-CUDA graph of `reps` back-to-back launches (so host launch cost is excluded), with
-PDL on/off and forced tile widths.  Prints one JSON line per case."""
+CUDA graph of `reps` back-to-back launches (so host launch cost is excluded), with forced
+tile widths and CTA grouping (1 = one CTA per 128-row tile, 2 = CTA pairs with
+cta_group::2 UMMAs).  The knobs are per ctx (flowmoe_test.h flowmoe_debug_set).
+Prints one JSON line per case.   python tools/gemm_microbench.py [prefix ...]"""
 import json
 import os
 import sys
@@ -21,28 +23,54 @@ SHAPES = {  # name: (M rows, N, K, batch, a_mmajor, b_kmajor, epi)
     "c4_e1": (128, 16384, 4096, 16, 0, 0, 0),
     "c4_qkv": (1024, 12288, 4096, 1, 0, 0, 0),
     "c4_dw1": (4096, 16384, 256, 16, 1, 0, 4),
+    # configs[4] DeepSeek-V2-S-shaped (the bench workload): T_r = 512, M = 5120, F = 1536,
+    # E = 16 experts x P·C = 256 capacity rows per chunk, K = R·P·C = 512 for the expert wgrads
+    "dsv2s_qkv": (512, 15360, 5120, 1, 0, 0, 0),
+    "dsv2s_oproj": (512, 5120, 5120, 1, 0, 0, 0),
+    "dsv2s_e1": (256, 1536, 5120, 16, 0, 0, 0),
+    "dsv2s_e2": (256, 5120, 1536, 16, 0, 0, 0),
+    "dsv2s_dgelu": (256, 1536, 5120, 16, 0, 1, 0),
+    "dsv2s_dxe": (256, 5120, 1536, 16, 0, 1, 0),
+    "dsv2s_dctx": (512, 5120, 5120, 1, 0, 1, 0),
+    "dsv2s_dx": (512, 5120, 15360, 1, 0, 1, 0),
+    "dsv2s_dw1": (5120, 1536, 512, 16, 1, 0, 4),
+    "dsv2s_dw2": (1536, 5120, 512, 16, 1, 0, 4),
+    "dsv2s_dwqkv": (5120, 15360, 1024, 1, 1, 0, 4),
+    "dsv2s_dwo": (5120, 5120, 1024, 1, 1, 0, 4),
 }
 
+_CTX = None
 
-def run(name, reps, bn, pdl):
+
+def knob_ctx():
+    """a small P=1 ctx that carries the GEMM knobs (flowmoe_debug_set is per ctx)"""
+    global _CTX
+    if _CTX is None:
+        _CTX = fm.FlowMoE(fm.BlockShape(B=256, seq_len=64, M=64, n_heads=1, E=2, top_k=1, d_ffn=64, R=1), 0)
+    return _CTX
+
+
+def run(name, reps, bn, pdl, cg=0):
     Mr, N, K, batch, am, bk, epi = SHAPES[name]
     dev = torch.device("cuda", 0)
     A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
     B = torch.randn(batch, (N if bk else K), (K if bk else N), device=dev).to(torch.bfloat16) * 0.05
     C = torch.zeros(batch, Mr, N, device=dev, dtype=torch.float32 if epi == 4 else torch.bfloat16)
-    fm.debug_set(5, bn)
-    fm.debug_set(4, pdl)
+    ctx = knob_ctx()
+    ctx.debug_set(5, bn)
+    ctx.debug_set(4, pdl)
+    ctx.debug_set(7, cg)
     kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
               ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi)
     s = torch.cuda.current_stream()
-    fm.test_gemm("bf16", A, B, C, stream=s, **kw)
+    fm.test_gemm("bf16", A, B, C, stream=s, ctx=ctx, **kw)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream()
     cap.wait_stream(s)
     with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
         for _ in range(reps):
-            fm.test_gemm("bf16", A, B, C, stream=torch.cuda.current_stream(), **kw)
+            fm.test_gemm("bf16", A, B, C, stream=torch.cuda.current_stream(), ctx=ctx, **kw)
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -54,16 +82,17 @@ def run(name, reps, bn, pdl):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
     flops = 2.0 * Mr * N * K * batch
-    print(json.dumps({"shape": name, "bn": bn, "pdl": pdl, "us_per_launch": round(us, 3),
+    print(json.dumps({"shape": name, "bn": bn, "cg": cg, "pdl": pdl, "us_per_launch": round(us, 3),
                       "tflops": round(flops / us / 1e6, 1)}), flush=True)
     del g
 
 
 if __name__ == "__main__":
+    pref = tuple(sys.argv[1:]) or ("",)
     for name in SHAPES:
+        if not name.startswith(pref):
+            continue
         reps = 200 if name.startswith("c2") else (50 if name.startswith("c3") else 10)
-        for bn in (0, 64, 128, 256):
-            for pdl in (1, 0):
-                if bn and pdl == 0:
-                    continue
-                run(name, reps, bn, pdl)
+        run(name, reps, 0, 1, 0)  # the library's automatic choice
+        for cg, bn in ((1, 128), (1, 256), (2, 128), (2, 256)):
+            run(name, reps, bn, 1, cg)
