@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if constexpr (CG == 2) {
       // drain: every stage's last release (the leader's multicast commit) has landed in this
       // CTA's smem before the pair may exit
-      for (int q = gk - STAGES; q < gk; ++q)
-        if (q >= 0) mbar_wait_cl(&empty[q % STAGES], ((q / STAGES) + 1) & 1);
+      for (int q = gk - STAGES; q < gk; ++q)  // release of use q / STAGES = that phase's completion
+        if (q >= 0) mbar_wait_cl(&empty[q % STAGES], (q / STAGES) & 1);
     }
   } else if (warp == 1 && (CG == 1 || leader)) {
     // ===== MMA issuer (whole warp waits, one elected lane issues; the pair's leader) =====

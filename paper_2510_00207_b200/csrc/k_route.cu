@@ -920,13 +920,160 @@ static void gather_gate_bwd_wide_launch(const void* dx, const int32_t* idx, cons
            dw, logits, (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, ldE);
 }
 
+// E <= 16, wide rows: a CTA stages the Wg rows of its 128 column vectors in shared memory
+// once and walks TB tokens, so Wg is read from L2 once per TB tokens instead of once per
+// token (the one-token-per-thread kernel above re-read ~2.5x the kernel's HBM bytes of Wg
+// from L2).  The tokens' dlogits come from shared memory (first TB threads); at k <= 4
+// two tokens' gathered rows + dO are requested together.
+constexpr int GGB_TB = 8, GGB_THREADS = 128;
+
+template <typename T, int E, int K>
+__global__ void __launch_bounds__(GGB_THREADS) gather_gate_bwd_tile_kernel(
+    const T* __restrict__ dx, const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
+    const float* __restrict__ w, const float* __restrict__ dw, const float* __restrict__ logits,
+    const T* __restrict__ wg, const T* __restrict__ dres, T* __restrict__ dA, float* __restrict__ dlogits, int T_,
+    int M, int ldE) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float dls[GGB_TB][E];
+  extern __shared__ uint4 wgs4[];  // [GGB_THREADS * V][E] storage elements: this CTA's Wg rows
+  FM_PDL_ENTRY();
+  const int nv = M / V;
+  const int cvec = blockIdx.x * GGB_THREADS + threadIdx.x;
+  {  // stage the CTA's Wg rows (contiguous in Wg [M][E]) with 16-byte loads
+    const int mrow0 = blockIdx.x * GGB_THREADS * V;
+    const int nrows = min(GGB_THREADS * V, M - mrow0);
+    const uint4* src = reinterpret_cast<const uint4*>(wg + (int64_t)mrow0 * E);
+    const int n16 = nrows * E * (int)sizeof(T) / 16;
+    for (int i = threadIdx.x; i < n16; i += GGB_THREADS) wgs4[i] = src[i];
+  }
+  const int t0 = blockIdx.y * GGB_TB;
+  const int m = cvec * V;
+  // dlogits of the tile's tokens (reading Q5), one thread per token
+  if (threadIdx.x < GGB_TB) {
+    const int t = t0 + threadIdx.x;
+    float dl[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) dl[e] = 0.f;
+    if (t < T_) {
+      if constexpr (K == 1) {
+        const float* lt = logits + (int64_t)t * E;
+        const int e0 = idx[t];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < E; ++e) mx = fmaxf(mx, lt[e]);
+        float den = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) { dl[e] = expf(lt[e] - mx); den += dl[e]; }
+        const float g0 = dw[t];
+        float pe0 = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) { dl[e] /= den; if (e == e0) pe0 = dl[e]; }
+#pragma unroll
+        for (int e = 0; e < E; ++e) dl[e] = dl[e] * ((e == e0 ? g0 : 0.f) - pe0 * g0);
+      } else {
+        float wj[K], dwj[K], inner = 0.f;
+        int ej[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          wj[j] = w[(int64_t)t * K + j];
+          dwj[j] = dw[(int64_t)t * K + j];
+          ej[j] = idx[(int64_t)t * K + j];
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) inner += wj[j] * dwj[j];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float v = wj[j] * (dwj[j] - inner);
+#pragma unroll
+          for (int e = 0; e < E; ++e) dl[e] += (e == ej[j]) ? v : 0.f;
+        }
+      }
+      if (blockIdx.x == 0)
+#pragma unroll
+        for (int e = 0; e < E; ++e) dlogits[(int64_t)t * E + e] = dl[e];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) dls[threadIdx.x][e] = dl[e];
+  }
+  __syncthreads();
+  if (cvec >= nv) return;
+  const T* wrow = reinterpret_cast<const T*>(wgs4) + (int64_t)threadIdx.x * V * E;  // my V rows
+  // PF tokens' gathered rows requested together (more loads in flight at small k)
+  constexpr int PF = K <= 4 ? 2 : 1;
+#pragma unroll 1
+  for (int i0 = 0; i0 < GGB_TB; i0 += PF) {
+    int pj[PF][K];
+    uint4 raw[PF][K], rres[PF];
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int t = t0 + i0 + q;
+      const bool ok = t < T_;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        pj[q][j] = ok ? pos[(int64_t)t * K + j] : -1;
+        raw[q][j] = make_uint4(0, 0, 0, 0);
+        if (pj[q][j] >= 0)
+          raw[q][j] = *reinterpret_cast<const uint4*>(dx + ((int64_t)idx[(int64_t)t * K + j] * ldE + pj[q][j]) * M + m);
+      }
+      rres[q] = make_uint4(0, 0, 0, 0);
+      if (dres && ok) rres[q] = *reinterpret_cast<const uint4*>(dres + (int64_t)t * M + m);
+    }
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int i = i0 + q, t = t0 + i;
+      if (t >= T_) break;
+      float acc[V], dl[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) dl[e] = dls[i][e];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float wr[E];
+        load_n<T, E>(wrow + v * E, wr);
+        float sum = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sum = fmaf(dl[e], wr[e], sum);
+        acc[v] = sum;
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (pj[q][j] >= 0) {
+          float v8[V];
+          load16<T>(reinterpret_cast<const T*>(&raw[q][j]), v8);
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] += v8[v];
+        }
+      if (dres) {
+        float v8[V];
+        load16<T>(reinterpret_cast<const T*>(&rres[q]), v8);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] += v8[v];
+      }
+      store16<T>(dA + (int64_t)t * M + m, acc);
+    }
+  }
+}
+
+template <typename T, int E, int K>
+static void gather_gate_bwd_tile_launch(const void* dx, const int32_t* idx, const int32_t* pos, const float* w,
+                                        const float* dw, const float* logits, const void* wg, const void* dres,
+                                        void* dA, float* dlogits, int T_, int M, int ldE, cudaStream_t s) {
+  const int nv = M / (16 / (int)sizeof(T));
+  dim3 grid((nv + GGB_THREADS - 1) / GGB_THREADS, (T_ + GGB_TB - 1) / GGB_TB);
+  const size_t smem = (size_t)GGB_THREADS * (16 / sizeof(T)) * E * sizeof(T);
+  launch_k(gather_gate_bwd_tile_kernel<T, E, K>, grid, GGB_THREADS, smem, s, (const T*)dx, idx, pos, w, dw, logits,
+           (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, ldE);
+}
+
 template <typename T, int E>
 struct GgbWide {
   template <int K>
   static void run(const void* dx, const int32_t* idx, const int32_t* pos, const float* w, const float* dw,
                   const float* logits, const void* wg, const void* dres, void* dA, float* dlogits, int T_, int M,
                   int ldE, cudaStream_t s) {
-    gather_gate_bwd_wide_launch<T, E, K>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s);
+    if constexpr (E <= 16)  // Wg rows register-resident over a tile of tokens
+      gather_gate_bwd_tile_launch<T, E, K>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s);
+    else
+      gather_gate_bwd_wide_launch<T, E, K>(dx, idx, pos, w, dw, logits, wg, dres, dA, dlogits, T_, M, ldE, s);
   }
 };
 

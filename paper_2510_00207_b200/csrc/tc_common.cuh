@@ -8,6 +8,28 @@ namespace fm {
 
 FM_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+#ifdef FM_HANGDBG
+// probe builds (tools/probe/gemm2_hang.cu): a wait that polls too long records
+// (block, thread, barrier smem offset, parity) into host-mapped memory and gives up the
+// wait (no trap: the kernel runs on to completion with wrong data)
+__device__ unsigned int* g_hang_log;
+FM_DEV bool hang_check(uint32_t& polls, uint32_t addr, uint32_t parity) {
+  if (++polls < (1u << 22)) return false;
+  unsigned int* L = g_hang_log;
+  const unsigned int i = atomicAdd(L, 1u);
+  if (i < 64) {
+    L[1 + 4 * i] = blockIdx.x; L[2 + 4 * i] = threadIdx.x; L[3 + 4 * i] = addr; L[4 + 4 * i] = parity;
+  }
+  __threadfence_system();
+  return true;
+}
+#define FM_HANG(addr, par) hang_check(polls_, addr, par)
+#define FM_HANG_DECL uint32_t polls_ = 0
+#else
+#define FM_HANG_DECL do {} while (0)
+#define FM_HANG(addr, par) false
+#endif
+
 FM_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -17,6 +39,7 @@ FM_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 FM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  FM_HANG_DECL;
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   do {
@@ -27,12 +50,14 @@ FM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity)
         : "memory");
+    if (!ok && FM_HANG(addr, parity)) ok = 1;
   } while (!ok);
 }
 // Same, backing off between polls: for long waits (epilogue warps idle through the
 // mainloop) so spinning warps do not steal issue slots / shared-memory bandwidth from
 // the producer and MMA warps.
 FM_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  FM_HANG_DECL;
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   while (true) {
@@ -43,7 +68,7 @@ FM_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity)
         : "memory");
-    if (ok) break;
+    if (ok || FM_HANG(addr, parity)) break;
     __nanosleep(64);
   }
 }
@@ -195,6 +220,7 @@ FM_DEV void cluster_sync_all() {
 // wait with cluster-scope acquire: the phase may be completed by the peer CTA
 // (tcgen05.commit multicast, remote arrive, or a peer TMA's complete_tx)
 FM_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  FM_HANG_DECL;
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   do {
@@ -205,9 +231,11 @@ FM_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity)
         : "memory");
+    if (!ok && FM_HANG(addr, parity)) ok = 1;
   } while (!ok);
 }
 FM_DEV void mbar_wait_cl_sleep(uint64_t* bar, uint32_t parity) {
+  FM_HANG_DECL;
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   while (true) {
@@ -218,7 +246,7 @@ FM_DEV void mbar_wait_cl_sleep(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity)
         : "memory");
-    if (ok) break;
+    if (ok || FM_HANG(addr, parity)) break;
     __nanosleep(64);
   }
 }
