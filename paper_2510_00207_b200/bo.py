@@ -89,8 +89,13 @@ class TuneResult:
 
 def bo_tune(objective: Callable[[float], float], lo: float, hi: float, budget: int = 8,
             xi: float = 0.1, seed: int = 0, candidates: int = 512,
-            quantum: float = 1.0) -> TuneResult:
-    """1 random initial sample, then budget−1 EI-maximising samples on (lo, hi]."""
+            quantum: float = 1.0, xi_relative: bool = False) -> TuneResult:
+    """1 random initial sample, then budget−1 EI-maximising samples on (lo, hi].
+
+    xi is EI's exploration margin in the objective's units (ξ = 0.1, SPEC bo_tuner /
+    Appendix D).  xi_relative=True instead scales it by the observed spread (ξ·σ_obs) — a
+    design choice for objectives whose units make an absolute 0.1 meaningless (DESIGN.md,
+    S_p auto-tuning); tools/tune_sp.py uses it for iteration times in ms."""
     rng = np.random.default_rng(seed)
     grid = lo + (hi - lo) * (np.arange(1, candidates + 1) / candidates)
     xs, ys, log = [], [], []
@@ -106,8 +111,7 @@ def bo_tune(objective: Callable[[float], float], lo: float, hi: float, budget: i
             sv = float(np.var(ya)) if len(ya) > 1 and np.var(ya) > 0 else max(1e-12, float(np.mean(np.abs(ya))) * 1e-2)
             gp = GP(length=0.2 * (hi - lo), signal_var=sv, noise_var=1e-6 * sv, mean0=float(np.mean(ya))).fit(xs, ya)
             mu, var = gp.posterior(grid)
-            # EI's ξ is in the objective's units; scale the paper's 0.1 by the observed spread
-            ei = expected_improvement(mu, var, float(np.min(ya)), xi * math.sqrt(sv))
+            ei = expected_improvement(mu, var, float(np.min(ya)), xi * math.sqrt(sv) if xi_relative else xi)
             order = np.argsort(-ei, kind="stable")
             x = None
             for i in order:  # skip candidates already sampled (after quantisation)

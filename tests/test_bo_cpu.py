@@ -44,6 +44,20 @@ def test_bo_finds_interior_minimum_of_quadratic():
     assert good >= 16
 
 
+def test_bo_xi_is_absolute_by_default():
+    """SPEC's ξ = 0.1 is in the objective's units: the acquisition depends on xi itself, and
+    the relative form (ξ·σ_obs) is an explicit opt-in; both still find the optimum."""
+    lo, hi = 0.0, 10.0
+    f = lambda x: (x - 2.5) ** 2 + 3.0  # noqa: E731
+    a = bo_tune(f, lo, hi, budget=8, seed=3, quantum=1e-3)
+    b = bo_tune(f, lo, hi, budget=8, seed=3, quantum=1e-3, xi=0.1)
+    assert [x for _, x, _, _ in a.log] == [x for _, x, _, _ in b.log]
+    c = bo_tune(f, lo, hi, budget=8, seed=3, quantum=1e-3, xi=100.0)  # large absolute margin: explores
+    assert [x for _, x, _, _ in c.log] != [x for _, x, _, _ in a.log]
+    d = bo_tune(f, lo, hi, budget=8, seed=3, quantum=1e-3, xi_relative=True)
+    assert d.best_time <= 1.2 * min(f(x) for x in np.linspace(lo + 1e-3, hi, 2001))
+
+
 def test_grid_random_constant_and_monotone():
     r = grid_tune(lambda x: 5.0, 0.0, 8.0)
     assert r.best_sp == 1.0 and r.best_time == 5.0

@@ -130,7 +130,7 @@ def main():
            "iters_per_sample": args.iters}
     ladder = [MiB // 2, MiB, 2 * MiB, 4 * MiB, 8 * MiB, ar_bytes]
     out["ladder_ms"] = driven(lambda f: {str(v): f(v) for v in ladder})
-    out["bo"] = driven(lambda f: bo.bo_tune(f, 0.0, ar_bytes, budget=8, seed=0, quantum=16).__dict__)
+    out["bo"] = driven(lambda f: bo.bo_tune(f, 0.0, ar_bytes, budget=8, seed=0, quantum=16, xi_relative=True).__dict__)
     out["grid"] = driven(lambda f: bo.grid_tune(f, 0.0, ar_bytes, points=8, quantum=16).__dict__)
     out["random"] = driven(lambda f: bo.random_tune(f, 0.0, ar_bytes, draws=8, seed=1, quantum=16).__dict__)
     if rank == 0:
