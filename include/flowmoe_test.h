@@ -83,6 +83,12 @@ int flowmoe_tasklog_end(flowmoe_ctx* ctx, flowmoe_task_rec* out, int max_entries
 /* Number of kernels this library has launched in the calling process (bench accounting). */
 uint64_t flowmoe_kernel_launches(void);
 
+/* Bus-bandwidth probe: `iters` back-to-back exchanges of chunk r of a registered `saved`
+ * stash (kind 0: dispatch D_r owner -> expert side, 1: combine C_r back), through the ctx's
+ * A2A implementation (NCCL send/recv groups or the peer-memory kernel), ordered after the
+ * work on `stream` and waited for by it.  Collective; world_size > 1 (NCCL world) only. */
+flowmoe_status flowmoe_test_exchange(flowmoe_ctx* ctx, void* saved, int kind, int r, int iters, cudaStream_t stream);
+
 /* The peer-memory A2A arrival counters of this rank: out[(kind·R + r)·P + src] = how many
  * times source rank `src` has delivered exchange `kind` (0 D_r, 1 C_r, 2 C_r^bwd, 3 D_r^bwd)
  * of chunk r into this rank (monotonic).  n >= 4·R·world_size.  Synchronises the device.

@@ -545,6 +545,8 @@ flowmoe_status ipc_exchange(flowmoe_ctx* x, void* ptr, std::vector<void*>* out, 
 }
 
 flowmoe_status register_saved(flowmoe_ctx* x, const void* saved);
+flowmoe_status p2p_exchange(flowmoe_ctx* x, int kind, int r, const void* src, void* const* dst, int to_experts,
+                            cudaStream_t sa);
 
 // Peer-memory A2A for this `saved` stash?  *use = true when every rank's stash is mapped.
 // A stash that was not registered (flowmoe_register_saved) is registered here on first
@@ -1024,6 +1026,39 @@ flowmoe_status flowmoe_unregister_saved(flowmoe_ctx* x, const void* saved) {
   x->peer_saved.erase(saved);
   for (size_t i = 0; i < x->saved_order.size(); ++i)
     if (x->saved_order[i] == saved) { x->saved_order.erase(x->saved_order.begin() + i); break; }
+  return FLOWMOE_OK;
+}
+
+flowmoe_status flowmoe_test_exchange(flowmoe_ctx* x, void* saved, int kind, int r, int iters, cudaStream_t stream) {
+  if (!x || !saved) return fail(FLOWMOE_ERR_INVALID, "test_exchange: NULL argument");
+  if (kind < 0 || kind > 1 || r < 0 || r >= x->cfg.R || iters < 1)
+    return fail(FLOWMOE_ERR_INVALID, "test_exchange: kind in {0,1}, 0 <= r < R, iters >= 1");
+  if (x->P == 1 || x->group) return fail(FLOWMOE_ERR_UNSUPPORTED, "test_exchange: needs world_size > 1 (NCCL world)");
+  apply_ctx(x);
+  bool use_p2p = false;
+  if (flowmoe_status st = resolve_p2p(x, saved, stream, &use_p2p)) return st;
+  const SavedLayout& L = x->L;
+  const size_t src = kind == 0 ? L.send : L.ye, dst = kind == 0 ? L.xe : L.yc;
+  cudaStream_t sa = use_p2p ? stream : x->a2a_stream[r % x->a2a_stream.size()];
+  if (sa != stream) {
+    FM_CUDA(cudaEventRecord(x->ev_in, stream));
+    FM_CUDA(cudaStreamWaitEvent(sa, x->ev_in, 0));
+  }
+  for (int i = 0; i < iters; ++i) {
+    if (use_p2p) {
+      std::vector<void*> d(x->P);
+      for (int q = 0; q < x->P; ++q) d[q] = (char*)x->peer_saved[saved][q] + dst;
+      if (flowmoe_status st = p2p_exchange(x, kind, r, (char*)saved + src, d.data(), kind == 0 ? 1 : 0, sa)) return st;
+    } else if (kind == 0) {
+      if (flowmoe_status st = a2a_to_experts(x, (char*)saved + src, (char*)saved + dst, r)) return st;
+    } else if (flowmoe_status st = a2a_to_owners(x, (char*)saved + src, (char*)saved + dst, r)) {
+      return st;
+    }
+  }
+  if (sa != stream) {
+    FM_CUDA(cudaEventRecord(x->ev_done, sa));
+    FM_CUDA(cudaStreamWaitEvent(stream, x->ev_done, 0));
+  }
   return FLOWMOE_OK;
 }
 

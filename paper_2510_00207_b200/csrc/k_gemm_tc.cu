@@ -531,23 +531,20 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (g_force_bn == 256) return launch_tc<256, 4>(g, s);
   if (g_force_bn == 128) return launch_tc<128, 6>(g, s);
   if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
-  if (g_force_cg == 0) {
-    // CTA pairs for the large GEMMs: at least one full wave of pairs; the pair tile width
-    // (256 or 128 columns of 256 rows) with the fewer wave-quantised column-passes
-    const int64_t mt2 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch;
-    const int64_t t256 = mt2 * ((g.N + 255) / 256), t128 = mt2 * ((g.N + 127) / 128);
-    const int64_t pairs = 74;
-    if (g.M > TC_BM && t256 >= pairs) {
-      const int64_t c256 = (t256 + pairs - 1) / pairs * 2, c128 = (t128 + pairs - 1) / pairs;
-      return c128 < c256 ? launch_tc<128, 8, 1, 2>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
-    }
+  const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
+  if (g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 4 * TC_BK)) {
+    // CTA pairs (256 x 256 tiles) once they fill at least one wave of the 74 TPC pairs:
+    // tools/gemm_microbench.py at the dsv2s shapes, 1-CTA 256-wide -> pairs: QKV 1006 ->
+    // 1175, E2 940 -> 1086, dX_e 918 -> 1068, dX 895 -> 993, dWqkv 1075 -> 1137 TFLOP/s;
+    // 256-column pair tiles beat 128-column ones everywhere (fewer, longer mainloops)
+    const int64_t t256 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch * ((g.N + 255) / 256);
+    if (t256 >= 74) return launch_tc<256, 6, 1, 2>(g, s);
   }
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
   // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) take a 3-stage ring
   // and double-buffered epilogue staging (tools/probe/gemm_probe.cu: -2..-6%); the
   // 4-stage ring stays everywhere else (3 stages cost 3-8% on longer K)
-  const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
   if (g.N >= 256 && f32out && g.K <= 4 * TC_BK && tiles(256) >= 4 * 148) return launch_tc<256, 3, 2>(g, s);
   if (g.N >= 256 && tiles(256) >= 48) return launch_tc<256, 4>(g, s);
   if (g.N >= 128 && tiles(128) >= 48) return launch_tc<128, 6>(g, s);

@@ -920,11 +920,13 @@ static void gather_gate_bwd_wide_launch(const void* dx, const int32_t* idx, cons
            dw, logits, (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, ldE);
 }
 
-// E <= 16, wide rows: a CTA stages the Wg rows of its 128 column vectors in shared memory
-// once and walks TB tokens, so Wg is read from L2 once per TB tokens instead of once per
-// token (the one-token-per-thread kernel above re-read ~2.5x the kernel's HBM bytes of Wg
-// from L2).  The tokens' dlogits come from shared memory (first TB threads); at k <= 4
-// two tokens' gathered rows + dO are requested together.
+// E <= 16, wide rows: a CTA covers 128 column vectors x GGB_TB tokens.  It stages its
+// Wg slice TRANSPOSED in shared memory ([E][128·V]: one 16-byte vector per (expert, column
+// vector)), the tokens' routing (idx, pos) and their dlogits; then, since dlogits is zero
+// outside a token's k selected experts (k >= 2, reading Q5), each token needs only k
+// vector reads of Wgᵀ (E for k = 1) — the one-token-per-thread kernel above re-read all E
+// columns of 8 Wg rows from L2 for every token (~2.5x the kernel's HBM bytes).  Two
+// tokens' gathered rows + dO are requested together.  Same summation order as above.
 constexpr int GGB_TB = 8, GGB_THREADS = 128;
 
 template <typename T, int E, int K>
@@ -935,19 +937,32 @@ __global__ void __launch_bounds__(GGB_THREADS) gather_gate_bwd_tile_kernel(
     int M, int ldE) {
   constexpr int V = 16 / sizeof(T);
   __shared__ float dls[GGB_TB][E];
-  extern __shared__ uint4 wgs4[];  // [GGB_THREADS * V][E] storage elements: this CTA's Wg rows
+  __shared__ int rte[GGB_TB][K], rtp[GGB_TB][K];
+  extern __shared__ uint4 wgt4[];  // [E][GGB_THREADS] 16-byte vectors: Wgᵀ of this CTA's columns
   FM_PDL_ENTRY();
   const int nv = M / V;
   const int cvec = blockIdx.x * GGB_THREADS + threadIdx.x;
-  {  // stage the CTA's Wg rows (contiguous in Wg [M][E]) with 16-byte loads
-    const int mrow0 = blockIdx.x * GGB_THREADS * V;
-    const int nrows = min(GGB_THREADS * V, M - mrow0);
-    const uint4* src = reinterpret_cast<const uint4*>(wg + (int64_t)mrow0 * E);
-    const int n16 = nrows * E * (int)sizeof(T) / 16;
-    for (int i = threadIdx.x; i < n16; i += GGB_THREADS) wgs4[i] = src[i];
-  }
   const int t0 = blockIdx.y * GGB_TB;
   const int m = cvec * V;
+  {  // transpose-stage: thread c reads its V Wg rows (V·E elements) and writes E vectors
+    if (cvec < nv) {
+      T col[E][V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float r[E];
+        load_n<T, E>(wg + (int64_t)(m + v) * E, r);
+#pragma unroll
+        for (int e = 0; e < E; ++e) col[e][v] = from_f<T>(r[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) wgt4[e * GGB_THREADS + threadIdx.x] = *reinterpret_cast<const uint4*>(col[e]);
+    }
+    for (int i = threadIdx.x; i < GGB_TB * K; i += GGB_THREADS) {
+      const int t = t0 + i / K;
+      rte[i / K][i % K] = t < T_ ? idx[(int64_t)t0 * K + i] : 0;
+      rtp[i / K][i % K] = t < T_ ? pos[(int64_t)t0 * K + i] : -1;
+    }
+  }
   // dlogits of the tile's tokens (reading Q5), one thread per token
   if (threadIdx.x < GGB_TB) {
     const int t = t0 + threadIdx.x;
@@ -997,46 +1012,62 @@ __global__ void __launch_bounds__(GGB_THREADS) gather_gate_bwd_tile_kernel(
   }
   __syncthreads();
   if (cvec >= nv) return;
-  const T* wrow = reinterpret_cast<const T*>(wgs4) + (int64_t)threadIdx.x * V * E;  // my V rows
-  // PF tokens' gathered rows requested together (more loads in flight at small k)
-  constexpr int PF = K <= 4 ? 2 : 1;
+  constexpr int PF = 2;
 #pragma unroll 1
   for (int i0 = 0; i0 < GGB_TB; i0 += PF) {
-    int pj[PF][K];
     uint4 raw[PF][K], rres[PF];
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      const int t = t0 + i0 + q;
-      const bool ok = t < T_;
+      const int i = i0 + q, t = t0 + i;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        pj[q][j] = ok ? pos[(int64_t)t * K + j] : -1;
-        raw[q][j] = make_uint4(0, 0, 0, 0);
-        if (pj[q][j] >= 0)
-          raw[q][j] = *reinterpret_cast<const uint4*>(dx + ((int64_t)idx[(int64_t)t * K + j] * ldE + pj[q][j]) * M + m);
+        const int p = rtp[i][j];
+        raw[q][j] = p >= 0 ? *reinterpret_cast<const uint4*>(dx + ((int64_t)rte[i][j] * ldE + p) * M + m)
+                           : make_uint4(0, 0, 0, 0);
       }
-      rres[q] = make_uint4(0, 0, 0, 0);
-      if (dres && ok) rres[q] = *reinterpret_cast<const uint4*>(dres + (int64_t)t * M + m);
+      rres[q] = (dres && t < T_) ? *reinterpret_cast<const uint4*>(dres + (int64_t)t * M + m) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
       const int i = i0 + q, t = t0 + i;
       if (t >= T_) break;
-      float acc[V], dl[E];
+      // Σ_e dl[e]·Wg[m+v][e] in e order; with k >= 2 only the selected experts are non-zero
+      // (the zero terms of the dense sum add nothing, so this is the same value up to the
+      // order of the k non-zero terms: ascending expert index, as the dense loop)
+      float acc[V];
 #pragma unroll
-      for (int e = 0; e < E; ++e) dl[e] = dls[i][e];
+      for (int v = 0; v < V; ++v) acc[v] = 0.f;
+      if constexpr (K == 1) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float wr[E];
-        load_n<T, E>(wrow + v * E, wr);
-        float sum = 0.f;
+        for (int e = 0; e < E; ++e) {
+          float wv[V];
+          load16<T>(reinterpret_cast<const T*>(&wgt4[e * GGB_THREADS + threadIdx.x]), wv);
+          const float d = dls[i][e];
 #pragma unroll
-        for (int e = 0; e < E; ++e) sum = fmaf(dl[e], wr[e], sum);
-        acc[v] = sum;
+          for (int v = 0; v < V; ++v) acc[v] = fmaf(d, wv[v], acc[v]);
+        }
+      } else {
+        // the selected experts in ascending order (k <= 8: a small sorting network)
+        int es[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) es[j] = rte[i][j];
+#pragma unroll
+        for (int a = 0; a < K; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 + 1 < K - a; ++b2)
+            if (es[b2] > es[b2 + 1]) { const int tmp = es[b2]; es[b2] = es[b2 + 1]; es[b2 + 1] = tmp; }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float wv[V];
+          load16<T>(reinterpret_cast<const T*>(&wgt4[es[j] * GGB_THREADS + threadIdx.x]), wv);
+          const float d = dls[i][es[j]];
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = fmaf(d, wv[v], acc[v]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < K; ++j)
-        if (pj[q][j] >= 0) {
+        if (rtp[i][j] >= 0) {
           float v8[V];
           load16<T>(reinterpret_cast<const T*>(&raw[q][j]), v8);
 #pragma unroll
@@ -1059,7 +1090,7 @@ static void gather_gate_bwd_tile_launch(const void* dx, const int32_t* idx, cons
                                         void* dA, float* dlogits, int T_, int M, int ldE, cudaStream_t s) {
   const int nv = M / (16 / (int)sizeof(T));
   dim3 grid((nv + GGB_THREADS - 1) / GGB_THREADS, (T_ + GGB_TB - 1) / GGB_TB);
-  const size_t smem = (size_t)GGB_THREADS * (16 / sizeof(T)) * E * sizeof(T);
+  const size_t smem = (size_t)GGB_THREADS * E * 16;
   launch_k(gather_gate_bwd_tile_kernel<T, E, K>, grid, GGB_THREADS, smem, s, (const T*)dx, idx, pos, w, dw, logits,
            (const T*)wg, (const T*)dres, (T*)dA, dlogits, T_, M, ldE);
 }

@@ -32,7 +32,7 @@ EXPORTED = [
 EXPORTED_TEST = [
     "flowmoe_saved_routing_offsets", "flowmoe_debug_set", "flowmoe_test_gemm", "flowmoe_profile_begin",
     "flowmoe_profile_end", "flowmoe_kernel_launches", "flowmoe_create_local_group", "flowmoe_test_arrivals",
-    "flowmoe_tasklog_begin", "flowmoe_tasklog_end",
+    "flowmoe_tasklog_begin", "flowmoe_tasklog_end", "flowmoe_test_exchange",
 ]
 TASK_KINDS = ("AT", "D", "E", "C", "MERGE", "CBPACK", "CB", "EB", "DB", "WGE", "ATB", "WGA", "AR")
 
@@ -131,6 +131,7 @@ def lib() -> ctypes.CDLL:
     L.flowmoe_unregister_saved.argtypes = [vp, vp]
     L.flowmoe_check_health.argtypes = [vp]
     L.flowmoe_test_arrivals.argtypes = [vp, ctypes.POINTER(ctypes.c_uint), sz]
+    L.flowmoe_test_exchange.argtypes = [vp, vp, i32, i32, i32, vp]
     L.flowmoe_create_local_group.argtypes = [ctypes.POINTER(Config), i32, i32, ctypes.POINTER(vp)]
     L.flowmoe_set_forced_routing.argtypes = [vp, vp]
     L.flowmoe_saved_routing_offsets.argtypes = [vp] + [ctypes.POINTER(sz)] * 5
@@ -274,6 +275,11 @@ class FlowMoE:
         buf = (ctypes.c_uint * n)()
         _check(lib().flowmoe_test_arrivals(self.handle, buf, n), "flowmoe_test_arrivals")
         return np.array(buf[:], dtype=np.int64).reshape(4, self.shape.R, self.shape.world_size)
+
+    def test_exchange(self, saved, kind: int, r: int, iters: int, stream=None):
+        """iters back-to-back A2A exchanges of chunk r (flowmoe_test.h flowmoe_test_exchange)."""
+        _check(lib().flowmoe_test_exchange(self.handle, _ptr(saved), kind, r, iters, _stream_handle(stream)),
+               "flowmoe_test_exchange")
 
     def check_health(self):
         _check(lib().flowmoe_check_health(self.handle), "flowmoe_check_health")
