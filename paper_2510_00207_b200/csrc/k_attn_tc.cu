@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 template <int DH>
 constexpr int DKDV_QSTAGES = DH == 64 ? 2 : 1;
 
-// grid (ceil(np/128) own key tiles, H, n_seq); query tiles are 128-aligned positions from
-// the key tile's diagonal (causal) to N.  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
+// grid (ceil(np/128) own key tiles, H, n_seq); query tiles of 128 rows from the key tile's
+// first row (causal) to N.  TMEM: S^T [0,128), dP^T [128,256), dV, dK.
 template <int DH>
 __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const CUtensorMap& tdo, const float* lse,
                                                    const bf16* ctxO, const bf16* dctx, bf16* dqkv, int N, int p0,
@@ -328,9 +328,13 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = p0 + kt * 128, row_base = sq * N;
-  const int nq_tiles = (N + 127) / 128;
-  const int qt0 = causal ? k0 / 128 : 0;
-  const int niter = nq_tiles - qt0;
+  // query tiles from the key tile's first row (causal) to N.  A token chunk's keys start
+  // mid-sequence (p0 not a multiple of 128): a 128-aligned first tile would also load the
+  // dO rows of EARLIER chunks, which this backward has not produced yet (stale or
+  // uninitialised memory: 0·NaN = NaN through P = 0 and dS = 0); tiles starting at k0 read
+  // only queries >= k0.  Whole-sequence chunks (p0 = 0) keep the 128-aligned tiles.
+  const int qs0 = causal ? k0 : 0;
+  const int niter = (N - qs0 + 127) / 128;
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_bar, 1);
@@ -358,7 +362,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
     }
     __syncwarp();
     for (int it = 0; it < niter; ++it) {
-      const int qr = row_base + (qt0 + it) * 128;
+      const int qr = row_base + qs0 + it * 128;
       const int st = it % QST;
       if (it >= QST) mbar_wait_sleep(&q_empty[st], ((it / QST) - 1) & 1);
       uint8_t* sQ = sQ0 + st * 2 * TILE;
@@ -416,7 +420,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tq, const 
     const int t256 = threadIdx.x - 64;  // 0..255
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int it = 0; it < niter; ++it) {
-      const int qbase = (qt0 + it) * 128;
+      const int qbase = qs0 + it * 128;
       named_bar_sync(1, 256);  // everyone is done reading sL/sD of the previous tile
       if (t256 < 128) {
         const int qi = qbase + t256;
