@@ -96,6 +96,26 @@ def expert_grads(eg: dict, lo: int, hi: int):
             for i, name in enumerate(("dw1", "db1", "dw2", "db2"))}
 
 
+class HostGate:
+    """Holds a stream at a device-side wait on a pinned host flag (cuStreamWaitValue32) until
+    release(): everything enqueued behind it is queued before the GPU starts, so measured
+    task timelines carry no host-enqueue gaps (the schedule-property checks compare task
+    start times with their ready times)."""
+
+    def __init__(self, stream):
+        import ctypes
+
+        import torch
+        self.flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+        cu = ctypes.CDLL("libcuda.so.1")
+        cu.cuStreamWaitValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
+        rc = cu.cuStreamWaitValue32(ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()), 1, 0)
+        assert rc == 0, f"cuStreamWaitValue32: CUresult {rc}"
+
+    def release(self):
+        self.flag[0] = 1
+
+
 def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: int = 1,
                   schedule: str = "flowmoe", graph: bool = False, device: int = 0,
                   api: str = "per_block", P: int = 1, rank: int = 0, uid: bytes | None = None,
@@ -141,10 +161,12 @@ def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: in
     s = torch.cuda.current_stream()
     iteration(s)
     log = None
-    if tasklog:  # a second eager iteration with the task log on (schedule properties)
-        torch.cuda.synchronize()
+    if tasklog:  # a second eager iteration with the task log on (schedule properties), fully
+        torch.cuda.synchronize()  # enqueued behind a host gate before the GPU runs any of it
         ctx.tasklog_begin()
+        gate = HostGate(s)
         iteration(s)
+        gate.release()
         log = ctx.tasklog_end()
     if graph:  # capture the same iteration and replay it twice (overwrite grads -> same values)
         for bt in bts:

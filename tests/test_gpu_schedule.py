@@ -70,7 +70,13 @@ def stack_logs(cfg, P, lanes, L=3, schedule="flowmoe", chunk_bytes=256 << 10):
     torch.cuda.synchronize()
     for c in ctxs:
         c.tasklog_begin()
-    run_all()
+    if P == 1:  # the whole iteration enqueued before the GPU starts it (no host gaps)
+        from tests.gpu_util import HostGate
+        gate = HostGate(s)
+        run_all()
+        gate.release()
+    else:  # the simulated ranks' host threads meet at barriers: they cannot all enqueue first
+        run_all()
     logs = [c.tasklog_end() for c in ctxs]
     for c in ctxs:
         c.close()

@@ -37,6 +37,9 @@ SHAPES = {  # name: (M rows, N, K, batch, a_mmajor, b_kmajor, epi)
     "dsv2s_dw2": (1536, 5120, 512, 16, 1, 0, 4),
     "dsv2s_dwqkv": (5120, 15360, 1024, 1, 1, 0, 4),
     "dsv2s_dwo": (5120, 5120, 1024, 1, 1, 0, 4),
+    # with the block's real epilogues: E1 bias + GELU saving GELU'(z) (5), dZ = dH ⊙ aux (6)
+    "dsv2s_e1gelu": (256, 1536, 5120, 16, 0, 0, 5),
+    "dsv2s_dgelu_mul": (256, 1536, 5120, 16, 0, 1, 6),
 }
 
 _CTX = None
@@ -56,12 +59,14 @@ def run(name, reps, bn, pdl, cg=0):
     A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
     B = torch.randn(batch, (N if bk else K), (K if bk else N), device=dev).to(torch.bfloat16) * 0.05
     C = torch.zeros(batch, Mr, N, device=dev, dtype=torch.float32 if epi == 4 else torch.bfloat16)
+    bias = torch.randn(batch, N, device=dev).to(torch.bfloat16) if epi == 5 else None
+    aux = torch.randn(batch, Mr, N, device=dev).to(torch.bfloat16) if epi in (5, 6) else None
     ctx = knob_ctx()
     ctx.debug_set(5, bn)
     ctx.debug_set(4, pdl)
     ctx.debug_set(7, cg)
     kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
-              ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi)
+              ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi, bias=bias, aux=aux)
     s = torch.cuda.current_stream()
     fm.test_gemm("bf16", A, B, C, stream=s, ctx=ctx, **kw)
     torch.cuda.synchronize()

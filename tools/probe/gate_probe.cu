@@ -59,5 +59,6 @@ int main() {
   run("c3ks2", 1024, 1024, 16, 2, 128);
   g_gate_force_ks = 0;
   run("c4", 1024, 4096, 16, 2, 128);
+  run("dsv2s", 512, 5120, 16, 8, 256);
   return 0;
 }
