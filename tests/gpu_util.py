@@ -97,23 +97,31 @@ def expert_grads(eg: dict, lo: int, hi: int):
 
 
 class HostGate:
-    """Holds a stream at a device-side wait on a pinned host flag (cuStreamWaitValue32) until
-    release(): everything enqueued behind it is queued before the GPU starts, so measured
-    task timelines carry no host-enqueue gaps (the schedule-property checks compare task
-    start times with their ready times)."""
+    """Holds a stream at a device-side wait (cuStreamWaitValue32, a stream memory operation —
+    no kernel spins) on a device flag until release() writes the flag from another stream:
+    everything enqueued behind the gate is queued before the GPU starts any of it, so measured
+    task timelines carry no host-enqueue gaps (the schedule-property checks compare task start
+    times with their ready times)."""
 
     def __init__(self, stream):
         import ctypes
 
         import torch
-        self.flag = torch.zeros(1, dtype=torch.int32).pin_memory()
-        cu = ctypes.CDLL("libcuda.so.1")
-        cu.cuStreamWaitValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
-        rc = cu.cuStreamWaitValue32(ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()), 1, 0)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=stream.device)
+        torch.cuda.synchronize()
+        self.cu = ctypes.CDLL("libcuda.so.1")
+        self.cu.cuStreamWaitValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
+        self.cu.cuStreamWriteValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
+        rc = self.cu.cuStreamWaitValue32(ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
+                                         1, 0)  # CU_STREAM_WAIT_VALUE_GEQ
         assert rc == 0, f"cuStreamWaitValue32: CUresult {rc}"
+        self.side = torch.cuda.Stream(device=stream.device)
 
     def release(self):
-        self.flag[0] = 1
+        import ctypes
+        rc = self.cu.cuStreamWriteValue32(ctypes.c_void_p(self.side.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
+                                          1, 0)
+        assert rc == 0, f"cuStreamWriteValue32: CUresult {rc}"
 
 
 def run_stack_gpu(cfg: BlockConfig, reps: list, wk: dict, *, compute_streams: int = 1,
