@@ -110,16 +110,16 @@ class HostGate:
         self.flag = torch.zeros(1, dtype=torch.int32, device=stream.device)
         torch.cuda.synchronize()
         self.cu = ctypes.CDLL("libcuda.so.1")
-        self.cu.cuStreamWaitValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
-        self.cu.cuStreamWriteValue32.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
-        rc = self.cu.cuStreamWaitValue32(ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
+        self.cu.cuStreamWaitValue32_v2.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
+        self.cu.cuStreamWriteValue32_v2.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint]
+        rc = self.cu.cuStreamWaitValue32_v2(ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
                                          1, 0)  # CU_STREAM_WAIT_VALUE_GEQ
         assert rc == 0, f"cuStreamWaitValue32: CUresult {rc}"
         self.side = torch.cuda.Stream(device=stream.device)
 
     def release(self):
         import ctypes
-        rc = self.cu.cuStreamWriteValue32(ctypes.c_void_p(self.side.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
+        rc = self.cu.cuStreamWriteValue32_v2(ctypes.c_void_p(self.side.cuda_stream), ctypes.c_uint64(self.flag.data_ptr()),
                                           1, 0)
         assert rc == 0, f"cuStreamWriteValue32: CUresult {rc}"
 
