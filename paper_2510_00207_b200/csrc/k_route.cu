@@ -38,7 +38,7 @@ FM_DEV uint32_t rt_mapa(uint32_t a, uint32_t rank) {
 }
 
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
-                                int E, int k, int C, int* hist, int* stage);
+                                int E, int k, int C, int* hist, int* warp_tot);
 
 // ------------------------------------------------------------------ K1
 // logits = A·Wg is a [T_r × M]·[M × E] product with E ≤ 64: HBM-bound on A.  A CTA
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
                                                         const int32_t* forced, float* logits,
                                                         int32_t* idx, float* w, int T_, int M, int MS,
                                                         int k, int32_t* pos, int32_t* counts,
-                                                        int32_t* src, int C, unsigned int* done, int staged) {
+                                                        int32_t* src, int C, unsigned int* done) {
   using G = GateTile<T, E>;
   constexpr int V = 16 / sizeof(T), TB = G::TB, EG = G::EG, NEG = G::NEG;
   extern __shared__ float gsm[];  // [8][TB][E] warp partials, [TB][E] CTA sum; later the scan's hist
@@ -197,75 +197,57 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
   for (int q = threadIdx.x; q < TB * E; q += blockDim.x)
     if (tt0 + q / E < T_) logits[(int64_t)tt0 * E + q] = red[q];
   if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(17);
-  {
-    // top-k on register-resident logits: G = 256 / TB lanes per token, each holding experts
-    // gl, gl + G, ...; every round picks the largest remaining logit with a butterfly over the
-    // token's lanes (strictly greater, equal values -> lower expert index: the serial rule)
-    constexpr int G = 256 / TB, EPL = (E + G - 1) / G;
-    const int tl = threadIdx.x / G, gl = threadIdx.x % G;
-    const int t = tt0 + tl;
-    const bool tok = t < T_;
-    float lv[EPL];
-    bool taken[EPL];
+  if (threadIdx.x < TB && tt0 + (int)threadIdx.x < T_) {
+    const int t = tt0 + threadIdx.x;
+    float lg[E];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
-      const int e = gl + i * G;
-      lv[i] = (e < E) ? red[tl * E + e] : -INFINITY;
-      taken[i] = e >= E;
-    }
-    float sv[8];
+    for (int e = 0; e < E; ++e) lg[e] = red[threadIdx.x * E + e];
+    // top-k selection on logits, register-resident (k <= 8 unrolled, E compile-time)
+    uint64_t taken = 0;
     int sel[8];
+    float sv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (j >= k) break;
-      float bv;
-      int bi;
-      if (forced) {
-        bi = tok ? forced[(int64_t)t * k + j] : 0;
-        bv = red[tl * E + bi];
-      } else {
-        bv = -INFINITY;
-        bi = E;
+      if (j < k) {
+        int best = -1;
+        float bv = 0.f;
+        if (forced) {
+          best = forced[(int64_t)t * k + j];
 #pragma unroll
-        for (int i = 0; i < EPL; ++i)
-          if (!taken[i] && (bi == E || lv[i] > bv)) { bv = lv[i]; bi = gl + i * G; }
+          for (int e = 0; e < E; ++e)
+            if (e == best) bv = lg[e];
+        } else {
 #pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (oi < E && (bi == E || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+          for (int e = 0; e < E; ++e)
+            if (!((taken >> e) & 1ull) && (best < 0 || lg[e] > bv)) { best = e; bv = lg[e]; }
         }
+        taken |= 1ull << best;
+        sel[j] = best;
+        sv[j] = bv;
+        idx[(int64_t)t * k + j] = best;
       }
-#pragma unroll
-      for (int i = 0; i < EPL; ++i)
-        if (gl + i * G == bi) taken[i] = true;
-      sel[j] = bi;
-      sv[j] = bv;
     }
     if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(18);
-    if (gl == 0 && tok) {
+    if (k == 1) {
+      // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
+      float den = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) den += expf(lg[e] - sv[0]);
+      w[t] = 1.f / den;
+    } else {
+      float mx = sv[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (j < k) mx = fmaxf(mx, sv[j]);
+      float den = 0.f, ex[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < k) idx[(int64_t)t * k + j] = sel[j];
-      if (k == 1) {
-        // w0 = p_{e0} = 1 / Σ_e exp(l_e - l_e0)
-        float den = 0.f;
-        for (int e = 0; e < E; ++e) den += expf(red[tl * E + e] - sv[0]);
-        w[t] = 1.f / den;
-      } else {
-        float mx = sv[0];
+        if (j < k) { ex[j] = expf(sv[j] - mx); den += ex[j]; }
 #pragma unroll
-        for (int j = 1; j < 8; ++j)
-          if (j < k) mx = fmaxf(mx, sv[j]);
-        float den = 0.f, ex[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < k) { ex[j] = expf(sv[j] - mx); den += ex[j]; }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < k) w[(int64_t)t * k + j] = ex[j] / den;
-      }
+      for (int j = 0; j < 8; ++j)
+        if (j < k) w[(int64_t)t * k + j] = ex[j] / den;
     }
+    (void)sel;
   }
   if (done == nullptr) return;
   if (blockIdx.x == 0 && blockIdx.y == 0) FM_GMARK(7);
@@ -279,9 +261,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
   FM_GMARK(8);
   // thread 0's acquire (the ticket) + the barrier above order every tile's idx before
   // this CTA's reads (the grid-sync pattern)
-  int* hist = reinterpret_cast<int*>(gsm);
-  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, staged ? hist + E * (256 + 8) : nullptr);
-  (void)warp_tot;
+  route_scan_body(idx, pos, counts, src, T_, E, k, C, reinterpret_cast<int*>(gsm), warp_tot);
   FM_GMARK(12);
   if (threadIdx.x == 0) *done = 0u;  // ready for the next use (stream-ordered)
 }
@@ -300,11 +280,12 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const T* a, const T* wg,
 // Slices of M per token tile: enough CTAs to cover ~2 waves of the 148 SMs, at most a
 // portable cluster (8), at least one 16-byte vector per warp.
 int g_gate_force_ks = 0;  // probe / A-B only: force the number of M slices (1..8)
+int g_route_stage = 0;    // probe compatibility (the shared-memory staged scan was measured slower and removed)
 
 static void gate_split(int T_, int M, int TB, int V, int* KS, int* MS) {
   const int tiles = (T_ + TB - 1) / TB, nvec = M / V;
   int ks = (2 * 148 + tiles - 1) / tiles;
-  ks = ks < 1 ? 1 : (ks > 16 ? 16 : ks);  // > 8: non-portable cluster size (enabled at launch)
+  ks = ks < 1 ? 1 : (ks > 8 ? 8 : ks);
   if (ks > nvec / 8) ks = nvec / 8 > 0 ? nvec / 8 : 1;
   if (g_gate_force_ks > 0) ks = g_gate_force_ks;
   const int msv = (nvec + ks - 1) / ks;
@@ -320,22 +301,10 @@ static void gate_topk_launch_t(const void* a, const void* wg, const int32_t* for
   int KS, MS;
   gate_split(T_, M, G::TB, 16 / (int)sizeof(T), &KS, &MS);
   auto kern = gate_topk_kernel<T, E>;
-  constexpr int kMaxSmem = 200 * 1024;
-  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
-                      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), true);
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem()), true);
   (void)once;
-  // the fused routing scan stages idx/pos and src in shared memory when they fit
-  size_t smem = G::smem(KS);
-  int staged = 0;
-  if (done) {
-    const size_t need = (size_t)E * (256 + 8) * 4 + ((size_t)T_ * k + (size_t)E * C) * 4;
-    if (need <= (size_t)kMaxSmem) {
-      staged = 1;
-      if (need > smem) smem = need;
-    }
-  }
-  launch_kc(kern, dim3((T_ + G::TB - 1) / G::TB, KS), 256, smem, s, dim3(1, KS, 1), (const T*)a,
-            (const T*)wg, forced, logits, idx, w, T_, M, MS, k, pos, counts, src, C, done, staged);
+  launch_kc(kern, dim3((T_ + G::TB - 1) / G::TB, KS), 256, G::smem(KS), s, dim3(1, KS, 1), (const T*)a,
+            (const T*)wg, forced, logits, idx, w, T_, M, MS, k, pos, counts, src, C, done);
 }
 
 template <int E>
@@ -378,12 +347,9 @@ constexpr int RS_THREADS = 512;
 
 // Block-wide deterministic routing scan (one CTA, blockDim a power of two in [32, 1024]):
 // hist is [E][blockDim.x + blockDim.x/32] ints of dynamic shared memory (padded rows).
-// stage (nullable): [T·k + E·C] ints of shared memory.  With it, idx is read into shared
-// memory with coalesced loads, pos and src are built there and written out coalesced at the
-// end (round 2: the strided idx loads, the src = -1 fill and the scattered pos / src stores
-// went to L2 one by one and took ~7 of the scan's ~9 µs at T_r·k = 4096, dsv2s).
 __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_,
-                                int E, int k, int C, int* hist, int* stage) {
+                                int E, int k, int C, int* hist, int* warp_tot) {
+  (void)warp_tot;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int n = T_ * k;
   const int seg = (n + nt - 1) / nt;
@@ -392,17 +358,6 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
   // lane-runs of the scan below (lane L reads threads L·per .. L·per+per-1) conflict-free
   const int rs = nt + nt / 32;
   const int my = tid + (tid >> 5);
-  int* sl = stage;                          // [n]: idx, then pos (token-major, as in global)
-  int* ss = stage ? stage + n : nullptr;    // [E·C]: src
-  if (stage) {
-    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0)
-      for (int i = tid; i < n / 4; i += nt) reinterpret_cast<int4*>(sl)[i] = reinterpret_cast<const int4*>(idx)[i];
-    else
-      for (int i = tid; i < n; i += nt) sl[i] = idx[i];
-    for (int i = tid; i < E * C; i += nt) ss[i] = -1;
-    __syncthreads();
-  }
-  const int32_t* isrc = stage ? sl : idx;
   // a thread's slots (slot-major: s = j·T + t) are loaded once, all in flight together,
   // and kept in registers for both passes when they fit (seg <= SCAN_REG): a dependent
   // L2 round trip per slot (the loop below) cost ~20 µs at T_r·k = 4096 slots
@@ -415,12 +370,11 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
     ev[i] = 0;
     if (in_reg && s < s1) {
       const int j = s / T_, t = s - j * T_;
-      ev[i] = isrc[(int64_t)t * k + j];
+      ev[i] = idx[(int64_t)t * k + j];
     }
   }
   for (int e = 0; e < E; ++e) hist[e * rs + my] = 0;
-  if (!stage)
-    for (int i = tid; i < E * C; i += nt) src[i] = -1;
+  for (int i = tid; i < E * C; i += nt) src[i] = -1;
   __syncthreads();
   FM_GMARK(9);
   if (in_reg) {
@@ -430,7 +384,7 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
   } else {
     for (int s = s0; s < s1; ++s) {
       const int j = s / T_, t = s - j * T_;
-      hist[isrc[(int64_t)t * k + j] * rs + my] += 1;
+      hist[idx[(int64_t)t * k + j] * rs + my] += 1;
     }
   }
   __syncthreads();
@@ -456,56 +410,42 @@ __device__ void route_scan_body(const int32_t* idx, int32_t* pos, int32_t* count
   }
   __syncthreads();
   FM_GMARK(11);
-  int32_t* pdst = stage ? sl : pos;
-  int32_t* sdst = stage ? ss : src;
   auto place = [&](int s, int e) {
     const int j = s / T_, t = s - j * T_;
     const int p = hist[e * rs + my]++;
     const bool kept = p < C;
-    pdst[(int64_t)t * k + j] = kept ? p : -1;
-    if (kept) sdst[e * C + p] = t * k + j;
+    pos[(int64_t)t * k + j] = kept ? p : -1;
+    if (kept) src[e * C + p] = t * k + j;
   };
   if (in_reg) {
 #pragma unroll
     for (int i = 0; i < SCAN_REG; ++i)
       if (s0 + i < s1) place(s0 + i, ev[i]);
-  } else {  // slots past the register segment: read before the pass overwrote them (own range only)
+  } else {
     for (int s = s0; s < s1; ++s) {
       const int j = s / T_, t = s - j * T_;
-      place(s, isrc[(int64_t)t * k + j]);
+      place(s, idx[(int64_t)t * k + j]);
     }
-  }
-  if (stage) {  // coalesced write-out of pos and src
-    __syncthreads();
-    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(pos) & 15) == 0)
-      for (int i = tid; i < n / 4; i += nt) reinterpret_cast<int4*>(pos)[i] = reinterpret_cast<const int4*>(sl)[i];
-    else
-      for (int i = tid; i < n; i += nt) pos[i] = sl[i];
-    for (int i = tid; i < E * C; i += nt) src[i] = ss[i];
   }
 }
 
 __global__ void __launch_bounds__(RS_THREADS) route_scan_kernel(const int32_t* idx, int32_t* pos,
                                                                 int32_t* counts, int32_t* src,
-                                                                int T_, int E, int k, int C, int staged) {
+                                                                int T_, int E, int k, int C) {
   FM_PDL_ENTRY();
-  extern __shared__ int hist[];  // [E][RS_THREADS + RS_THREADS/32] (+ staging [T·k + E·C])
-  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist,
-                  staged ? hist + E * (RS_THREADS + RS_THREADS / 32) : nullptr);
+  extern __shared__ int hist[];  // [E][RS_THREADS + RS_THREADS/32]
+  __shared__ int warp_tot[32];
+  route_scan_body(idx, pos, counts, src, T_, E, k, C, hist, warp_tot);
 }
 
 int route_scan(const int32_t* idx, int32_t* pos, int32_t* counts, int32_t* src, int T_, int E,
                int k, int C, cudaStream_t s) {
   constexpr int RS_ROW = RS_THREADS + RS_THREADS / 32;
-  constexpr int kMaxSmem = 200 * 1024;
   size_t smem = (size_t)E * RS_ROW * sizeof(int);
-  const size_t stage = ((size_t)T_ * k + (size_t)E * C) * sizeof(int);
-  const int staged = smem + stage <= (size_t)kMaxSmem;
-  if (staged) smem += stage;
-  static bool once = (cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
-                      true);
+  static bool once = (cudaFuncSetAttribute(route_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           64 * RS_ROW * (int)sizeof(int)), true);
   (void)once;
-  launch_k(route_scan_kernel, 1, RS_THREADS, smem, s, idx, pos, counts, src, T_, E, k, C, staged);
+  launch_k(route_scan_kernel, 1, RS_THREADS, smem, s, idx, pos, counts, src, T_, E, k, C);
   return (int)cudaGetLastError();
 }
 
