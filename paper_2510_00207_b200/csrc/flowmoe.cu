@@ -801,7 +801,7 @@ namespace {
 int ar_max_ctas() {
   const char* e = getenv("FLOWMOE_AR_MAX_CTAS");
   const int v = e ? atoi(e) : 0;
-  return v > 0 ? v : 16;
+  return v > 0 ? v : 32;
 }
 
 // `g` non-null: a member of the in-process simulated world (no NCCL; peers wired later)

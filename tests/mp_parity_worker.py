@@ -115,7 +115,7 @@ def main():
         res = check_schedule(g["log"], L, cfg.R, P)
         v = violations(res)
         results[f"sched_{a2a}"] = {"violations": {k: len(x) for k, x in v.items()},
-                                   "examples": {k: [list(map(str, e)) for e in x[:3]] for k, x in v.items()},
+                                   "examples": {k: [list(map(str, e)) for e in x[:6]] for k, x in v.items()},
                                    "checked": res["checked"], "priority": res["priority_stats"]}
     out = [None] * P
     dist.all_gather_object(out, results)
