@@ -1291,9 +1291,12 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     FM_KP(KK_PACK, 1, 0, 2.0 * E * C * M * es, sc,
           permute_pack(dt, a, src, at<char>(saved, L.send + r * C * M * es), (int)E, (int)C, (int)ldE, (int)M,
                        (int)k, sc));
+    // the task's end marker before the event D_r waits on: a marker recorded after the
+    // release can be stamped later than the waiting stream's start (front-end skew)
+    if (x->at_split) task_end(x, tk_at, TK_AT, ai, sc);
     FM_CUDA(cudaEventRecord(x->ev_at[r], sc));
    }
-    task_end(x, tk_at, TK_AT, x->at_split ? ai : -1, sc);
+    if (!x->at_split) task_end(x, tk_at, TK_AT, -1, sc);
   }
   // ---- D_1..D_R (Eq.(4)) on the high-priority A2A stream
   if (P > 1)

@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = p.g;
-  const uint32_t tmem_cols = single ? BN : 2 * BN;
+  // TMEM allocations are powers of two >= 32 columns (BN = 192: 256 / 512)
+  const uint32_t tmem_cols = single ? (BN <= 64 ? 64u : BN <= 128 ? 128u : 256u) : (BN <= 64 ? 128u : BN <= 128 ? 256u : 512u);
   if (threadIdx.x == 0) FM_MARK(0);
 
   if (warp == 0 && lane == 0) {
@@ -529,24 +530,38 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   // and more CTAs.
   if (g_force_cg == 2) return g_force_bn == 128 ? launch_tc<128, 8, 1, 2>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
   if (g_force_bn == 256) return launch_tc<256, 4>(g, s);
+  if (g_force_bn == 192) return launch_tc<192, 4>(g, s);
   if (g_force_bn == 128) return launch_tc<128, 6>(g, s);
   if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
   const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
-  if (g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 4 * TC_BK)) {
-    // CTA pairs (256 x 256 tiles) once they fill at least one wave of the 74 TPC pairs:
-    // tools/gemm_microbench.py at the dsv2s shapes, 1-CTA 256-wide -> pairs: QKV 1006 ->
-    // 1175, E2 940 -> 1086, dX_e 918 -> 1068, dX 895 -> 993, dWqkv 1075 -> 1137 TFLOP/s;
-    // 256-column pair tiles beat 128-column ones everywhere (fewer, longer mainloops)
-    const int64_t t256 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch * ((g.N + 255) / 256);
-    if (t256 >= 74) return launch_tc<256, 6, 1, 2>(g, s);
-  }
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
   // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) take a 3-stage ring
   // and double-buffered epilogue staging (tools/probe/gemm_probe.cu: -2..-6%); the
   // 4-stage ring stays everywhere else (3 stages cost 3-8% on longer K)
   if (g.N >= 256 && f32out && g.K <= 4 * TC_BK && tiles(256) >= 4 * 148) return launch_tc<256, 3, 2>(g, s);
-  if (g.N >= 256 && tiles(256) >= 48) return launch_tc<256, 4>(g, s);
+  if (g.N >= 256 && tiles(256) >= 48) {
+    // Wave-quantised cost of the candidate tilings: waves x BN / eff, eff measured per SM at
+    // the dsv2s / c3 / c4 shapes (tools/gemm_microbench.py, r02): CTA pairs on 256 x 256
+    // tiles (cta_group::2, half the B operand per SM: the L2-bound mainloop) 1.0, one CTA
+    // 128 x 256 0.89, one CTA 128 x 192 0.78.  192 columns only as a single wave: they fill
+    // the SMs where 256 leave most of a wave idle (the T_r-row MHA projections: 80 -> 108 of
+    // 148 SMs, 32 -> 28 us); with every SM busy the extra operand bytes per FLOP lose to the
+    // pairs (dsv2s E1 73 vs 68 us), and so they do on long K (> 8192).  Short-K fp32 wgrads
+    // (K <= 512) stay on single CTAs: epilogue-bound, the pair gains nothing (dW1 171 vs 156).
+    auto cost = [](int64_t t, int slots, double w) { return (double)((t + slots - 1) / slots) * w; };
+    int pick = 1;
+    double best = cost(tiles(256), 148, 256 / 0.89);
+    if (g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 8 * TC_BK)) {
+      const int64_t t256 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch * ((g.N + 255) / 256);
+      const double c = cost(t256, 74, 256);
+      if (c <= best) { best = c; pick = 2; }
+    }
+    if (g.K <= 8192 && tiles(192) <= 148 && cost(tiles(192), 148, 192 / 0.78) < best) pick = 3;
+    if (pick == 2) return launch_tc<256, 6, 1, 2>(g, s);
+    if (pick == 3) return launch_tc<192, 4>(g, s);
+    return launch_tc<256, 4>(g, s);
+  }
   if (g.N >= 128 && tiles(128) >= 48) return launch_tc<128, 6>(g, s);
   return launch_tc<64, 8>(g, s);
 }

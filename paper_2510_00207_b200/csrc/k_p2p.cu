@@ -68,6 +68,22 @@ FM_DEV int64_t expert_off(int el, int r, int q, int R, int P, int64_t blk) {
   return (((int64_t)el * R + r) * P + q) * blk;
 }
 
+// one CTA's piece [v0, v1) of 16-byte words: 8 loads in flight per thread before the (remote)
+// stores — a plain load->store loop keeps one load per thread outstanding and is bound by
+// HBM latency, not by NVLink
+FM_DEV void copy_piece(uint4* __restrict__ d, const uint4* __restrict__ s, int64_t v0, int64_t v1) {
+  const int bd = blockDim.x;
+  int64_t i = v0 + threadIdx.x;
+  for (; i + 7 * bd < v1; i += 8 * bd) {
+    uint4 t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = __ldg(s + i + j * bd);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[i + j * bd] = t[j];
+  }
+  for (; i < v1; i += bd) d[i] = __ldg(s + i);
+}
+
 // grid (pieces, El, P): x = piece of the block, y = local expert, z = destination rank
 __global__ void __launch_bounds__(256) a2a_p2p_send_kernel(P2PArgs a) {
   FM_PDL_ENTRY();
@@ -84,7 +100,7 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_kernel(P2PArgs a) {
   const int64_t v0 = piece * per, v1 = min(a.blk_bytes / 16, v0 + per);
   const uint4* s = reinterpret_cast<const uint4*>(a.src + soff);
   uint4* d = reinterpret_cast<uint4*>(a.dst[q] + doff);
-  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) d[i] = __ldg(s + i);
+  copy_piece(d, s, v0, v1);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -121,7 +137,7 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_wait_kernel(P2PArgs a) {
   const int64_t v0 = piece * per, v1 = min(a.blk_bytes / 16, v0 + per);
   const uint4* s = reinterpret_cast<const uint4*>(a.src + soff);
   uint4* d = reinterpret_cast<uint4*>(a.dst[q] + doff);
-  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) d[i] = __ldg(s + i);
+  copy_piece(d, s, v0, v1);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -247,7 +247,7 @@ def knob_ctx(cg=0, bn=0):
     return _KNOB_CTX[(cg, bn)]
 
 
-GEMM_CG = [(0, 0), (2, 256), (2, 128)]  # automatic; CTA pairs (cta_group::2) with 256 / 128 columns
+GEMM_CG = [(0, 0), (0, 192), (2, 256), (2, 128)]  # automatic; 192-column tiles; CTA pairs (cta_group::2) with 256 / 128 columns
 
 
 @pytest.mark.parametrize("cg,bn", GEMM_CG)

@@ -99,5 +99,5 @@ if __name__ == "__main__":
             continue
         reps = 200 if name.startswith("c2") else (50 if name.startswith("c3") else 10)
         run(name, reps, 0, 1, 0)  # the library's automatic choice
-        for cg, bn in ((1, 128), (1, 256), (2, 128), (2, 256)):
+        for cg, bn in ((1, 128), (1, 192), (1, 256), (2, 128), (2, 256)):
             run(name, reps, bn, 1, cg)
