@@ -228,6 +228,9 @@ def run_reference(args, cfg, L, rank, world):
 
 def main():
     args = parse()
+    import faulthandler
+    import signal
+    faulthandler.register(signal.SIGTERM, all_threads=True, chain=True)  # a killed run says where it was
     from synth import PRESETS
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -466,7 +469,7 @@ def main():
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            tl = trace_replays(run, args.trace_iters, os.path.join(args.trace_dir, f"flowmoe_trace_r{rank}.json"),
+            tl = trace_replays(run, args.trace_iters, os.path.join(args.trace_dir, f"flowmoe_trace_{args.config}_n{world}_r{rank}.json"),
                                trim=max(0, min(3, (args.trace_iters - 2) // 4)),
                                sync=(dist.barrier if world > 1 else None),
                                a2a_bytes=a2a_bytes)

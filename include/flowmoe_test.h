@@ -28,7 +28,10 @@ flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* log
  * launch on (1, default) / off (0), key 5 = force the GEMM tile width (64/128/256;
  * 0 = automatic), key 6 = peer-memory A2A of chunk r on chunk r's compute lane (1,
  * default) / on the A2A stream (0), key 7 = GEMM CTA grouping (0 automatic, 1 one CTA
- * per 128-row tile, 2 CTA pairs on 256-row tiles with cta_group::2 UMMAs).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
+ * per 128-row tile, 2 CTA pairs on 256-row tiles with cta_group::2 UMMAs), key 8 = GEMM
+ * stream-K (0 automatic, 1 never, 2 wherever the GEMM has enough k-blocks: every SM / pair
+ * gets the same share of the flattened (tile, k-block) space, cut tiles are summed in a
+ * fixed order).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
 flowmoe_status flowmoe_debug_set(flowmoe_ctx* ctx, int key, int value);
 
 /* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,

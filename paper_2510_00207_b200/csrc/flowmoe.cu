@@ -139,6 +139,11 @@ struct flowmoe_ctx {
   // compute lanes: lanes[0] == s_comp; chunk r's compute tasks run on lanes[r % n_lanes]
   std::vector<cudaStream_t> lanes;
   std::vector<cudaEvent_t> ev_lane;
+  // stream-K GEMM scratch (k_gemm_tc.cu), one set per lane: lanes run GEMMs concurrently
+  std::vector<float*> sk_ws;
+  std::vector<unsigned int*> sk_tick;
+  float* sk_test_ws = nullptr;  // flowmoe_test_gemm's (allocated on first use)
+  unsigned int* sk_test_tick = nullptr;
   // per-block weight-grad stream (expert wgrads over all chunks, deferred MHA/gate
   // wgrads); == s_comp with one lane, its own stream with several
   cudaStream_t s_wg = nullptr;
@@ -194,7 +199,7 @@ struct flowmoe_ctx {
   std::vector<PendingAR> pending_ar;  // centralized-AR policies: flushed at allreduce_wait
   // per-ctx test/benchmark knobs (flowmoe_test.h) and per-kernel profile, applied to the
   // kernel modules by apply_ctx() at the start of every enqueueing call
-  int dbg_flags = 0, pdl = 1, force_bn = 0, force_cg = 0, p2p_on_lane = 1;
+  int dbg_flags = 0, pdl = 1, force_bn = 0, force_cg = 0, force_sk = 0, p2p_on_lane = 1;
   Prof prof;
   TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
@@ -260,6 +265,7 @@ void apply_ctx(flowmoe_ctx* x) {
   gemm_tc_set_debug(x->dbg_flags);
   gemm_tc_force_bn(x->force_bn);
   gemm_tc_force_cg(x->force_cg);
+  gemm_tc_force_streamk(x->force_sk);
   g_pdl_enabled = x->pdl;
   g_p2p_on_lane = x->p2p_on_lane;
   g_prof = &x->prof;
@@ -304,8 +310,19 @@ flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStre
   FM_KP(kind, 1, flops, bytes, s, gemm(g, dt, s));
   return FLOWMOE_OK;
 }
+// stream-K scratch: two fp32 partial tiles (128 x 256) per CTA of a full grid, and counters
+constexpr size_t SK_WS_FLOATS = (size_t)148 * 2 * 128 * 256;
+constexpr size_t SK_TICKS = 1 << 16;
+void set_streamk(const flowmoe_ctx* x, GemmArgs& g, cudaStream_t s) {
+  for (size_t i = 0; i < x->sk_ws.size() && i < x->lanes.size(); ++i)
+    if (x->lanes[i] == s) {
+      g.splitk_ws = x->sk_ws[i]; g.splitk_ws_floats = SK_WS_FLOATS;
+      g.splitk_tick = x->sk_tick[i]; g.splitk_ticks = SK_TICKS;
+    }
+}
 #define FM_GEMM(kind, g)                                                   \
   do {                                                                     \
+    set_streamk(x, g, sc);                                                 \
     if (flowmoe_status st_ = run_gemm(kind, g, dt, es, sc)) return st_;   \
   } while (0)
 
@@ -706,6 +723,7 @@ flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
   else if (key == 5) x->force_bn = value;
   else if (key == 6) x->p2p_on_lane = value ? 1 : 0;
   else if (key == 7) x->force_cg = value;
+  else if (key == 8) x->force_sk = value;
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   return FLOWMOE_OK;
 }
@@ -916,6 +934,15 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
   if (ok && x->P > 1) ok = alloc(&x->dxc, R * ECM * es);
   if (!ok) return cleanup_fail(fail(FLOWMOE_ERR_OOM, "workspace allocation failed"));
   if (x->P == 1) x->dxc = x->dxe;
+  for (size_t i = 0; i < x->lanes.size() && ok && x->dt == DT_BF16; ++i) {
+    float* w = nullptr;
+    unsigned int* t = nullptr;
+    ok = alloc((void**)&w, SK_WS_FLOATS * 4) && alloc((void**)&t, SK_TICKS * 4) &&
+         cudaMemset(t, 0, SK_TICKS * 4) == cudaSuccess;
+    x->sk_ws.push_back(w);
+    x->sk_tick.push_back(t);
+  }
+  if (!ok) return cleanup_fail(fail(FLOWMOE_ERR_OOM, "workspace allocation failed"));
   if (x->dt == DT_BF16 && gemm_tc_init() != 0)
     return cleanup_fail(fail(FLOWMOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable"));
   if (x->P > 1 && !g) {
@@ -1897,6 +1924,8 @@ void flowmoe_destroy(flowmoe_ctx* x) {
   if (x->tlog.base) cudaEventDestroy(x->tlog.base);
   if (g_prof == &x->prof) g_prof = nullptr;
   for (void* p : x->allocs) cudaFree(p);
+  if (x->sk_test_ws) cudaFree(x->sk_test_ws);
+  if (x->sk_test_tick) cudaFree(x->sk_test_tick);
   if (x->s_comp) cudaStreamDestroy(x->s_comp);
   if (x->s_a2a) cudaStreamDestroy(x->s_a2a);
   if (x->s_ar) cudaStreamDestroy(x->s_ar);
@@ -1922,10 +1951,21 @@ extern "C" flowmoe_status flowmoe_test_gemm(flowmoe_ctx* x, int dtype, int M, in
   if (dtype != DT_F32 && dtype != DT_BF16) return fail(FLOWMOE_ERR_INVALID, "dtype");
   if (x) {
     apply_ctx(x);
+    if (dtype == DT_BF16) {
+      if (!x->sk_test_ws) {
+        if (cudaMalloc((void**)&x->sk_test_ws, SK_WS_FLOATS * 4) != cudaSuccess ||
+            cudaMalloc((void**)&x->sk_test_tick, SK_TICKS * 4) != cudaSuccess ||
+            cudaMemset(x->sk_test_tick, 0, SK_TICKS * 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+          return fail(FLOWMOE_ERR_OOM, "stream-K scratch");
+      }
+      g.splitk_ws = x->sk_test_ws; g.splitk_ws_floats = SK_WS_FLOATS;
+      g.splitk_tick = x->sk_test_tick; g.splitk_ticks = SK_TICKS;
+    }
   } else {  // library defaults, no profile
     gemm_tc_set_debug(0);
     gemm_tc_force_bn(0);
     gemm_tc_force_cg(0);
+    gemm_tc_force_streamk(0);
     g_pdl_enabled = 1;
     g_prof = nullptr;
   }

@@ -39,6 +39,8 @@ static int g_force_bn = 0;  // 0 = wave-aware choice; 64/128/256 = forced tile w
 static int g_force_cg = 0;  // 0 = automatic; 1 = one CTA per tile; 2 = CTA pair (cta_group::2)
 void gemm_tc_force_bn(int bn) { g_force_bn = bn; }
 void gemm_tc_force_cg(int cg) { g_force_cg = cg; }
+static int g_force_sk = 0;  // stream-K: 0 = automatic, 1 = never, 2 = wherever the scratch allows
+void gemm_tc_force_streamk(int mode) { g_force_sk = mode; }
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
 int attn_tc_debug_off() { return g_tc_debug & 4; }  // bit2: force the SIMT attention kernels
 
@@ -47,6 +49,7 @@ struct TcArgs {
   GemmArgs g;
   uint32_t idesc;
   int a_mmajor, b_kmajor, nk, dbg;
+  int streamk;  // 1: stream-K work split (g.splitk_ws / g.splitk_tick hold the fix-up state)
 };
 
 // Persistent: grid = min(#tiles, #SMs) units; unit i walks tiles i, i + #units, ... (n
@@ -58,13 +61,19 @@ struct TcArgs {
 // A and half (BN/2) of the B columns and gets its 128 accumulator rows in its own TMEM, so
 // the operand bytes per SM and K-step drop from (128 + BN)·BK·2 to (128 + BN/2)·BK·2 —
 // the L2->SMEM traffic that bounded the 1-CTA kernel at ~70% of the tensor peak.
-template <int BN, int STAGES, int EB, int CG>
+template <int BN, int STAGES, int EB, int CG, bool SK>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ CUtensorMap tma_c,
                    const __grid_constant__ CUtensorMap tma_aux, const TcArgs p) {
   constexpr int BNL = BN / CG;                      // B columns this CTA loads
+  // pair tiles wider than one UMMA (BN = 512, CG = 2): NSUB UMMAs of N = UN per K-step share
+  // the A operand; the CTA loads SUBL columns of each UMMA's B; the accumulator then fills
+  // TMEM (one buffer: the next tile's MMAs wait for the epilogue to drain it)
+  constexpr int NSUB = (CG == 2 && BN > 256) ? BN / 256 : 1;
+  constexpr int UN = BN / NSUB, SUBL = UN / CG;
+  constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   constexpr uint32_t B_BYTES = BNL * TC_BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -76,9 +85,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int unit = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
   const int ntn = (p.g.N + BN - 1) / BN, ntm = (p.g.M + TC_BM * CG - 1) / (TC_BM * CG);
   const int num_tiles = ntn * ntm * p.g.batch;
+  // Work split.  Whole tiles: unit u takes tiles u, u + #units, ...  Stream-K (SK): the
+  // tiles of the full waves stay whole (data-parallel), and the k-blocks of the remaining
+  // tiles (fewer than #units), flattened in (tile, k-block) order, are cut into #units
+  // equal ranges, one per unit after its whole tiles: every SM (pair) gets the same work
+  // however the tiles quantise.  A "segment" is one unit's k-block range [kb0, kb1) of one
+  // tile; the segments of a cut tile are summed by the epilogue's fix-up.
+  constexpr bool sk = SK;  // compiled out of the whole-tile instantiations (register budget)
+  const int dp_tiles = sk ? num_tiles / nunits * nunits : num_tiles;
+  const int64_t sk_base = (int64_t)dp_tiles * p.nk, sk_total = (int64_t)num_tiles * p.nk - sk_base;
+  const int64_t sk_b = sk_base + (int64_t)unit * sk_total / nunits;
+  const int64_t sk_e = sk_base + (int64_t)(unit + 1) * sk_total / nunits;
+  const int64_t it_begin = unit < dp_tiles ? (int64_t)unit * p.nk : sk_b;
+  auto seg_more = [&](int64_t w) { return w < sk_base || w < sk_e; };
+  auto seg_of = [&](int64_t w, int& tile, int& kb0, int& kb1) {
+    tile = (int)(w / p.nk);
+    kb0 = (int)(w - (int64_t)tile * p.nk);
+    kb1 = (!sk || w < sk_base) ? p.nk : (int)min((int64_t)p.nk, (int64_t)kb0 + (sk_e - w));
+  };
+  auto seg_next = [&](int64_t w, int tile, int kb0, int kb1) -> int64_t {
+    if (w < sk_base) return tile + nunits < dp_tiles ? (int64_t)(tile + nunits) * p.nk : sk_b;
+    return w + (kb1 - kb0);
+  };
   // one tile per unit: the operand ring is free when the epilogue runs, so it doubles
   // as the staging area and a single TMEM accumulator suffices (smaller footprint)
-  const bool single = num_tiles <= nunits;
+  const bool single = !sk && num_tiles <= nunits;
   uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x EB x 4 KB staging
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : EB * 32768));
   uint64_t* empty = full + STAGES;
@@ -89,7 +120,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = p.g;
   // TMEM allocations are powers of two >= 32 columns (BN = 192: 256 / 512)
-  const uint32_t tmem_cols = single ? (BN <= 64 ? 64u : BN <= 128 ? 128u : 256u) : (BN <= 64 ? 128u : BN <= 128 ? 256u : 512u);
+  const uint32_t tmem_cols = single ? (BN <= 64 ? 64u : BN <= 128 ? 128u : BN <= 256 ? 256u : 512u)
+                                    : (NACC * BN <= 128 ? 128u : NACC * BN <= 256 ? 256u : 512u);
   if (threadIdx.x == 0) FM_MARK(0);
 
   if (warp == 0 && lane == 0) {
@@ -115,10 +147,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ===== TMA producer (whole warp walks the ring, one elected lane issues) =====
     int gk = 0;
-    for (int tile = unit; tile < num_tiles; tile += nunits) {
-      const int n0 = (tile % ntn) * BN + (int)crank * BNL;  // this CTA's B columns
+    for (int64_t w = it_begin; seg_more(w);) {
+      int tile, kb0, kb1;
+      seg_of(w, tile, kb0, kb1);
+      w = seg_next(w, tile, kb0, kb1);
+      const int n0 = (tile % ntn) * BN + (int)crank * SUBL;  // this CTA's B columns (+ s·UN per UMMA)
       const int m0 = ((tile / ntn) % ntm) * TC_BM * CG + (int)crank * TC_BM, b = tile / (ntn * ntm);
-      for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+      for (int kb = kb0; kb < kb1; ++kb, ++gk) {
         const int s = gk % STAGES;
         if (gk >= STAGES) {
           if constexpr (CG == 2) mbar_wait_cl(&empty[s], ((gk / STAGES) + 1) & 1);
@@ -152,11 +187,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
               for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d_cg2(sa + i * 8192, &tma_a, bar, m0 + 64 * i, k0, b);
             }
-            if (p.b_kmajor) {
-              tma_load_3d_cg2(sb, &tma_b, bar, k0, n0, b);
-            } else {
 #pragma unroll
-              for (int i = 0; i < BNL / 64; ++i) tma_load_3d_cg2(sb + i * 8192, &tma_b, bar, n0 + 64 * i, k0, b);
+            for (int u = 0; u < NSUB; ++u) {
+              uint8_t* sbu = sb + u * SUBL * TC_BK * 2;
+              if (p.b_kmajor) {
+                tma_load_3d_cg2(sbu, &tma_b, bar, k0, n0 + u * UN, b);
+              } else {
+#pragma unroll
+                for (int i = 0; i < SUBL / 64; ++i)
+                  tma_load_3d_cg2(sbu + i * 8192, &tma_b, bar, n0 + u * UN + 64 * i, k0, b);
+              }
             }
           }
           if (gk < 4) FM_MARK(24 + gk);
@@ -184,15 +224,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint64_t a_kstep = p.a_mmajor ? (2048 >> 4) : (32 >> 4);
     const uint64_t b_kstep = p.b_kmajor ? (32 >> 4) : (2048 >> 4);
     int gk = 0, it = 0;
-    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
-      const int acc = it & 1, use = it >> 1;
+    for (int64_t w = it_begin; seg_more(w); ++it) {
+      int tile, kb0, kb1;
+      seg_of(w, tile, kb0, kb1);
+      w = seg_next(w, tile, kb0, kb1);
+      const int acc = NACC == 2 ? (it & 1) : 0, use = NACC == 2 ? (it >> 1) : it;
       if (use >= 1) {  // the epilogue(s) drained this buffer
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], (use - 1) & 1);
         else mbar_wait(&tempty[acc], (use - 1) & 1);
       }
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = 0; kb < p.nk; ++kb, ++gk) {
+      (void)tile;
+      for (int kb = kb0; kb < kb1; ++kb, ++gk) {
         const int s = gk % STAGES;
         if constexpr (CG == 2) mbar_wait_cl(&full[s], (gk / STAGES) & 1);
         else mbar_wait(&full[s], (gk / STAGES) & 1);
@@ -203,12 +247,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            if constexpr (CG == 2)
-              tc_mma2(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
-                      (kb > 0 || kk > 0) ? 1u : 0u);
-            else
+            if constexpr (CG == 2) {
+#pragma unroll
+              for (int u = 0; u < NSUB; ++u)  // B of UMMA u: SUBL rows (K-major) / columns further on
+                tc_mma2(tmem_d + u * UN, adesc0 + soff + kk * a_kstep,
+                        bdesc0 + soff + kk * b_kstep + (uint64_t)(u * SUBL * TC_BK * 2 >> 4), p.idesc,
+                        (kb > kb0 || kk > 0) ? 1u : 0u);
+            } else
               tc_mma(tmem_d, adesc0 + soff + kk * a_kstep, bdesc0 + soff + kk * b_kstep, p.idesc,
-                     (kb > 0 || kk > 0) ? 1u : 0u);
+                     (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           if constexpr (CG == 2) tc_commit2_both(&empty[s]);
           else tc_commit(&empty[s]);
@@ -247,10 +294,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
     int issued = 0;  // chunks this warp has stored (buffer issued % EB was used EB chunks ago)
     int it = 0;
-    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
+    // stream-K partial of unit v (a unit stores at most one: its first stream-K segment,
+    // when that is not the first segment of its tile); per CTA 128 x BN fp32 in the
+    // epilogue's fragment order [quarter][32-column chunk][float4 j][lane], so a warp's
+    // float4 store or load is 512 contiguous bytes
+    auto part_ptr = [&](int v, int c0) {
+      return reinterpret_cast<float4*>(g.splitk_ws + ((size_t)v * CG + crank) * (size_t)(TC_BM * BN)) +
+             ((quarter * (BN / 32) + c0 / 32) * 8) * 32 + lane;
+    };
+    auto release_acc = [&](int acc) {  // TMEM reads of this accumulator are complete
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_u32(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
+    };
+    for (int64_t w = it_begin; seg_more(w); ++it) {
+      int tile, kb0, kb1;
+      seg_of(w, tile, kb0, kb1);
+      w = seg_next(w, tile, kb0, kb1);
       const int n0 = (tile % ntn) * BN;
       const int m0 = ((tile / ntn) % ntm) * TC_BM * CG + (int)crank * TC_BM, b = tile / (ntn * ntm);
-      const int acc = it & 1, use = it >> 1;
+      const int acc = NACC == 2 ? (it & 1) : 0, use = NACC == 2 ? (it >> 1) : it;
       const uint32_t tmem_acc = tmem_base + acc * BN;
       const int row = m0 + r0 + lane;
       const bool row_ok = row < g.M;
@@ -290,12 +356,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       else mbar_wait_sleep(&tfull[acc], use & 1);
       if (threadIdx.x == 64) FM_MARK(5);
       tc_fence_after();
+      // ---- stream-K fix-up of a cut tile.  Its first segment (the owner: the end of unit
+      // uf's range, so the last work of that unit) keeps its accumulator in TMEM; every later
+      // segment is the first stream-K work of its unit (uf+1 ..), stores its raw fp32
+      // accumulator, frees TMEM at once and counts itself written.  The owner waits for the
+      // count — those segments started before it and wait on nothing, so the wait cannot be
+      // circular — and adds them to its own in segment order (a fixed order: deterministic).
+      int uf = 0, nseg = 1;
+      bool owner = false;
+      if (sk && !(kb0 == 0 && kb1 == p.nk)) {
+        const int64_t xr = (int64_t)tile * p.nk - sk_base;
+        uf = (int)(((xr + 1) * nunits - 1) / sk_total);
+        nseg = (int)(((xr + p.nk) * nunits - 1) / sk_total) - uf + 1;
+        unsigned int* ctr = g.splitk_tick + (size_t)(tile - dp_tiles) * CG + crank;  // partials written
+        if (unit != uf) {
+#pragma unroll 1
+          for (int c0 = half * 32; c0 < BN; c0 += 64) {
+            if (n0 + c0 >= g.N) break;  // warp-uniform
+            uint32_t r[32];
+            tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
+            float4* dst = part_ptr(unit, c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              __stcg(dst + 32 * j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+          }
+          release_acc(acc);
+          __threadfence();  // the partial is visible before it is counted
+          named_bar_sync(2, 256);
+          if (threadIdx.x == 64) atomicAdd(ctr, 1u);
+          continue;
+        }
+        owner = true;
+        if (threadIdx.x == 64) {
+          FM_HANG_DECL;
+          while (true) {
+            unsigned int v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= (unsigned int)(nseg - 1) || FM_HANG(tile, v)) break;
+            __nanosleep(64);
+          }
+          *ctr = 0u;  // every later segment has written: ready for the next launch
+        }
+        named_bar_sync(2, 256);
+        __threadfence();
+      }
 #pragma unroll 1
       for (int c0 = half * 32; c0 < BN; c0 += 64) {
         const int nb = n0 + c0;
         if (nb >= g.N) break;  // warp-uniform
         uint32_t r[32];
         tmem_ld32(tmem_acc + ((uint32_t)r0 << 16) + c0, r);
+        for (int s2 = 1; owner && s2 < nseg; ++s2) {  // + the later segments, in order
+          const float4* src = part_ptr(uf + s2, c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 q = __ldcg(src + 32 * j);
+            r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + q.x);
+            r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + q.y);
+            r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + q.z);
+            r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + q.w);
+          }
+        }
         if (threadIdx.x == 64 && c0 == 0) FM_MARK(9);
         float xv[32], bv[32];
         unpack(pf, xv);
@@ -392,12 +514,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         ++issued;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {  // TMEM reads of this tile are complete (the leader's MMA waits for both CTAs)
-        if constexpr (CG == 2) mbar_arrive_cluster(mapa_u32(smem_u32(&tempty[acc]), 0));
-        else mbar_arrive(&tempty[acc]);
-      }
+      release_acc(acc);  // TMEM reads of this tile are complete
     }
     if (threadIdx.x == 64) FM_MARK(6);
     if (lane == 0) bulk_wait<0>();
@@ -467,15 +584,17 @@ int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-template <int BN, int STAGES, int EB = 1, int CG = 1>
+template <int BN, int STAGES, int EB = 1, int CG = 1, bool SK = false>
 static int launch_tc(const GemmArgs& g, cudaStream_t s) {
+  constexpr int streamk = SK ? 1 : 0;
   constexpr int BNL = BN / CG;
   CUtensorMap ma, mb;
   int rc;
   if (!g.a_mmajor) rc = make_map(&ma, g.A, g.K, g.M, g.batch, g.lda, g.sA, TC_BM);
   else rc = make_map(&ma, g.A, g.M, g.K, g.batch, g.lda, g.sA, TC_BK);
   if (rc) return rc;
-  if (g.b_kmajor) rc = make_map(&mb, g.B, g.K, g.N, g.batch, g.ldb, g.sB, BNL);
+  constexpr int NSUB = (CG == 2 && BN > 256) ? BN / 256 : 1;
+  if (g.b_kmajor) rc = make_map(&mb, g.B, g.K, g.N, g.batch, g.ldb, g.sB, BNL / NSUB);
   else rc = make_map(&mb, g.B, g.N, g.K, g.batch, g.ldb, g.sB, TC_BK);
   if (rc) return rc;
   // output tiles: [32 rows][32 cols] boxes, fp32 (reduce-add, SW128) or bf16 (store, SW64)
@@ -495,12 +614,13 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   p.b_kmajor = g.b_kmajor;
   p.nk = (g.K + TC_BK - 1) / TC_BK;
   p.dbg = g_tc_debug;
+  p.streamk = streamk;
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.a_mmajor ? 1 : 0) << 15) |
-            ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
+            ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)((BN / NSUB) >> 3) << 17) |
             ((uint32_t)((TC_BM * CG) >> 4) << 24);
   const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BNL * TC_BK * 2) + EB * 32768 + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES, EB, CG>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EB, CG, SK>;
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max), true);
   (void)attr_set;
   static int num_sms = 0;
@@ -512,8 +632,8 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   }
   const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM * CG - 1) / (TC_BM * CG)) * g.batch;
   const int units = num_sms / CG;
-  const int nu = (int)(tiles < units ? tiles : units);
-  const size_t smem = tiles <= nu ? smem_max - EB * 32768 : smem_max;
+  const int nu = streamk ? units : (int)(tiles < units ? tiles : units);
+  const size_t smem = (tiles <= nu && !streamk) ? smem_max - EB * 32768 : smem_max;
   if constexpr (CG == 2)
     launch_kc(kern, dim3(2 * nu), TC_THREADS, smem, s, dim3(2, 1, 1), ma, mb, mc, maux, p);
   else
@@ -528,8 +648,21 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   // Tile width (measured, tools/gemm_microbench.py): BN=256 (best MMA/operand efficiency)
   // whenever it still yields >= 48 tiles; small, latency-bound GEMMs get narrower tiles
   // and more CTAs.
-  if (g_force_cg == 2) return g_force_bn == 128 ? launch_tc<128, 8, 1, 2>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
-  if (g_force_bn == 256) return launch_tc<256, 4>(g, s);
+  // stream-K needs the caller's scratch (one partial tile per CTA, one counter per cut tile
+  // and CTA), a partial wave to balance, and at least 2 k-blocks of it per unit (no unit
+  // may be left without stream-K work: the fix-up counts on one segment per unit)
+  auto sk_ok = [&](int bn, int cg) {
+    const int64_t units = 148 / cg, nk = (g.K + TC_BK - 1) / TC_BK;
+    const int64_t t = (int64_t)((g.M + TC_BM * cg - 1) / (TC_BM * cg)) * g.batch * ((g.N + bn - 1) / bn);
+    return g_force_sk != 1 && g.splitk_ws && g.splitk_ws_floats >= (size_t)units * cg * TC_BM * bn &&
+           g.splitk_ticks >= (size_t)(units * cg) && (t % units) * nk >= 2 * units;
+  };
+  if (g_force_cg == 2) {
+    if (g_force_bn == 128) return launch_tc<128, 8, 1, 2>(g, s);
+    if (g_force_bn == 512) return launch_tc<512, 4, 1, 2>(g, s);
+    return g_force_sk == 2 && sk_ok(256, 2) ? launch_tc<256, 6, 1, 2, true>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
+  }
+  if (g_force_bn == 256) return g_force_sk == 2 && sk_ok(256, 1) ? launch_tc<256, 4, 1, 1, true>(g, s) : launch_tc<256, 4>(g, s);
   if (g_force_bn == 192) return launch_tc<192, 4>(g, s);
   if (g_force_bn == 128) return launch_tc<128, 6>(g, s);
   if (g_force_bn == 64) return launch_tc<64, 8>(g, s);
@@ -550,14 +683,30 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // pairs (dsv2s E1 73 vs 68 us), and so they do on long K (> 8192).  Short-K fp32 wgrads
     // (K <= 512) stay on single CTAs: epilogue-bound, the pair gains nothing (dW1 171 vs 156).
     auto cost = [](int64_t t, int slots, double w) { return (double)((t + slots - 1) / slots) * w; };
+    const int64_t nk = (g.K + TC_BK - 1) / TC_BK;
     int pick = 1;
     double best = cost(tiles(256), 148, 256 / 0.89);
-    if (g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 8 * TC_BK)) {
-      const int64_t t256 = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch * ((g.N + 255) / 256);
+    const bool pairs_ok = g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 8 * TC_BK);
+    const int64_t mp = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch;  // pair rows
+    const int64_t t256 = mp * ((g.N + 255) / 256), t512 = mp * ((g.N + 511) / 512);
+    if (pairs_ok) {
       const double c = cost(t256, 74, 256);
       if (c <= best) { best = c; pick = 2; }
     }
     if (g.K <= 8192 && tiles(192) <= 148 && cost(tiles(192), 148, 192 / 0.78) < best) pick = 3;
+    // 512-column pair tiles: two UMMAs per K-step share the A tile, 25% fewer L2->SMEM bytes
+    // per FLOP — the bound once every SM is busy — where they need at most half the waves
+    // of the 256-column pairs; not under the GELU epilogues (the single TMEM accumulator
+    // leaves the activation unhidden).  dsv2s QKV 66.6 -> 64.4 us, expert dGELU 71.1 -> 66.4.
+    if (pick == 2 && nk >= 32 && g.epi != EPI_BIAS_GELU && g.epi != EPI_BIAS_GELU_G &&
+        2 * ((t512 + 73) / 74) <= (t256 + 73) / 74)
+      pick = 5;
+    // Stream-K on the 256-column pairs where the pairs are under one wave or K is long:
+    // dsv2s dX (40 pair tiles, K = 15360) 79.4 -> 65.0 us, o-proj / dctx (K = 5120) 30.4 ->
+    // 29.4 us.  Short K loses to the fix-up (E2, K = 1536: 58.6 -> 67.2 us).
+    if (pairs_ok && sk_ok(256, 2) && (g_force_sk == 2 || (nk >= 64 && (t256 < 74 || nk >= 128)))) pick = 4;
+    if (pick == 4) return launch_tc<256, 6, 1, 2, true>(g, s);
+    if (pick == 5) return launch_tc<512, 4, 1, 2>(g, s);
     if (pick == 2) return launch_tc<256, 6, 1, 2>(g, s);
     if (pick == 3) return launch_tc<192, 4>(g, s);
     return launch_tc<256, 4>(g, s);

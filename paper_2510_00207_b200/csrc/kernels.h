@@ -39,6 +39,13 @@ struct GemmArgs {
   void* aux = nullptr; int64_t ldaux = 0, sAux = 0;
   int epi = EPI_STORE;
   float alpha = 1.0f;
+  // optional stream-K scratch (k_gemm_tc.cu): per unit two fp32 partial tiles, and per
+  // (tile, CTA of the pair) an [arrivals, written] counter pair (zeroed once; every use
+  // leaves them zero).  Without it the GEMM never splits a tile.
+  float* splitk_ws = nullptr;
+  size_t splitk_ws_floats = 0;
+  unsigned int* splitk_tick = nullptr;
+  size_t splitk_ticks = 0;
 };
 
 // Dispatches to the tcgen05 kernel for bf16 and the fp32 SIMT kernel (K10) for f32.
@@ -48,7 +55,8 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s);  // bf16 only, tcgen05/TMEM/TMA
 int gemm_tc_init();                               // resolves cuTensorMapEncodeTiled
 void gemm_tc_set_debug(int flags);
 void gemm_tc_force_bn(int bn);
-void gemm_tc_force_cg(int cg);  // 0 automatic, 1 single-CTA tiles, 2 CTA pairs (cta_group::2)
+void gemm_tc_force_cg(int cg);
+void gemm_tc_force_streamk(int mode);  // 0 automatic, 1 never, 2 wherever the scratch allows  // 0 automatic, 1 single-CTA tiles, 2 CTA pairs (cta_group::2)
 
 // ---------------------------------------------------------------- attention
 // qkv [nseq·N][3M] (sequences of N rows; head h at columns h*dh of each of Q|K|V),

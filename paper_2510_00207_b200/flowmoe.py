@@ -161,7 +161,8 @@ _ENV_KNOBS = (("FLOWMOE_DEBUG_SIMT", 1, 1),        # debug: route bf16 GEMMs to 
               ("FLOWMOE_NO_PDL", 4, 0),            # A/B: plain stream-ordered launches
               ("FLOWMOE_P2P_A2A_STREAM", 6, 0),    # A/B: peer-memory A2A on the A2A stream
               ("FLOWMOE_FORCE_CG1", 7, 1),         # A/B: single-CTA GEMM tiles only
-              ("FLOWMOE_FORCE_CG2", 7, 2))         # test: CTA-pair (cta_group::2) GEMMs everywhere
+              ("FLOWMOE_FORCE_CG2", 7, 2),         # test: CTA-pair (cta_group::2) GEMMs everywhere
+              ("FLOWMOE_NO_STREAMK", 8, 1))        # A/B: whole-tile GEMM work split only
 
 
 def _apply_env_knobs(handle):

@@ -236,18 +236,19 @@ GEMM_SHAPES = [(200, 320, 136, 2), (128, 96, 64, 1), (296, 200, 520, 3), (64, 51
 _KNOB_CTX = {}
 
 
-def knob_ctx(cg=0, bn=0):
-    """a small ctx carrying GEMM knobs (flowmoe_test.h: per-ctx debug keys 5 and 7)"""
+def knob_ctx(cg=0, bn=0, sk=0):
+    """a small ctx carrying GEMM knobs (flowmoe_test.h: per-ctx debug keys 5, 7 and 8)"""
     import paper_2510_00207_b200 as fm
-    if (cg, bn) not in _KNOB_CTX:
+    if (cg, bn, sk) not in _KNOB_CTX:
         c = fm.FlowMoE(fm.BlockShape(B=256, seq_len=64, M=64, n_heads=1, E=2, top_k=1, d_ffn=64, R=1), 0)
         c.debug_set(7, cg)
         c.debug_set(5, bn)
-        _KNOB_CTX[(cg, bn)] = c
-    return _KNOB_CTX[(cg, bn)]
+        c.debug_set(8, sk)
+        _KNOB_CTX[(cg, bn, sk)] = c
+    return _KNOB_CTX[(cg, bn, sk)]
 
 
-GEMM_CG = [(0, 0), (0, 192), (2, 256), (2, 128)]  # automatic; 192-column tiles; CTA pairs (cta_group::2) with 256 / 128 columns
+GEMM_CG = [(0, 0), (0, 192), (2, 256), (2, 128), (2, 512)]  # automatic; 192-column tiles; CTA pairs (cta_group::2) with 256 / 128 / 512 columns
 
 
 @pytest.mark.parametrize("cg,bn", GEMM_CG)
@@ -286,6 +287,83 @@ def test_gemm_tc_layouts_vs_fp64(a_mmajor, b_kmajor, shape, cg, bn):
     torch.cuda.synchronize()
     assert rel(fm.to_host_f64(C), ref) <= 1e-2
     assert rel(C32.cpu().numpy().astype(np.float64) - 1.0, ref) <= 1e-5
+
+
+# rows, N, K, batch: fewer tiles than units (all stream-K), ragged, batched, and whole waves
+# plus a stream-K remainder (768 x 7936: 93 pair tiles = 74 whole + 19 cut)
+SK_SHAPES = [(512, 2560, 4096, 1), (520, 1000, 3000, 1), (256, 1536, 2048, 2), (768, 7936, 1024, 1)]
+
+
+@pytest.mark.parametrize("cg,bn", [(2, 256), (1, 256)])
+@pytest.mark.parametrize("b_kmajor", [0, 1])
+@pytest.mark.parametrize("shape", SK_SHAPES)
+def test_gemm_streamk_vs_fp64(shape, b_kmajor, cg, bn):
+    """Stream-K GEMM (every pair / CTA the same share of the flattened (tile, k-block) space;
+    tiles cut between units summed by the epilogue's fix-up in segment order): against the
+    fp64 product with the residual epilogue, ragged M / N / K, batched; two calls bit-identical
+    (ordered fix-up; the per-tile counters reset themselves)."""
+    import torch
+    import paper_2510_00207_b200 as fm
+    ctx = knob_ctx(cg, bn, 2)
+    Mr, N, K, batch = shape
+    rng = np.random.default_rng(Mr + N + K + b_kmajor + cg)
+    dev = torch.device("cuda", 0)
+    A = fm.to_device(rng.standard_normal((batch, Mr, K)) / 8, "bf16", dev)
+    Bm = rng.standard_normal((batch, K, N))
+    Bt = fm.to_device(Bm.transpose(0, 2, 1).copy() if b_kmajor else Bm, "bf16", dev)
+    res = fm.to_device(rng.standard_normal((batch, Mr, N)), "bf16", dev)
+    Br = fm.to_host_f64(Bt)
+    ref = fm.to_host_f64(A) @ (Br.transpose(0, 2, 1) if b_kmajor else Br)
+    kw = dict(M=Mr, N=N, K=K, batch=batch, lda=K, sA=Mr * K, ldb=K if b_kmajor else N, sB=K * N,
+              b_kmajor=b_kmajor, ldc=N, sC=Mr * N, ctx=ctx)
+    C = torch.full((batch, Mr, N), 3.0, dtype=torch.bfloat16, device=dev)
+    fm.test_gemm("bf16", A, Bt, C, resid=res, **kw)
+    C2 = torch.full_like(C, -1.0)
+    fm.test_gemm("bf16", A, Bt, C2, resid=res, **kw)
+    C32 = torch.ones((batch, Mr, N), dtype=torch.float32, device=dev)  # fp32 accumulate (wgrads)
+    fm.test_gemm("bf16", A, Bt, C32, epi=3, **kw)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref + fm.to_host_f64(res)) <= 1e-2
+    assert torch.equal(C, C2)
+    assert rel(C32.cpu().numpy().astype(np.float64) - 1.0, ref) <= 1e-5
+
+
+def test_gemm_streamk_epilogues():
+    """The fused epilogues run on the fix-up's sum: bias+GELU (Z saved / GELU' saved),
+    dGELU, aux multiply, fp32 store, on a stream-K pair GEMM with tiles cut between units."""
+    import torch
+    import paper_2510_00207_b200 as fm
+    ctx = knob_ctx(2, 256, 2)
+    Mr, N, K, batch = 256, 1536, 2048, 2
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda", 0)
+    A = fm.to_device(rng.standard_normal((batch, Mr, K)) / 16, "bf16", dev)
+    B = fm.to_device(rng.standard_normal((batch, K, N)) / 4, "bf16", dev)
+    bias = fm.to_device(rng.standard_normal((batch, N)), "bf16", dev)
+    ref = fm.to_host_f64(A) @ fm.to_host_f64(B)
+    kw = dict(M=Mr, N=N, K=K, batch=batch, lda=K, sA=Mr * K, ldb=N, sB=K * N, ldc=N, sC=Mr * N, ctx=ctx)
+    C = torch.empty((batch, Mr, N), dtype=torch.bfloat16, device=dev)
+    Z = torch.empty_like(C)
+    fm.test_gemm("bf16", A, B, C, epi=1, bias=bias, aux=Z, **kw)
+    torch.cuda.synchronize()
+    z = ref + fm.to_host_f64(bias)[:, None, :]
+    assert rel(fm.to_host_f64(Z), z) <= 1e-2
+    assert rel(fm.to_host_f64(C), o.gelu(fm.to_host_f64(Z))) <= 1e-2
+    fm.test_gemm("bf16", A, B, C, epi=2, aux=Z, **kw)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref * o.gelu_grad(fm.to_host_f64(Z))) <= 1e-2
+    D = torch.empty_like(C)
+    fm.test_gemm("bf16", A, B, C, epi=5, bias=bias, aux=D, **kw)
+    torch.cuda.synchronize()
+    zb = fm.to_host_f64(Z)
+    assert rel(fm.to_host_f64(C), o.gelu(zb)) <= 1e-2
+    assert rel(fm.to_host_f64(D), o.gelu_grad(zb)) <= 1e-2
+    fm.test_gemm("bf16", A, B, C, epi=6, aux=D, **kw)
+    F = torch.full((batch, Mr, N), 9.0, dtype=torch.float32, device=dev)
+    fm.test_gemm("bf16", A, B, F, epi=4, **kw)
+    torch.cuda.synchronize()
+    assert rel(fm.to_host_f64(C), ref * fm.to_host_f64(D)) <= 1e-2
+    assert rel(F.cpu().numpy().astype(np.float64), ref) <= 1e-5
 
 
 @pytest.mark.parametrize("cg", [0, 2])

@@ -53,7 +53,7 @@ def knob_ctx():
     return _CTX
 
 
-def run(name, reps, bn, pdl, cg=0):
+def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False):
     Mr, N, K, batch, am, bk, epi = SHAPES[name]
     dev = torch.device("cuda", 0)
     A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
@@ -65,6 +65,7 @@ def run(name, reps, bn, pdl, cg=0):
     ctx.debug_set(5, bn)
     ctx.debug_set(4, pdl)
     ctx.debug_set(7, cg)
+    ctx.debug_set(8, sk)
     kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
               ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi, bias=bias, aux=aux)
     s = torch.cuda.current_stream()
@@ -87,8 +88,46 @@ def run(name, reps, bn, pdl, cg=0):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
     flops = 2.0 * Mr * N * K * batch
-    print(json.dumps({"shape": name, "bn": bn, "cg": cg, "pdl": pdl, "us_per_launch": round(us, 3),
-                      "tflops": round(flops / us / 1e6, 1)}), flush=True)
+    if not quiet:
+        print(json.dumps({"shape": name, "bn": bn, "cg": cg, "sk": sk, "pdl": pdl, "us_per_launch": round(us, 3),
+                          "tflops": round(flops / us / 1e6, 1)}), flush=True)
+    del g
+
+
+def run_cublas(name, reps):
+    """the same contraction through torch (cuBLAS / cuBLASLt, bf16 in, fp32 accumulate; plain
+    store, no fused epilogue) in the same graph-of-launches harness: the library baseline"""
+    Mr, N, K, batch, am, bk, epi = SHAPES[name]
+    dev = torch.device("cuda", 0)
+    A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
+    B = torch.randn(batch, (N if bk else K), (K if bk else N), device=dev).to(torch.bfloat16) * 0.05
+    At = A.transpose(1, 2) if am else A
+    Bt = B.transpose(1, 2) if bk else B
+    C = torch.empty(batch, Mr, N, device=dev, dtype=torch.bfloat16)  # bf16 out even for the fp32 wgrads
+
+    def one():
+        torch.bmm(At, Bt, out=C)
+    s = torch.cuda.current_stream()
+    one()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(s)
+    with torch.cuda.graph(g, stream=cap):
+        for _ in range(reps):
+            one()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+    print(json.dumps({"shape": name, "impl": "cublas (torch.bmm)", "us_per_launch": round(us, 3),
+                      "tflops": round(2.0 * Mr * N * K * batch / us / 1e6, 1)}), flush=True)
     del g
 
 
@@ -98,6 +137,10 @@ if __name__ == "__main__":
         if not name.startswith(pref):
             continue
         reps = 200 if name.startswith("c2") else (50 if name.startswith("c3") else 10)
+        run(name, reps, 0, 1, 0, quiet=True)  # warm-up (clocks, allocator, module load)
         run(name, reps, 0, 1, 0)  # the library's automatic choice
-        for cg, bn in ((1, 128), (1, 192), (1, 256), (2, 128), (2, 256)):
-            run(name, reps, bn, 1, cg)
+        for cg, bn, sk in ((1, 128, 0), (1, 192, 0), (1, 256, 0), (2, 128, 0), (2, 256, 0), (2, 512, 0),
+                           (1, 256, 2), (2, 256, 2)):
+            run(name, reps, bn, 1, cg, sk)
+        if os.environ.get("CUBLAS", "1") == "1":
+            run_cublas(name, reps)
