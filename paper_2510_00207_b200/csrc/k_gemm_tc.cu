@@ -680,7 +680,8 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // 128 x 256 0.89, one CTA 128 x 192 0.78.  192 columns only as a single wave: they fill
     // the SMs where 256 leave most of a wave idle (the T_r-row MHA projections: 80 -> 108 of
     // 148 SMs, 32 -> 28 us); with every SM busy the extra operand bytes per FLOP lose to the
-    // pairs (dsv2s E1 73 vs 68 us), and so they do on long K (> 8192).  Short-K fp32 wgrads
+    // pairs (dsv2s E1 73 vs 68 us), and so they do on long K (> 8192); measured on the
+    // unbatched projections only, so the batched expert GEMMs keep 256.  Short-K fp32 wgrads
     // (K <= 512) stay on single CTAs: epilogue-bound, the pair gains nothing (dW1 171 vs 156).
     auto cost = [](int64_t t, int slots, double w) { return (double)((t + slots - 1) / slots) * w; };
     const int64_t nk = (g.K + TC_BK - 1) / TC_BK;
@@ -693,7 +694,7 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
       const double c = cost(t256, 74, 256);
       if (c <= best) { best = c; pick = 2; }
     }
-    if (g.K <= 8192 && tiles(192) <= 148 && cost(tiles(192), 148, 192 / 0.78) < best) pick = 3;
+    if (g.batch == 1 && g.K <= 8192 && tiles(192) <= 148 && cost(tiles(192), 148, 192 / 0.78) < best) pick = 3;
     // 512-column pair tiles: two UMMAs per K-step share the A tile, 25% fewer L2->SMEM bytes
     // per FLOP — the bound once every SM is busy — where they need at most half the waves
     // of the 256-column pairs; not under the GELU epilogues (the single TMEM accumulator

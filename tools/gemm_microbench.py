@@ -20,6 +20,10 @@ SHAPES = {  # name: (M rows, N, K, batch, a_mmajor, b_kmajor, epi)
     "c2_dwqkv": (256, 768, 1024, 1, 1, 0, 4),
     "c3_e1": (128, 2048, 1024, 16, 0, 0, 0),
     "c3_qkv": (1024, 3072, 1024, 1, 0, 0, 0),
+    "c3_e2": (128, 1024, 2048, 16, 0, 0, 0),
+    "c3_dxe": (128, 1024, 2048, 16, 0, 1, 0),
+    "c3_oproj": (1024, 1024, 1024, 1, 0, 0, 0),
+    "c3_dx": (1024, 1024, 3072, 1, 0, 1, 0),
     "c4_e1": (128, 16384, 4096, 16, 0, 0, 0),
     "c4_qkv": (1024, 12288, 4096, 1, 0, 0, 0),
     "c4_dw1": (4096, 16384, 256, 16, 1, 0, 4),
@@ -94,6 +98,27 @@ def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False):
     del g
 
 
+def run_plain(name, bn, cg, sk, times=2):
+    """`times` plain launches of one forced variant (no graph): what ncu captures"""
+    Mr, N, K, batch, am, bk, epi = SHAPES[name]
+    dev = torch.device("cuda", 0)
+    A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
+    B = torch.randn(batch, (N if bk else K), (K if bk else N), device=dev).to(torch.bfloat16) * 0.05
+    C = torch.zeros(batch, Mr, N, device=dev, dtype=torch.float32 if epi == 4 else torch.bfloat16)
+    bias = torch.randn(batch, N, device=dev).to(torch.bfloat16) if epi == 5 else None
+    aux = torch.randn(batch, Mr, N, device=dev).to(torch.bfloat16) if epi in (5, 6) else None
+    ctx = knob_ctx()
+    ctx.debug_set(5, bn)
+    ctx.debug_set(7, cg)
+    ctx.debug_set(8, sk)
+    kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
+              ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi, bias=bias, aux=aux)
+    for _ in range(times):
+        fm.test_gemm("bf16", A, B, C, stream=torch.cuda.current_stream(), ctx=ctx, **kw)
+    torch.cuda.synchronize()
+    print(json.dumps({"shape": name, "bn": bn, "cg": cg, "sk": sk, "plain_launches": times}), flush=True)
+
+
 def run_cublas(name, reps):
     """the same contraction through torch (cuBLAS / cuBLASLt, bf16 in, fp32 accumulate; plain
     store, no fused epilogue) in the same graph-of-launches harness: the library baseline"""
@@ -137,6 +162,11 @@ if __name__ == "__main__":
         if not name.startswith(pref):
             continue
         reps = 200 if name.startswith("c2") else (50 if name.startswith("c3") else 10)
+        if os.environ.get("ONLY"):  # variants "cg,bn,sk;cg,bn,sk" launched twice each, no graph (ncu runs)
+            for spec in os.environ["ONLY"].split(";"):
+                cg, bn, sk = (int(v) for v in spec.split(","))
+                run_plain(name, bn, cg, sk)
+            continue
         run(name, reps, 0, 1, 0, quiet=True)  # warm-up (clocks, allocator, module load)
         run(name, reps, 0, 1, 0)  # the library's automatic choice
         for cg, bn, sk in ((1, 128, 0), (1, 192, 0), (1, 256, 0), (2, 128, 0), (2, 256, 0), (2, 512, 0),
