@@ -31,7 +31,10 @@ flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* log
  * per 128-row tile, 2 CTA pairs on 256-row tiles with cta_group::2 UMMAs), key 8 = GEMM
  * stream-K (0 automatic, 1 never, 2 wherever the GEMM has enough k-blocks: every SM / pair
  * gets the same share of the flattened (tile, k-block) space, cut tiles are summed in a
- * fixed order).  Returns FLOWMOE_ERR_INVALID on an unknown key. */
+ * fixed order), key 9 = SMs the backward GEMMs leave free for the all-reduce at P > 1 (the
+ * persistent GEMM grids shrink to 148 - value SMs; default the AR communicator's CTA cap,
+ * 32, on a multi-process ctx, 0 in the simulated world).  Returns
+ * FLOWMOE_ERR_INVALID on an unknown key. */
 flowmoe_status flowmoe_debug_set(flowmoe_ctx* ctx, int key, int value);
 
 /* Test hook: one GEMM through the block's GEMM kernels (tcgen05 for BF16,

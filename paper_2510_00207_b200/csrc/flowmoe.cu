@@ -200,6 +200,9 @@ struct flowmoe_ctx {
   // per-ctx test/benchmark knobs (flowmoe_test.h) and per-kernel profile, applied to the
   // kernel modules by apply_ctx() at the start of every enqueueing call
   int dbg_flags = 0, pdl = 1, force_bn = 0, force_cg = 0, force_sk = 0, p2p_on_lane = 1;
+  // SMs the backward GEMMs leave to the all-reduce at P > 1 (the AR communicator's CTA cap
+  // on a real multi-GPU ctx; key 9 overrides, 0 = none) and the cap of the GEMMs being enqueued
+  int bwd_sm_reserve = 0, gemm_max_sms = 0;
   Prof prof;
   TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
@@ -323,6 +326,7 @@ void set_streamk(const flowmoe_ctx* x, GemmArgs& g, cudaStream_t s) {
 #define FM_GEMM(kind, g)                                                   \
   do {                                                                     \
     set_streamk(x, g, sc);                                                 \
+    g.max_sms = x->gemm_max_sms;                                           \
     if (flowmoe_status st_ = run_gemm(kind, g, dt, es, sc)) return st_;   \
   } while (0)
 
@@ -724,6 +728,7 @@ flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
   else if (key == 6) x->p2p_on_lane = value ? 1 : 0;
   else if (key == 7) x->force_cg = value;
   else if (key == 8) x->force_sk = value;
+  else if (key == 9) x->bwd_sm_reserve = value < 0 ? 0 : (value > 120 ? 120 : value);
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   return FLOWMOE_OK;
 }
@@ -959,6 +964,10 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
     ncclConfig_t nc2 = NCCL_CONFIG_INITIALIZER;
     nc2.blocking = 1;
     nc2.maxCTAs = ar_max_ctas();
+    // and the backward GEMMs (persistent grids: one CTA per SM) leave as many SMs free, so
+    // an AR chunk's CTAs start at once instead of after the GEMM holding their SMs
+    // (dsv2s N=2: 9.23 -> 9.03 ms; key 9 overrides)
+    x->bwd_sm_reserve = ar_max_ctas();
     if (ncclCommSplit(x->comm_a2a, 0, cfg->rank, &x->comm_ar, &nc2) != ncclSuccess)
       return cleanup_fail(fail(FLOWMOE_ERR_NCCL, "ncclCommSplit failed"));
     x->a2a_comm.push_back(x->comm_a2a);
@@ -1239,6 +1248,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   if (!x || !p || !xin || !y || !saved) return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL argument");
   if (!p->wqkv || !p->wo || !p->wg || !p->w1 || !p->b1 || !p->w2 || !p->b2)
     return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL parameter pointer");
+  x->gemm_max_sms = 0;
   const int dt = x->dt;
   const size_t es = x->es;
   const int R = x->cfg.R;
@@ -1412,6 +1422,7 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: NULL gradient pointer");
   if (chunk_bytes == 0 || chunk_bytes % 16)
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: chunk_bytes (S_p) must be a positive multiple of 16");
+  x->gemm_max_sms = (x->P > 1 && x->bwd_sm_reserve > 0) ? 148 - x->bwd_sm_reserve : 0;
   const int dt = x->dt;
   const size_t es = x->es;
   const int R = x->cfg.R;

@@ -631,7 +631,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
     if (num_sms <= 0) num_sms = 148;
   }
   const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM * CG - 1) / (TC_BM * CG)) * g.batch;
-  const int units = num_sms / CG;
+  const int units = (g.max_sms > 0 && g.max_sms < num_sms ? g.max_sms : num_sms) / CG;
   const int nu = streamk ? units : (int)(tiles < units ? tiles : units);
   const size_t smem = (tiles <= nu && !streamk) ? smem_max - EB * 32768 : smem_max;
   if constexpr (CG == 2)

@@ -46,6 +46,7 @@ struct GemmArgs {
   size_t splitk_ws_floats = 0;
   unsigned int* splitk_tick = nullptr;
   size_t splitk_ticks = 0;
+  int max_sms = 0;  // > 0: persistent grid on at most this many SMs (the rest left to a collective)
 };
 
 // Dispatches to the tcgen05 kernel for bf16 and the fp32 SIMT kernel (K10) for f32.

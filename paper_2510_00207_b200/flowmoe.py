@@ -163,12 +163,16 @@ _ENV_KNOBS = (("FLOWMOE_DEBUG_SIMT", 1, 1),        # debug: route bf16 GEMMs to 
               ("FLOWMOE_FORCE_CG1", 7, 1),         # A/B: single-CTA GEMM tiles only
               ("FLOWMOE_FORCE_CG2", 7, 2),         # test: CTA-pair (cta_group::2) GEMMs everywhere
               ("FLOWMOE_NO_STREAMK", 8, 1))        # A/B: whole-tile GEMM work split only
+_ENV_VALUE_KNOBS = (("FLOWMOE_BWD_SM_RESERVE", 9),)  # A/B: SMs the backward GEMMs leave to the AR (P > 1)
 
 
 def _apply_env_knobs(handle):
     for env, key, val in _ENV_KNOBS:
         if os.environ.get(env):
             _check(lib().flowmoe_debug_set(handle, key, val), "flowmoe_debug_set")
+    for env, key in _ENV_VALUE_KNOBS:
+        if os.environ.get(env):
+            _check(lib().flowmoe_debug_set(handle, key, int(os.environ[env])), "flowmoe_debug_set")
 
 
 def _check(rc: int, what: str):

@@ -9,7 +9,7 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --mas
 for c in ${CONFIGS:-c2 c3 dsv2s}; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29760 \
     bench.py --gpus $N --config $c --steps 20 --warmup 5 --trace-dir $O > $O/bench_$c.json 2> $O/bench_$c.err
-  echo "bench $c rc=$?"; python - <<PY
+  echo "bench $c rc=$?"; rm -f $O/flowmoe_trace_*_r[1-9].json; gzip -f $O/flowmoe_trace_*_r0.json 2>/dev/null; python - <<PY
 import json
 d=[json.loads(l) for l in open("$O/bench_$c.json") if l.startswith("{")][-1]
 x=d.get("exposed_comm") or {}
