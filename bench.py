@@ -458,6 +458,7 @@ def main():
 
     # ---- CUPTI timeline of graph replays: steady-state kernel times, idle, exposed comm
     tl = None
+    tl_nopdl = None
     # bytes one exchange moves over NVLink (send side): E·C·M·es·(P-1)/P, C per chunk
     import math
     C_ = cfg.T // cfg.R if cfg.capacity_factor == 0 else \
@@ -475,6 +476,29 @@ def main():
                                a2a_bytes=a2a_bytes)
         except Exception as e:  # the timeline is diagnostics, never the measurement
             tl = {"error": repr(e)}
+        # Kernel execution intervals for the roofline (N = 1): with programmatic dependent
+        # launch a kernel is pre-launched and its CUPTI interval includes the wait for its
+        # predecessor, so the same iteration is captured once more with PDL off and traced;
+        # its group intervals are the kernels' execution (the other lane still contends).
+        if world == 1 and not args.no_graph:
+            try:
+                ctx.debug_set(4, 0)
+                graph2 = torch.cuda.CUDAGraph()
+                cap2 = torch.cuda.Stream()
+                cap2.wait_stream(stream)
+                with torch.cuda.graph(graph2, stream=cap2, capture_error_mode="thread_local"):
+                    iteration(torch.cuda.current_stream())
+                ctx.debug_set(4, 1)
+                for _ in range(3):
+                    graph2.replay()
+                torch.cuda.synchronize()
+                tl_nopdl = trace_replays(graph2.replay, args.trace_iters,
+                                         os.path.join(args.trace_dir, f"flowmoe_trace_{args.config}_n1_nopdl.json"),
+                                         trim=max(0, min(3, (args.trace_iters - 2) // 4)), a2a_bytes=a2a_bytes)
+                del graph2
+            except Exception as e:
+                ctx.debug_set(4, 1)
+                tl_nopdl = {"error": repr(e)}
         if world > 1:
             allt = [None] * world
             dist.all_gather_object(allt, tl)
@@ -521,6 +545,9 @@ def main():
             rr = tl["per_rank"] if "per_rank" in tl else [tl]
             tl0 = rr[0] if rr and rr[0] and "groups" in rr[0] else None
         tgroups = tl0["groups"] if tl0 else {}
+        tgroups_pdl = tgroups
+        if tl_nopdl is not None and "groups" in tl_nopdl:
+            tgroups = tl_nopdl["groups"]
 
         def roof(g):
             bound, unit, peak, psrc = bound_of(g)
@@ -529,13 +556,16 @@ def main():
             tg = tgroups.get(g)
             if tg and tg["busy_us_per_iter"] > 0:
                 busy_s, sum_s, n = tg["busy_us_per_iter"] * 1e-6, tg["sum_us_per_iter"] * 1e-6, tg["launches_per_iter"]
-                src = "CUPTI trace of the CUDA-graph replays"
+                src = ("CUPTI trace of the CUDA-graph replays, graph captured with PDL off (intervals = execution)"
+                       if tgroups is not tgroups_pdl else "CUPTI trace of the CUDA-graph replays")
             else:  # no trace: the eager per-launch event timing (lanes collapsed)
                 busy_s = sum_s = a_["eager_ms"] * 1e-3
                 n = a_["launches"]
                 src = "eager per-launch CUDA events (lanes collapsed)"
             ach = work / busy_s
-            return {"bound": bound, "unit": unit, "achieved": ach, "peak": peak, "frac": ach / peak,
+            tp = tgroups_pdl.get(g) if tgroups is not tgroups_pdl else None
+            extra = {"busy_ms_per_step_pdl_trace": tp["busy_us_per_iter"] * 1e-3} if tp else {}
+            return {**extra, "bound": bound, "unit": unit, "achieved": ach, "peak": peak, "frac": ach / peak,
                     "peak_source": psrc, "busy_ms_per_step": busy_s * 1e3, "sum_launch_ms_per_step": sum_s * 1e3,
                     "launches_per_step": n, "per_launch_us": sum_s / max(n, 1) * 1e6,
                     "achieved_per_launch": work / sum_s, "timing": src,
@@ -575,6 +605,7 @@ def main():
                          "unit": R_["unit"], "frac": R_["frac"], "traffic": traffic,
                          "peak_source": R_["peak_source"], "timing": R_["timing"],
                          "busy_ms_per_step": R_["busy_ms_per_step"],
+                         "busy_ms_per_step_pdl_trace": R_.get("busy_ms_per_step_pdl_trace"),
                          "sum_launch_ms_per_step": R_["sum_launch_ms_per_step"],
                          "launches_per_step": R_["launches_per_step"], "per_launch_us": R_["per_launch_us"],
                          "achieved_per_launch": R_["achieved_per_launch"],

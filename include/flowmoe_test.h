@@ -33,7 +33,8 @@ flowmoe_status flowmoe_saved_routing_offsets(const flowmoe_ctx* ctx, size_t* log
  * gets the same share of the flattened (tile, k-block) space, cut tiles are summed in a
  * fixed order), key 9 = SMs the backward GEMMs leave free for the all-reduce at P > 1 (the
  * persistent GEMM grids shrink to 148 - value SMs; default the AR communicator's CTA cap,
- * 32, on a multi-process ctx, 0 in the simulated world).  Returns
+ * 32, on a multi-process ctx, 0 in the simulated world), key 10 = SMs every GEMM leaves to
+ * the other lanes' kernels (0 default).  Returns
  * FLOWMOE_ERR_INVALID on an unknown key. */
 flowmoe_status flowmoe_debug_set(flowmoe_ctx* ctx, int key, int value);
 

@@ -203,6 +203,7 @@ struct flowmoe_ctx {
   // SMs the backward GEMMs leave to the all-reduce at P > 1 (the AR communicator's CTA cap
   // on a real multi-GPU ctx; key 9 overrides, 0 = none) and the cap of the GEMMs being enqueued
   int bwd_sm_reserve = 0, gemm_max_sms = 0;
+  int sm_reserve = 0;  // key 10: SMs every GEMM leaves to the other lanes' kernels (A/B; 0 = none)
   Prof prof;
   TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
@@ -729,6 +730,7 @@ flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
   else if (key == 7) x->force_cg = value;
   else if (key == 8) x->force_sk = value;
   else if (key == 9) x->bwd_sm_reserve = value < 0 ? 0 : (value > 120 ? 120 : value);
+  else if (key == 10) x->sm_reserve = value < 0 ? 0 : (value > 120 ? 120 : value);
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   return FLOWMOE_OK;
 }
@@ -1248,7 +1250,7 @@ flowmoe_status enqueue_fwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
   if (!x || !p || !xin || !y || !saved) return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL argument");
   if (!p->wqkv || !p->wo || !p->wg || !p->w1 || !p->b1 || !p->w2 || !p->b2)
     return fail(FLOWMOE_ERR_INVALID, "block_fwd: NULL parameter pointer");
-  x->gemm_max_sms = 0;
+  x->gemm_max_sms = x->sm_reserve > 0 ? 148 - x->sm_reserve : 0;
   const int dt = x->dt;
   const size_t es = x->es;
   const int R = x->cfg.R;
@@ -1422,7 +1424,10 @@ flowmoe_status enqueue_bwd(flowmoe_ctx* x, const flowmoe_params* p, const void* 
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: NULL gradient pointer");
   if (chunk_bytes == 0 || chunk_bytes % 16)
     return fail(FLOWMOE_ERR_INVALID, "block_bwd: chunk_bytes (S_p) must be a positive multiple of 16");
-  x->gemm_max_sms = (x->P > 1 && x->bwd_sm_reserve > 0) ? 148 - x->bwd_sm_reserve : 0;
+  {
+    const int res = (x->P > 1 && x->bwd_sm_reserve > x->sm_reserve) ? x->bwd_sm_reserve : x->sm_reserve;
+    x->gemm_max_sms = res > 0 ? 148 - res : 0;
+  }
   const int dt = x->dt;
   const size_t es = x->es;
   const int R = x->cfg.R;

@@ -163,7 +163,8 @@ _ENV_KNOBS = (("FLOWMOE_DEBUG_SIMT", 1, 1),        # debug: route bf16 GEMMs to 
               ("FLOWMOE_FORCE_CG1", 7, 1),         # A/B: single-CTA GEMM tiles only
               ("FLOWMOE_FORCE_CG2", 7, 2),         # test: CTA-pair (cta_group::2) GEMMs everywhere
               ("FLOWMOE_NO_STREAMK", 8, 1))        # A/B: whole-tile GEMM work split only
-_ENV_VALUE_KNOBS = (("FLOWMOE_BWD_SM_RESERVE", 9),)  # A/B: SMs the backward GEMMs leave to the AR (P > 1)
+_ENV_VALUE_KNOBS = (("FLOWMOE_BWD_SM_RESERVE", 9),  # A/B: SMs the backward GEMMs leave to the AR (P > 1)
+                    ("FLOWMOE_SM_RESERVE", 10))     # A/B: SMs every GEMM leaves to the other lanes
 
 
 def _apply_env_knobs(handle):
