@@ -681,13 +681,14 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // the SMs where 256 leave most of a wave idle (the T_r-row MHA projections: 80 -> 108 of
     // 148 SMs, 32 -> 28 us); with every SM busy the extra operand bytes per FLOP lose to the
     // pairs (dsv2s E1 73 vs 68 us), and so they do on long K (> 8192); measured on the
-    // unbatched projections only, so the batched expert GEMMs keep 256.  Short-K fp32 wgrads
-    // (K <= 512) stay on single CTAs: epilogue-bound, the pair gains nothing (dW1 171 vs 156).
+    // unbatched projections only, so the batched expert GEMMs keep 256.  The fp32 wgrads pair
+    // too (dsv2s dW1, K = 512: 174 -> 136 us) since the epilogue's remote TMEM-release arrive
+    // no longer carries a GPU-scope fence (tc_common.cuh mbar_arrive_cluster).
     auto cost = [](int64_t t, int slots, double w) { return (double)((t + slots - 1) / slots) * w; };
     const int64_t nk = (g.K + TC_BK - 1) / TC_BK;
     int pick = 1;
     double best = cost(tiles(256), 148, 256 / 0.89);
-    const bool pairs_ok = g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 8 * TC_BK);
+    const bool pairs_ok = g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 4 * TC_BK);
     const int64_t mp = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch;  // pair rows
     const int64_t t256 = mp * ((g.N + 255) / 256), t512 = mp * ((g.N + 511) / 512);
     if (pairs_ok) {

@@ -217,8 +217,11 @@ FM_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// wait with cluster-scope acquire: the phase may be completed by the peer CTA
-// (tcgen05.commit multicast, remote arrive, or a peer TMA's complete_tx)
+// wait on a phase the peer CTA may complete (tcgen05.commit multicast, remote arrive, or a
+// peer TMA's complete_tx).  Default (.acquire.cta) semantics: what follows the wait reads
+// smem through the async proxy (UMMA, TMA) or TMEM (ordered by the tcgen05 fences), never
+// generic memory the peer wrote — .acquire.cluster added an L1 invalidation (CCTL.IVALL)
+// after every completed wait.
 FM_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
   FM_HANG_DECL;
   const uint32_t addr = smem_u32(bar);
@@ -226,7 +229,7 @@ FM_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(addr), "r"(parity)
@@ -241,7 +244,7 @@ FM_DEV void mbar_wait_cl_sleep(uint64_t* bar, uint32_t parity) {
   while (true) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(addr), "r"(parity)
@@ -251,8 +254,13 @@ FM_DEV void mbar_wait_cl_sleep(uint64_t* bar, uint32_t parity) {
   }
 }
 // arrive on the barrier at shared::cluster address `cl_addr` (a mapa'd peer barrier)
+// Arrive on a barrier of another CTA of the cluster.  The default (.release.cta) form: the
+// signal is "this CTA's TMEM reads are done", ordered by tcgen05.wait::ld + the tcgen05 fences,
+// not by generic memory — .release.cluster compiles to MEMBAR.ALL.GPU + ERRBAR, which waited
+// for the epilogue's outstanding TMA stores (24% of the pair kernel's stall samples on the
+// store-heavy fp32 wgrads, profiles/r02/ncu_dw1_pair.md).
 FM_DEV void mbar_arrive_cluster(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
 // TMA load into this CTA's smem, completing bytes on the leader's barrier (cl_bar: a
 // shared::cluster address, e.g. mapa(bar, 0))
