@@ -669,10 +669,11 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
   const bool f32out = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
   const int64_t mt = (int64_t)((g.M + TC_BM - 1) / TC_BM) * g.batch;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
-  // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) take a 3-stage ring
-  // and double-buffered epilogue staging (tools/probe/gemm_probe.cu: -2..-6%); the
-  // 4-stage ring stays everywhere else (3 stages cost 3-8% on longer K)
-  if (g.N >= 256 && f32out && g.K <= 4 * TC_BK && tiles(256) >= 4 * 148) return launch_tc<256, 3, 2>(g, s);
+  // write-bound fp32 wgrads (K <= 256, many tiles: the c4 expert dW) on single CTAs take a
+  // 3-stage ring and double-buffered epilogue staging (tools/probe/gemm_probe.cu: -2..-6%);
+  // with more than 128 rows they go to the CTA pairs below (c4 dW1 1016 -> 957 us)
+  if (g.N >= 256 && f32out && g.K <= 4 * TC_BK && tiles(256) >= 4 * 148 && (g.M <= TC_BM || g_force_cg == 1))
+    return launch_tc<256, 3, 2>(g, s);
   if (g.N >= 256 && tiles(256) >= 48) {
     // Wave-quantised cost of the candidate tilings: waves x BN / eff, eff measured per SM at
     // the dsv2s / c3 / c4 shapes (tools/gemm_microbench.py, r02): CTA pairs on 256 x 256
@@ -688,7 +689,7 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int64_t nk = (g.K + TC_BK - 1) / TC_BK;
     int pick = 1;
     double best = cost(tiles(256), 148, 256 / 0.89);
-    const bool pairs_ok = g_force_cg == 0 && g.M > TC_BM && !(f32out && g.K <= 4 * TC_BK);
+    const bool pairs_ok = g_force_cg == 0 && g.M > TC_BM;
     const int64_t mp = (int64_t)((g.M + 2 * TC_BM - 1) / (2 * TC_BM)) * g.batch;  // pair rows
     const int64_t t256 = mp * ((g.N + 255) / 256), t512 = mp * ((g.N + 511) / 512);
     if (pairs_ok) {

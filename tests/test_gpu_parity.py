@@ -366,12 +366,13 @@ def test_gemm_streamk_epilogues():
     assert rel(F.cpu().numpy().astype(np.float64), ref) <= 1e-5
 
 
-@pytest.mark.parametrize("cg", [0, 2])
+@pytest.mark.parametrize("cg", [0, 1, 2])
 @pytest.mark.parametrize("epi", [3, 4])
 def test_gemm_tc_wgrad_variant_vs_fp64(epi, cg):
-    """The write-bound wgrad configuration (fp32 out, K <= 256, >= 4·148 tiles of 256
-    columns: 3-stage ring, double-buffered epilogue staging) on an m-major A like the
-    expert dW, ragged N and K, against the fp64 product: store (4) and accumulate (3)."""
+    """The write-bound wgrad shape (fp32 out, K <= 256, >= 4·148 tiles of 256 columns) on an
+    m-major A like the expert dW, ragged N and K, against the fp64 product: store (4) and
+    accumulate (3); automatic (CTA pairs), single CTAs (cg = 1: the 3-stage ring with
+    double-buffered epilogue staging) and forced pairs."""
     import torch
     import paper_2510_00207_b200 as fm
     Mr, N, K = 2048, 9480, 200  # 16 x 38 = 608 tiles
