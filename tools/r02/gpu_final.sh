@@ -4,7 +4,7 @@
 # list of the default bench command (after that command exited 0 without ncu).
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/r02/${TAG:-final}; mkdir -p $O
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
+mkdir -p $O; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 -rs > $O/pytest.log 2>&1; echo "pytest rc=$?"; tail -4 $O/pytest.log
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?"
 timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo "bench reference rc=$?"; tail -1 $O/bench_reference.json | cut -c1-400
