@@ -314,8 +314,8 @@ flowmoe_status run_gemm(int kind, const GemmArgs& g, int dt, size_t es, cudaStre
   FM_KP(kind, 1, flops, bytes, s, gemm(g, dt, s));
   return FLOWMOE_OK;
 }
-// stream-K scratch: two fp32 partial tiles (128 x 256) per CTA of a full grid, and counters
-constexpr size_t SK_WS_FLOATS = (size_t)148 * 2 * 128 * 256;
+// stream-K scratch: one fp32 partial tile (128 x 256) per CTA of a full grid, and counters
+constexpr size_t SK_WS_FLOATS = (size_t)148 * 128 * 256;
 constexpr size_t SK_TICKS = 1 << 16;
 void set_streamk(const flowmoe_ctx* x, GemmArgs& g, cudaStream_t s) {
   for (size_t i = 0; i < x->sk_ws.size() && i < x->lanes.size(); ++i)
