@@ -39,9 +39,9 @@ struct GemmArgs {
   void* aux = nullptr; int64_t ldaux = 0, sAux = 0;
   int epi = EPI_STORE;
   float alpha = 1.0f;
-  // optional stream-K scratch (k_gemm_tc.cu): per unit two fp32 partial tiles, and per
-  // (tile, CTA of the pair) an [arrivals, written] counter pair (zeroed once; every use
-  // leaves them zero).  Without it the GEMM never splits a tile.
+  // optional stream-K scratch (k_gemm_tc.cu): one fp32 128 x BN partial tile per CTA of the
+  // grid, and one "partials written" counter per cut tile and CTA of the pair (zeroed once;
+  // every use leaves them zero).  Without it the GEMM never splits a tile.
   float* splitk_ws = nullptr;
   size_t splitk_ws_floats = 0;
   unsigned int* splitk_tick = nullptr;
