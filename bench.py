@@ -563,8 +563,19 @@ def main():
                 n = a_["launches"]
                 src = "eager per-launch CUDA events (lanes collapsed)"
             ach = work / busy_s
+            # the per-launch roofline of a mixed group: each call site's launches bounded by
+            # max(FLOPs / tensor peak, bytes / HBM peak) — the weight-streaming expert GEMMs and
+            # the fp32 wgrads sit on the HBM side of the ridge (§6)
+            lb_s = 0.0
+            for p_ in compute:
+                if kgroup(p_["name"]) == g and p_["launches"] > 0:
+                    fl, by = p_["flops"] / p_["launches"], p_["bytes"] / p_["launches"]
+                    lb_s += p_["launches"] * max(fl / (peaks["bf16_tflops_sustained"] * 1e12) if unit == "TFLOP/s" else 0.0,
+                                                 by / (peaks["hbm_gbs"] * 1e9))
             tp = tgroups_pdl.get(g) if tgroups is not tgroups_pdl else None
             extra = {"busy_ms_per_step_pdl_trace": tp["busy_us_per_iter"] * 1e-3} if tp else {}
+            extra["per_launch_bound_ms_per_step"] = lb_s * 1e3
+            extra["frac_of_per_launch_bound"] = lb_s / busy_s if busy_s > 0 else None
             return {**extra, "bound": bound, "unit": unit, "achieved": ach, "peak": peak, "frac": ach / peak,
                     "peak_source": psrc, "busy_ms_per_step": busy_s * 1e3, "sum_launch_ms_per_step": sum_s * 1e3,
                     "launches_per_step": n, "per_launch_us": sum_s / max(n, 1) * 1e6,
@@ -606,6 +617,8 @@ def main():
                          "peak_source": R_["peak_source"], "timing": R_["timing"],
                          "busy_ms_per_step": R_["busy_ms_per_step"],
                          "busy_ms_per_step_pdl_trace": R_.get("busy_ms_per_step_pdl_trace"),
+                         "per_launch_bound_ms_per_step": R_.get("per_launch_bound_ms_per_step"),
+                         "frac_of_per_launch_bound": R_.get("frac_of_per_launch_bound"),
                          "sum_launch_ms_per_step": R_["sum_launch_ms_per_step"],
                          "launches_per_step": R_["launches_per_step"], "per_launch_us": R_["per_launch_us"],
                          "achieved_per_launch": R_["achieved_per_launch"],
