@@ -546,7 +546,11 @@ def main():
             tl0 = rr[0] if rr and rr[0] and "groups" in rr[0] else None
         tgroups = tl0["groups"] if tl0 else {}
         tgroups_pdl = tgroups
-        if tl_nopdl is not None and "groups" in tl_nopdl:
+        # the PDL-off intervals stand for the kernels' execution only where PDL does not
+        # change the schedule (the GEMM-bound configs); where it does (latency-bound c2:
+        # every launch gap shows), the PDL trace stays the measurement
+        if tl_nopdl is not None and "groups" in tl_nopdl and tl0 and \
+                tl_nopdl.get("span_us_per_iter", 0) <= 1.05 * tl0.get("span_us_per_iter", 0):
             tgroups = tl_nopdl["groups"]
 
         def roof(g):
