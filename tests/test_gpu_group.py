@@ -68,6 +68,13 @@ def test_local_group_block_parity(name, P):
     _check(name, P, lanes=CASES[name].R)
 
 
+@pytest.mark.parametrize("name", ["bf16_p", "bf16_k3_drop"])
+def test_local_group_block_parity_eight_ranks(name):
+    """P = 8 (one expert per rank, the largest world the peer-memory A2A supports and the
+    driver's 8-GPU scaling point): the same checks on eight simulated ranks."""
+    _check(name, 8, lanes=CASES[name].R)
+
+
 def test_local_group_one_lane_and_flowmoe_ar():
     """The paper's single compute stream, and the FLOWMOE_AR policy (AT unsplit)."""
     _check("bf16_p", 2, lanes=1)
@@ -99,7 +106,7 @@ def test_local_group_stack_per_block_parity():
         assert not bad, (q, bad, res)
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("s_p", [16, 4096 + 16, 1 << 20, 1 << 30])
 def test_local_group_chunked_allreduce_matches_oracle(P, s_p):
     """flowmoe_allreduce_submit on P simulated ranks: the S_p partition (chunks of S_p plus
@@ -109,7 +116,7 @@ def test_local_group_chunked_allreduce_matches_oracle(P, s_p):
     import torch
     import paper_2510_00207_b200 as fm
     from tests.gpu_util import shape_of
-    cfg = CASES["c1_f32"].replace(P=P)
+    cfg = (CASES["c1_f32"] if P <= 4 else CASES["bf16_p"].replace(dtype="f32")).replace(P=P)  # E % P == 0
     ctxs = fm.FlowMoE.local_group(shape_of(cfg, P, 0, "overwrite", 1, "flowmoe", "p2p"), P, 0)
     n = 100_003  # odd: every S_p leaves a remainder chunk
     rng = np.random.default_rng(P * 31 + s_p % 97)
