@@ -204,7 +204,6 @@ struct flowmoe_ctx {
   // on a real multi-GPU ctx; key 9 overrides, 0 = none) and the cap of the GEMMs being enqueued
   int bwd_sm_reserve = 0, gemm_max_sms = 0;
   int sm_reserve = 0;  // key 10: SMs every GEMM leaves to the other lanes' kernels (A/B; 0 = none)
-  int force_ar = 0;    // key 11: A-resident pair GEMMs (0 automatic, 1 never, 2 forced where K <= 512)
   Prof prof;
   TaskLog tlog;
   // saved stashes registered for peer-memory A2A, in registration order (collective)
@@ -271,7 +270,6 @@ void apply_ctx(flowmoe_ctx* x) {
   gemm_tc_force_bn(x->force_bn);
   gemm_tc_force_cg(x->force_cg);
   gemm_tc_force_streamk(x->force_sk);
-  gemm_tc_force_aresident(x->force_ar);
   g_pdl_enabled = x->pdl;
   g_p2p_on_lane = x->p2p_on_lane;
   g_prof = &x->prof;
@@ -733,7 +731,6 @@ flowmoe_status flowmoe_debug_set(flowmoe_ctx* x, int key, int value) {
   else if (key == 8) x->force_sk = value;
   else if (key == 9) x->bwd_sm_reserve = value < 0 ? 0 : (value > 120 ? 120 : value);
   else if (key == 10) x->sm_reserve = value < 0 ? 0 : (value > 120 ? 120 : value);
-  else if (key == 11) x->force_ar = value;
   else return fail(FLOWMOE_ERR_INVALID, "flowmoe_debug_set: unknown key");
   return FLOWMOE_OK;
 }
@@ -1985,7 +1982,6 @@ extern "C" flowmoe_status flowmoe_test_gemm(flowmoe_ctx* x, int dtype, int M, in
     gemm_tc_force_bn(0);
     gemm_tc_force_cg(0);
     gemm_tc_force_streamk(0);
-    gemm_tc_force_aresident(0);
     g_pdl_enabled = 1;
     g_prof = nullptr;
   }

@@ -41,8 +41,6 @@ void gemm_tc_force_bn(int bn) { g_force_bn = bn; }
 void gemm_tc_force_cg(int cg) { g_force_cg = cg; }
 static int g_force_sk = 0;  // stream-K: 0 = automatic, 1 = never, 2 = wherever the scratch allows
 void gemm_tc_force_streamk(int mode) { g_force_sk = mode; }
-static int g_force_ar = 0;  // A-resident pairs: 0 = automatic, 1 = never, 2 = wherever K <= 512 allows
-void gemm_tc_force_aresident(int mode) { g_force_ar = mode; }
 void gemm_tc_set_debug(int flags) { g_tc_debug = flags; }
 int attn_tc_debug_off() { return g_tc_debug & 4; }  // bit2: force the SIMT attention kernels
 
@@ -63,11 +61,7 @@ struct TcArgs {
 // A and half (BN/2) of the B columns and gets its 128 accumulator rows in its own TMEM, so
 // the operand bytes per SM and K-step drop from (128 + BN)·BK·2 to (128 + BN/2)·BK·2 —
 // the L2->SMEM traffic that bounded the 1-CTA kernel at ~70% of the tensor peak.
-// AR (A resident; CG = 2, K <= 512, the short-K fp32 wgrads): a unit takes a contiguous range
-// of tiles (n fastest), keeps its 128-row A panel for the whole K in shared memory while it
-// walks the N tiles of that row block, and streams only B through the ring — the A re-reads
-// (half of the L2->SMEM bytes of those output-bound GEMMs) drop to one per row block.
-template <int BN, int STAGES, int EB, int CG, bool SK, bool AR>
+template <int BN, int STAGES, int EB, int CG, bool SK>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b,
@@ -82,14 +76,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   constexpr uint32_t B_BYTES = BNL * TC_BK * 2;
-  static_assert(!AR || (CG == 2 && BN == 256 && !SK), "A-resident: 256-column pairs, whole tiles");
-  constexpr uint32_t STAGE_BYTES = AR ? B_BYTES : A_BYTES + B_BYTES;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t RING = STAGES * STAGE_BYTES;
-  constexpr uint32_t A_RES = AR ? 8 * A_BYTES : 0;  // the resident A panel, K <= 8 k-blocks
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* const sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* const a_res = sbase;      // [8][A_BYTES] (AR only)
-  uint8_t* const smem = sbase + A_RES;  // the operand ring
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
   const bool leader = crank == 0;
   const int unit = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
@@ -106,31 +96,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int64_t sk_base = (int64_t)dp_tiles * p.nk, sk_total = (int64_t)num_tiles * p.nk - sk_base;
   const int64_t sk_b = sk_base + (int64_t)unit * sk_total / nunits;
   const int64_t sk_e = sk_base + (int64_t)(unit + 1) * sk_total / nunits;
-  const int ar_t0 = (int)((int64_t)unit * num_tiles / nunits), ar_t1 = (int)((int64_t)(unit + 1) * num_tiles / nunits);
-  const int64_t it_begin = AR ? (int64_t)ar_t0 * p.nk
-                              : (unit < dp_tiles ? (int64_t)unit * p.nk : sk_b);
-  auto seg_more = [&](int64_t w) { return AR ? w < (int64_t)ar_t1 * p.nk : (w < sk_base || w < sk_e); };
+  const int64_t it_begin = unit < dp_tiles ? (int64_t)unit * p.nk : sk_b;
+  auto seg_more = [&](int64_t w) { return w < sk_base || w < sk_e; };
   auto seg_of = [&](int64_t w, int& tile, int& kb0, int& kb1) {
     tile = (int)(w / p.nk);
     kb0 = (int)(w - (int64_t)tile * p.nk);
     kb1 = (!sk || w < sk_base) ? p.nk : (int)min((int64_t)p.nk, (int64_t)kb0 + (sk_e - w));
   };
   auto seg_next = [&](int64_t w, int tile, int kb0, int kb1) -> int64_t {
-    if (AR) return w + p.nk;  // the next tile of the unit's contiguous range
     if (w < sk_base) return tile + nunits < dp_tiles ? (int64_t)(tile + nunits) * p.nk : sk_b;
     return w + (kb1 - kb0);
   };
   // one tile per unit: the operand ring is free when the epilogue runs, so it doubles
   // as the staging area and a single TMEM accumulator suffices (smaller footprint)
-  const bool single = !sk && !AR && num_tiles <= nunits;
+  const bool single = !sk && num_tiles <= nunits;
   uint8_t* epi_smem = single ? smem : smem + RING;  // 8 epilogue warps x EB x 4 KB staging
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING + (single ? 0 : EB * 32768));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the 4 epilogue warps
-  uint64_t* a_full = tempty + 2;     // AR: the A panel landed (leader's; both CTAs' bytes)
-  uint64_t* a_empty = a_full + 1;    // AR: the MMAs reading the A panel are done (both CTAs)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = p.g;
@@ -142,8 +127,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8 * CG); }
-    mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -164,34 +147,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ===== TMA producer (whole warp walks the ring, one elected lane issues) =====
     int gk = 0;
-    int ar_row = -1, ar_n = 0;  // AR: the resident A panel's row block, panels loaded so far
     for (int64_t w = it_begin; seg_more(w);) {
       int tile, kb0, kb1;
       seg_of(w, tile, kb0, kb1);
       w = seg_next(w, tile, kb0, kb1);
       const int n0 = (tile % ntn) * BN + (int)crank * SUBL;  // this CTA's B columns (+ s·UN per UMMA)
       const int m0 = ((tile / ntn) % ntm) * TC_BM * CG + (int)crank * TC_BM, b = tile / (ntn * ntm);
-      if constexpr (AR) {
-        if (tile / ntn != ar_row) {  // a new row block: reload the A panel once the MMAs are off it
-          if (ar_n >= 1) mbar_wait_cl(a_empty, (ar_n - 1) & 1);
-          if (elect_one()) {
-            if (leader) mbar_expect_tx(a_full, 2 * (uint32_t)p.nk * A_BYTES);
-            const uint32_t bar = mapa_u32(smem_u32(a_full), 0);
-            for (int kb = 0; kb < p.nk; ++kb) {
-              uint8_t* sa = a_res + kb * A_BYTES;
-              if (!p.a_mmajor) {
-                tma_load_3d_cg2(sa, &tma_a, bar, kb * TC_BK, m0, b);
-              } else {
-#pragma unroll
-                for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d_cg2(sa + i * 8192, &tma_a, bar, m0 + 64 * i, kb * TC_BK, b);
-              }
-            }
-          }
-          __syncwarp();
-          ar_row = tile / ntn;
-          ++ar_n;
-        }
-      }
       for (int kb = kb0; kb < kb1; ++kb, ++gk) {
         const int s = gk % STAGES;
         if (gk >= STAGES) {
@@ -199,7 +160,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           else mbar_wait(&empty[s], ((gk / STAGES) + 1) & 1);
         }
         uint8_t* sa = smem + s * STAGE_BYTES;
-        uint8_t* sb = AR ? sa : sa + A_BYTES;
+        uint8_t* sb = sa + A_BYTES;
         const int k0 = kb * TC_BK;
         if (elect_one()) {
           if constexpr (CG == 1) {
@@ -220,13 +181,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // both CTAs' bytes complete on the leader's barrier, armed by the leader alone
             if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
             const uint32_t bar = mapa_u32(smem_u32(&full[s]), 0);
-            if constexpr (!AR) {
-              if (!p.a_mmajor) {
-                tma_load_3d_cg2(sa, &tma_a, bar, k0, m0, b);
-              } else {
+            if (!p.a_mmajor) {
+              tma_load_3d_cg2(sa, &tma_a, bar, k0, m0, b);
+            } else {
 #pragma unroll
-                for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d_cg2(sa + i * 8192, &tma_a, bar, m0 + 64 * i, k0, b);
-              }
+              for (int i = 0; i < TC_BM / 64; ++i) tma_load_3d_cg2(sa + i * 8192, &tma_a, bar, m0 + 64 * i, k0, b);
             }
 #pragma unroll
             for (int u = 0; u < NSUB; ++u) {
@@ -260,11 +219,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // K-major: +32 B per UMMA_K=16 inside the 128-B swizzle row; SBO = 8 rows * 128 B.
     // MN-major: +16 K-rows * 128 B; LBO = 64-element MN block stride (one TMA box).
     const uint32_t s0 = smem_u32(smem);
-    // AR: A from the resident panel (k-block kb at kb·A_BYTES), B alone in the ring
-    const uint32_t sa0 = AR ? smem_u32(a_res) : s0, sb0r = AR ? s0 : s0 + A_BYTES;
-    const uint64_t adesc0 = p.a_mmajor ? umma_desc(sa0, mn_lbo, mn_sbo) : umma_desc(sa0, 16, 1024);
-    const uint64_t bdesc0 = p.b_kmajor ? umma_desc(sb0r, 16, 1024) : umma_desc(sb0r, mn_lbo, mn_sbo);
-    int ar_row = -1, ar_n = 0;
+    const uint64_t adesc0 = p.a_mmajor ? umma_desc(s0, mn_lbo, mn_sbo) : umma_desc(s0, 16, 1024);
+    const uint64_t bdesc0 = p.b_kmajor ? umma_desc(s0 + A_BYTES, 16, 1024) : umma_desc(s0 + A_BYTES, mn_lbo, mn_sbo);
     const uint64_t a_kstep = p.a_mmajor ? (2048 >> 4) : (32 >> 4);
     const uint64_t b_kstep = p.b_kmajor ? (32 >> 4) : (2048 >> 4);
     int gk = 0, it = 0;
@@ -277,15 +233,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], (use - 1) & 1);
         else mbar_wait(&tempty[acc], (use - 1) & 1);
       }
-      if constexpr (AR) {
-        if (tile / ntn != ar_row) {
-          if (elect_one() && ar_n >= 1) tc_commit2_both(a_empty);  // after the last MMA on the old panel
-          __syncwarp();
-          mbar_wait_cl(a_full, ar_n & 1);
-          ar_row = tile / ntn;
-          ++ar_n;
-        }
-      }
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
       (void)tile;
@@ -297,14 +244,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0 && gk < 8) FM_MARK(16 + gk);
         tc_fence_after();
         const uint64_t soff = (uint64_t)((uint32_t)s * STAGE_BYTES >> 4);
-        const uint64_t aoff = AR ? (uint64_t)((uint32_t)kb * A_BYTES >> 4) : soff;
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
             if constexpr (CG == 2) {
 #pragma unroll
               for (int u = 0; u < NSUB; ++u)  // B of UMMA u: SUBL rows (K-major) / columns further on
-                tc_mma2(tmem_d + u * UN, adesc0 + aoff + kk * a_kstep,
+                tc_mma2(tmem_d + u * UN, adesc0 + soff + kk * a_kstep,
                         bdesc0 + soff + kk * b_kstep + (uint64_t)(u * SUBL * TC_BK * 2 >> 4), p.idesc,
                         (kb > kb0 || kk > 0) ? 1u : 0u);
             } else
@@ -638,7 +584,7 @@ int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-template <int BN, int STAGES, int EB = 1, int CG = 1, bool SK = false, bool AR = false>
+template <int BN, int STAGES, int EB = 1, int CG = 1, bool SK = false>
 static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   constexpr int streamk = SK ? 1 : 0;
   constexpr int BNL = BN / CG;
@@ -673,9 +619,8 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.a_mmajor ? 1 : 0) << 15) |
             ((uint32_t)(g.b_kmajor ? 0 : 1) << 16) | ((uint32_t)((BN / NSUB) >> 3) << 17) |
             ((uint32_t)((TC_BM * CG) >> 4) << 24);
-  const size_t smem_max = AR ? (size_t)8 * TC_BM * TC_BK * 2 + (size_t)STAGES * BNL * TC_BK * 2 + EB * 32768 + 1024 + 256
-                             : (size_t)STAGES * (TC_BM * TC_BK * 2 + BNL * TC_BK * 2) + EB * 32768 + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES, EB, CG, SK, AR>;
+  const size_t smem_max = (size_t)STAGES * (TC_BM * TC_BK * 2 + BNL * TC_BK * 2) + EB * 32768 + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, STAGES, EB, CG, SK>;
   static bool attr_set = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max), true);
   (void)attr_set;
   static int num_sms = 0;
@@ -688,7 +633,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t s) {
   const int64_t tiles = (int64_t)((g.N + BN - 1) / BN) * ((g.M + TC_BM * CG - 1) / (TC_BM * CG)) * g.batch;
   const int units = (g.max_sms > 0 && g.max_sms < num_sms ? g.max_sms : num_sms) / CG;
   const int nu = streamk ? units : (int)(tiles < units ? tiles : units);
-  const size_t smem = (tiles <= nu && !streamk && !AR) ? smem_max - EB * 32768 : smem_max;
+  const size_t smem = (tiles <= nu && !streamk) ? smem_max - EB * 32768 : smem_max;
   if constexpr (CG == 2)
     launch_kc(kern, dim3(2 * nu), TC_THREADS, smem, s, dim3(2, 1, 1), ma, mb, mc, maux, p);
   else
@@ -712,9 +657,7 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     return g_force_sk != 1 && g.splitk_ws && g.splitk_ws_floats >= (size_t)units * cg * TC_BM * bn &&
            g.splitk_ticks >= (size_t)(units * cg) && (t % units) * nk >= 2 * units;
   };
-  const bool ar_ok = g.K <= 8 * TC_BK && g.M > TC_BM && g_force_ar != 1;
   if (g_force_cg == 2) {
-    if (g_force_ar == 2 && ar_ok && (g_force_bn == 0 || g_force_bn == 256)) return launch_tc<256, 4, 1, 2, false, true>(g, s);
     if (g_force_bn == 128) return launch_tc<128, 8, 1, 2>(g, s);
     if (g_force_bn == 512) return launch_tc<512, 4, 1, 2>(g, s);
     return g_force_sk == 2 && sk_ok(256, 2) ? launch_tc<256, 6, 1, 2, true>(g, s) : launch_tc<256, 6, 1, 2>(g, s);
@@ -765,10 +708,6 @@ int gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // dsv2s dX (40 pair tiles, K = 15360) 79.4 -> 65.0 us, o-proj / dctx (K = 5120) 30.4 ->
     // 29.4 us.  Short K loses to the fix-up (E2, K = 1536: 58.6 -> 67.2 us).
     if (pairs_ok && sk_ok(256, 2) && (g_force_sk == 2 || (nk >= 64 && (t256 < 74 || nk >= 128)))) pick = 4;
-    // A-resident pairs for the short-K fp32 wgrads with several row blocks per pair: the A
-    // panel stays in shared memory across the N tiles of its row block
-    if (pick == 2 && ar_ok && f32out && t256 >= 2 * 74) pick = 6;
-    if (pick == 6) return launch_tc<256, 4, 1, 2, false, true>(g, s);
     if (pick == 4) return launch_tc<256, 6, 1, 2, true>(g, s);
     if (pick == 5) return launch_tc<512, 4, 1, 2>(g, s);
     if (pick == 2) return launch_tc<256, 6, 1, 2>(g, s);

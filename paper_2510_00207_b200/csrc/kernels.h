@@ -57,8 +57,7 @@ int gemm_tc_init();                               // resolves cuTensorMapEncodeT
 void gemm_tc_set_debug(int flags);
 void gemm_tc_force_bn(int bn);
 void gemm_tc_force_cg(int cg);
-void gemm_tc_force_streamk(int mode);  // 0 automatic, 1 never, 2 wherever the scratch allows
-void gemm_tc_force_aresident(int mode);  // 0 automatic, 1 never, 2 wherever K <= 512 (pairs)  // 0 automatic, 1 single-CTA tiles, 2 CTA pairs (cta_group::2)
+void gemm_tc_force_streamk(int mode);  // 0 automatic, 1 never, 2 wherever the scratch allows  // 0 automatic, 1 single-CTA tiles, 2 CTA pairs (cta_group::2)
 
 // ---------------------------------------------------------------- attention
 // qkv [nseq·N][3M] (sequences of N rows; head h at columns h*dh of each of Q|K|V),

@@ -57,7 +57,7 @@ def knob_ctx():
     return _CTX
 
 
-def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False, ar=0):
+def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False):
     Mr, N, K, batch, am, bk, epi = SHAPES[name]
     dev = torch.device("cuda", 0)
     A = torch.randn(batch, (K if am else Mr), (Mr if am else K), device=dev).to(torch.bfloat16)
@@ -70,7 +70,6 @@ def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False, ar=0):
     ctx.debug_set(4, pdl)
     ctx.debug_set(7, cg)
     ctx.debug_set(8, sk)
-    ctx.debug_set(11, ar)
     kw = dict(M=Mr, N=N, K=K, batch=batch, lda=(Mr if am else K), sA=Mr * K, a_mmajor=am,
               ldb=(K if bk else N), sB=K * N, b_kmajor=bk, ldc=N, sC=Mr * N, epi=epi, bias=bias, aux=aux)
     s = torch.cuda.current_stream()
@@ -94,7 +93,7 @@ def run(name, reps, bn, pdl, cg=0, sk=0, quiet=False, ar=0):
     us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
     flops = 2.0 * Mr * N * K * batch
     if not quiet:
-        print(json.dumps({"shape": name, "bn": bn, "cg": cg, "sk": sk, "ar": ar, "pdl": pdl, "us_per_launch": round(us, 3),
+        print(json.dumps({"shape": name, "bn": bn, "cg": cg, "sk": sk, "pdl": pdl, "us_per_launch": round(us, 3),
                           "tflops": round(flops / us / 1e6, 1)}), flush=True)
     del g
 
@@ -173,7 +172,5 @@ if __name__ == "__main__":
         for cg, bn, sk in ((1, 128, 0), (1, 192, 0), (1, 256, 0), (2, 128, 0), (2, 256, 0), (2, 512, 0),
                            (1, 256, 2), (2, 256, 2)):
             run(name, reps, bn, 1, cg, sk)
-        if SHAPES[name][2] <= 512:  # K <= 512: the A-resident pairs
-            run(name, reps, 0, 1, 2, 0, ar=2)
         if os.environ.get("CUBLAS", "1") == "1":
             run_cublas(name, reps)
