@@ -188,10 +188,6 @@ struct flowmoe_ctx {
   unsigned int *flags = nullptr, *piece_cnt = nullptr, *seen = nullptr, *p2p_err = nullptr;
   unsigned int* grid_cnt = nullptr;      // [4*R] CTA counters of the fused send+wait kernel
   std::vector<unsigned int*> peer_flags; // per rank: its flags array (mapped)
-  // peer-memory all-reduce (FLOWMOE_P2P_AR): every rank's mapping of a registered grad buffer
-  struct ArReg { float* ptr; unsigned long long base; std::vector<float*> peers; bool ok; };
-  std::vector<ArReg> ar_regs;
-  bool p2p_ar = false;
   std::vector<void*> peer_dxc;           // per rank: its dispatch-bwd receive buffer (mapped)
   std::map<const void*, std::vector<void*>> peer_saved;  // my saved ptr -> each rank's saved ptr
   std::map<const void*, std::vector<void*>> saved_opened;  // my saved ptr -> peer mappings opened for it
@@ -658,41 +654,6 @@ flowmoe_status group_flush(LocalGroup* g) {
   }
 }
 
-// Peer mappings of the grad buffer containing buf (registered on first use, collectively:
-// every rank submits its all-reduces in the same order, so every rank registers the same
-// buffer at the same call; never while the AR stream is being captured).  false: NCCL.
-int ar_max_ctas();
-bool ar_peers(flowmoe_ctx* x, float* buf, std::vector<float*>* out) {
-  static PFN_getAddressRange get_range = nullptr;
-  if (!get_range) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
-      get_range = reinterpret_cast<PFN_getAddressRange>(fn);
-  }
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  if (!get_range || get_range(&base, &size, (CUdeviceptr)buf) != CUDA_SUCCESS) return false;
-  for (const flowmoe_ctx::ArReg& r : x->ar_regs)
-    if (r.base == (unsigned long long)base) {
-      if (!r.ok) return false;
-      out->resize(r.peers.size());
-      for (size_t q = 0; q < r.peers.size(); ++q) (*out)[q] = r.peers[q] + (buf - r.ptr);
-      return true;
-    }
-  if (capture_id(x->s_ar)) return false;
-  std::vector<void*> v;
-  flowmoe_ctx::ArReg reg{buf, (unsigned long long)base, {}, false};
-  if (ipc_exchange(x, buf, &v, &x->ipc_opened) == FLOWMOE_OK) {
-    reg.ok = true;
-    for (void* q : v) reg.peers.push_back(reinterpret_cast<float*>(q));
-  }
-  x->ar_regs.push_back(reg);
-  if (!reg.ok) return false;
-  *out = reg.peers;
-  return true;
-}
-
 flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_bytes,
                          cudaEvent_t ready) {
   if (ready) FM_CUDA(cudaStreamWaitEvent(x->s_ar, ready, 0));
@@ -711,19 +672,10 @@ flowmoe_status submit_ar(flowmoe_ctx* x, float* buf, size_t count, size_t chunk_
     return group_flush(g);
   }
   int ci = 0;
-  std::vector<float*> peers;
-  const bool p2p = x->p2p_ar && ar_peers(x, buf, &peers);
   return for_each_ar_chunk(count, chunk_bytes, [&](size_t off, size_t n) {
     const int tk = task_begin(x, x->s_ar);
     int pi = prof_start(x->s_ar);
-    if (p2p) {
-      std::vector<float*> pc(peers.size());
-      for (size_t q = 0; q < peers.size(); ++q) pc[q] = peers[q] + off;
-      FM_K(5, ar_p2p(buf + off, pc.data(), x->peer_flags.data(), x->flags, x->seen, x->p2p_err, (int)x->P,
-                     x->cfg.rank, x->cfg.R, (int64_t)n, ar_max_ctas(), x->s_ar));
-    } else {
-      FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
-    }
+    FM_NCCL(ncclAllReduce(buf + off, buf + off, n, ncclFloat, ncclSum, x->comm_ar, x->s_ar));
     prof_stop(pi, KK_AR, 0, 4.0 * n * 2.0 * (x->P - 1) / x->P, x->s_ar);
     task_end(x, tk, TK_AR, ci++, x->s_ar);
     return FLOWMOE_OK;
@@ -1024,17 +976,15 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
   }
   if (x->P > 1) x->a2a_stream.push_back(x->s_a2a);
   if (x->P > 1 && (g || cfg->a2a_impl == FLOWMOE_A2A_P2P)) {
-    // arrival counters [kind][R][P]: kinds 0-3 the A2A exchanges, 4-6 the peer-memory AR's
-    // barriers; seen [8][R]; err; grid counters [4][R]
-    const size_t nfl = (size_t)7 * x->cfg.R * x->P;
-    const size_t bytes = (2 * nfl + 12 * x->cfg.R + 1) * sizeof(unsigned int);
+    const size_t nfl = (size_t)4 * x->cfg.R * x->P;
+    const size_t bytes = (2 * nfl + 8 * x->cfg.R + 1) * sizeof(unsigned int);
     if (!alloc(&x->p2p_arena, bytes) || cudaMemset(x->p2p_arena, 0, bytes) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess)
       return cleanup_fail(fail(FLOWMOE_ERR_OOM, "p2p arena allocation failed"));
     x->flags = reinterpret_cast<unsigned int*>(x->p2p_arena);
     x->piece_cnt = x->flags + nfl;
     x->seen = x->piece_cnt + nfl;
-    x->p2p_err = x->seen + 8 * x->cfg.R;
+    x->p2p_err = x->seen + 4 * x->cfg.R;
     x->grid_cnt = x->p2p_err + 1;
     if (!g) {
       std::vector<void*> v;
@@ -1043,7 +993,6 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
       for (void* q : v) x->peer_flags.push_back(reinterpret_cast<unsigned int*>(q));
       if (ipc_exchange(x, x->dxc, &x->peer_dxc, &x->ipc_opened) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
       x->p2p = true;
-      x->p2p_ar = getenv("FLOWMOE_P2P_AR") != nullptr;  // A/B: peer-memory all-reduce instead of NCCL
     }
   }
   // A2A lanes (NCCL path only: the peer-memory exchanges run on the compute lanes)

@@ -214,126 +214,6 @@ __global__ void __launch_bounds__(256) local_allreduce_kernel(LocalArArgs a) {
   }
 }
 
-// ---- peer-memory all-reduce of one fp32 chunk across P GPUs (reduce-scatter + all-gather
-// through CUDA-IPC pointers to every rank's buffer).  Rank q owns the q-th of P equal
-// float4 ranges; the sums are taken in rank order, so every rank ends with the same bits.
-// Per chunk, on the AR stream: barrier(ready) -> RS (owner sums its range from all ranks,
-// in place) -> barrier(reduced) -> AG (copies every other owner's range) -> barrier(read),
-// the last so that no rank overwrites its buffer (next iteration's grads) while a peer still
-// reads it.  A barrier signals every rank's arrival counter of that phase (kinds 4-6 of the
-// peer-memory arena) and waits for all P, like the A2A's arrival counters.
-struct ArArgs {
-  float* mine;
-  float* peers[8];
-  unsigned int* peer_flags[8];
-  unsigned int* my_flags;
-  unsigned int* seen;
-  unsigned int* err;
-  int P, me, R, kind;
-  int64_t n;
-};
-
-__global__ void ar_p2p_barrier_kernel(ArArgs a) {
-  griddep_wait();  // the previous phase's kernel is complete (its writes visible)
-  __threadfence_system();
-  if (threadIdx.x < a.P)
-    atomicAdd_system(a.peer_flags[threadIdx.x] + ((int64_t)a.kind * a.R) * a.P + a.me, 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) p2p_wait_sources(a.my_flags, a.seen, a.err, a.kind, 0, a.R, a.P);
-  __syncthreads();
-  griddep_launch();  // dependents only after every rank has arrived (see the send+wait kernel)
-}
-
-FM_DEV void ar_range(int64_t nv, int P, int q, int64_t& v0, int64_t& v1) {
-  v0 = nv * q / P;
-  v1 = nv * (q + 1) / P;
-}
-
-__global__ void __launch_bounds__(512) ar_p2p_rs_kernel(ArArgs a) {
-  FM_PDL_ENTRY();
-  const int64_t nv = a.n / 4;
-  int64_t v0, v1;
-  ar_range(nv, a.P, a.me, v0, v1);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < v1; i += 2 * stride) {
-    const bool two = i + stride < v1;
-    float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
-    float4 x0[8], x1[8];  // every rank's values in flight before the adds
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q < a.P) {
-        const float4* src = reinterpret_cast<const float4*>(q == a.me ? a.mine : a.peers[q]);
-        x0[q] = __ldcg(src + i);
-        if (two) x1[q] = __ldcg(src + i + stride);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q < a.P) {
-        acc0.x += x0[q].x; acc0.y += x0[q].y; acc0.z += x0[q].z; acc0.w += x0[q].w;
-        if (two) { acc1.x += x1[q].x; acc1.y += x1[q].y; acc1.z += x1[q].z; acc1.w += x1[q].w; }
-      }
-    }
-    reinterpret_cast<float4*>(a.mine)[i] = acc0;
-    if (two) reinterpret_cast<float4*>(a.mine)[i + stride] = acc1;
-  }
-  if (a.me == a.P - 1)  // the scalar tail belongs to the last rank
-    for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride) {
-      float acc = 0.f;
-      for (int q = 0; q < a.P; ++q) acc += __ldcg((q == a.me ? a.mine : a.peers[q]) + i);
-      a.mine[i] = acc;
-    }
-}
-
-__global__ void __launch_bounds__(512) ar_p2p_ag_kernel(ArArgs a) {
-  FM_PDL_ENTRY();
-  const int64_t nv = a.n / 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int q = 0; q < a.P; ++q) {
-    if (q == a.me) continue;
-    int64_t v0, v1;
-    ar_range(nv, a.P, q, v0, v1);
-    const float4* src = reinterpret_cast<const float4*>(a.peers[q]);
-    float4* dst = reinterpret_cast<float4*>(a.mine);
-    for (int64_t i = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < v1; i += 4 * stride) {
-      float4 t[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (i + j * stride < v1) t[j] = __ldcg(src + i + j * stride);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (i + j * stride < v1) dst[i + j * stride] = t[j];
-    }
-  }
-  if (a.me != a.P - 1)
-    for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride)
-      a.mine[i] = __ldcg(a.peers[a.P - 1] + i);
-}
-
-int ar_p2p(float* mine, float* const* peers, unsigned int* const* peer_flags, unsigned int* my_flags,
-           unsigned int* seen, unsigned int* err, int P, int me, int R, int64_t n, int ctas, cudaStream_t s) {
-  if (P > 8 || n <= 0) return (int)cudaErrorInvalidValue;
-  for (int q = 0; q < P; ++q)
-    if ((reinterpret_cast<uintptr_t>(q == me ? mine : peers[q]) & 15) != 0) return (int)cudaErrorMisalignedAddress;
-  ArArgs a;
-  a.mine = mine;
-  for (int q = 0; q < 8; ++q) {
-    a.peers[q] = q < P ? peers[q] : nullptr;
-    a.peer_flags[q] = q < P ? peer_flags[q] : nullptr;
-  }
-  a.my_flags = my_flags; a.seen = seen; a.err = err;
-  a.P = P; a.me = me; a.R = R; a.n = n;
-  for (int phase = 0; phase < 3; ++phase) {
-    a.kind = 4 + phase;
-    launch_k(ar_p2p_barrier_kernel, 1, 32, 0, s, a);
-    if (cudaError_t e = cudaGetLastError()) return (int)e;
-    if (phase == 0) launch_k(ar_p2p_rs_kernel, ctas, 512, 0, s, a);
-    if (phase == 1) launch_k(ar_p2p_ag_kernel, ctas, 512, 0, s, a);
-    if (cudaError_t e = cudaGetLastError()) return (int)e;
-  }
-  return 0;
-}
-
 int local_allreduce(float* const* bufs, int P, int64_t off, int64_t n, cudaStream_t s) {
   if (P > 8 || n < 0) return (int)cudaErrorInvalidValue;
   LocalArArgs a;

@@ -141,9 +141,5 @@ int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, 
 // Simulated world all-reduce (flowmoe_create_local_group): bufs[q][off, off+n) of the P
 // ranks summed in rank order and written back to all of them; 16-byte aligned chunk starts.
 int local_allreduce(float* const* bufs, int P, int64_t off, int64_t n, cudaStream_t s);
-// peer-memory all-reduce of one fp32 chunk (k_p2p.cu): barrier, reduce-scatter, barrier,
-// all-gather, barrier on stream s; peers[q] = rank q's chunk (mine for q == me)
-int ar_p2p(float* mine, float* const* peers, unsigned int* const* peer_flags, unsigned int* my_flags,
-           unsigned int* seen, unsigned int* err, int P, int me, int R, int64_t n, int ctas, cudaStream_t s);
 
 }  // namespace fm
