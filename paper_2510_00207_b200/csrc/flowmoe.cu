@@ -188,7 +188,6 @@ struct flowmoe_ctx {
   unsigned int *flags = nullptr, *piece_cnt = nullptr, *seen = nullptr, *p2p_err = nullptr;
   unsigned int* grid_cnt = nullptr;      // [4*R] CTA counters of the fused send+wait kernel
   std::vector<unsigned int*> peer_flags; // per rank: its flags array (mapped)
-  bool ce_a2a = false;                   // FLOWMOE_CE_A2A (A/B): exchanges by copy engine
   std::vector<void*> peer_dxc;           // per rank: its dispatch-bwd receive buffer (mapped)
   std::map<const void*, std::vector<void*>> peer_saved;  // my saved ptr -> each rank's saved ptr
   std::map<const void*, std::vector<void*>> saved_opened;  // my saved ptr -> peer mappings opened for it
@@ -994,7 +993,6 @@ flowmoe_status create_impl(const flowmoe_config* cfg, const uint8_t id[128], int
       for (void* q : v) x->peer_flags.push_back(reinterpret_cast<unsigned int*>(q));
       if (ipc_exchange(x, x->dxc, &x->peer_dxc, &x->ipc_opened) != FLOWMOE_OK) return cleanup_fail(FLOWMOE_ERR_CUDA);
       x->p2p = true;
-      x->ce_a2a = getenv("FLOWMOE_CE_A2A") != nullptr;
     }
   }
   // A2A lanes (NCCL path only: the peer-memory exchanges run on the compute lanes)
@@ -1229,11 +1227,6 @@ flowmoe_status p2p_exchange(flowmoe_ctx* x, int kind, int r, const void* src, vo
   const int R = x->cfg.R;
   const int64_t blk = x->C * x->M * (int64_t)x->es;
   LocalGroup* g = x->group;
-  if (x->ce_a2a && !g) {
-    FM_K(1, a2a_ce(src, dst, x->peer_flags.data(), x->flags, x->seen, x->p2p_err, kind, r, R, (int)x->P,
-                   (int)x->El, x->cfg.rank, to_experts, blk, sa));
-    return FLOWMOE_OK;
-  }
   FM_K(1, a2a_p2p(src, dst, x->peer_flags.data(), x->piece_cnt, x->flags, x->seen, x->p2p_err, kind, r, R,
                   (int)x->P, (int)x->El, x->cfg.rank, to_experts, blk, sa, sa, true, g == nullptr,
                   g ? nullptr : x->grid_cnt));

@@ -12,7 +12,6 @@
 //             every source, then seen += 1.  Counters are monotonic, so graph replays
 //             and repeated blocks need no resets.  A spin bounded by ~10 s sets an error
 //             word instead of hanging (checked by flowmoe_allreduce_wait).
-#include <cstring>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -64,8 +63,8 @@ FM_DEV void p2p_wait_sources(const unsigned int* flags, unsigned int* seen, unsi
   seen[kind * R + r] = expect;
 }
 
-__host__ __device__ __forceinline__ int64_t owner_off(int e, int r, int R, int64_t blk) { return ((int64_t)e * R + r) * blk; }
-__host__ __device__ __forceinline__ int64_t expert_off(int el, int r, int q, int R, int P, int64_t blk) {
+FM_DEV int64_t owner_off(int e, int r, int R, int64_t blk) { return ((int64_t)e * R + r) * blk; }
+FM_DEV int64_t expert_off(int el, int r, int q, int R, int P, int64_t blk) {
   return (((int64_t)el * R + r) * P + q) * blk;
 }
 
@@ -159,43 +158,6 @@ __global__ void __launch_bounds__(256) a2a_p2p_send_wait_kernel(P2PArgs a) {
     __syncthreads();
     griddep_launch();
   }
-}
-
-// copy-engine exchange (cudaMemcpy2DAsync per destination on the same stream, then this
-// kernel): publish (kind, r) to every destination and wait for every source
-__global__ void a2a_ce_signal_wait_kernel(P2PArgs a) {
-  griddep_wait();
-  __threadfence_system();
-  if (threadIdx.x < a.P)
-    atomicAdd_system(a.peer_flags[threadIdx.x] + ((int64_t)a.kind * a.R + a.r) * a.P + a.me, 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) p2p_wait_sources(a.my_flags, a.seen, a.err, a.kind, a.r, a.R, a.P);
-  __syncthreads();
-  griddep_launch();
-}
-
-int a2a_ce(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* my_flags,
-           unsigned int* seen, unsigned int* err, int kind, int r, int R, int P, int El, int me, int to_experts,
-           int64_t blk_bytes, cudaStream_t s) {
-  if (P > 8) return (int)cudaErrorInvalidValue;
-  const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
-  for (int q = 0; q < P; ++q) {
-    // to experts: my owner-side blocks of q's experts (pitch R blocks) -> q's expert side
-    // slot (el, r, me) (pitch R·P blocks); combine: the reverse
-    const int64_t soff = to_experts ? owner_off(q * El, r, R, blk_bytes) : expert_off(0, r, q, R, P, blk_bytes);
-    const int64_t doff = to_experts ? expert_off(0, r, me, R, P, blk_bytes) : owner_off(me * El, r, R, blk_bytes);
-    const size_t sp = (size_t)(to_experts ? R : R * P) * blk_bytes, dp = (size_t)(to_experts ? R * P : R) * blk_bytes;
-    if (cudaError_t e = cudaMemcpy2DAsync(reinterpret_cast<uint8_t*>(dst[q]) + doff, dp, sb + soff, sp,
-                                          (size_t)blk_bytes, (size_t)El, cudaMemcpyDeviceToDevice, s))
-      return (int)e;
-  }
-  P2PArgs a;
-  memset(&a, 0, sizeof(a));
-  for (int q = 0; q < 8; ++q) a.peer_flags[q] = q < P ? peer_flags[q] : nullptr;
-  a.my_flags = my_flags; a.seen = seen; a.err = err;
-  a.kind = kind; a.r = r; a.R = R; a.P = P; a.El = El; a.me = me;
-  launch_k(a2a_ce_signal_wait_kernel, 1, 32, 0, s, a);
-  return (int)cudaGetLastError();
 }
 
 // one CTA of P threads: wait for all sources of (kind, r)

@@ -141,10 +141,5 @@ int a2a_p2p(const void* src, void* const* dst, unsigned int* const* peer_flags, 
 // Simulated world all-reduce (flowmoe_create_local_group): bufs[q][off, off+n) of the P
 // ranks summed in rank order and written back to all of them; 16-byte aligned chunk starts.
 int local_allreduce(float* const* bufs, int P, int64_t off, int64_t n, cudaStream_t s);
-// copy-engine variant of the A2A exchange (k_p2p.cu): one cudaMemcpy2DAsync per destination
-// (El blocks of blk_bytes, strided), then one kernel that publishes and waits like a2a_p2p
-int a2a_ce(const void* src, void* const* dst, unsigned int* const* peer_flags, unsigned int* my_flags,
-           unsigned int* seen, unsigned int* err, int kind, int r, int R, int P, int El, int me, int to_experts,
-           int64_t blk_bytes, cudaStream_t s);
 
 }  // namespace fm
